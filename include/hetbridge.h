@@ -1,0 +1,163 @@
+/*
+ * hetbridge — C-ABI of the B200-native boundary communicator.
+ *
+ * Drop-in boundary for the reference's hetsim::grid / hetsim::bridge API
+ * (/root/reference/proj/core/include/hetsim/{grid,bridge}.hpp). The reference
+ * is C++ with no FFI; each entry point below names the reference declaration
+ * it replaces. Plain pointers and sizes only — no C++ or torch types.
+ *
+ * Status convention: 0 = OK; otherwise the reference ErrorCode ordinal + 1
+ * (error.hpp:13-38: 1 RankOutOfModule, 2 CoordOutOfBounds, 3 IndivisibleBatch,
+ * 4 PartialOverlap, 5 NonIntegerFan, 6 PlanInfeasible, 7 ShardIntervalMismatch,
+ * 8 MissingSourceShard, 9 GradIntervalMismatch, 10 UnknownMicrobatch, ...,
+ * 13 ShapeMismatch, 16 DivisibilityViolation, 20 NotColocated,
+ * 24 InvalidArgument) and two device-runtime additions: 25 CudaError,
+ * 26 Timeout. hb_last_error() returns the message of the calling thread's last
+ * failure. No exception crosses this boundary.
+ */
+#ifndef HETBRIDGE_H_
+#define HETBRIDGE_H_
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HB_OK 0
+#define HB_ERR_CUDA 25
+#define HB_ERR_TIMEOUT 26
+
+/* dtypes */
+#define HB_BF16 0
+#define HB_FP16 1
+#define HB_FP32 2
+#define HB_FP64 3
+
+/* placement (grid.hpp:61) and DpKind (bridge.hpp:38) */
+#define HB_COLOCATED 0
+#define HB_NONCOLOCATED 1
+#define HB_EQUAL 0
+#define HB_FANIN 1
+#define HB_FANOUT 2
+
+/* per-logical-rank buffer slots */
+#define HB_SLOT_SRC_ACT 0  /* source shard: forward input                     */
+#define HB_SLOT_DST_ACT 1  /* destination shard / CP token slice: fwd output  */
+#define HB_SLOT_DST_GRAD 2 /* destination gradient: backward input            */
+#define HB_SLOT_SRC_GRAD 3 /* source gradient: backward output (accumulated)  */
+#define HB_SLOT_TEXT 4     /* text embedding rows: splice forward input       */
+
+/* splice text numbering */
+#define HB_TEXT_FULL 0  /* text buffer row = global text index (-1-code)    */
+#define HB_TEXT_SLICE 1 /* text buffer row = k-th text position of the slice */
+
+typedef struct hb_plan hb_plan;
+typedef struct hb_splice hb_splice;
+typedef struct hb_exec hb_exec;
+
+/* hetsim::grid::ModuleLayout (grid.hpp:16-31) */
+typedef struct {
+  const char* name;
+  int tp, cp, pp, dp, rank_offset;
+} hb_layout;
+
+/* hetsim::grid::BoundaryEdge (grid.hpp:55-60) */
+typedef struct {
+  hb_layout source, dest;
+  int global_batch;
+  int feature_width;
+} hb_edge;
+
+/* ---- errors ---------------------------------------------------------------- */
+size_t hb_last_error(char* buf, size_t cap);
+const char* hb_error_name(int status); /* error.cpp error_code_name */
+int hb_abi_version(void);
+
+/* ---- grid (grid.hpp:64-92) --------------------------------------------------- */
+int hb_coord_of_rank(const hb_layout* l, int rank, int coord4[4]);      /* grid.hpp:64 */
+int hb_rank_of_coord(const hb_layout* l, const int coord4[4], int* rank); /* grid.hpp:67 */
+int hb_partition_batch(int batch, int dp, int* start_len, int cap_pairs); /* grid.hpp:70 */
+int hb_leader_rank(const hb_layout* l, int pp, int dp, int* rank);       /* grid.hpp:74 */
+int hb_placement_of_edge(const hb_edge* e, int* placement);              /* grid.hpp:78 */
+int hb_ranks_of_stage(const hb_layout* l, int pp, int* out, int cap, int* n); /* grid.hpp:82 */
+int hb_replica_group(const hb_layout* l, int pp, int dp, int* out, int cap, int* n); /* :86 */
+
+/* ---- plan (bridge.hpp:137-142) ----------------------------------------------- */
+int hb_classify_dp_relation(const hb_edge* e, int* kind, int* factor); /* bridge.hpp:137 */
+int hb_plan_create(const hb_edge* e, hb_plan** out);                   /* bridge.hpp:138 plan_bridge */
+void hb_plan_destroy(hb_plan* p);
+int hb_plan_export(const hb_plan* p, int elem_bytes, char* buf, size_t cap, size_t* len); /* :142 */
+int hb_plan_info(const hb_plan* p, int* placement, int* kind, int* factor,
+                 int* cross_boundary_messages, int* world); /* BridgePlan fields, :122-135 */
+
+/* ---- splice (tinymodel.hpp:94-112) -------------------------------------------- */
+int hb_cp_token_slice(int seq_len, int cp, int cp_idx, int* start, int* length); /* :95 */
+/* codes[Q*S]: >= 0 vision row (local sample j)*S_v + token t; < 0 text row -1-code. */
+int hb_splice_create(int Q, int S, int d_h, int S_v, int text_mode, const int* codes,
+                     hb_splice** out);
+void hb_splice_destroy(hb_splice* s);
+
+/* ---- ownership index maps (host only; for inspection and tests) --------------- */
+typedef struct {
+  int src_rank, src_slot;
+  long long src_off;
+  int dst_rank, dst_slot;
+  long long dst_off;
+  long long n; /* elements */
+} hb_copy_seg;
+typedef struct {
+  int rank, slot;
+  long long off;
+} hb_ref;
+typedef struct {
+  int dst_rank, dst_slot;
+  long long dst_off;
+  long long n;
+  int nterms, term0;
+} hb_reduce_seg;
+int hb_index_forward(const hb_plan* p, const hb_splice* s, hb_copy_seg* out, size_t cap, size_t* n);
+int hb_index_backward(const hb_plan* p, const hb_splice* s, hb_reduce_seg* out, size_t cap,
+                      size_t* n, hb_ref* terms, size_t tcap, size_t* tn);
+int hb_index_buffer_elems(const hb_plan* p, const hb_splice* s, int rank, int slot,
+                          long long* elems);
+
+/* ---- device execution (replaces BridgeRuntime, bridge.hpp:146-173, and the
+ *      whole-edge bridge_forward/bridge_backward, :175-185) --------------------- */
+typedef struct {
+  int act_dtype;      /* HB_BF16 ... activations (source/destination shards)  */
+  int grad_in_dtype;  /* destination gradients                                  */
+  int grad_out_dtype; /* source gradients (fp32 recommended for accumulation)   */
+  int mb_slots;       /* buffer sets for microbatches in flight                 */
+  int internal_alloc; /* 1: allocate the IPC-exported device region            */
+  int blocks_per_sm;
+  int threads;
+  double timeout_s; /* cross-GPU flag wait timeout                            */
+} hb_exec_config;
+void hb_exec_config_default(hb_exec_config* c);
+
+/* rank_to_gpu[n_ranks]: the GPU (0..n_gpus-1) hosting each logical rank; this
+ * process drives GPU my_gpu (the current CUDA device). Collective over the
+ * processes of the exec group when n_gpus > 1. */
+int hb_exec_create(const hb_plan* p, const hb_splice* s, int n_gpus, int my_gpu,
+                   const int* rank_to_gpu, int n_ranks, const hb_exec_config* cfg,
+                   hb_exec** out);
+void hb_exec_destroy(hb_exec* x);
+int hb_exec_ipc_handle(hb_exec* x, void* out64);
+int hb_exec_open_peers(hb_exec* x, const void* handles, size_t nbytes); /* n_gpus*64 bytes */
+int hb_exec_buffer(hb_exec* x, int rank, int slot, int mb_slot, void** ptr, size_t* bytes);
+int hb_exec_bind(hb_exec* x, int rank, int slot, int mb_slot, void* ptr, size_t bytes);
+/* forward: BridgeRuntime::forward_{source,dest,colocated} for every resident rank */
+int hb_exec_forward(hb_exec* x, int mb, void* cuda_stream);
+/* backward: BridgeRuntime::backward_* ; src_grad = beta*src_grad + returned gradient */
+int hb_exec_backward(hb_exec* x, int mb, float beta, void* cuda_stream);
+int hb_exec_seed_forward_record(hb_exec* x, int mb); /* bridge.hpp:165 */
+int hb_exec_status(hb_exec* x, unsigned* device_error);
+int hb_exec_stats(hb_exec* x, long long* fwd_segments, long long* bwd_segments,
+                  long long* fwd_bytes, long long* bwd_elems, long long* launches);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HETBRIDGE_H_ */

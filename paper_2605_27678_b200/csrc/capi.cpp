@@ -1,0 +1,379 @@
+// hetbridge — C-ABI implementation (include/hetbridge.h). Every entry point
+// catches hb::Error and maps it to `ErrorCode ordinal + 1`; nothing throws
+// across the boundary.
+#include "hetbridge.h"
+
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "hb/bridge.hpp"
+#include "hb/index_map.hpp"
+#include "hb/runtime.hpp"
+
+struct hb_plan {
+  hb::bridge::BridgePlan plan;
+};
+struct hb_splice {
+  hb::index::SpliceSpec spec;
+};
+struct hb_exec {
+  std::unique_ptr<hb::rt::Exec> x;
+};
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return HB_OK;
+  } catch (const hb::Error& e) {
+    g_err = e.what();
+    return static_cast<int>(e.code()) + 1;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return static_cast<int>(hb::ErrorCode::InvalidArgument) + 1;
+  }
+}
+
+void need(const void* p, const char* what) {
+  if (!p) hb::raise(hb::ErrorCode::InvalidArgument, std::string("null ") + what);
+}
+
+hb::grid::ModuleLayout layout(const hb_layout* l) {
+  need(l, "layout");
+  hb::grid::ModuleLayout m;
+  m.name = l->name ? l->name : "";
+  m.tp = l->tp;
+  m.cp = l->cp;
+  m.pp = l->pp;
+  m.dp = l->dp;
+  m.rank_offset = l->rank_offset;
+  return m;
+}
+
+hb::grid::BoundaryEdge edge(const hb_edge* e) {
+  need(e, "edge");
+  return {layout(&e->source), layout(&e->dest), e->global_batch, e->feature_width};
+}
+
+void fill(const std::vector<int>& v, int* out, int cap, int* n) {
+  need(n, "count");
+  *n = static_cast<int>(v.size());
+  for (int i = 0; i < cap && i < *n; ++i) out[i] = v[i];
+}
+
+const hb::index::SpliceSpec* spec(const hb_splice* s) { return s ? &s->spec : nullptr; }
+}  // namespace
+
+extern "C" {
+
+size_t hb_last_error(char* buf, size_t cap) {
+  if (buf && cap) {
+    const size_t n = std::min(cap - 1, g_err.size());
+    std::memcpy(buf, g_err.data(), n);
+    buf[n] = 0;
+  }
+  return g_err.size();
+}
+
+const char* hb_error_name(int status) {
+  if (status == HB_OK) return "OK";
+  return hb::error_code_name(static_cast<hb::ErrorCode>(status - 1));
+}
+
+int hb_abi_version(void) { return 1; }
+
+int hb_coord_of_rank(const hb_layout* l, int rank, int coord4[4]) {
+  return guard([&] {
+    need(coord4, "coord");
+    const auto c = hb::grid::coord_of_rank(layout(l), rank);
+    coord4[0] = c.tp_idx;
+    coord4[1] = c.cp_idx;
+    coord4[2] = c.pp_idx;
+    coord4[3] = c.dp_idx;
+  });
+}
+
+int hb_rank_of_coord(const hb_layout* l, const int coord4[4], int* rank) {
+  return guard([&] {
+    need(coord4, "coord");
+    need(rank, "rank");
+    *rank = hb::grid::rank_of_coord(layout(l), {coord4[0], coord4[1], coord4[2], coord4[3]});
+  });
+}
+
+int hb_partition_batch(int batch, int dp, int* start_len, int cap_pairs) {
+  return guard([&] {
+    const auto v = hb::grid::partition_batch(batch, dp);
+    for (int i = 0; i < cap_pairs && i < static_cast<int>(v.size()); ++i) {
+      start_len[2 * i] = v[i].start;
+      start_len[2 * i + 1] = v[i].length;
+    }
+  });
+}
+
+int hb_leader_rank(const hb_layout* l, int pp, int dp, int* rank) {
+  return guard([&] {
+    need(rank, "rank");
+    *rank = hb::grid::leader_rank(layout(l), pp, dp);
+  });
+}
+
+int hb_placement_of_edge(const hb_edge* e, int* placement) {
+  return guard([&] {
+    need(placement, "placement");
+    *placement = static_cast<int>(hb::grid::placement_of_edge(edge(e)));
+  });
+}
+
+int hb_ranks_of_stage(const hb_layout* l, int pp, int* out, int cap, int* n) {
+  return guard([&] { fill(hb::grid::ranks_of_stage(layout(l), pp), out, cap, n); });
+}
+
+int hb_replica_group(const hb_layout* l, int pp, int dp, int* out, int cap, int* n) {
+  return guard([&] { fill(hb::grid::replica_group(layout(l), pp, dp), out, cap, n); });
+}
+
+int hb_classify_dp_relation(const hb_edge* e, int* kind, int* factor) {
+  return guard([&] {
+    need(kind, "kind");
+    need(factor, "factor");
+    const auto r = hb::bridge::classify_dp_relation(edge(e));
+    *kind = static_cast<int>(r.kind);
+    *factor = r.factor;
+  });
+}
+
+int hb_plan_create(const hb_edge* e, hb_plan** out) {
+  return guard([&] {
+    need(out, "out");
+    *out = nullptr;
+    auto p = std::make_unique<hb_plan>();
+    p->plan = hb::bridge::plan_bridge(edge(e));
+    *out = p.release();
+  });
+}
+
+void hb_plan_destroy(hb_plan* p) { delete p; }
+
+int hb_plan_export(const hb_plan* p, int elem_bytes, char* buf, size_t cap, size_t* len) {
+  return guard([&] {
+    need(p, "plan");
+    if (elem_bytes < 1) hb::raise(hb::ErrorCode::InvalidArgument, "elem_bytes must be >= 1");
+    const std::string s = hb::bridge::export_plan(p->plan, elem_bytes);
+    if (len) *len = s.size();
+    if (buf && cap) {
+      const size_t n = std::min(cap - 1, s.size());
+      std::memcpy(buf, s.data(), n);
+      buf[n] = 0;
+    }
+  });
+}
+
+int hb_plan_info(const hb_plan* p, int* placement, int* kind, int* factor, int* xmsgs, int* world) {
+  return guard([&] {
+    need(p, "plan");
+    const auto& b = p->plan;
+    if (placement) *placement = static_cast<int>(b.placement);
+    if (kind) *kind = static_cast<int>(b.relation.kind);
+    if (factor) *factor = b.relation.factor;
+    if (xmsgs) *xmsgs = b.cross_boundary_messages();
+    if (world) *world = std::max(b.edge.source.rank_end(), b.edge.dest.rank_end());
+  });
+}
+
+int hb_cp_token_slice(int seq_len, int cp, int cp_idx, int* start, int* length) {
+  return guard([&] {
+    need(start, "start");
+    need(length, "length");
+    if (cp < 1 || cp_idx < 0 || cp_idx >= cp) hb::raise(hb::ErrorCode::InvalidArgument, "cp index out of range");
+    if (seq_len % cp)
+      hb::raise(hb::ErrorCode::DivisibilityViolation, "seq_len not divisible by cp");
+    *length = seq_len / cp;
+    *start = cp_idx * *length;
+  });
+}
+
+int hb_splice_create(int Q, int S, int d_h, int S_v, int text_mode, const int* codes, hb_splice** out) {
+  return guard([&] {
+    need(out, "out");
+    need(codes, "codes");
+    if (Q < 1 || S < 1) hb::raise(hb::ErrorCode::InvalidArgument, "Q and S must be >= 1");
+    if (text_mode != HB_TEXT_FULL && text_mode != HB_TEXT_SLICE)
+      hb::raise(hb::ErrorCode::InvalidArgument, "unknown text mode");
+    auto s = std::make_unique<hb_splice>();
+    s->spec.Q = Q;
+    s->spec.S = S;
+    s->spec.d_h = d_h;
+    s->spec.S_v = S_v;
+    s->spec.text_mode = static_cast<hb::index::TextMode>(text_mode);
+    s->spec.codes.assign(codes, codes + static_cast<size_t>(Q) * S);
+    *out = s.release();
+  });
+}
+
+void hb_splice_destroy(hb_splice* s) { delete s; }
+
+int hb_index_forward(const hb_plan* p, const hb_splice* s, hb_copy_seg* out, size_t cap, size_t* n) {
+  return guard([&] {
+    need(p, "plan");
+    need(n, "count");
+    const auto m = hb::index::build_index_map(p->plan, spec(s));
+    *n = m.fwd.size();
+    for (size_t i = 0; out && i < cap && i < m.fwd.size(); ++i) {
+      const auto& c = m.fwd[i];
+      out[i] = {c.src.rank, c.src.slot, c.src.off, c.dst.rank, c.dst.slot, c.dst.off, c.n};
+    }
+  });
+}
+
+int hb_index_backward(const hb_plan* p, const hb_splice* s, hb_reduce_seg* out, size_t cap, size_t* n,
+                      hb_ref* terms, size_t tcap, size_t* tn) {
+  return guard([&] {
+    need(p, "plan");
+    need(n, "count");
+    const auto m = hb::index::build_index_map(p->plan, spec(s));
+    *n = m.bwd.size();
+    size_t t = 0;
+    for (size_t i = 0; i < m.bwd.size(); ++i) {
+      const auto& r = m.bwd[i];
+      if (out && i < cap)
+        out[i] = {r.dst.rank, r.dst.slot, r.dst.off, r.n, static_cast<int>(r.terms.size()), static_cast<int>(t)};
+      for (const auto& x : r.terms) {
+        if (terms && t < tcap) terms[t] = {x.rank, x.slot, x.off};
+        ++t;
+      }
+    }
+    if (tn) *tn = t;
+  });
+}
+
+int hb_index_buffer_elems(const hb_plan* p, const hb_splice* s, int rank, int slot, long long* elems) {
+  return guard([&] {
+    need(p, "plan");
+    need(elems, "elems");
+    const auto m = hb::index::build_index_map(p->plan, spec(s));
+    if (rank < 0 || rank >= m.world || slot < 0 || slot >= hb::index::kNumSlots)
+      hb::raise(hb::ErrorCode::InvalidArgument, "rank/slot out of range");
+    *elems = m.elems[rank][slot];
+  });
+}
+
+void hb_exec_config_default(hb_exec_config* c) {
+  if (!c) return;
+  hb::rt::ExecConfig d;
+  c->act_dtype = d.act_dtype;
+  c->grad_in_dtype = d.grad_in_dtype;
+  c->grad_out_dtype = d.grad_out_dtype;
+  c->mb_slots = d.mb_slots;
+  c->internal_alloc = d.internal_alloc;
+  c->blocks_per_sm = d.blocks_per_sm;
+  c->threads = d.threads;
+  c->timeout_s = d.timeout_s;
+}
+
+int hb_exec_create(const hb_plan* p, const hb_splice* s, int n_gpus, int my_gpu, const int* rank_to_gpu,
+                   int n_ranks, const hb_exec_config* cfg, hb_exec** out) {
+  return guard([&] {
+    need(p, "plan");
+    need(out, "out");
+    *out = nullptr;
+    hb::rt::ExecConfig c;
+    if (cfg) {
+      c.act_dtype = cfg->act_dtype;
+      c.grad_in_dtype = cfg->grad_in_dtype;
+      c.grad_out_dtype = cfg->grad_out_dtype;
+      c.mb_slots = cfg->mb_slots;
+      c.internal_alloc = cfg->internal_alloc;
+      c.blocks_per_sm = cfg->blocks_per_sm > 0 ? cfg->blocks_per_sm : c.blocks_per_sm;
+      c.threads = cfg->threads > 0 ? cfg->threads : c.threads;
+      c.timeout_s = cfg->timeout_s > 0 ? cfg->timeout_s : c.timeout_s;
+    }
+    std::vector<int> map;
+    if (rank_to_gpu) map.assign(rank_to_gpu, rank_to_gpu + n_ranks);
+    else map.assign(n_ranks, 0);
+    auto x = std::make_unique<hb_exec>();
+    x->x = std::make_unique<hb::rt::Exec>(p->plan, spec(s), n_gpus, my_gpu, std::move(map), c);
+    *out = x.release();
+  });
+}
+
+void hb_exec_destroy(hb_exec* x) { delete x; }
+
+int hb_exec_ipc_handle(hb_exec* x, void* out64) {
+  return guard([&] {
+    need(x, "exec");
+    need(out64, "out");
+    x->x->ipc_handle(out64);
+  });
+}
+
+int hb_exec_open_peers(hb_exec* x, const void* handles, size_t nbytes) {
+  return guard([&] {
+    need(x, "exec");
+    need(handles, "handles");
+    (void)nbytes;
+    x->x->open_peers(handles);
+  });
+}
+
+int hb_exec_buffer(hb_exec* x, int rank, int slot, int mb_slot, void** ptr, size_t* bytes) {
+  return guard([&] {
+    need(x, "exec");
+    need(ptr, "ptr");
+    *ptr = x->x->buffer(rank, slot, mb_slot, bytes);
+  });
+}
+
+int hb_exec_bind(hb_exec* x, int rank, int slot, int mb_slot, void* ptr, size_t bytes) {
+  return guard([&] {
+    need(x, "exec");
+    x->x->bind(rank, slot, mb_slot, ptr, bytes);
+  });
+}
+
+int hb_exec_forward(hb_exec* x, int mb, void* stream) {
+  return guard([&] {
+    need(x, "exec");
+    x->x->forward(mb, stream);
+  });
+}
+
+int hb_exec_backward(hb_exec* x, int mb, float beta, void* stream) {
+  return guard([&] {
+    need(x, "exec");
+    x->x->backward(mb, beta, stream);
+  });
+}
+
+int hb_exec_seed_forward_record(hb_exec* x, int mb) {
+  return guard([&] {
+    need(x, "exec");
+    x->x->seed_forward_record(mb);
+  });
+}
+
+int hb_exec_status(hb_exec* x, unsigned* device_error) {
+  return guard([&] {
+    need(x, "exec");
+    const unsigned e = x->x->device_error();
+    if (device_error) *device_error = e;
+    if (e) hb::raise(hb::ErrorCode::Timeout, "cross-GPU flag wait timed out on the device");
+  });
+}
+
+int hb_exec_stats(hb_exec* x, long long* fs, long long* bs, long long* fb, long long* be, long long* nl) {
+  return guard([&] {
+    need(x, "exec");
+    if (fs) *fs = x->x->local_fwd_segments();
+    if (bs) *bs = x->x->local_bwd_segments();
+    if (fb) *fb = static_cast<long long>(x->x->local_fwd_bytes());
+    if (be) *be = static_cast<long long>(x->x->local_bwd_elems());
+    if (nl) *nl = x->x->launches();
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,277 @@
+// hetbridge — per-edge device runtime (see runtime.hpp).
+#include "hb/runtime.hpp"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+
+namespace hb::rt {
+
+namespace {
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    raise(ErrorCode::CudaError, std::string(what) + ": " + cudaGetErrorString(e));
+}
+constexpr uint64_t kPadBytes = 4096;
+constexpr uint64_t kAlign = 256;
+uint64_t align_up(uint64_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+}  // namespace
+
+Exec::Exec(const bridge::BridgePlan& plan, const index::SpliceSpec* splice, int n_gpus, int my_gpu,
+           std::vector<int> rank_to_gpu, const ExecConfig& cfg)
+    : plan_(plan), n_gpus_(n_gpus), my_gpu_(my_gpu), rank_to_gpu_(std::move(rank_to_gpu)), cfg_(cfg) {
+  if (n_gpus < 1 || n_gpus > dev::kMaxGpus || my_gpu < 0 || my_gpu >= n_gpus)
+    raise(ErrorCode::InvalidArgument, "bad GPU count / index");
+  if (cfg.mb_slots < 1) raise(ErrorCode::InvalidArgument, "mb_slots must be >= 1");
+  for (int dt : {cfg.act_dtype, cfg.grad_in_dtype, cfg.grad_out_dtype})
+    if (dt < dev::kBF16 || dt > dev::kFP64) raise(ErrorCode::InvalidArgument, "unknown dtype");
+  if (cfg.grad_in_dtype == dev::kFP64 || cfg.grad_out_dtype == dev::kFP64)
+    raise(ErrorCode::InvalidArgument, "fp64 gradients are not supported on the device path");
+  map_ = index::build_index_map(plan_, splice);
+  if (static_cast<int>(rank_to_gpu_.size()) < map_.world)
+    raise(ErrorCode::InvalidArgument, "rank_to_gpu must cover every logical rank of the edge");
+  for (int r = 0; r < map_.world; ++r)
+    if (rank_to_gpu_[r] < 0 || rank_to_gpu_[r] >= n_gpus)
+      raise(ErrorCode::InvalidArgument, "rank_to_gpu entry out of range");
+
+  // Exec group: GPUs hosting any rank with a buffer.
+  for (int r = 0; r < map_.world; ++r)
+    for (int s = 0; s < index::kNumSlots; ++s)
+      if (map_.elems[r][s]) group_mask_ |= 1u << gpu_of(r);
+
+  // Deterministic per-GPU layouts.
+  offsets_.assign(n_gpus, std::vector<uint64_t>(map_.world * index::kNumSlots, 0));
+  mb_stride_.assign(n_gpus, 0);
+  for (int g = 0; g < n_gpus; ++g) {
+    uint64_t off = 0;
+    for (int r = 0; r < map_.world; ++r) {
+      if (gpu_of(r) != g) continue;
+      for (int s = 0; s < index::kNumSlots; ++s) {
+        offsets_[g][r * index::kNumSlots + s] = off;
+        off += align_up(static_cast<uint64_t>(map_.elems[r][s]) * dev::dtype_size(slot_dtype(s)));
+      }
+    }
+    mb_stride_[g] = off;
+    region_bytes_ = std::max(region_bytes_, kPadBytes + off * cfg.mb_slots);
+  }
+  bound_.assign(map_.world * index::kNumSlots, std::vector<void*>(cfg.mb_slots, nullptr));
+
+  for (const auto& s : map_.fwd)
+    if (gpu_of(s.dst.rank) == my_gpu_) fwd_local_.push_back(s);
+  for (const auto& s : map_.bwd)
+    if (gpu_of(s.dst.rank) == my_gpu_) bwd_local_.push_back(s);
+
+  ck(cudaGetDevice(&device_), "cudaGetDevice");
+  sm_count_ = dev::device_sm_count();
+  if (cfg_.internal_alloc || n_gpus_ > 1) {
+    ck(cudaMalloc(&local_base_, region_bytes_), "cudaMalloc(region)");
+    ck(cudaMemset(local_base_, 0, kPadBytes), "cudaMemset(pad)");
+  }
+  ck(cudaMalloc(&ctr_, 64), "cudaMalloc(ctr)");
+  ck(cudaMemset(ctr_, 0, 64), "cudaMemset(ctr)");
+  peer_base_.assign(n_gpus_, nullptr);
+  peer_base_[my_gpu_] = local_base_;
+  tables_.resize(cfg.mb_slots);
+}
+
+Exec::~Exec() {
+  for (auto& t : tables_) {
+    cudaFree(t.copy);
+    cudaFree(t.reduce);
+    cudaFree(t.terms);
+  }
+  for (int g = 0; g < n_gpus_; ++g)
+    if (g != my_gpu_ && peer_base_[g]) cudaIpcCloseMemHandle(peer_base_[g]);
+  cudaFree(local_base_);
+  cudaFree(ctr_);
+}
+
+int Exec::slot_dtype(int slot) const {
+  switch (slot) {
+    case index::kDstGrad: return cfg_.grad_in_dtype;
+    case index::kSrcGrad: return cfg_.grad_out_dtype;
+    default: return cfg_.act_dtype;
+  }
+}
+
+uint64_t Exec::offset_of(int gpu, int rank, int slot, int mb_slot) const {
+  return kPadBytes + mb_stride_[gpu] * mb_slot + offsets_[gpu][rank * index::kNumSlots + slot];
+}
+
+size_t Exec::buffer_bytes(int rank, int slot) const {
+  if (rank < 0 || rank >= map_.world || slot < 0 || slot >= index::kNumSlots)
+    raise(ErrorCode::InvalidArgument, "buffer index out of range");
+  return static_cast<size_t>(map_.elems[rank][slot]) * dev::dtype_size(slot_dtype(slot));
+}
+
+void Exec::ipc_handle(void* out64) const {
+  if (!local_base_) raise(ErrorCode::InvalidArgument, "no device region to export");
+  cudaIpcMemHandle_t h;
+  ck(cudaIpcGetMemHandle(&h, local_base_), "cudaIpcGetMemHandle");
+  static_assert(sizeof(h) == 64, "IPC handle size");
+  std::memcpy(out64, &h, 64);
+}
+
+void Exec::open_peers(const void* handles) {
+  for (int g = 0; g < n_gpus_; ++g) {
+    if (g == my_gpu_ || !((group_mask_ >> g) & 1u) || peer_base_[g]) continue;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, static_cast<const unsigned char*>(handles) + 64 * g, 64);
+    void* p = nullptr;
+    ck(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    peer_base_[g] = static_cast<unsigned char*>(p);
+  }
+  dirty_ = true;
+}
+
+void* Exec::buffer(int rank, int slot, int mb_slot, size_t* bytes) const {
+  const size_t n = buffer_bytes(rank, slot);
+  if (bytes) *bytes = n;
+  if (mb_slot < 0 || mb_slot >= cfg_.mb_slots) raise(ErrorCode::InvalidArgument, "mb slot out of range");
+  if (void* b = bound_[rank * index::kNumSlots + slot][mb_slot]) return b;
+  if (gpu_of(rank) != my_gpu_) raise(ErrorCode::InvalidArgument, "rank is not resident on this GPU");
+  if (!local_base_ || n == 0) return nullptr;
+  return local_base_ + offset_of(my_gpu_, rank, slot, mb_slot);
+}
+
+void Exec::bind(int rank, int slot, int mb_slot, void* ptr, size_t bytes) {
+  const size_t n = buffer_bytes(rank, slot);
+  if (mb_slot < 0 || mb_slot >= cfg_.mb_slots) raise(ErrorCode::InvalidArgument, "mb slot out of range");
+  if (bytes < n) raise(ErrorCode::ShapeMismatch, "bound buffer smaller than the planned shard");
+  if (gpu_of(rank) != my_gpu_) raise(ErrorCode::InvalidArgument, "can only bind resident ranks");
+  if (n_gpus_ > 1)
+    raise(ErrorCode::InvalidArgument, "external buffers are single-GPU only; use buffer() on multi-GPU");
+  bound_[rank * index::kNumSlots + slot][mb_slot] = ptr;
+  dirty_ = true;
+}
+
+const void* Exec::resolve(int rank, int slot, int mb_slot) const {
+  if (void* b = bound_[rank * index::kNumSlots + slot][mb_slot]) return b;
+  const int g = gpu_of(rank);
+  if (!peer_base_[g])
+    raise(ErrorCode::InvalidArgument, "buffer of rank " + std::to_string(rank) +
+                                          " unavailable (peer not opened or not bound)");
+  return peer_base_[g] + offset_of(g, rank, slot, mb_slot);
+}
+
+void Exec::prepare() {
+  if (!dirty_) return;
+  for (int mb = 0; mb < cfg_.mb_slots; ++mb) {
+    DevTables& T = tables_[mb];
+    std::vector<dev::CopySeg> cs;
+    uint64_t chunk = 0;
+    for (const auto& s : fwd_local_) {
+      const int es_src = dev::dtype_size(slot_dtype(s.src.slot));
+      const uint64_t nbytes = static_cast<uint64_t>(s.n) * es_src;
+      cs.push_back({static_cast<const unsigned char*>(resolve(s.src.rank, s.src.slot, mb)) + s.src.off * es_src,
+                    static_cast<unsigned char*>(const_cast<void*>(resolve(s.dst.rank, s.dst.slot, mb))) +
+                        s.dst.off * es_src,
+                    nbytes, chunk});
+      chunk += (nbytes + dev::kCopyChunk - 1) / dev::kCopyChunk;
+    }
+    T.copy_chunks = chunk;
+    std::vector<dev::ReduceSeg> rs;
+    std::vector<const void*> terms;
+    chunk = 0;
+    const int es_in = dev::dtype_size(cfg_.grad_in_dtype), es_out = dev::dtype_size(cfg_.grad_out_dtype);
+    for (const auto& s : bwd_local_) {
+      dev::ReduceSeg d{};
+      d.dst = static_cast<unsigned char*>(const_cast<void*>(resolve(s.dst.rank, s.dst.slot, mb))) +
+              s.dst.off * es_out;
+      d.nelem = s.n;
+      d.chunk0 = chunk;
+      d.nterms = static_cast<int32_t>(s.terms.size());
+      d.term0 = static_cast<int32_t>(terms.size());
+      for (const auto& t : s.terms)
+        terms.push_back(static_cast<const unsigned char*>(resolve(t.rank, t.slot, mb)) + t.off * es_in);
+      rs.push_back(d);
+      chunk += (s.n + dev::kReduceChunk - 1) / dev::kReduceChunk;
+    }
+    T.reduce_chunks = chunk;
+    cudaFree(T.copy);
+    cudaFree(T.reduce);
+    cudaFree(T.terms);
+    T.copy = nullptr;
+    T.reduce = nullptr;
+    T.terms = nullptr;
+    if (!cs.empty()) {
+      ck(cudaMalloc(&T.copy, cs.size() * sizeof(dev::CopySeg)), "cudaMalloc(copy table)");
+      ck(cudaMemcpy(T.copy, cs.data(), cs.size() * sizeof(dev::CopySeg), cudaMemcpyHostToDevice), "upload");
+    }
+    if (!rs.empty()) {
+      ck(cudaMalloc(&T.reduce, rs.size() * sizeof(dev::ReduceSeg)), "cudaMalloc(reduce table)");
+      ck(cudaMemcpy(T.reduce, rs.data(), rs.size() * sizeof(dev::ReduceSeg), cudaMemcpyHostToDevice), "upload");
+    }
+    if (!terms.empty()) {
+      ck(cudaMalloc(&T.terms, terms.size() * sizeof(void*)), "cudaMalloc(terms)");
+      ck(cudaMemcpy(T.terms, terms.data(), terms.size() * sizeof(void*), cudaMemcpyHostToDevice), "upload");
+    }
+  }
+  dirty_ = false;
+}
+
+dev::SyncArgs Exec::sync_args() const {
+  dev::SyncArgs s{};
+  s.pad = reinterpret_cast<uint32_t*>(local_base_);
+  s.ctr = ctr_;
+  s.my_gpu = my_gpu_;
+  if (n_gpus_ > 1 && ((group_mask_ >> my_gpu_) & 1u)) {
+    const uint32_t peers = group_mask_ & ~(1u << my_gpu_);
+    s.wait_mask = peers;
+    s.post_mask = peers;
+    for (int g = 0; g < n_gpus_; ++g)
+      if ((peers >> g) & 1u) s.peer_pad[g] = reinterpret_cast<uint32_t*>(peer_base_[g]);
+  }
+  int khz = 0;
+  cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, device_);
+  s.timeout_cycles = static_cast<uint64_t>(cfg_.timeout_s * (khz > 0 ? khz : 2000000) * 1e3);
+  return s;
+}
+
+void Exec::forward(int mb, void* stream) {
+  if (fwd_done_.count(mb))
+    raise(ErrorCode::InvalidArgument, "microbatch " + std::to_string(mb) + " forwarded twice without backward");
+  prepare();
+  const DevTables& T = tables_[mb % cfg_.mb_slots];
+  dev::launch_copy(T.copy, static_cast<int>(fwd_local_.size()), T.copy_chunks, sync_args(),
+                   {sm_count_ * cfg_.blocks_per_sm, cfg_.threads}, stream);
+  ck(cudaGetLastError(), "copy_segments launch");
+  ++launches_;
+  fwd_done_.insert(mb);
+}
+
+void Exec::backward(int mb, float beta, void* stream) {
+  if (!fwd_done_.count(mb))
+    raise(ErrorCode::UnknownMicrobatch, "no forward record for microbatch " + std::to_string(mb));
+  prepare();
+  const DevTables& T = tables_[mb % cfg_.mb_slots];
+  dev::launch_reduce(T.reduce, static_cast<int>(bwd_local_.size()), T.terms, T.reduce_chunks,
+                     cfg_.grad_in_dtype, cfg_.grad_out_dtype, beta, sync_args(),
+                     {sm_count_ * cfg_.blocks_per_sm, cfg_.threads}, stream);
+  ck(cudaGetLastError(), "reduce_segments launch");
+  ++launches_;
+  fwd_done_.erase(mb);
+}
+
+void Exec::seed_forward_record(int mb) { fwd_done_.insert(mb); }
+
+uint32_t Exec::device_error() const {
+  uint32_t v[3] = {0, 0, 0};
+  ck(cudaMemcpy(v, ctr_, sizeof(v), cudaMemcpyDeviceToHost), "read status");
+  return v[2];
+}
+
+uint64_t Exec::local_fwd_bytes() const {
+  uint64_t b = 0;
+  for (const auto& s : fwd_local_) b += static_cast<uint64_t>(s.n) * dev::dtype_size(slot_dtype(s.src.slot));
+  return b;
+}
+
+uint64_t Exec::local_bwd_elems() const {
+  uint64_t b = 0;
+  for (const auto& s : bwd_local_) b += s.n;
+  return b;
+}
+
+}  // namespace hb::rt

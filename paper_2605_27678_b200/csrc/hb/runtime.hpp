@@ -1,0 +1,110 @@
+// hetbridge — per-edge device runtime (the B200 replacement for
+// hetsim::bridge::BridgeRuntime, bridge.hpp:146-173, and for simnet as the
+// transport, simnet.hpp:86-148).
+//
+// One Exec per (edge, process). A process drives one GPU and executes, in one
+// kernel launch per boundary op, the work of every logical rank that the
+// rank->GPU map places on it: with 1 GPU all logical ranks are resident (HBM
+// only); with N GPUs each process pulls the rows its ranks need straight from
+// the owners' HBM over NVSwitch through CUDA-IPC-mapped peer buffers.
+//
+// Buffer layout: each GPU owns one device region (cudaMalloc, IPC-exported)
+// holding a 4 KiB signal pad followed by the buffers of its resident ranks in
+// a layout every process can compute from the plan alone, so a peer buffer's
+// address is peer_base + offset with no table exchange (a symmetric-heap
+// discipline, as NVSHMEM uses, without the library).
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <set>
+#include <vector>
+
+#include "hb/bridge.hpp"
+#include "hb/index_map.hpp"
+#include "kernels/boundary_kernels.cuh"
+
+namespace hb::rt {
+
+struct ExecConfig {
+  int act_dtype = dev::kBF16;       // source / destination activations (copy width)
+  int grad_in_dtype = dev::kBF16;   // destination gradients
+  int grad_out_dtype = dev::kFP32;  // source gradients (accumulator)
+  int mb_slots = 1;                 // buffer sets for microbatches in flight
+  int internal_alloc = 1;           // allocate the device region (else bind() every buffer)
+  int blocks_per_sm = 4;
+  int threads = 512;
+  double timeout_s = 20.0;          // flag-wait timeout
+};
+
+class Exec {
+ public:
+  Exec(const bridge::BridgePlan& plan, const index::SpliceSpec* splice, int n_gpus, int my_gpu,
+       std::vector<int> rank_to_gpu, const ExecConfig& cfg);
+  ~Exec();
+  Exec(const Exec&) = delete;
+  Exec& operator=(const Exec&) = delete;
+
+  // Multi-GPU setup (collective across the exec group's processes).
+  void ipc_handle(void* out64) const;
+  void open_peers(const void* handles);  // n_gpus * 64 bytes, ordered by GPU index
+
+  // Buffers of logical rank `rank` (must be resident here unless peer-mapped read-only use).
+  void* buffer(int rank, int slot, int mb_slot, size_t* bytes) const;
+  void bind(int rank, int slot, int mb_slot, void* ptr, size_t bytes);
+  size_t buffer_bytes(int rank, int slot) const;
+
+  void forward(int mb, void* stream);
+  void backward(int mb, float beta, void* stream);
+  void seed_forward_record(int mb);
+  uint32_t device_error() const;  // synchronises
+
+  const index::IndexMap& map() const { return map_; }
+  int local_fwd_segments() const { return static_cast<int>(fwd_local_.size()); }
+  int local_bwd_segments() const { return static_cast<int>(bwd_local_.size()); }
+  uint64_t local_fwd_bytes() const;
+  uint64_t local_bwd_elems() const;
+  int launches() const { return launches_; }
+  const bridge::BridgePlan& plan() const { return plan_; }
+
+ private:
+  int gpu_of(int rank) const { return rank_to_gpu_.at(rank); }
+  int slot_dtype(int slot) const;
+  uint64_t offset_of(int gpu, int rank, int slot, int mb_slot) const;
+  const void* resolve(int rank, int slot, int mb_slot) const;
+  void prepare();  // resolve pointers, upload descriptors (after bind/open)
+  dev::SyncArgs sync_args() const;
+
+  bridge::BridgePlan plan_;
+  index::IndexMap map_;
+  int n_gpus_, my_gpu_, device_;
+  std::vector<int> rank_to_gpu_;
+  ExecConfig cfg_;
+  uint32_t group_mask_ = 0;
+
+  // layout: offsets_[gpu][rank*kNumSlots+slot] (for mb slot 0), stride per mb slot
+  std::vector<std::vector<uint64_t>> offsets_;
+  std::vector<uint64_t> mb_stride_;  // per gpu
+  uint64_t region_bytes_ = 0;
+  unsigned char* local_base_ = nullptr;
+  std::vector<unsigned char*> peer_base_;
+  std::vector<std::vector<void*>> bound_;  // [rank*kNumSlots+slot][mb] external binding
+
+  std::vector<index::CopySeg> fwd_local_;
+  std::vector<index::ReduceSeg> bwd_local_;
+
+  struct DevTables {
+    dev::CopySeg* copy = nullptr;
+    dev::ReduceSeg* reduce = nullptr;
+    const void** terms = nullptr;
+    uint64_t copy_chunks = 0, reduce_chunks = 0;
+  };
+  std::vector<DevTables> tables_;  // per mb slot
+  bool dirty_ = true;
+  uint32_t* ctr_ = nullptr;  // device counters
+  int sm_count_ = 0;
+  int launches_ = 0;
+  std::set<int> fwd_done_;
+};
+
+}  // namespace hb::rt

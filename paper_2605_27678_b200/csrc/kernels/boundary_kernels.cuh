@@ -1,0 +1,62 @@
+// hetbridge — device-side descriptors shared by the runtime and the kernels.
+#pragma once
+
+#include <cstdint>
+
+namespace hb::dev {
+
+enum Dtype : int { kBF16 = 0, kFP16 = 1, kFP32 = 2, kFP64 = 3 };
+
+inline int dtype_size(int dt) { return dt == kFP32 ? 4 : dt == kFP64 ? 8 : 2; }
+
+// One contiguous byte run: destination bytes [dst, dst+nbytes) come from
+// [src, src+nbytes). `chunk0` is the first global work-chunk index.
+struct CopySeg {
+  const unsigned char* src;
+  unsigned char* dst;
+  uint64_t nbytes;
+  uint64_t chunk0;
+};
+
+// dst[i] = beta*dst[i] + sum_t term_t[i], i in [0, nelem), fp32 accumulation,
+// terms summed in order starting from +0.0f. term pointers live in a side array.
+struct ReduceSeg {
+  void* dst;
+  uint64_t nelem;
+  uint64_t chunk0;
+  int32_t nterms;
+  int32_t term0;
+};
+
+// Cross-GPU epoch barrier over peer-mapped flag words. Every GPU of an exec
+// group launches exactly one kernel per boundary op, so the per-exec op
+// counters stay in lockstep: at op e each GPU posts e to every peer's pad and
+// waits until every peer posted e to its own pad.
+constexpr int kMaxGpus = 32;
+struct SyncArgs {
+  uint32_t* pad;                  // local pad: pad[g] = last epoch posted by GPU g
+  uint32_t* peer_pad[kMaxGpus];   // peers' pads (nullptr for self / non-members)
+  uint32_t* ctr;                  // local: [0] epoch, [1] finished-CTA count, [2] error flag
+  uint32_t wait_mask;             // GPUs to wait for
+  uint32_t post_mask;             // GPUs to post to
+  int my_gpu;
+  uint64_t timeout_cycles;
+};
+
+constexpr uint64_t kCopyChunk = 64 * 1024;    // bytes per work chunk
+constexpr uint64_t kReduceChunk = 16 * 1024;  // elements per work chunk
+
+struct LaunchCfg {
+  int grid;
+  int block;
+};
+
+// Host-side launchers (defined in boundary_kernels.cu).
+void launch_copy(const CopySeg* segs, int nseg, uint64_t total_chunks, const SyncArgs& sync,
+                 LaunchCfg cfg, void* stream);
+void launch_reduce(const ReduceSeg* segs, int nseg, const void* const* terms,
+                   uint64_t total_chunks, int in_dtype, int out_dtype, float beta,
+                   const SyncArgs& sync, LaunchCfg cfg, void* stream);
+int device_sm_count();
+
+}  // namespace hb::dev
