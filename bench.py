@@ -1,0 +1,508 @@
+#!/usr/bin/env python
+"""Boundary communicator benchmark (BASELINE.json metric).
+
+metric : boundary reshard GB/s (fwd+bwd), whole job; per-GPU and tokens/s ride along.
+step   : one forward reshard (+ CP splice for C4) and one backward gradient return
+         with fp32 sum-accumulate (beta=1), over one microbatch of synthetic
+         activations of the config's shape, inputs resident in HBM.
+N=1    : every logical rank of the 8-rank layout is resident on GPU 0 (HBM only).
+N>1    : one process per GPU (torchrun), logical rank r on GPU floor(r*N/8);
+         peers' rows are pulled over NVSwitch by the same kernels.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c3|c4|c5|c1]
+  python bench.py --impl reference ...   # the reference CPU path (oracle over the
+                                          # reference simnet/grid), host cores only
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+L2_BYTES = 126 * 1024 * 1024
+DT_SIZE = {"bf16": 2, "fp16": 2, "fp32": 4, "fp64": 8}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--blocks-per-sm", type=int, default=0)
+    ap.add_argument("--threads", type=int, default=0)
+    ap.add_argument("--slots", type=int, default=0, help="buffer sets rotated across steps (0=auto)")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- accounting
+
+
+def payload_bytes(cfg):
+    """Algorithmic boundary payload per step: destination shards materialised
+    (fwd, act dtype) + gradients returned to source owners (bwd, grad_in dtype),
+    summed over all logical ranks. Identical for every implementation."""
+    from paper_2605_27678_b200 import bridge as hbb
+
+    plan = hbb.plan_bridge(cfg.edge())
+    sp = make_splice(cfg)
+    fwd = bwd = 0
+    for r in range(plan.world):
+        fwd += hbb.buffer_elems(plan, r, hbb.SLOT_DST_ACT, sp) * DT_SIZE[cfg.act]
+        bwd += hbb.buffer_elems(plan, r, hbb.SLOT_SRC_GRAD, sp) * DT_SIZE[cfg.grad_in]
+    return fwd, bwd
+
+
+def make_splice(cfg):
+    from paper_2605_27678_b200 import bridge as hbb
+
+    if not cfg.splice:
+        return None
+    s = cfg.splice
+    return hbb.SpliceSpec(s["Q"], s["S"], cfg.hidden, cfg.tokens, s["codes"], s["text_mode"])
+
+
+def traffic_model(cfg, n_gpus):
+    """Per-GPU algorithmic bytes from the index map: HBM reads+writes (incl. bytes
+    served to peers and the fp32 accumulator read-modify-write) and NVLink ingress."""
+    from paper_2605_27678_b200 import bridge as hbb
+    from paper_2605_27678_b200 import configs
+
+    plan = hbb.plan_bridge(cfg.edge())
+    sp = make_splice(cfg)
+    r2g = configs.rank_to_gpu(plan.world, n_gpus)
+    a, gi, go = DT_SIZE[cfg.act], DT_SIZE[cfg.grad_in], DT_SIZE[cfg.grad_out]
+    z = lambda: [0] * n_gpus  # noqa: E731
+    f_hbm, f_nvl, b_hbm, b_nvl = z(), z(), z(), z()
+    for (sr, ss, so, dr, ds, do, n) in hbb.index_forward(plan, sp):
+        g_src, g_dst = r2g[sr], r2g[dr]
+        f_hbm[g_dst] += n * a            # write
+        f_hbm[g_src] += n * a            # read at the owner (local or served to a peer)
+        if g_src != g_dst:
+            f_nvl[g_dst] += n * a
+    for (dr, ds, do, n, terms) in hbb.index_backward(plan, sp):
+        g_dst = r2g[dr]
+        b_hbm[g_dst] += n * go * (2 if cfg.beta else 1)
+        for (tr, ts, to) in terms:
+            b_hbm[r2g[tr]] += n * gi
+            if r2g[tr] != g_dst:
+                b_nvl[g_dst] += n * gi
+    return {"fwd_hbm": f_hbm, "fwd_nvl": f_nvl, "bwd_hbm": b_hbm, "bwd_nvl": b_nvl}
+
+
+def peaks():
+    p = {"hbm_gbs": 6539.2, "src": "fallback (B200_PROFILING.md)"}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        p = {"hbm_gbs": float(m["hbm_gbs"]), "src": "measured (MEASURED_PEAKS.json)"}
+    except Exception:
+        pass
+    p["nvl_gbs"] = 770.0  # measured peer copy per direction (B200_PROFILING.md); 900 nominal
+    return p
+
+
+# ----------------------------------------------------------------------------- clocks
+
+
+class ClockSampler:
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.path = None
+        self.t_on = self.t_off = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        q = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", "20",
+                 "-i", str(self.dev)], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def mark(self, on: bool):
+        if on:
+            self.t_on = time.time()
+        else:
+            self.t_off = time.time()
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.05)
+        self.proc.terminate()
+        self.proc.wait()
+        rows = []
+        with open(self.path) as f:
+            for line in f:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    ts = time.mktime(time.strptime(parts[0].split(".")[0], "%Y/%m/%d %H:%M:%S"))
+                    rows.append((ts, float(parts[1]), float(parts[2]), parts[4:9]))
+                except Exception:
+                    continue
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        lo, hi = (self.t_on or 0) - 1, (self.t_off or 1e18) + 1
+        inwin = [r for r in rows if lo <= r[0] <= hi] or rows
+        names = ["active", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in inwin:
+            for nm, v in zip(names[1:], r[3][1:]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(r[1] for r in inwin), "sm_max_mhz": max(r[2] for r in inwin),
+                "reasons": sorted(reasons), "samples": len(inwin)}
+
+
+# ----------------------------------------------------------------------------- CPU leg
+
+
+def cpu_reference_run(cfg, sample_batch: int, repeats: int = 1):
+    """Time the oracle (restated bridge over the reference's own simnet+grid,
+    compiled from /root/reference sources into oracle/_ref) on a bounded
+    sample: the config's layouts with `sample_batch` samples of full width.
+    Returns (payload GB/s, seconds per fwd+bwd, description)."""
+    import numpy as np
+
+    from oracle import oracle as O
+
+    src = O.Layout(cfg.src.name, cfg.src.tp, cfg.src.cp, cfg.src.pp, cfg.src.dp, cfg.src.rank_offset)
+    dst = O.Layout(cfg.dst.name, cfg.dst.tp, cfg.dst.cp, cfg.dst.pp, cfg.dst.dp, cfg.dst.rank_offset)
+    B, W = sample_batch, cfg.width
+    rng = np.random.default_rng(7)
+    SI = O.intervals(B, src.dp)
+    DI = O.intervals(B, dst.dp)
+    shards = {r: rng.standard_normal((SI[src.coord(r)[3]][1], W)) for r in src.stage_ranks(src.pp - 1)}
+    grads = {r: rng.standard_normal((DI[dst.coord(r)[3]][1], W)) for r in dst.stage_ranks(0)}
+    best = math.inf
+    for _ in range(repeats):
+        _, _, tf = O.bridge_forward(src, dst, B, W, shards)
+        _, _, tb = O.bridge_backward(src, dst, B, W, grads)
+        best = min(best, tf + tb)
+    fwd_b = sum(DI[dst.coord(r)[3]][1] * W * DT_SIZE[cfg.act] for r in dst.stage_ranks(0))
+    bwd_b = sum(SI[src.coord(r)[3]][1] * W * DT_SIZE[cfg.grad_in] for r in src.stage_ranks(src.pp - 1))
+    desc = (f"{cfg.name} layouts with B={B} samples x {cfg.tokens}x{cfg.hidden} (full width), "
+            f"oracle bridge_forward+bridge_backward over reference simnet (doubles), best of {repeats}")
+    return (fwd_b + bwd_b) / best / 1e9, best, desc
+
+
+def cpu_sample_batch(cfg):
+    # smallest batch the layouts admit (divisible by both dp): bounded CPU work
+    return max(cfg.src.dp, cfg.dst.dp)
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_2605_27678_b200 import configs
+
+    cfg = configs.get(args.config)
+    B = cpu_sample_batch(cfg)
+    times = []
+    desc = ""
+    for _ in range(args.warmup if args.warmup < 2 else 1):
+        cpu_reference_run(cfg, B)
+    for _ in range(max(1, min(args.steps, 3))):
+        gbs, sec, desc = cpu_reference_run(cfg, B)
+        times.append(sec)
+    sec = min(times)
+    fwd_b, bwd_b = 0, 0
+    from oracle import oracle as O
+    SI = O.intervals(B, cfg.src.dp)
+    DI = O.intervals(B, cfg.dst.dp)
+    fwd_b = len(O.Layout("d", cfg.dst.tp, cfg.dst.cp, 1, cfg.dst.dp).stage_ranks(0)) * DI[0][1] * cfg.width * DT_SIZE[cfg.act]
+    bwd_b = len(O.Layout("s", cfg.src.tp, cfg.src.cp, 1, cfg.src.dp).stage_ranks(0)) * SI[0][1] * cfg.width * DT_SIZE[cfg.grad_in]
+    value = (fwd_b + bwd_b) / sec / 1e9
+    tokens = B * cfg.tokens / sec
+    line = {
+        "impl": "reference", "metric": "boundary reshard GB/s per GPU (fwd+bwd) vs NVLink/HBM roofline at 1/2/4/8 GPUs",
+        "value": round(value, 4), "unit": "GB/s", "n_gpus": args.gpus, "steps": len(times),
+        "warmup": args.warmup, "ms_per_step": round(sec * 1e3, 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg.description, "sample_batch": B, "width": cfg.width},
+        "tokens_per_s": round(tokens, 1),
+        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": 1, "kind": "port",
+                         "sample": desc},
+        "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "reference bridge body is a stub (bridge.cpp); oracle restatement runs over the "
+                "reference's own simnet/grid compiled from /root/reference sources; simnet admits one "
+                "runnable rank at a time, so 1 effective core",
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU leg
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_27678_b200 import bridge as hbb
+    from paper_2605_27678_b200 import configs
+
+    world_size = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world_size > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    N = world_size
+    cfg = configs.get(args.config)
+    plan = hbb.plan_bridge(cfg.edge())
+    sp = make_splice(cfg)
+    r2g = configs.rank_to_gpu(plan.world, N)
+    local = [r for r in range(plan.world) if r2g[r] == rank]
+    tdt = {"bf16": torch.bfloat16, "fp16": torch.float16, "fp32": torch.float32}
+
+    tm = traffic_model(cfg, N)
+    per_gpu_step = tm["fwd_hbm"][rank] + tm["bwd_hbm"][rank]
+    slots = args.slots or max(1, min(8, math.ceil(3 * L2_BYTES / max(per_gpu_step, 1))))
+
+    rt = hbb.BridgeRuntime(plan, sp, n_gpus=N, my_gpu=rank, rank_to_gpu=r2g, act_dtype=tdt[cfg.act],
+                           grad_in_dtype=tdt[cfg.grad_in], grad_out_dtype=tdt[cfg.grad_out],
+                           mb_slots=slots, blocks_per_sm=args.blocks_per_sm, threads=args.threads)
+    if N > 1:
+        rt.exchange_handles()
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
+    for s in range(slots):
+        for r in local:
+            for slot in (hbb.SLOT_SRC_ACT, hbb.SLOT_DST_GRAD, hbb.SLOT_TEXT, hbb.SLOT_SRC_GRAD):
+                b = rt.buffer(r, slot, s)
+                if b is None:
+                    continue
+                if slot == hbb.SLOT_SRC_GRAD:
+                    b.zero_()
+                else:
+                    b.copy_(torch.randn(b.numel(), generator=gen, device=dev, dtype=torch.float32).to(b.dtype))
+    torch.cuda.synchronize()
+    stream = torch.cuda.Stream(priority=-1)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if N > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    mb = 0
+    for _ in range(max(args.warmup, 3)):
+        rt.forward(mb, stream)
+        rt.backward(mb, cfg.beta, stream)
+        mb += 1
+    barrier()
+    if rt.status():
+        raise RuntimeError("device flag wait timed out during warm-up")
+
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    time.sleep(0.1)
+    K = args.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    launches0 = rt.stats()["launches"]
+    barrier()
+    sampler.mark(True)
+    for i in range(K):
+        e0, e1, e2 = ev[i]
+        e0.record(stream)
+        rt.forward(mb, stream)
+        e1.record(stream)
+        rt.backward(mb, cfg.beta, stream)
+        e2.record(stream)
+        mb += 1
+    stream.synchronize()
+    sampler.mark(False)
+    barrier()
+    launches = rt.stats()["launches"] - launches0
+    total_ms = ev[0][0].elapsed_time(ev[-1][2])
+    fwd_ms = sum(e[0].elapsed_time(e[1]) for e in ev) / K
+    bwd_ms = sum(e[1].elapsed_time(e[2]) for e in ev) / K
+    t = torch.tensor([total_ms, fwd_ms, bwd_ms], dtype=torch.float64, device=dev)
+    if N > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms, fwd_ms, bwd_ms = t.tolist()
+    ms_step = total_ms / K
+    clocks = sampler.stop()
+    if rt.status():
+        raise RuntimeError("device flag wait timed out")
+
+    fwd_b, bwd_b = payload_bytes(cfg)
+    value = (fwd_b + bwd_b) / (ms_step * 1e-3) / 1e9
+    tokens_s = cfg.batch * cfg.tokens / (ms_step * 1e-3)
+
+    # roofline of the dominant kernel on this GPU (bytes from the index map)
+    pk = peaks()
+    def bound(hbm, nvl, ms):
+        t_hbm = hbm / (pk["hbm_gbs"] * 1e9)
+        t_nvl = nvl / (pk["nvl_gbs"] * 1e9)
+        if t_nvl > t_hbm:
+            return "nvlink", nvl / (ms * 1e-3) / 1e9, pk["nvl_gbs"], max(t_hbm, t_nvl)
+        return "hbm", hbm / (ms * 1e-3) / 1e9, pk["hbm_gbs"], max(t_hbm, t_nvl)
+    fb = bound(tm["fwd_hbm"][rank], tm["fwd_nvl"][rank], fwd_ms)
+    bb = bound(tm["bwd_hbm"][rank], tm["bwd_nvl"][rank], bwd_ms)
+    dom_is_fwd = fwd_ms >= bwd_ms
+    kind, achieved, peak, tstar = fb if dom_is_fwd else bb
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", f"traffic_{cfg.name}_n{N}.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as f:
+                traffic = json.load(f).get("fwd" if dom_is_fwd else "bwd")
+        except Exception:
+            traffic = None
+    roofline = {
+        "bound": "hbm" if kind == "hbm" else "nvlink", "kernel": "copy_segments_kernel" if dom_is_fwd else "reduce_segments_kernel",
+        "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
+        "traffic": traffic, "peak_source": pk["src"] if kind == "hbm" else "measured peer copy 770 GB/s (B200_PROFILING.md)",
+        "per_kernel": {
+            "fwd": {"ms": round(fwd_ms, 4), "bound": fb[0], "achieved_gbs": round(fb[1], 1),
+                    "frac": round(fb[1] / fb[2], 4), "hbm_bytes": tm["fwd_hbm"][rank], "nvl_in_bytes": tm["fwd_nvl"][rank]},
+            "bwd": {"ms": round(bwd_ms, 4), "bound": bb[0], "achieved_gbs": round(bb[1], 1),
+                    "frac": round(bb[1] / bb[2], 4), "hbm_bytes": tm["bwd_hbm"][rank], "nvl_in_bytes": tm["bwd_nvl"][rank]},
+        },
+        "step_tstar_ms_measured_peaks": round((fb[3] + bb[3]) * 1e3, 4),
+        "step_frac_of_tstar": round((fb[3] + bb[3]) * 1e3 / ms_step, 4),
+    }
+    # nominal (900 GB/s NVLink, 8 TB/s HBM) T* of BASELINE.md, max over GPUs
+    def tstar_nominal(h, n):
+        return max(max(hh / 8e12, nn / 9e11) for hh, nn in zip(h, n))
+    roofline["step_tstar_ms_nominal"] = round((tstar_nominal(tm["fwd_hbm"], tm["fwd_nvl"]) +
+                                               tstar_nominal(tm["bwd_hbm"], tm["bwd_nvl"])) * 1e3, 4)
+
+    # ---- end to end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, cfg, rt, local, stream, N, dev, barrier, fwd_b + bwd_b, slots)
+
+    cpu = None
+    if rank == 0 and N == 1 and not args.no_cpu:
+        try:
+            B = cpu_sample_batch(cfg)
+            gbs, sec, desc = cpu_reference_run(cfg, B)
+            cpu = {"value": round(gbs, 4), "unit": "GB/s", "cores": 1, "kind": "port", "sample": desc,
+                   "cpu": _cpu_model(), "nproc": os.cpu_count()}
+        except Exception as exc:  # the oracle is a reported baseline, never the product
+            cpu = {"value": None, "unit": "GB/s", "cores": 1, "kind": "port", "sample": f"unavailable: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": "boundary reshard GB/s per GPU (fwd+bwd) vs NVLink/HBM roofline at 1/2/4/8 GPUs",
+            "value": round(value, 2), "unit": "GB/s", "n_gpus": N, "steps": K, "warmup": args.warmup,
+            "ms_per_step": round(ms_step, 5), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": cfg.act, "data": "synthetic",
+            "config": {"workload": cfg.description, "name": cfg.name, "global_batch": cfg.batch,
+                       "tokens_per_sample": cfg.tokens, "hidden": cfg.hidden,
+                       "logical_ranks": plan.world, "rank_to_gpu": r2g,
+                       "grad_in": cfg.grad_in, "grad_out": cfg.grad_out, "beta": cfg.beta,
+                       "l2": f"inputs rotate over {slots} buffer set(s); per-GPU bytes per step "
+                             f"{per_gpu_step / 1e6:.1f} MB x {slots} sets > 126 MB L2"},
+            "per_gpu_gbs": round(value / N, 2), "tokens_per_s": round(tokens_s, 1),
+            "payload_bytes_per_step": {"fwd": fwd_b, "bwd": bwd_b},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    rt.close()
+    if N > 1:
+        dist.destroy_process_group()
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def run_e2e(args, cfg, rt, local, stream, N, dev, barrier, payload, slots):
+    """Same metric through the public API with pinned HOST buffers: every step
+    copies its inputs host->device (source shards, destination gradients, text),
+    runs forward+backward, and reads the outputs back (destination shards and
+    source gradients), all inside the timed region."""
+    import torch
+
+    from paper_2605_27678_b200 import bridge as hbb
+
+    ins, outs = [], []
+    for r in local:
+        for slot in (hbb.SLOT_SRC_ACT, hbb.SLOT_TEXT, hbb.SLOT_DST_GRAD):
+            b = rt.buffer(r, slot, 0)
+            if b is not None:
+                ins.append((slot, b, torch.empty(b.shape, dtype=b.dtype, pin_memory=True).copy_(b.cpu())))
+        for slot in (hbb.SLOT_DST_ACT, hbb.SLOT_SRC_GRAD):
+            b = rt.buffer(r, slot, 0)
+            if b is not None:
+                outs.append((b, torch.empty(b.shape, dtype=b.dtype, pin_memory=True)))
+    h2d = sum(h.numel() * h.element_size() for _, _, h in ins)
+    d2h = sum(h.numel() * h.element_size() for _, h in outs)
+    K = max(1, args.e2e_steps)
+    mb = 10_000_000
+    slot_mb = lambda m: m - (m % slots)  # noqa: E731  (always buffer set 0)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for i in range(K):
+            m = slot_mb(mb + i * slots)
+            for slot, b, h in ins:
+                if slot != hbb.SLOT_DST_GRAD:
+                    b.copy_(h, non_blocking=True)
+            rt.forward(m, stream)
+            for slot, b, h in ins:
+                if slot == hbb.SLOT_DST_GRAD:
+                    b.copy_(h, non_blocking=True)
+            rt.backward(m, cfg.beta, stream)
+            for b, h in outs:
+                h.copy_(b, non_blocking=True)
+        e1.record(stream)
+    stream.synchronize()
+    ms = e0.elapsed_time(e1) / K
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if N > 1:
+        import torch.distributed as dist
+
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = t.item()
+    barrier()
+    return {"value": round(payload / (ms * 1e-3) / 1e9, 3), "unit": "GB/s", "ms_per_step": round(ms, 3),
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": K,
+            "path": "BridgeRuntime.forward/backward (C-ABI hb_exec_*) with pinned host buffers"}
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,93 @@
+"""Named boundary configurations of BASELINE.json / SURVEY.md §8 (C1-C5).
+
+Each config is an edge (source + destination layouts, batch, width), the
+dtypes the boundary carries, and for C4 the placeholder table of the fused
+CP-sharded sequence. ``scale`` shrinks the per-sample width for parity tests
+while keeping the layouts, which is what the index maps depend on.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .grid import BoundaryEdge, ModuleLayout
+
+
+@dataclass
+class BoundaryConfig:
+    name: str
+    description: str
+    src: ModuleLayout
+    dst: ModuleLayout
+    batch: int
+    tokens: int          # vision tokens per sample (S_v)
+    hidden: int          # d_h
+    act: str = "bf16"
+    grad_in: str = "bf16"
+    grad_out: str = "fp32"
+    beta: float = 1.0    # backward accumulates into the source-gradient buffer
+    splice: dict | None = None  # {"Q", "S", "codes", "text_mode"}
+    logical_world: int = 8
+    extra: dict = field(default_factory=dict)
+
+    @property
+    def width(self) -> int:
+        return self.tokens * self.hidden
+
+    def edge(self) -> BoundaryEdge:
+        return BoundaryEdge(self.src, self.dst, self.batch, self.width)
+
+
+def cp_splice_codes(n_images: int, tokens: int, seq_len: int, stride: int, lead: int, seed: int):
+    """C4 placeholder table: slot j starts at j*stride+lead and holds image perm[j]."""
+    perm = np.random.default_rng(seed).permutation(n_images)
+    codes = np.full(seq_len, 0, dtype=np.int64)
+    vis = np.zeros(seq_len, dtype=bool)
+    for j in range(n_images):
+        st = j * stride + lead
+        codes[st:st + tokens] = perm[j] * tokens + np.arange(tokens)
+        vis[st:st + tokens] = True
+    text_idx = np.cumsum(~vis) - 1
+    codes[~vis] = -1 - text_idx[~vis]
+    return codes.astype(np.int32), perm
+
+
+def get(name: str, scale: int = 1) -> BoundaryConfig:
+    """scale > 1 divides the hidden width (parity runs); layouts are unchanged."""
+    name = name.lower()
+    h = lambda x: max(8, x // scale)  # noqa: E731
+    if name == "c1":
+        return BoundaryConfig("c1", "equal-DP enc{dp2} -> llm{dp2}, fp32, 2 simulated ranks",
+                              ModuleLayout("encoder", dp=2), ModuleLayout("llm", dp=2), 2, 576,
+                              h(4096), act="fp32", grad_in="fp32", grad_out="fp32", logical_world=2)
+    if name == "c2":
+        return BoundaryConfig("c2", "fan-in colocated vit{dp8} -> llm{tp4,dp2}, bf16 h4096, 64 img x 576",
+                              ModuleLayout("vit", dp=8), ModuleLayout("llm", tp=4, dp=2), 64, 576, h(4096))
+    if name == "c3":
+        return BoundaryConfig("c3", "fan-out colocated enc{tp4,dp2} -> llm{dp8}, bf16 h5120, 64 img x 576",
+                              ModuleLayout("encoder", tp=4, dp=2), ModuleLayout("llm", dp=8), 64, 576,
+                              h(5120))
+    if name == "c4":
+        S = 32768 if scale == 1 else 32768 // scale
+        stride = S // 16
+        lead = max(1, stride // 32)
+        tokens = 576 if scale == 1 else max(4, 576 // scale)
+        codes, perm = cp_splice_codes(16, tokens, S, stride, lead, seed=1234)
+        return BoundaryConfig("c4", "CP splice vit{dp8} -> llm{tp2,cp4}, S=32768, 16 img x 576 at placeholders",
+                              ModuleLayout("vit", dp=8), ModuleLayout("llm", tp=2, cp=4), 16, tokens, h(4096),
+                              splice={"Q": 1, "S": S, "codes": codes, "text_mode": 1},
+                              extra={"perm": perm.tolist()})
+    if name == "c5":
+        return BoundaryConfig("c5", "non-colocated vit{dp2}@0-1 -> llm{tp2,pp3}@2-7, bf16 h4096, 16 img x 576",
+                              ModuleLayout("vit", dp=2), ModuleLayout("llm", tp=2, pp=3, rank_offset=2), 16,
+                              576, h(4096))
+    raise KeyError(name)
+
+
+ALL = ["c1", "c2", "c3", "c4", "c5"]
+
+
+def rank_to_gpu(world: int, n_gpus: int) -> list[int]:
+    """logical rank r -> GPU floor(r*N/world) (contiguous blocks)."""
+    return [r * n_gpus // world for r in range(world)]
