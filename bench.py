@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--blocks-per-sm", type=int, default=0)
     ap.add_argument("--threads", type=int, default=0)
     ap.add_argument("--slots", type=int, default=0, help="buffer sets rotated across steps (0=auto)")
+    ap.add_argument("--no-clocks", action="store_true", help="skip nvidia-smi sampling")
+    ap.add_argument("--clock-ms", type=int, default=200)
     return ap.parse_args()
 
 
@@ -120,13 +122,17 @@ def peaks():
 
 
 class ClockSampler:
-    def __init__(self, device_index: int):
+    def __init__(self, device_index: int, interval_ms: int = 200, enabled: bool = True):
         self.dev = device_index
+        self.interval = interval_ms
+        self.enabled = enabled
         self.proc = None
         self.path = None
         self.t_on = self.t_off = None
 
     def start(self):
+        if not self.enabled:
+            return
         fd, self.path = tempfile.mkstemp(suffix=".csv")
         os.close(fd)
         q = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -134,7 +140,7 @@ class ClockSampler:
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", "20",
+                ["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", str(self.interval),
                  "-i", str(self.dev)], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
@@ -147,7 +153,8 @@ class ClockSampler:
 
     def stop(self):
         if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+            return {"sm_mhz": None, "sm_max_mhz": None,
+                    "reasons": ["not sampled" if not self.enabled else "nvidia-smi unavailable"]}
         time.sleep(0.05)
         self.proc.terminate()
         self.proc.wait()
@@ -324,7 +331,7 @@ def main():
     if rt.status():
         raise RuntimeError("device flag wait timed out during warm-up")
 
-    sampler = ClockSampler(local_rank)
+    sampler = ClockSampler(local_rank, args.clock_ms, not args.no_clocks)
     sampler.start()
     time.sleep(0.1)
     K = args.steps

@@ -16,6 +16,7 @@ void ck(cudaError_t e, const char* what) {
 constexpr uint64_t kPadBytes = 4096;
 constexpr uint64_t kAlign = 256;
 uint64_t align_up(uint64_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+uint64_t pad_q(uint64_t x) { return (x + dev::kQuantum - 1) / dev::kQuantum * dev::kQuantum; }
 }  // namespace
 
 Exec::Exec(const bridge::BridgePlan& plan, const index::SpliceSpec* splice, int n_gpus, int my_gpu,
@@ -73,6 +74,10 @@ Exec::Exec(const bridge::BridgePlan& plan, const index::SpliceSpec* splice, int 
   peer_base_.assign(n_gpus_, nullptr);
   peer_base_[my_gpu_] = local_base_;
   tables_.resize(cfg.mb_slots);
+  int khz = 0;
+  cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, device_);
+  clock_khz_ = khz > 0 ? khz : 2000000;
+  sync_ = make_sync_args();
 }
 
 Exec::~Exec() {
@@ -81,6 +86,8 @@ Exec::~Exec() {
     cudaFree(t.reduce);
     cudaFree(t.terms);
   }
+  cudaFree(fwd_part_.first_seg);
+  cudaFree(bwd_part_.first_seg);
   for (int g = 0; g < n_gpus_; ++g)
     if (g != my_gpu_ && peer_base_[g]) cudaIpcCloseMemHandle(peer_base_[g]);
   cudaFree(local_base_);
@@ -122,7 +129,8 @@ void Exec::open_peers(const void* handles) {
     ck(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
     peer_base_[g] = static_cast<unsigned char*>(p);
   }
-  dirty_ = true;
+  sync_ = make_sync_args();
+  dirty_fwd_ = dirty_bwd_ = true;
 }
 
 void* Exec::buffer(int rank, int slot, int mb_slot, size_t* bytes) const {
@@ -143,7 +151,7 @@ void Exec::bind(int rank, int slot, int mb_slot, void* ptr, size_t bytes) {
   if (n_gpus_ > 1)
     raise(ErrorCode::InvalidArgument, "external buffers are single-GPU only; use buffer() on multi-GPU");
   bound_[rank * index::kNumSlots + slot][mb_slot] = ptr;
-  dirty_ = true;
+  dirty_fwd_ = dirty_bwd_ = true;
 }
 
 const void* Exec::resolve(int rank, int slot, int mb_slot) const {
@@ -155,50 +163,89 @@ const void* Exec::resolve(int rank, int slot, int mb_slot) const {
   return peer_base_[g] + offset_of(g, rank, slot, mb_slot);
 }
 
-void Exec::prepare() {
-  if (!dirty_) return;
+void Exec::build_partition(const std::vector<uint64_t>& w0, const std::vector<uint64_t>& n, int grid,
+                           DevPartition* out) {
+  const uint64_t total = w0.empty() ? 0 : w0.back() + n.back();
+  const uint64_t per_raw = (total + grid - 1) / grid;
+  const uint64_t per = std::max<uint64_t>(dev::kQuantum, pad_q(per_raw));
+  std::vector<int32_t> first(grid, static_cast<int32_t>(w0.size()));
+  size_t s = 0;
+  for (int b = 0; b < grid; ++b) {
+    const uint64_t lo = static_cast<uint64_t>(b) * per;
+    while (s < w0.size() && w0[s] + n[s] <= lo) ++s;  // first segment ending after lo
+    first[b] = static_cast<int32_t>(s);
+  }
+  cudaFree(out->first_seg);
+  out->first_seg = nullptr;
+  ck(cudaMalloc(&out->first_seg, grid * sizeof(int32_t)), "cudaMalloc(partition)");
+  ck(cudaMemcpy(out->first_seg, first.data(), grid * sizeof(int32_t), cudaMemcpyHostToDevice), "upload");
+  out->per_cta = per;
+  out->grid = grid;
+}
+
+void Exec::prepare_fwd() {
+  if (!dirty_fwd_) return;
+  std::vector<uint64_t> w0s, ns;
   for (int mb = 0; mb < cfg_.mb_slots; ++mb) {
     DevTables& T = tables_[mb];
     std::vector<dev::CopySeg> cs;
-    uint64_t chunk = 0;
+    uint64_t w = 0;
+    w0s.clear();
+    ns.clear();
     for (const auto& s : fwd_local_) {
-      const int es_src = dev::dtype_size(slot_dtype(s.src.slot));
-      const uint64_t nbytes = static_cast<uint64_t>(s.n) * es_src;
-      cs.push_back({static_cast<const unsigned char*>(resolve(s.src.rank, s.src.slot, mb)) + s.src.off * es_src,
+      const int es = dev::dtype_size(slot_dtype(s.src.slot));
+      const uint64_t nbytes = static_cast<uint64_t>(s.n) * es;
+      cs.push_back({static_cast<const unsigned char*>(resolve(s.src.rank, s.src.slot, mb)) + s.src.off * es,
                     static_cast<unsigned char*>(const_cast<void*>(resolve(s.dst.rank, s.dst.slot, mb))) +
-                        s.dst.off * es_src,
-                    nbytes, chunk});
-      chunk += (nbytes + dev::kCopyChunk - 1) / dev::kCopyChunk;
+                        s.dst.off * es,
+                    nbytes, w});
+      w0s.push_back(w);
+      ns.push_back(nbytes);
+      w = pad_q(w + nbytes);
     }
-    T.copy_chunks = chunk;
+    cudaFree(T.copy);
+    T.copy = nullptr;
+    if (!cs.empty()) {
+      ck(cudaMalloc(&T.copy, cs.size() * sizeof(dev::CopySeg)), "cudaMalloc(copy table)");
+      ck(cudaMemcpy(T.copy, cs.data(), cs.size() * sizeof(dev::CopySeg), cudaMemcpyHostToDevice), "upload");
+    }
+  }
+  const int bps = cfg_.blocks_per_sm > 0 ? std::min(cfg_.blocks_per_sm, dev::copy_blocks_per_sm(cfg_.threads))
+                                         : dev::copy_blocks_per_sm(cfg_.threads);
+  build_partition(w0s, ns, sm_count_ * bps, &fwd_part_);
+  dirty_fwd_ = false;
+}
+
+void Exec::prepare_bwd() {
+  if (!dirty_bwd_) return;
+  const int es_in = dev::dtype_size(cfg_.grad_in_dtype), es_out = dev::dtype_size(cfg_.grad_out_dtype);
+  std::vector<uint64_t> w0s, ns;
+  for (int mb = 0; mb < cfg_.mb_slots; ++mb) {
+    DevTables& T = tables_[mb];
     std::vector<dev::ReduceSeg> rs;
     std::vector<const void*> terms;
-    chunk = 0;
-    const int es_in = dev::dtype_size(cfg_.grad_in_dtype), es_out = dev::dtype_size(cfg_.grad_out_dtype);
+    uint64_t w = 0;
+    w0s.clear();
+    ns.clear();
     for (const auto& s : bwd_local_) {
       dev::ReduceSeg d{};
       d.dst = static_cast<unsigned char*>(const_cast<void*>(resolve(s.dst.rank, s.dst.slot, mb))) +
               s.dst.off * es_out;
       d.nelem = s.n;
-      d.chunk0 = chunk;
+      d.w0 = w;
       d.nterms = static_cast<int32_t>(s.terms.size());
       d.term0 = static_cast<int32_t>(terms.size());
       for (const auto& t : s.terms)
         terms.push_back(static_cast<const unsigned char*>(resolve(t.rank, t.slot, mb)) + t.off * es_in);
       rs.push_back(d);
-      chunk += (s.n + dev::kReduceChunk - 1) / dev::kReduceChunk;
+      w0s.push_back(w);
+      ns.push_back(s.n);
+      w = pad_q(w + s.n);
     }
-    T.reduce_chunks = chunk;
-    cudaFree(T.copy);
     cudaFree(T.reduce);
     cudaFree(T.terms);
-    T.copy = nullptr;
     T.reduce = nullptr;
     T.terms = nullptr;
-    if (!cs.empty()) {
-      ck(cudaMalloc(&T.copy, cs.size() * sizeof(dev::CopySeg)), "cudaMalloc(copy table)");
-      ck(cudaMemcpy(T.copy, cs.data(), cs.size() * sizeof(dev::CopySeg), cudaMemcpyHostToDevice), "upload");
-    }
     if (!rs.empty()) {
       ck(cudaMalloc(&T.reduce, rs.size() * sizeof(dev::ReduceSeg)), "cudaMalloc(reduce table)");
       ck(cudaMemcpy(T.reduce, rs.data(), rs.size() * sizeof(dev::ReduceSeg), cudaMemcpyHostToDevice), "upload");
@@ -208,10 +255,13 @@ void Exec::prepare() {
       ck(cudaMemcpy(T.terms, terms.data(), terms.size() * sizeof(void*), cudaMemcpyHostToDevice), "upload");
     }
   }
-  dirty_ = false;
+  const int occ = dev::reduce_blocks_per_sm(cfg_.threads, cfg_.grad_in_dtype, cfg_.grad_out_dtype);
+  const int bps = cfg_.blocks_per_sm > 0 ? std::min(cfg_.blocks_per_sm, occ) : occ;
+  build_partition(w0s, ns, sm_count_ * bps, &bwd_part_);
+  dirty_bwd_ = false;
 }
 
-dev::SyncArgs Exec::sync_args() const {
+dev::SyncArgs Exec::make_sync_args() const {
   dev::SyncArgs s{};
   s.pad = reinterpret_cast<uint32_t*>(local_base_);
   s.ctr = ctr_;
@@ -223,19 +273,17 @@ dev::SyncArgs Exec::sync_args() const {
     for (int g = 0; g < n_gpus_; ++g)
       if ((peers >> g) & 1u) s.peer_pad[g] = reinterpret_cast<uint32_t*>(peer_base_[g]);
   }
-  int khz = 0;
-  cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, device_);
-  s.timeout_cycles = static_cast<uint64_t>(cfg_.timeout_s * (khz > 0 ? khz : 2000000) * 1e3);
+  s.timeout_cycles = static_cast<uint64_t>(cfg_.timeout_s * clock_khz_ * 1e3);
   return s;
 }
 
 void Exec::forward(int mb, void* stream) {
   if (fwd_done_.count(mb))
     raise(ErrorCode::InvalidArgument, "microbatch " + std::to_string(mb) + " forwarded twice without backward");
-  prepare();
+  prepare_fwd();
   const DevTables& T = tables_[mb % cfg_.mb_slots];
-  dev::launch_copy(T.copy, static_cast<int>(fwd_local_.size()), T.copy_chunks, sync_args(),
-                   {sm_count_ * cfg_.blocks_per_sm, cfg_.threads}, stream);
+  dev::launch_copy(T.copy, static_cast<int>(fwd_local_.size()), {fwd_part_.first_seg, fwd_part_.per_cta},
+                   sync_, {fwd_part_.grid, cfg_.threads}, stream);
   ck(cudaGetLastError(), "copy_segments launch");
   ++launches_;
   fwd_done_.insert(mb);
@@ -244,11 +292,11 @@ void Exec::forward(int mb, void* stream) {
 void Exec::backward(int mb, float beta, void* stream) {
   if (!fwd_done_.count(mb))
     raise(ErrorCode::UnknownMicrobatch, "no forward record for microbatch " + std::to_string(mb));
-  prepare();
+  prepare_bwd();
   const DevTables& T = tables_[mb % cfg_.mb_slots];
-  dev::launch_reduce(T.reduce, static_cast<int>(bwd_local_.size()), T.terms, T.reduce_chunks,
-                     cfg_.grad_in_dtype, cfg_.grad_out_dtype, beta, sync_args(),
-                     {sm_count_ * cfg_.blocks_per_sm, cfg_.threads}, stream);
+  dev::launch_reduce(T.reduce, static_cast<int>(bwd_local_.size()), T.terms,
+                     {bwd_part_.first_seg, bwd_part_.per_cta}, cfg_.grad_in_dtype, cfg_.grad_out_dtype, beta,
+                     sync_, {bwd_part_.grid, cfg_.threads}, stream);
   ck(cudaGetLastError(), "reduce_segments launch");
   ++launches_;
   fwd_done_.erase(mb);

@@ -32,7 +32,7 @@ struct ExecConfig {
   int grad_out_dtype = dev::kFP32;  // source gradients (accumulator)
   int mb_slots = 1;                 // buffer sets for microbatches in flight
   int internal_alloc = 1;           // allocate the device region (else bind() every buffer)
-  int blocks_per_sm = 4;
+  int blocks_per_sm = 0;  // 0: as many as fit (occupancy)
   int threads = 512;
   double timeout_s = 20.0;          // flag-wait timeout
 };
@@ -72,8 +72,9 @@ class Exec {
   int slot_dtype(int slot) const;
   uint64_t offset_of(int gpu, int rank, int slot, int mb_slot) const;
   const void* resolve(int rank, int slot, int mb_slot) const;
-  void prepare();  // resolve pointers, upload descriptors (after bind/open)
-  dev::SyncArgs sync_args() const;
+  void prepare_fwd();  // resolve pointers, upload descriptors (after bind/open)
+  void prepare_bwd();
+  dev::SyncArgs make_sync_args() const;
 
   bridge::BridgePlan plan_;
   index::IndexMap map_;
@@ -97,11 +98,21 @@ class Exec {
     dev::CopySeg* copy = nullptr;
     dev::ReduceSeg* reduce = nullptr;
     const void** terms = nullptr;
-    uint64_t copy_chunks = 0, reduce_chunks = 0;
   };
   std::vector<DevTables> tables_;  // per mb slot
-  bool dirty_ = true;
+  // Static contiguous partition of each direction's work space over the grid.
+  struct DevPartition {
+    int32_t* first_seg = nullptr;
+    uint64_t per_cta = 0;
+    int grid = 1;
+  };
+  DevPartition fwd_part_, bwd_part_;
+  void build_partition(const std::vector<uint64_t>& w0, const std::vector<uint64_t>& n, int grid,
+                       DevPartition* out);
+  bool dirty_fwd_ = true, dirty_bwd_ = true;
   uint32_t* ctr_ = nullptr;  // device counters
+  dev::SyncArgs sync_{};
+  int clock_khz_ = 2000000;
   int sm_count_ = 0;
   int launches_ = 0;
   std::set<int> fwd_done_;

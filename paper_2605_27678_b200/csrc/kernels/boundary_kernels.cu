@@ -29,9 +29,12 @@ namespace hb::dev {
 
 namespace {
 
+// Plain (coherent) global load that skips L1 allocation. Deliberately not
+// `.nc`: ptxas may sink non-coherent loads below the stores that follow them,
+// which collapses the 8-deep load batch to ~4 in flight (seen in SASS).
 __device__ __forceinline__ uint4 ld_stream(const void* p) {
   uint4 v;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+  asm volatile("ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
                : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
                : "l"(p));
   return v;
@@ -99,16 +102,6 @@ __device__ void epoch_finish(const SyncArgs& s, uint32_t e) {
   }
 }
 
-template <class S>
-__device__ __forceinline__ int find_seg(const S* segs, int nseg, uint64_t chunk) {
-  int lo = 0, hi = nseg - 1;
-  while (lo < hi) {  // last seg with chunk0 <= chunk
-    const int mid = (lo + hi + 1) >> 1;
-    if (segs[mid].chunk0 <= chunk) lo = mid; else hi = mid - 1;
-  }
-  return lo;
-}
-
 template <class T>
 __device__ __forceinline__ void copy_scalar(const unsigned char* src, unsigned char* dst, uint64_t lo,
                                             uint64_t hi) {
@@ -117,38 +110,46 @@ __device__ __forceinline__ void copy_scalar(const unsigned char* src, unsigned c
   for (uint64_t i = lo / sizeof(T) + threadIdx.x; i < hi / sizeof(T); i += blockDim.x) d[i] = s[i];
 }
 
-constexpr int kUnroll = 4;
+constexpr int kUnroll = 8;
+
+// Copies bytes [a, b) of one segment with the whole CTA.
+__device__ __forceinline__ void copy_range(const unsigned char* __restrict__ src,
+                                           unsigned char* __restrict__ dst, uint64_t a, uint64_t b) {
+  const uint64_t align = reinterpret_cast<uint64_t>(src) | reinterpret_cast<uint64_t>(dst) | a;
+  if ((align & 15) == 0) {
+    const uint64_t vend = a + ((b - a) & ~uint64_t(15));
+    const uint64_t step = static_cast<uint64_t>(blockDim.x) * 16;
+    uint64_t i = a + threadIdx.x * 16;
+    for (; i + (kUnroll - 1) * step < vend; i += kUnroll * step) {
+      uint4 v[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) v[u] = ld_stream(src + i + u * step);
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) st_vec(dst + i + u * step, v[u]);
+    }
+    for (; i < vend; i += step) st_vec(dst + i, ld_stream(src + i));
+    for (uint64_t j = vend + threadIdx.x; j < b; j += blockDim.x) dst[j] = src[j];
+  } else {
+    const uint64_t al = align | b;
+    if ((al & 3) == 0) copy_scalar<uint32_t>(src, dst, a, b);
+    else if ((al & 1) == 0) copy_scalar<uint16_t>(src, dst, a, b);
+    else copy_scalar<unsigned char>(src, dst, a, b);
+  }
+}
 
 __global__ void __launch_bounds__(512) copy_segments_kernel(const CopySeg* __restrict__ segs, int nseg,
-                                                            uint64_t total_chunks, SyncArgs sync) {
+                                                            Partition part, SyncArgs sync) {
   uint32_t epoch;
   const bool ok = epoch_barrier(sync, &epoch);
   if (ok && nseg > 0) {
-    for (uint64_t chunk = blockIdx.x; chunk < total_chunks; chunk += gridDim.x) {
-      const CopySeg sg = segs[find_seg(segs, nseg, chunk)];
-      const uint64_t lo = (chunk - sg.chunk0) * kCopyChunk;
-      const uint64_t hi = min(lo + kCopyChunk, sg.nbytes);
-      const uint64_t align = reinterpret_cast<uint64_t>(sg.src) | reinterpret_cast<uint64_t>(sg.dst) | sg.nbytes;
-      if ((align & 15) == 0) {
-        const unsigned char* s = sg.src;
-        unsigned char* d = sg.dst;
-        const uint64_t step = static_cast<uint64_t>(blockDim.x) * 16;
-        uint64_t i = lo + threadIdx.x * 16;
-        for (; i + (kUnroll - 1) * step < hi; i += kUnroll * step) {
-          uint4 v[kUnroll];
-#pragma unroll
-          for (int u = 0; u < kUnroll; ++u) v[u] = ld_stream(s + i + u * step);
-#pragma unroll
-          for (int u = 0; u < kUnroll; ++u) st_vec(d + i + u * step, v[u]);
-        }
-        for (; i < hi; i += step) st_vec(d + i, ld_stream(s + i));
-      } else if ((align & 3) == 0) {
-        copy_scalar<uint32_t>(sg.src, sg.dst, lo, hi);
-      } else if ((align & 1) == 0) {
-        copy_scalar<uint16_t>(sg.src, sg.dst, lo, hi);
-      } else {
-        copy_scalar<unsigned char>(sg.src, sg.dst, lo, hi);
-      }
+    const uint64_t lo = blockIdx.x * part.per_cta, hi = lo + part.per_cta;
+    for (int s = part.first_seg[blockIdx.x]; s < nseg; ++s) {
+      const CopySeg sg = segs[s];
+      if (sg.w0 >= hi) break;
+      const uint64_t a = (lo > sg.w0 ? lo : sg.w0) - sg.w0;
+      const uint64_t e = sg.w0 + sg.nbytes;
+      const uint64_t b = (hi < e ? hi : e) - sg.w0;
+      if (a < b) copy_range(sg.src, sg.dst, a, b);
     }
   }
   epoch_finish(sync, epoch);
@@ -205,51 +206,71 @@ __device__ __forceinline__ void store8(T* p, const float (&f)[8]) {
 }
 
 template <class TIn, class TOut>
+__device__ __forceinline__ void reduce_range(TOut* __restrict__ dst, const TIn* const* __restrict__ tp, int nterms,
+                                             uint64_t a, uint64_t b, float beta) {
+  uint64_t align = reinterpret_cast<uint64_t>(dst + a);
+  for (int t = 0; t < nterms; ++t) align |= reinterpret_cast<uint64_t>(tp[t] + a);
+  uint64_t i = a;
+  if ((align & 15) == 0) {
+    const uint64_t vend = a + ((b - a) & ~uint64_t(7));
+    const uint64_t step = static_cast<uint64_t>(blockDim.x) * 8;
+    for (i = a + threadIdx.x * 8; i < vend; i += 2 * step) {
+      const bool two = i + step < vend;
+      float acc0[8], acc1[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc0[k] = acc1[k] = 0.0f;
+      for (int t = 0; t < nterms; ++t) {
+        float v0[8], v1[8];
+        load8(tp[t] + i, v0);
+        if (two) load8(tp[t] + i + step, v1);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc0[k] += v0[k];
+        if (two) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) acc1[k] += v1[k];
+        }
+      }
+      if (beta != 0.0f) {
+        float o0[8], o1[8];
+        load8_coherent(dst + i, o0);
+        if (two) load8_coherent(dst + i + step, o1);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc0[k] = fmaf(beta, o0[k], acc0[k]);
+        if (two) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) acc1[k] = fmaf(beta, o1[k], acc1[k]);
+        }
+      }
+      store8(dst + i, acc0);
+      if (two) store8(dst + i + step, acc1);
+    }
+    i = vend;
+  }
+  for (uint64_t e = i + threadIdx.x; e < b; e += blockDim.x) {  // tail / unaligned
+    float acc = 0.0f;
+    for (int t = 0; t < nterms; ++t) acc += Cvt<TIn>::to(tp[t][e]);
+    if (beta != 0.0f) acc = fmaf(beta, Cvt<TOut>::to(dst[e]), acc);
+    dst[e] = Cvt<TOut>::from(acc);
+  }
+}
+
+template <class TIn, class TOut>
 __global__ void __launch_bounds__(512) reduce_segments_kernel(const ReduceSeg* __restrict__ segs, int nseg,
                                                               const void* const* __restrict__ terms,
-                                                              uint64_t total_chunks, float beta,
-                                                              SyncArgs sync) {
+                                                              Partition part, float beta, SyncArgs sync) {
   uint32_t epoch;
   const bool ok = epoch_barrier(sync, &epoch);
   if (ok && nseg > 0) {
-    for (uint64_t chunk = blockIdx.x; chunk < total_chunks; chunk += gridDim.x) {
-      const ReduceSeg sg = segs[find_seg(segs, nseg, chunk)];
-      const uint64_t lo = (chunk - sg.chunk0) * kReduceChunk;
-      const uint64_t hi = min(lo + kReduceChunk, sg.nelem);
-      TOut* dst = static_cast<TOut*>(sg.dst);
-      const TIn* const* tp = reinterpret_cast<const TIn* const*>(terms + sg.term0);
-      uint64_t align = reinterpret_cast<uint64_t>(dst + lo);
-      for (int t = 0; t < sg.nterms; ++t) align |= reinterpret_cast<uint64_t>(tp[t] + lo);
-      uint64_t i = lo;
-      if ((align & 15) == 0) {
-        const uint64_t vec_hi = lo + ((hi - lo) & ~uint64_t(7));
-        for (i = lo + threadIdx.x * 8; i < vec_hi; i += static_cast<uint64_t>(blockDim.x) * 8) {
-          float acc[8];
-#pragma unroll
-          for (int k = 0; k < 8; ++k) acc[k] = 0.0f;
-          for (int t = 0; t < sg.nterms; ++t) {
-            float v[8];
-            load8(tp[t] + i, v);
-#pragma unroll
-            for (int k = 0; k < 8; ++k) acc[k] += v[k];
-          }
-          if (beta != 0.0f) {
-            float o[8];
-            load8_coherent(dst + i, o);
-#pragma unroll
-            for (int k = 0; k < 8; ++k) acc[k] = fmaf(beta, o[k], acc[k]);
-          }
-          store8(dst + i, acc);
-        }
-        i = vec_hi;
-      }
-      // scalar tail / unaligned path
-      for (uint64_t e = i + threadIdx.x; e < hi; e += blockDim.x) {
-        float acc = 0.0f;
-        for (int t = 0; t < sg.nterms; ++t) acc += Cvt<TIn>::to(tp[t][e]);
-        if (beta != 0.0f) acc = fmaf(beta, Cvt<TOut>::to(dst[e]), acc);
-        dst[e] = Cvt<TOut>::from(acc);
-      }
+    const uint64_t lo = blockIdx.x * part.per_cta, hi = lo + part.per_cta;
+    for (int s = part.first_seg[blockIdx.x]; s < nseg; ++s) {
+      const ReduceSeg sg = segs[s];
+      if (sg.w0 >= hi) break;
+      const uint64_t a = (lo > sg.w0 ? lo : sg.w0) - sg.w0;
+      const uint64_t e = sg.w0 + sg.nelem;
+      const uint64_t b = (hi < e ? hi : e) - sg.w0;
+      if (a < b)
+        reduce_range<TIn, TOut>(static_cast<TOut*>(sg.dst),
+                                reinterpret_cast<const TIn* const*>(terms + sg.term0), sg.nterms, a, b, beta);
     }
   }
   epoch_finish(sync, epoch);
@@ -264,37 +285,57 @@ int device_sm_count() {
   return n;
 }
 
-void launch_copy(const CopySeg* segs, int nseg, uint64_t total_chunks, const SyncArgs& sync,
-                 LaunchCfg cfg, void* stream) {
-  const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(cfg.grid, total_chunks)));
-  copy_segments_kernel<<<grid, cfg.block, 0, static_cast<cudaStream_t>(stream)>>>(segs, nseg, total_chunks,
-                                                                                  sync);
+int copy_blocks_per_sm(int threads) {
+  int n = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, copy_segments_kernel, threads, 0);
+  return n > 0 ? n : 1;
+}
+
+void launch_copy(const CopySeg* segs, int nseg, Partition part, const SyncArgs& sync, LaunchCfg cfg,
+                 void* stream) {
+  copy_segments_kernel<<<cfg.grid, cfg.block, 0, static_cast<cudaStream_t>(stream)>>>(segs, nseg, part, sync);
 }
 
 template <class TIn, class TOut>
-static void launch_reduce_t(const ReduceSeg* segs, int nseg, const void* const* terms, uint64_t total_chunks,
+static void launch_reduce_t(const ReduceSeg* segs, int nseg, const void* const* terms, Partition part,
                             float beta, const SyncArgs& sync, int grid, int block, cudaStream_t st) {
-  reduce_segments_kernel<TIn, TOut><<<grid, block, 0, st>>>(segs, nseg, terms, total_chunks, beta, sync);
+  reduce_segments_kernel<TIn, TOut><<<grid, block, 0, st>>>(segs, nseg, terms, part, beta, sync);
 }
 
-void launch_reduce(const ReduceSeg* segs, int nseg, const void* const* terms, uint64_t total_chunks,
-                   int in_dtype, int out_dtype, float beta, const SyncArgs& sync, LaunchCfg cfg,
-                   void* stream) {
-  const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(cfg.grid, total_chunks)));
-  auto st = static_cast<cudaStream_t>(stream);
-#define HB_RED(TI, TO) launch_reduce_t<TI, TO>(segs, nseg, terms, total_chunks, beta, sync, grid, cfg.block, st)
-  switch (in_dtype * 4 + out_dtype) {
-    case kBF16 * 4 + kBF16: HB_RED(__nv_bfloat16, __nv_bfloat16); break;
-    case kBF16 * 4 + kFP16: HB_RED(__nv_bfloat16, __half); break;
-    case kBF16 * 4 + kFP32: HB_RED(__nv_bfloat16, float); break;
-    case kFP16 * 4 + kBF16: HB_RED(__half, __nv_bfloat16); break;
-    case kFP16 * 4 + kFP16: HB_RED(__half, __half); break;
-    case kFP16 * 4 + kFP32: HB_RED(__half, float); break;
-    case kFP32 * 4 + kBF16: HB_RED(float, __nv_bfloat16); break;
-    case kFP32 * 4 + kFP16: HB_RED(float, __half); break;
-    case kFP32 * 4 + kFP32: HB_RED(float, float); break;
-    default: break;  // validated on the host
+template <class TIn, class TOut>
+static int occ_t(int threads) {
+  int n = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, reduce_segments_kernel<TIn, TOut>, threads, 0);
+  return n > 0 ? n : 1;
+}
+
+#define HB_DISPATCH(IN, OUT, MACRO)                                   \
+  switch ((IN) * 4 + (OUT)) {                                         \
+    case kBF16 * 4 + kBF16: MACRO(__nv_bfloat16, __nv_bfloat16); break; \
+    case kBF16 * 4 + kFP16: MACRO(__nv_bfloat16, __half); break;        \
+    case kBF16 * 4 + kFP32: MACRO(__nv_bfloat16, float); break;         \
+    case kFP16 * 4 + kBF16: MACRO(__half, __nv_bfloat16); break;        \
+    case kFP16 * 4 + kFP16: MACRO(__half, __half); break;               \
+    case kFP16 * 4 + kFP32: MACRO(__half, float); break;                \
+    case kFP32 * 4 + kBF16: MACRO(float, __nv_bfloat16); break;         \
+    case kFP32 * 4 + kFP16: MACRO(float, __half); break;                \
+    case kFP32 * 4 + kFP32: MACRO(float, float); break;                 \
+    default: break;                                                   \
   }
+
+int reduce_blocks_per_sm(int threads, int in_dtype, int out_dtype) {
+  int n = 1;
+#define HB_OCC(TI, TO) n = occ_t<TI, TO>(threads)
+  HB_DISPATCH(in_dtype, out_dtype, HB_OCC)
+#undef HB_OCC
+  return n;
+}
+
+void launch_reduce(const ReduceSeg* segs, int nseg, const void* const* terms, Partition part, int in_dtype,
+                   int out_dtype, float beta, const SyncArgs& sync, LaunchCfg cfg, void* stream) {
+  auto st = static_cast<cudaStream_t>(stream);
+#define HB_RED(TI, TO) launch_reduce_t<TI, TO>(segs, nseg, terms, part, beta, sync, cfg.grid, cfg.block, st)
+  HB_DISPATCH(in_dtype, out_dtype, HB_RED)
 #undef HB_RED
 }
 

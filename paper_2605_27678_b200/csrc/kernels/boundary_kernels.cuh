@@ -9,23 +9,33 @@ enum Dtype : int { kBF16 = 0, kFP16 = 1, kFP32 = 2, kFP64 = 3 };
 
 inline int dtype_size(int dt) { return dt == kFP32 ? 4 : dt == kFP64 ? 8 : 2; }
 
-// One contiguous byte run: destination bytes [dst, dst+nbytes) come from
-// [src, src+nbytes). `chunk0` is the first global work-chunk index.
+// Work space: every segment occupies [w0, w0 + n) of a padded linear work
+// space (bytes for copies, elements for reductions); w0 is rounded up to
+// kQuantum so every CTA boundary is 16-B aligned inside each segment. CTA b
+// owns the contiguous range [b*per_cta, (b+1)*per_cta) and starts at segment
+// first_seg[b] (precomputed on the host): no per-chunk searches.
+constexpr uint64_t kQuantum = 4096;
+
 struct CopySeg {
   const unsigned char* src;
   unsigned char* dst;
   uint64_t nbytes;
-  uint64_t chunk0;
+  uint64_t w0;
 };
 
-// dst[i] = beta*dst[i] + sum_t term_t[i], i in [0, nelem), fp32 accumulation,
-// terms summed in order starting from +0.0f. term pointers live in a side array.
+// dst[i] = beta*dst[i] + sum_t term_t[i], fp32 accumulation, terms summed in
+// order starting from +0.0f; term pointers live in a side array.
 struct ReduceSeg {
   void* dst;
   uint64_t nelem;
-  uint64_t chunk0;
+  uint64_t w0;
   int32_t nterms;
   int32_t term0;
+};
+
+struct Partition {
+  const int32_t* first_seg;  // [grid]
+  uint64_t per_cta;          // work units per CTA (multiple of kQuantum)
 };
 
 // Cross-GPU epoch barrier over peer-mapped flag words. Every GPU of an exec
@@ -43,20 +53,19 @@ struct SyncArgs {
   uint64_t timeout_cycles;
 };
 
-constexpr uint64_t kCopyChunk = 64 * 1024;    // bytes per work chunk
-constexpr uint64_t kReduceChunk = 16 * 1024;  // elements per work chunk
-
 struct LaunchCfg {
   int grid;
   int block;
 };
 
 // Host-side launchers (defined in boundary_kernels.cu).
-void launch_copy(const CopySeg* segs, int nseg, uint64_t total_chunks, const SyncArgs& sync,
-                 LaunchCfg cfg, void* stream);
-void launch_reduce(const ReduceSeg* segs, int nseg, const void* const* terms,
-                   uint64_t total_chunks, int in_dtype, int out_dtype, float beta,
-                   const SyncArgs& sync, LaunchCfg cfg, void* stream);
+void launch_copy(const CopySeg* segs, int nseg, Partition part, const SyncArgs& sync, LaunchCfg cfg,
+                 void* stream);
+void launch_reduce(const ReduceSeg* segs, int nseg, const void* const* terms, Partition part,
+                   int in_dtype, int out_dtype, float beta, const SyncArgs& sync, LaunchCfg cfg,
+                   void* stream);
 int device_sm_count();
+int copy_blocks_per_sm(int threads);
+int reduce_blocks_per_sm(int threads, int in_dtype, int out_dtype);
 
 }  // namespace hb::dev

@@ -146,9 +146,9 @@ def test_configs_scaled_vs_oracle(name, beta):
 def test_reference_layout_splice_vs_oracle():
     """Reference-faithful splice: each sample one sequence, vision at [0,S_v) (tinymodel.hpp:24-26)."""
     cfg = configs.get("c4", scale=64)
-    n = 2  # samples (= sequences) per destination shard
+    n = 8  # samples (= sequences) per destination shard
     S, S_v = 64, cfg.tokens
-    cfg.src = hbg.ModuleLayout("vit", dp=2)
+    cfg.src = hbg.ModuleLayout("vit", dp=8)
     cfg.dst = hbg.ModuleLayout("llm", tp=2, cp=4)
     cfg.batch = n
     q = np.arange(n)[:, None]
