@@ -69,10 +69,11 @@ def get(name: str, scale: int = 1) -> BoundaryConfig:
                               ModuleLayout("encoder", tp=4, dp=2), ModuleLayout("llm", dp=8), 64, 576,
                               h(5120))
     if name == "c4":
-        S = 32768 if scale == 1 else 32768 // scale
+        tokens = 576 if scale == 1 else max(4, 576 // scale)
+        S = 32768 if scale == 1 else max(32768 // scale, 16 * 2 * tokens)
+        S = (S + 63) // 64 * 64
         stride = S // 16
         lead = max(1, stride // 32)
-        tokens = 576 if scale == 1 else max(4, 576 // scale)
         codes, perm = cp_splice_codes(16, tokens, S, stride, lead, seed=1234)
         return BoundaryConfig("c4", "CP splice vit{dp8} -> llm{tp2,cp4}, S=32768, 16 img x 576 at placeholders",
                               ModuleLayout("vit", dp=8), ModuleLayout("llm", tp=2, cp=4), 16, tokens, h(4096),
