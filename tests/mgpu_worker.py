@@ -54,7 +54,7 @@ def run(name, rank, N, dev, steps=3):
     shards = {}
     for r in src.stage_ranks(src.pp - 1):
         t, c, p, d = src.coord(r)
-        shards[r] = X[SI[d][0]:SI[d][0] + SI[d][1]] + (8.0 * t if t else 0.0)
+        shards[r] = bf16_round(X[SI[d][0]:SI[d][0] + SI[d][1]] + (8.0 * t if t else 0.0))
         if r in local:
             rt.buffer(r, hbb.SLOT_SRC_ACT).copy_(torch.from_numpy(shards[r].reshape(-1)).to(dev).to(torch.bfloat16))
     L = cfg.splice["S"] // dst.cp if sp else 0
