@@ -1,4 +1,4 @@
-exec > gpurun_out/mgpu2.log 2>&1
+exec > gpurun_out/mgpu${N}.log 2>&1
 nvidia-smi topo -m
 N=${N:-2}
 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29511 tests/mgpu_worker.py c2 c5 c4 c3 c1; echo parity=$?
