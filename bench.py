@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--slots", type=int, default=0, help="buffer sets rotated across steps (0=auto)")
     ap.add_argument("--no-clocks", action="store_true", help="skip nvidia-smi sampling")
     ap.add_argument("--clock-ms", type=int, default=200)
+    ap.add_argument("--fwd-mode", type=int, default=0, help="forward: 0 auto, 1 pull, 2 push")
+    ap.add_argument("--partition", type=int, default=0, help="0 auto, 1 contiguous, 2 interleaved")
     return ap.parse_args()
 
 
@@ -90,9 +92,15 @@ def traffic_model(cfg, n_gpus):
     a, gi, go = DT_SIZE[cfg.act], DT_SIZE[cfg.grad_in], DT_SIZE[cfg.grad_out]
     z = lambda: [0] * n_gpus  # noqa: E731
     f_hbm, f_nvl, b_hbm, b_nvl = z(), z(), z(), z()
+    seen = set()  # remote runs cross NVLink once per consuming GPU, then fan out locally
     for (sr, ss, so, dr, ds, do, n) in hbb.index_forward(plan, sp):
         g_src, g_dst = r2g[sr], r2g[dr]
         f_hbm[g_dst] += n * a            # write
+        key = (sr, ss, so, n, g_dst)
+        if g_src != g_dst and key in seen:
+            f_hbm[g_dst] += n * a        # local re-read of the first consumer's copy
+            continue
+        seen.add(key)
         f_hbm[g_src] += n * a            # read at the owner (local or served to a peer)
         if g_src != g_dst:
             f_nvl[g_dst] += n * a
@@ -298,7 +306,8 @@ def main():
 
     rt = hbb.BridgeRuntime(plan, sp, n_gpus=N, my_gpu=rank, rank_to_gpu=r2g, act_dtype=tdt[cfg.act],
                            grad_in_dtype=tdt[cfg.grad_in], grad_out_dtype=tdt[cfg.grad_out],
-                           mb_slots=slots, blocks_per_sm=args.blocks_per_sm, threads=args.threads)
+                           mb_slots=slots, blocks_per_sm=args.blocks_per_sm, threads=args.threads,
+                           fwd_mode=args.fwd_mode, partition=args.partition)
     if N > 1:
         rt.exchange_handles()
     gen = torch.Generator(device=dev)
@@ -364,22 +373,53 @@ def main():
     if rt.status():
         raise RuntimeError("device flag wait timed out")
 
+    # isolated per-kernel timing (for the roofline of each kernel; not the headline)
+    iso = []
+    for i in range(min(K, 20)):
+        row = []
+        for op in ("fwd", "bwd"):
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            if op == "fwd":
+                rt.forward(mb, stream)
+            else:
+                rt.backward(mb, cfg.beta, stream)
+            e1.record(stream)
+            stream.synchronize()
+            row.append(e0.elapsed_time(e1))
+        mb += 1
+        iso.append(row)
+    t = torch.tensor([sum(r[0] for r in iso) / len(iso), sum(r[1] for r in iso) / len(iso)],
+                     dtype=torch.float64, device=dev)
+    if N > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    iso_fwd_ms, iso_bwd_ms = t.tolist()
+
     fwd_b, bwd_b = payload_bytes(cfg)
     value = (fwd_b + bwd_b) / (ms_step * 1e-3) / 1e9
     tokens_s = cfg.batch * cfg.tokens / (ms_step * 1e-3)
 
     # roofline of the dominant kernel on this GPU (bytes from the index map)
     pk = peaks()
-    def bound(hbm, nvl, ms):
-        t_hbm = hbm / (pk["hbm_gbs"] * 1e9)
-        t_nvl = nvl / (pk["nvl_gbs"] * 1e9)
-        if t_nvl > t_hbm:
-            return "nvlink", nvl / (ms * 1e-3) / 1e9, pk["nvl_gbs"], max(t_hbm, t_nvl)
-        return "hbm", hbm / (ms * 1e-3) / 1e9, pk["hbm_gbs"], max(t_hbm, t_nvl)
-    fb = bound(tm["fwd_hbm"][rank], tm["fwd_nvl"][rank], fwd_ms)
-    bb = bound(tm["bwd_hbm"][rank], tm["bwd_nvl"][rank], bwd_ms)
-    dom_is_fwd = fwd_ms >= bwd_ms
-    kind, achieved, peak, tstar = fb if dom_is_fwd else bb
+    def bound(kind, ms):
+        """T* of one kernel = max over GPUs of max(HBM/peak, NVLink ingress/peak); achieved
+        = the critical GPU's binding bytes / measured kernel time (max over ranks)."""
+        best = None
+        for g in range(N):
+            h, n = tm[kind + "_hbm"][g], tm[kind + "_nvl"][g]
+            t_h, t_n = h / (pk["hbm_gbs"] * 1e9), n / (pk["nvl_gbs"] * 1e9)
+            cand = ("nvlink", n, pk["nvl_gbs"], t_n, g) if t_n > t_h else ("hbm", h, pk["hbm_gbs"], t_h, g)
+            if best is None or cand[3] > best[3]:
+                best = cand
+        res, nbytes, peak, tstar, g = best
+        ach = nbytes / (ms * 1e-3) / 1e9 if ms > 0 else 0.0
+        return {"ms": round(ms, 4), "bound": res, "critical_gpu": g, "bytes": nbytes, "achieved_gbs": round(ach, 1),
+                "peak_gbs": peak, "frac": round(ach / peak, 4), "tstar_ms": round(tstar * 1e3, 4),
+                "hbm_bytes_per_gpu": tm[kind + "_hbm"], "nvl_in_bytes_per_gpu": tm[kind + "_nvl"]}
+    fk, bk = bound("fwd", iso_fwd_ms), bound("bwd", iso_bwd_ms)
+    dom_is_fwd = iso_fwd_ms >= iso_bwd_ms
+    dom = fk if dom_is_fwd else bk
     traffic = None
     prof = os.path.join(ROOT, "profiles", f"traffic_{cfg.name}_n{N}.json")
     if os.path.exists(prof):
@@ -388,18 +428,17 @@ def main():
                 traffic = json.load(f).get("fwd" if dom_is_fwd else "bwd")
         except Exception:
             traffic = None
+    tstar_step = fk["tstar_ms"] + bk["tstar_ms"]
     roofline = {
-        "bound": "hbm" if kind == "hbm" else "nvlink", "kernel": "copy_segments_kernel" if dom_is_fwd else "reduce_segments_kernel",
-        "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
-        "traffic": traffic, "peak_source": pk["src"] if kind == "hbm" else "measured peer copy 770 GB/s (B200_PROFILING.md)",
-        "per_kernel": {
-            "fwd": {"ms": round(fwd_ms, 4), "bound": fb[0], "achieved_gbs": round(fb[1], 1),
-                    "frac": round(fb[1] / fb[2], 4), "hbm_bytes": tm["fwd_hbm"][rank], "nvl_in_bytes": tm["fwd_nvl"][rank]},
-            "bwd": {"ms": round(bwd_ms, 4), "bound": bb[0], "achieved_gbs": round(bb[1], 1),
-                    "frac": round(bb[1] / bb[2], 4), "hbm_bytes": tm["bwd_hbm"][rank], "nvl_in_bytes": tm["bwd_nvl"][rank]},
-        },
-        "step_tstar_ms_measured_peaks": round((fb[3] + bb[3]) * 1e3, 4),
-        "step_frac_of_tstar": round((fb[3] + bb[3]) * 1e3 / ms_step, 4),
+        "bound": dom["bound"], "kernel": "copy_segments_kernel" if dom_is_fwd else "reduce_segments_kernel",
+        "achieved": dom["achieved_gbs"], "peak": dom["peak_gbs"], "unit": "GB/s", "frac": dom["frac"],
+        "traffic": traffic,
+        "peak_source": pk["src"] if dom["bound"] == "hbm" else "measured peer copy 770 GB/s (B200_PROFILING.md)",
+        "per_kernel": {"fwd": fk, "bwd": bk,
+                       "timing": "isolated: each kernel bracketed by a device+host barrier, CUDA events, "
+                                 "mean over steps, max over ranks"},
+        "step_tstar_ms_measured_peaks": round(tstar_step, 4),
+        "step_frac_of_tstar": round(tstar_step / ms_step, 4),
     }
     # nominal (900 GB/s NVLink, 8 TB/s HBM) T* of BASELINE.md, max over GPUs
     def tstar_nominal(h, n):

@@ -133,6 +133,8 @@ typedef struct {
   int blocks_per_sm;
   int threads;
   double timeout_s; /* cross-GPU flag wait timeout                            */
+  int fwd_mode;     /* forward: 0 auto, 1 consumers pull, 2 owners push         */
+  int partition;    /* CTA work split: 0 auto, 1 contiguous, 2 interleaved      */
 } hb_exec_config;
 void hb_exec_config_default(hb_exec_config* c);
 

@@ -73,7 +73,8 @@ class ExecConfig(ctypes.Structure):
     _fields_ = [("act_dtype", ctypes.c_int), ("grad_in_dtype", ctypes.c_int),
                 ("grad_out_dtype", ctypes.c_int), ("mb_slots", ctypes.c_int),
                 ("internal_alloc", ctypes.c_int), ("blocks_per_sm", ctypes.c_int),
-                ("threads", ctypes.c_int), ("timeout_s", ctypes.c_double)]
+                ("threads", ctypes.c_int), ("timeout_s", ctypes.c_double), ("fwd_mode", ctypes.c_int),
+                ("partition", ctypes.c_int)]
 
 
 _lib = None

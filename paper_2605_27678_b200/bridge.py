@@ -195,7 +195,8 @@ class BridgeRuntime:
     def __init__(self, plan: BridgePlan, splice: SpliceSpec | None = None, *, n_gpus: int = 1,
                  my_gpu: int = 0, rank_to_gpu=None, act_dtype=None, grad_in_dtype=None,
                  grad_out_dtype=None, mb_slots: int = 1, internal_alloc: bool = True,
-                 blocks_per_sm: int = 0, threads: int = 0, timeout_s: float = 0.0):
+                 blocks_per_sm: int = 0, threads: int = 0, timeout_s: float = 0.0,
+                 fwd_mode: int = 0, partition: int = 0):
         import torch
 
         self.plan, self.splice = plan, splice
@@ -215,6 +216,8 @@ class BridgeRuntime:
         cfg.blocks_per_sm = blocks_per_sm
         cfg.threads = threads
         cfg.timeout_s = timeout_s
+        cfg.fwd_mode = fwd_mode  # 0 auto, 1 pull, 2 push
+        cfg.partition = partition
         if not torch.cuda.is_available():
             raise HetBridgeError(25, "BridgeRuntime needs a CUDA device (no CPU fallback)")
         m = (ctypes.c_int * len(self.rank_to_gpu))(*self.rank_to_gpu)

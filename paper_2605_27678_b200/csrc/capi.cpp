@@ -84,7 +84,7 @@ const char* hb_error_name(int status) {
   return hb::error_code_name(static_cast<hb::ErrorCode>(status - 1));
 }
 
-int hb_abi_version(void) { return 1; }
+int hb_abi_version(void) { return 4; }
 
 int hb_coord_of_rank(const hb_layout* l, int rank, int coord4[4]) {
   return guard([&] {
@@ -273,6 +273,8 @@ void hb_exec_config_default(hb_exec_config* c) {
   c->blocks_per_sm = d.blocks_per_sm;
   c->threads = d.threads;
   c->timeout_s = d.timeout_s;
+  c->fwd_mode = d.fwd_mode;
+  c->partition = d.partition;
 }
 
 int hb_exec_create(const hb_plan* p, const hb_splice* s, int n_gpus, int my_gpu, const int* rank_to_gpu,
@@ -291,6 +293,8 @@ int hb_exec_create(const hb_plan* p, const hb_splice* s, int n_gpus, int my_gpu,
       c.blocks_per_sm = cfg->blocks_per_sm > 0 ? cfg->blocks_per_sm : c.blocks_per_sm;
       c.threads = cfg->threads > 0 ? cfg->threads : c.threads;
       c.timeout_s = cfg->timeout_s > 0 ? cfg->timeout_s : c.timeout_s;
+      c.fwd_mode = cfg->fwd_mode;
+      c.partition = cfg->partition;
     }
     std::vector<int> map;
     if (rank_to_gpu) map.assign(rank_to_gpu, rank_to_gpu + n_ranks);

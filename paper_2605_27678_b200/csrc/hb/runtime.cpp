@@ -5,6 +5,8 @@
 
 #include <algorithm>
 #include <cstring>
+#include <map>
+#include <tuple>
 
 namespace hb::rt {
 
@@ -58,8 +60,46 @@ Exec::Exec(const bridge::BridgePlan& plan, const index::SpliceSpec* splice, int 
   }
   bound_.assign(map_.world * index::kNumSlots, std::vector<void*>(cfg.mb_slots, nullptr));
 
-  for (const auto& s : map_.fwd)
-    if (gpu_of(s.dst.rank) == my_gpu_) fwd_local_.push_back(s);
+  // Forward mode. Pull needs one barrier; push needs a second ("writes done")
+  // but its remote stores never stall the issuing warp. Auto picks push when
+  // the NVLink traffic is bidirectional (every GPU that receives also sends),
+  // pull when it is one-way (measured: one-way pull 755 GB/s vs push 701;
+  // bidirectional push 653 vs pull 613, scripts/nvl_probe.py).
+  if (cfg_.fwd_mode == 2) {
+    fwd_push_ = true;
+  } else if (cfg_.fwd_mode == 0 && n_gpus_ > 1) {
+    std::vector<uint64_t> sent(n_gpus_, 0), recv(n_gpus_, 0);
+    for (const auto& s : map_.fwd) {
+      const int gs = gpu_of(s.src.rank), gd = gpu_of(s.dst.rank);
+      if (gs != gd) {
+        sent[gs] += s.n;
+        recv[gd] += s.n;
+      }
+    }
+    bool any = false, bidir = true;
+    for (int g = 0; g < n_gpus_; ++g) {
+      any |= recv[g] > 0;
+      if ((sent[g] > 0) != (recv[g] > 0)) bidir = false;
+    }
+    fwd_push_ = any && bidir;
+  }
+  // Dedup: a remote source run needed by several ranks of one GPU crosses
+  // NVLink once (to the first of them); the others copy it locally in phase 2.
+  // Decided on the global map so every process agrees.
+  std::map<std::tuple<int, int, int64_t, int64_t, int>, index::Ref> first_copy;
+  for (const auto& s : map_.fwd) {
+    const int gs = gpu_of(s.src.rank), gd = gpu_of(s.dst.rank);
+    if (gs != gd) {
+      const auto key = std::make_tuple(s.src.rank, s.src.slot, s.src.off, s.n, gd);
+      auto it = first_copy.find(key);
+      if (it != first_copy.end()) {
+        if (gd == my_gpu_) fwd_second_local_.push_back({it->second, s.dst, s.n});
+        continue;
+      }
+      first_copy.emplace(key, s.dst);
+    }
+    if (gpu_of(fwd_push_ ? s.src.rank : s.dst.rank) == my_gpu_) fwd_local_.push_back(s);
+  }
   for (const auto& s : map_.bwd)
     if (gpu_of(s.dst.rank) == my_gpu_) bwd_local_.push_back(s);
 
@@ -68,9 +108,12 @@ Exec::Exec(const bridge::BridgePlan& plan, const index::SpliceSpec* splice, int 
   if (cfg_.internal_alloc || n_gpus_ > 1) {
     ck(cudaMalloc(&local_base_, region_bytes_), "cudaMalloc(region)");
     ck(cudaMemset(local_base_, 0, kPadBytes), "cudaMemset(pad)");
+    static_assert(2 * dev::kMaxGpus * sizeof(uint32_t) <= kPadBytes, "pad holds start and done flags");
   }
   ck(cudaMalloc(&ctr_, 64), "cudaMalloc(ctr)");
   ck(cudaMemset(ctr_, 0, 64), "cudaMemset(ctr)");
+  ck(cudaMalloc(&ctr2_, 64), "cudaMalloc(ctr2)");
+  ck(cudaMemset(ctr2_, 0, 64), "cudaMemset(ctr2)");
   peer_base_.assign(n_gpus_, nullptr);
   peer_base_[my_gpu_] = local_base_;
   tables_.resize(cfg.mb_slots);
@@ -78,6 +121,8 @@ Exec::Exec(const bridge::BridgePlan& plan, const index::SpliceSpec* splice, int 
   cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, device_);
   clock_khz_ = khz > 0 ? khz : 2000000;
   sync_ = make_sync_args();
+  sync_push_ = sync_;
+  sync_push_.end_sync = 1;
 }
 
 Exec::~Exec() {
@@ -87,6 +132,9 @@ Exec::~Exec() {
     cudaFree(t.terms);
   }
   cudaFree(fwd_part_.first_seg);
+  cudaFree(fwd2_part_.first_seg);
+  for (auto& t : tables_) cudaFree(t.copy2);
+  cudaFree(ctr2_);
   cudaFree(bwd_part_.first_seg);
   for (int g = 0; g < n_gpus_; ++g)
     if (g != my_gpu_ && peer_base_[g]) cudaIpcCloseMemHandle(peer_base_[g]);
@@ -130,6 +178,8 @@ void Exec::open_peers(const void* handles) {
     peer_base_[g] = static_cast<unsigned char*>(p);
   }
   sync_ = make_sync_args();
+  sync_push_ = sync_;
+  sync_push_.end_sync = 1;
   dirty_fwd_ = dirty_bwd_ = true;
 }
 
@@ -163,6 +213,14 @@ const void* Exec::resolve(int rank, int slot, int mb_slot) const {
   return peer_base_[g] + offset_of(g, rank, slot, mb_slot);
 }
 
+bool Exec::interleave(size_t nseg, int grid) const {
+  if (cfg_.partition == 1) return false;
+  if (cfg_.partition == 2) return true;
+  (void)nseg;
+  (void)grid;
+  return false;  // auto: contiguous ranges (measured faster on HBM-bound launches)
+}
+
 void Exec::build_partition(const std::vector<uint64_t>& w0, const std::vector<uint64_t>& n, int grid,
                            DevPartition* out) {
   const uint64_t total = w0.empty() ? 0 : w0.back() + n.back();
@@ -177,42 +235,50 @@ void Exec::build_partition(const std::vector<uint64_t>& w0, const std::vector<ui
   }
   cudaFree(out->first_seg);
   out->first_seg = nullptr;
+  out->grid = grid;
+  if (interleave(w0.size(), grid)) return;  // first_seg == nullptr -> interleaved shares
   ck(cudaMalloc(&out->first_seg, grid * sizeof(int32_t)), "cudaMalloc(partition)");
   ck(cudaMemcpy(out->first_seg, first.data(), grid * sizeof(int32_t), cudaMemcpyHostToDevice), "upload");
   out->per_cta = per;
   out->grid = grid;
 }
 
+void Exec::upload_copies(const std::vector<index::CopySeg>& segs, int mb, dev::CopySeg** out,
+                         std::vector<uint64_t>* w0s, std::vector<uint64_t>* ns) {
+  std::vector<dev::CopySeg> cs;
+  uint64_t w = 0;
+  w0s->clear();
+  ns->clear();
+  for (const auto& s : segs) {
+    const int es = dev::dtype_size(slot_dtype(s.src.slot));
+    const uint64_t nbytes = static_cast<uint64_t>(s.n) * es;
+    cs.push_back({static_cast<const unsigned char*>(resolve(s.src.rank, s.src.slot, mb)) + s.src.off * es,
+                  static_cast<unsigned char*>(const_cast<void*>(resolve(s.dst.rank, s.dst.slot, mb))) +
+                      s.dst.off * es,
+                  nbytes, w});
+    w0s->push_back(w);
+    ns->push_back(nbytes);
+    w = pad_q(w + nbytes);
+  }
+  cudaFree(*out);
+  *out = nullptr;
+  if (!cs.empty()) {
+    ck(cudaMalloc(out, cs.size() * sizeof(dev::CopySeg)), "cudaMalloc(copy table)");
+    ck(cudaMemcpy(*out, cs.data(), cs.size() * sizeof(dev::CopySeg), cudaMemcpyHostToDevice), "upload");
+  }
+}
+
 void Exec::prepare_fwd() {
   if (!dirty_fwd_) return;
-  std::vector<uint64_t> w0s, ns;
+  std::vector<uint64_t> w0s, ns, w0s2, ns2;
   for (int mb = 0; mb < cfg_.mb_slots; ++mb) {
-    DevTables& T = tables_[mb];
-    std::vector<dev::CopySeg> cs;
-    uint64_t w = 0;
-    w0s.clear();
-    ns.clear();
-    for (const auto& s : fwd_local_) {
-      const int es = dev::dtype_size(slot_dtype(s.src.slot));
-      const uint64_t nbytes = static_cast<uint64_t>(s.n) * es;
-      cs.push_back({static_cast<const unsigned char*>(resolve(s.src.rank, s.src.slot, mb)) + s.src.off * es,
-                    static_cast<unsigned char*>(const_cast<void*>(resolve(s.dst.rank, s.dst.slot, mb))) +
-                        s.dst.off * es,
-                    nbytes, w});
-      w0s.push_back(w);
-      ns.push_back(nbytes);
-      w = pad_q(w + nbytes);
-    }
-    cudaFree(T.copy);
-    T.copy = nullptr;
-    if (!cs.empty()) {
-      ck(cudaMalloc(&T.copy, cs.size() * sizeof(dev::CopySeg)), "cudaMalloc(copy table)");
-      ck(cudaMemcpy(T.copy, cs.data(), cs.size() * sizeof(dev::CopySeg), cudaMemcpyHostToDevice), "upload");
-    }
+    upload_copies(fwd_local_, mb, &tables_[mb].copy, &w0s, &ns);
+    upload_copies(fwd_second_local_, mb, &tables_[mb].copy2, &w0s2, &ns2);
   }
   const int bps = cfg_.blocks_per_sm > 0 ? std::min(cfg_.blocks_per_sm, dev::copy_blocks_per_sm(cfg_.threads))
                                          : dev::copy_blocks_per_sm(cfg_.threads);
   build_partition(w0s, ns, sm_count_ * bps, &fwd_part_);
+  if (!fwd_second_local_.empty()) build_partition(w0s2, ns2, sm_count_ * bps, &fwd2_part_);
   dirty_fwd_ = false;
 }
 
@@ -283,9 +349,18 @@ void Exec::forward(int mb, void* stream) {
   prepare_fwd();
   const DevTables& T = tables_[mb % cfg_.mb_slots];
   dev::launch_copy(T.copy, static_cast<int>(fwd_local_.size()), {fwd_part_.first_seg, fwd_part_.per_cta},
-                   sync_, {fwd_part_.grid, cfg_.threads}, stream);
+                   fwd_push_ && n_gpus_ > 1 ? sync_push_ : sync_, {fwd_part_.grid, cfg_.threads}, stream);
   ck(cudaGetLastError(), "copy_segments launch");
   ++launches_;
+  if (!fwd_second_local_.empty()) {
+    dev::SyncArgs local{};
+    local.ctr = ctr2_;
+    local.my_gpu = my_gpu_;
+    dev::launch_copy(T.copy2, static_cast<int>(fwd_second_local_.size()),
+                     {fwd2_part_.first_seg, fwd2_part_.per_cta}, local, {fwd2_part_.grid, cfg_.threads}, stream);
+    ck(cudaGetLastError(), "copy_segments (phase 2) launch");
+    ++launches_;
+  }
   fwd_done_.insert(mb);
 }
 
@@ -313,6 +388,7 @@ uint32_t Exec::device_error() const {
 uint64_t Exec::local_fwd_bytes() const {
   uint64_t b = 0;
   for (const auto& s : fwd_local_) b += static_cast<uint64_t>(s.n) * dev::dtype_size(slot_dtype(s.src.slot));
+  for (const auto& s : fwd_second_local_) b += static_cast<uint64_t>(s.n) * dev::dtype_size(slot_dtype(s.src.slot));
   return b;
 }
 

@@ -35,6 +35,8 @@ struct ExecConfig {
   int blocks_per_sm = 0;  // 0: as many as fit (occupancy)
   int threads = 512;
   double timeout_s = 20.0;          // flag-wait timeout
+  int fwd_mode = 0;                 // forward: 0 auto, 1 consumers pull from owners, 2 owners push
+  int partition = 0;                // 0 auto, 1 contiguous ranges per CTA, 2 interleaved shares
 };
 
 class Exec {
@@ -60,7 +62,7 @@ class Exec {
   uint32_t device_error() const;  // synchronises
 
   const index::IndexMap& map() const { return map_; }
-  int local_fwd_segments() const { return static_cast<int>(fwd_local_.size()); }
+  int local_fwd_segments() const { return static_cast<int>(fwd_local_.size() + fwd_second_local_.size()); }
   int local_bwd_segments() const { return static_cast<int>(bwd_local_.size()); }
   uint64_t local_fwd_bytes() const;
   uint64_t local_bwd_elems() const;
@@ -82,6 +84,7 @@ class Exec {
   std::vector<int> rank_to_gpu_;
   ExecConfig cfg_;
   uint32_t group_mask_ = 0;
+  bool fwd_push_ = false;  // resolved forward mode
 
   // layout: offsets_[gpu][rank*kNumSlots+slot] (for mb slot 0), stride per mb slot
   std::vector<std::vector<uint64_t>> offsets_;
@@ -92,10 +95,14 @@ class Exec {
   std::vector<std::vector<void*>> bound_;  // [rank*kNumSlots+slot][mb] external binding
 
   std::vector<index::CopySeg> fwd_local_;
+  // Phase 2 of the forward: copies of rows a remote owner already delivered to
+  // another rank on this GPU (dedup of repeated remote fetches; local HBM only).
+  std::vector<index::CopySeg> fwd_second_local_;
   std::vector<index::ReduceSeg> bwd_local_;
 
   struct DevTables {
     dev::CopySeg* copy = nullptr;
+    dev::CopySeg* copy2 = nullptr;
     dev::ReduceSeg* reduce = nullptr;
     const void** terms = nullptr;
   };
@@ -106,12 +113,16 @@ class Exec {
     uint64_t per_cta = 0;
     int grid = 1;
   };
-  DevPartition fwd_part_, bwd_part_;
+  DevPartition fwd_part_, fwd2_part_, bwd_part_;
+  uint32_t* ctr2_ = nullptr;  // phase-2 counters (local-only launch)
+  void upload_copies(const std::vector<index::CopySeg>& segs, int mb, dev::CopySeg** out,
+                     std::vector<uint64_t>* w0s, std::vector<uint64_t>* ns);
   void build_partition(const std::vector<uint64_t>& w0, const std::vector<uint64_t>& n, int grid,
                        DevPartition* out);
+  bool interleave(size_t nseg, int grid) const;
   bool dirty_fwd_ = true, dirty_bwd_ = true;
   uint32_t* ctr_ = nullptr;  // device counters
-  dev::SyncArgs sync_{};
+  dev::SyncArgs sync_{}, sync_push_{};
   int clock_khz_ = 2000000;
   int sm_count_ = 0;
   int launches_ = 0;

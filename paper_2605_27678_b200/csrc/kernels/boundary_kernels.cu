@@ -89,16 +89,38 @@ __device__ bool epoch_barrier(const SyncArgs& s, uint32_t* target_out) {
   return ok != 0;
 }
 
+// Last CTA to finish bumps the local epoch. In push mode it first publishes
+// "my writes into your buffers are done" (release, system scope) and waits for
+// every writer into this GPU's buffers, so kernel completion implies the
+// outputs are complete.
 __device__ void epoch_finish(const SyncArgs& s, uint32_t e) {
+  __shared__ int last;
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
-    const uint32_t done = atomicAdd(s.ctr + 1, 1u);
-    if (done == gridDim.x - 1) {
-      s.ctr[1] = 0;
-      __threadfence();
-      atomicExch(s.ctr, e);
+    __threadfence_system();
+    last = atomicAdd(s.ctr + 1, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  if (s.end_sync) {
+    const int g = threadIdx.x;
+    if (g < kMaxGpus && ((s.post_mask >> g) & 1u)) st_release_sys(s.peer_pad[g] + kMaxGpus + s.my_gpu, e);
+    if (g < kMaxGpus && ((s.wait_mask >> g) & 1u)) {
+      const long long t0 = clock64();
+      while (static_cast<int32_t>(ld_acquire_sys(s.pad + kMaxGpus + g) - e) < 0) {
+        __nanosleep(64);
+        if (static_cast<uint64_t>(clock64() - t0) > s.timeout_cycles) {
+          atomicExch(s.ctr + 2, 1u);
+          break;
+        }
+      }
     }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    s.ctr[1] = 0;
+    __threadfence();
+    atomicExch(s.ctr, e);
   }
 }
 
@@ -137,11 +159,28 @@ __device__ __forceinline__ void copy_range(const unsigned char* __restrict__ src
   }
 }
 
+// Interleaved partition: CTA b takes quanta [q*b/G, q*(b+1)/G) of *every*
+// segment, so each CTA carries the same local/remote mix and finishes with
+// the others whatever the HBM:NVLink speed ratio.
+__device__ __forceinline__ bool cta_share(uint64_t n, uint64_t* a, uint64_t* b) {
+  const uint64_t q = (n + kQuantum - 1) / kQuantum;
+  *a = (q * blockIdx.x / gridDim.x) * kQuantum;
+  const uint64_t e = (q * (blockIdx.x + 1) / gridDim.x) * kQuantum;
+  *b = e < n ? e : n;
+  return *a < *b;
+}
+
 __global__ void __launch_bounds__(512) copy_segments_kernel(const CopySeg* __restrict__ segs, int nseg,
                                                             Partition part, SyncArgs sync) {
   uint32_t epoch;
   const bool ok = epoch_barrier(sync, &epoch);
-  if (ok && nseg > 0) {
+  if (ok && nseg > 0 && part.first_seg == nullptr) {
+    for (int s = 0; s < nseg; ++s) {
+      const CopySeg sg = segs[s];
+      uint64_t a, b;
+      if (cta_share(sg.nbytes, &a, &b)) copy_range(sg.src, sg.dst, a, b);
+    }
+  } else if (ok && nseg > 0) {
     const uint64_t lo = blockIdx.x * part.per_cta, hi = lo + part.per_cta;
     for (int s = part.first_seg[blockIdx.x]; s < nseg; ++s) {
       const CopySeg sg = segs[s];
@@ -260,7 +299,15 @@ __global__ void __launch_bounds__(512) reduce_segments_kernel(const ReduceSeg* _
                                                               Partition part, float beta, SyncArgs sync) {
   uint32_t epoch;
   const bool ok = epoch_barrier(sync, &epoch);
-  if (ok && nseg > 0) {
+  if (ok && nseg > 0 && part.first_seg == nullptr) {
+    for (int s = 0; s < nseg; ++s) {
+      const ReduceSeg sg = segs[s];
+      uint64_t a, b;
+      if (cta_share(sg.nelem, &a, &b))
+        reduce_range<TIn, TOut>(static_cast<TOut*>(sg.dst),
+                                reinterpret_cast<const TIn* const*>(terms + sg.term0), sg.nterms, a, b, beta);
+    }
+  } else if (ok && nseg > 0) {
     const uint64_t lo = blockIdx.x * part.per_cta, hi = lo + part.per_cta;
     for (int s = part.first_seg[blockIdx.x]; s < nseg; ++s) {
       const ReduceSeg sg = segs[s];

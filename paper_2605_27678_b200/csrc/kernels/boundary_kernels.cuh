@@ -33,6 +33,8 @@ struct ReduceSeg {
   int32_t term0;
 };
 
+// first_seg == nullptr selects the interleaved partition (every CTA takes an
+// equal quantum-aligned share of every segment).
 struct Partition {
   const int32_t* first_seg;  // [grid]
   uint64_t per_cta;          // work units per CTA (multiple of kQuantum)
@@ -49,6 +51,7 @@ struct SyncArgs {
   uint32_t* ctr;                  // local: [0] epoch, [1] finished-CTA count, [2] error flag
   uint32_t wait_mask;             // GPUs to wait for
   uint32_t post_mask;             // GPUs to post to
+  int end_sync;                   // push mode: also post/wait "writes done" (pad[32+g]) before exit
   int my_gpu;
   uint64_t timeout_cycles;
 };
