@@ -18,7 +18,6 @@ void ck(cudaError_t e, const char* what) {
 constexpr uint64_t kPadBytes = 4096;
 constexpr uint64_t kAlign = 256;
 uint64_t align_up(uint64_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
-uint64_t pad_q(uint64_t x) { return (x + dev::kQuantum - 1) / dev::kQuantum * dev::kQuantum; }
 }  // namespace
 
 Exec::Exec(const bridge::BridgePlan& plan, const index::SpliceSpec* splice, int n_gpus, int my_gpu,
@@ -213,19 +212,44 @@ const void* Exec::resolve(int rank, int slot, int mb_slot) const {
   return peer_base_[g] + offset_of(g, rank, slot, mb_slot);
 }
 
-bool Exec::interleave(size_t nseg, int grid) const {
-  if (cfg_.partition == 1) return false;
-  if (cfg_.partition == 2) return true;
-  (void)nseg;
-  (void)grid;
-  return false;  // auto: contiguous ranges (measured faster on HBM-bound launches)
+namespace {
+constexpr uint64_t kDynCopyChunk = 128 * 1024;   // bytes per dynamic copy chunk
+constexpr uint64_t kDynReduceChunk = 32 * 1024;  // elements per dynamic reduce chunk
+uint64_t pad_to(uint64_t x, uint64_t q) { return (x + q - 1) / q * q; }
+}  // namespace
+
+int Exec::copy_mode() const {
+  switch (cfg_.partition) {
+    case 2: return dev::kPartInterleaved;
+    case 3: return dev::kPartDynamic;
+    case 4: return dev::kPartTma;
+    default: return dev::kPartContiguous;  // 0 auto / 1 contiguous
+  }
 }
 
-void Exec::build_partition(const std::vector<uint64_t>& w0, const std::vector<uint64_t>& n, int grid,
-                           DevPartition* out) {
+int Exec::reduce_mode() const {
+  const int m = copy_mode();
+  return m == dev::kPartTma ? dev::kPartDynamic : m;
+}
+
+uint64_t Exec::pad_unit(int mode, bool copy) const {
+  if (mode == dev::kPartTma) return dev::tma_chunk_bytes();
+  if (mode == dev::kPartDynamic) return copy ? kDynCopyChunk : kDynReduceChunk;
+  return dev::kQuantum;
+}
+
+void Exec::build_partition(const std::vector<uint64_t>& w0, const std::vector<uint64_t>& n, int grid, int mode,
+                           uint64_t unit, DevPartition* out) {
   const uint64_t total = w0.empty() ? 0 : w0.back() + n.back();
-  const uint64_t per_raw = (total + grid - 1) / grid;
-  const uint64_t per = std::max<uint64_t>(dev::kQuantum, pad_q(per_raw));
+  cudaFree(out->first_seg);
+  out->first_seg = nullptr;
+  out->grid = grid;
+  out->mode = mode;
+  out->chunk = unit;
+  out->total_chunks = static_cast<uint32_t>((total + unit - 1) / unit);
+  out->per_cta = 0;
+  if (mode != dev::kPartContiguous) return;
+  const uint64_t per = std::max<uint64_t>(dev::kQuantum, pad_to((total + grid - 1) / grid, dev::kQuantum));
   std::vector<int32_t> first(grid, static_cast<int32_t>(w0.size()));
   size_t s = 0;
   for (int b = 0; b < grid; ++b) {
@@ -233,17 +257,12 @@ void Exec::build_partition(const std::vector<uint64_t>& w0, const std::vector<ui
     while (s < w0.size() && w0[s] + n[s] <= lo) ++s;  // first segment ending after lo
     first[b] = static_cast<int32_t>(s);
   }
-  cudaFree(out->first_seg);
-  out->first_seg = nullptr;
-  out->grid = grid;
-  if (interleave(w0.size(), grid)) return;  // first_seg == nullptr -> interleaved shares
   ck(cudaMalloc(&out->first_seg, grid * sizeof(int32_t)), "cudaMalloc(partition)");
   ck(cudaMemcpy(out->first_seg, first.data(), grid * sizeof(int32_t), cudaMemcpyHostToDevice), "upload");
   out->per_cta = per;
-  out->grid = grid;
 }
 
-void Exec::upload_copies(const std::vector<index::CopySeg>& segs, int mb, dev::CopySeg** out,
+void Exec::upload_copies(const std::vector<index::CopySeg>& segs, int mb, uint64_t unit, dev::CopySeg** out,
                          std::vector<uint64_t>* w0s, std::vector<uint64_t>* ns) {
   std::vector<dev::CopySeg> cs;
   uint64_t w = 0;
@@ -258,7 +277,7 @@ void Exec::upload_copies(const std::vector<index::CopySeg>& segs, int mb, dev::C
                   nbytes, w});
     w0s->push_back(w);
     ns->push_back(nbytes);
-    w = pad_q(w + nbytes);
+    w = pad_to(w + nbytes, unit);
   }
   cudaFree(*out);
   *out = nullptr;
@@ -268,22 +287,30 @@ void Exec::upload_copies(const std::vector<index::CopySeg>& segs, int mb, dev::C
   }
 }
 
+int Exec::copy_grid() const {
+  if (copy_mode() == dev::kPartTma) return sm_count_ * dev::tma_blocks_per_sm();
+  const int occ = dev::copy_blocks_per_sm(cfg_.threads);
+  return sm_count_ * (cfg_.blocks_per_sm > 0 ? std::min(cfg_.blocks_per_sm, occ) : occ);
+}
+
 void Exec::prepare_fwd() {
   if (!dirty_fwd_) return;
+  const int mode = copy_mode();
+  const uint64_t unit = pad_unit(mode, true);
   std::vector<uint64_t> w0s, ns, w0s2, ns2;
   for (int mb = 0; mb < cfg_.mb_slots; ++mb) {
-    upload_copies(fwd_local_, mb, &tables_[mb].copy, &w0s, &ns);
-    upload_copies(fwd_second_local_, mb, &tables_[mb].copy2, &w0s2, &ns2);
+    upload_copies(fwd_local_, mb, unit, &tables_[mb].copy, &w0s, &ns);
+    upload_copies(fwd_second_local_, mb, unit, &tables_[mb].copy2, &w0s2, &ns2);
   }
-  const int bps = cfg_.blocks_per_sm > 0 ? std::min(cfg_.blocks_per_sm, dev::copy_blocks_per_sm(cfg_.threads))
-                                         : dev::copy_blocks_per_sm(cfg_.threads);
-  build_partition(w0s, ns, sm_count_ * bps, &fwd_part_);
-  if (!fwd_second_local_.empty()) build_partition(w0s2, ns2, sm_count_ * bps, &fwd2_part_);
+  build_partition(w0s, ns, copy_grid(), mode, unit, &fwd_part_);
+  if (!fwd_second_local_.empty()) build_partition(w0s2, ns2, copy_grid(), mode, unit, &fwd2_part_);
   dirty_fwd_ = false;
 }
 
 void Exec::prepare_bwd() {
   if (!dirty_bwd_) return;
+  const int mode = reduce_mode();
+  const uint64_t unit = pad_unit(mode, false);
   const int es_in = dev::dtype_size(cfg_.grad_in_dtype), es_out = dev::dtype_size(cfg_.grad_out_dtype);
   std::vector<uint64_t> w0s, ns;
   for (int mb = 0; mb < cfg_.mb_slots; ++mb) {
@@ -306,7 +333,7 @@ void Exec::prepare_bwd() {
       rs.push_back(d);
       w0s.push_back(w);
       ns.push_back(s.n);
-      w = pad_q(w + s.n);
+      w = pad_to(w + s.n, unit);
     }
     cudaFree(T.reduce);
     cudaFree(T.terms);
@@ -323,7 +350,7 @@ void Exec::prepare_bwd() {
   }
   const int occ = dev::reduce_blocks_per_sm(cfg_.threads, cfg_.grad_in_dtype, cfg_.grad_out_dtype);
   const int bps = cfg_.blocks_per_sm > 0 ? std::min(cfg_.blocks_per_sm, occ) : occ;
-  build_partition(w0s, ns, sm_count_ * bps, &bwd_part_);
+  build_partition(w0s, ns, sm_count_ * bps, mode, unit, &bwd_part_);
   dirty_bwd_ = false;
 }
 
@@ -348,7 +375,7 @@ void Exec::forward(int mb, void* stream) {
     raise(ErrorCode::InvalidArgument, "microbatch " + std::to_string(mb) + " forwarded twice without backward");
   prepare_fwd();
   const DevTables& T = tables_[mb % cfg_.mb_slots];
-  dev::launch_copy(T.copy, static_cast<int>(fwd_local_.size()), {fwd_part_.first_seg, fwd_part_.per_cta},
+  dev::launch_copy(T.copy, static_cast<int>(fwd_local_.size()), fwd_part_.dev(),
                    fwd_push_ && n_gpus_ > 1 ? sync_push_ : sync_, {fwd_part_.grid, cfg_.threads}, stream);
   ck(cudaGetLastError(), "copy_segments launch");
   ++launches_;
@@ -357,7 +384,7 @@ void Exec::forward(int mb, void* stream) {
     local.ctr = ctr2_;
     local.my_gpu = my_gpu_;
     dev::launch_copy(T.copy2, static_cast<int>(fwd_second_local_.size()),
-                     {fwd2_part_.first_seg, fwd2_part_.per_cta}, local, {fwd2_part_.grid, cfg_.threads}, stream);
+                     fwd2_part_.dev(), local, {fwd2_part_.grid, cfg_.threads}, stream);
     ck(cudaGetLastError(), "copy_segments (phase 2) launch");
     ++launches_;
   }
@@ -370,7 +397,7 @@ void Exec::backward(int mb, float beta, void* stream) {
   prepare_bwd();
   const DevTables& T = tables_[mb % cfg_.mb_slots];
   dev::launch_reduce(T.reduce, static_cast<int>(bwd_local_.size()), T.terms,
-                     {bwd_part_.first_seg, bwd_part_.per_cta}, cfg_.grad_in_dtype, cfg_.grad_out_dtype, beta,
+                     bwd_part_.dev(), cfg_.grad_in_dtype, cfg_.grad_out_dtype, beta,
                      sync_, {bwd_part_.grid, cfg_.threads}, stream);
   ck(cudaGetLastError(), "reduce_segments launch");
   ++launches_;

@@ -36,7 +36,7 @@ struct ExecConfig {
   int threads = 512;
   double timeout_s = 20.0;          // flag-wait timeout
   int fwd_mode = 0;                 // forward: 0 auto, 1 consumers pull from owners, 2 owners push
-  int partition = 0;                // 0 auto, 1 contiguous ranges per CTA, 2 interleaved shares
+  int partition = 0;                // 0 auto, 1 contiguous, 2 interleaved, 3 dynamic, 4 TMA bulk (copy)
 };
 
 class Exec {
@@ -112,14 +112,21 @@ class Exec {
     int32_t* first_seg = nullptr;
     uint64_t per_cta = 0;
     int grid = 1;
+    int mode = 0;
+    uint32_t total_chunks = 0;
+    uint64_t chunk = 0;
+    dev::Partition dev() const { return {first_seg, per_cta, mode, total_chunks, chunk}; }
   };
   DevPartition fwd_part_, fwd2_part_, bwd_part_;
   uint32_t* ctr2_ = nullptr;  // phase-2 counters (local-only launch)
-  void upload_copies(const std::vector<index::CopySeg>& segs, int mb, dev::CopySeg** out,
+  void upload_copies(const std::vector<index::CopySeg>& segs, int mb, uint64_t unit, dev::CopySeg** out,
                      std::vector<uint64_t>* w0s, std::vector<uint64_t>* ns);
-  void build_partition(const std::vector<uint64_t>& w0, const std::vector<uint64_t>& n, int grid,
-                       DevPartition* out);
-  bool interleave(size_t nseg, int grid) const;
+  int copy_mode() const;
+  int reduce_mode() const;
+  uint64_t pad_unit(int mode, bool copy) const;
+  int copy_grid() const;
+  void build_partition(const std::vector<uint64_t>& w0, const std::vector<uint64_t>& n, int grid, int mode,
+                       uint64_t unit, DevPartition* out);
   bool dirty_fwd_ = true, dirty_bwd_ = true;
   uint32_t* ctr_ = nullptr;  // device counters
   dev::SyncArgs sync_{}, sync_push_{};

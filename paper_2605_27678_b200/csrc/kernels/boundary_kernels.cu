@@ -4,24 +4,28 @@
 //        destination element has exactly one source element (index_map.hpp),
 //        so forward is a persistent gather over (src, dst, bytes) runs whose
 //        sources are local HBM or a peer GPU's HBM mapped over NVSwitch.
-//        128-bit coalesced loads/stores, 4 independent 16 B loads in flight
-//        per thread before any store.
+//        Two engines: (a) LDG/STG.128 with 8 independent 16 B loads in flight
+//        per thread, (b) TMA bulk copies (cp.async.bulk global->smem->global,
+//        mbarrier-tracked, one issuing lane per CTA, 3-stage smem ring).
 // K3/K4  reduce_segments: backward gradient return with fp32 sum-accumulate
 //        (dst = beta*dst + sum of terms in fixed order from +0.0f). Terms are
 //        the cp-replica contributions (or the single owner) pulled from peers.
 //
+// Work split over CTAs (Partition::mode): contiguous ranges with a host-built
+// first-segment table, interleaved equal shares of every segment, or dynamic
+// chunks handed out by an atomic counter (monotone per-CTA segment cursor).
+//
 // Both kernels open with an epoch barrier on peer-mapped flag words (release
 // stores / acquire loads at system scope) so a GPU reads a peer's buffers only
 // after that peer's preceding stream work is done; with one GPU the barrier is
-// compiled in but has empty masks.
+// compiled in but has empty masks. In push mode the last CTA also publishes
+// "writes done" and waits for every writer into this GPU before the kernel ends.
 //
 // Roofline (pure data movement; tensor cores not applicable): time >=
 // max(HBM bytes / HBM BW, NVLink ingress / NVLink BW); see DESIGN.md.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
-
-#include <cstdio>
 
 #include "kernels/boundary_kernels.cuh"
 
@@ -89,10 +93,10 @@ __device__ bool epoch_barrier(const SyncArgs& s, uint32_t* target_out) {
   return ok != 0;
 }
 
-// Last CTA to finish bumps the local epoch. In push mode it first publishes
-// "my writes into your buffers are done" (release, system scope) and waits for
-// every writer into this GPU's buffers, so kernel completion implies the
-// outputs are complete.
+// Last CTA to finish bumps the local epoch (and resets the dynamic work
+// counter). In push mode it first publishes "my writes into your buffers are
+// done" (release, system scope) and waits for every writer into this GPU's
+// buffers, so kernel completion implies the outputs are complete.
 __device__ void epoch_finish(const SyncArgs& s, uint32_t e) {
   __shared__ int last;
   __syncthreads();
@@ -119,8 +123,59 @@ __device__ void epoch_finish(const SyncArgs& s, uint32_t e) {
   }
   if (threadIdx.x == 0) {
     s.ctr[1] = 0;
+    s.ctr[3] = 0;  // dynamic work counter
     __threadfence();
     atomicExch(s.ctr, e);
+  }
+}
+
+// Interleaved partition: CTA b takes quanta [q*b/G, q*(b+1)/G) of a segment.
+__device__ __forceinline__ bool cta_share(uint64_t n, uint64_t* a, uint64_t* b) {
+  const uint64_t q = (n + kQuantum - 1) / kQuantum;
+  *a = (q * blockIdx.x / gridDim.x) * kQuantum;
+  const uint64_t e = (q * (blockIdx.x + 1) / gridDim.x) * kQuantum;
+  *b = e < n ? e : n;
+  return *a < *b;
+}
+
+// Drives `body(seg, a, b)` over this CTA's work under the partition's mode.
+// Segment fields used: w0 (work-space start) and a length accessor.
+template <int MODE, class S, class Len, class Body>
+__device__ __forceinline__ void for_each_share(const S* __restrict__ segs, int nseg, const Partition& part,
+                                               uint32_t* work_ctr, Len len, Body body) {
+  if constexpr (MODE == kPartInterleaved) {
+    for (int s = 0; s < nseg; ++s) {
+      const S sg = segs[s];
+      uint64_t a, b;
+      if (cta_share(len(sg), &a, &b)) body(sg, a, b);
+    }
+  } else if constexpr (MODE == kPartDynamic) {
+    __shared__ uint32_t next;
+    if (threadIdx.x == 0) next = atomicAdd(work_ctr, 1u);
+    __syncthreads();
+    uint32_t c = next;
+    int s = 0;
+    while (c < part.total_chunks) {
+      __syncthreads();
+      if (threadIdx.x == 0) next = atomicAdd(work_ctr, 1u);  // prefetch the next chunk index
+      const uint64_t w = static_cast<uint64_t>(c) * part.chunk;
+      while (segs[s].w0 + len(segs[s]) <= w) ++s;  // chunks are handed out in increasing order
+      const S sg = segs[s];
+      const uint64_t a = w - sg.w0, e = a + part.chunk, n = len(sg);
+      body(sg, a, e < n ? e : n);
+      __syncthreads();
+      c = next;
+    }
+  } else {
+    const uint64_t lo = blockIdx.x * part.per_cta, hi = lo + part.per_cta;
+    for (int s = part.first_seg[blockIdx.x]; s < nseg; ++s) {
+      const S sg = segs[s];
+      if (sg.w0 >= hi) break;
+      const uint64_t a = (lo > sg.w0 ? lo : sg.w0) - sg.w0;
+      const uint64_t e = sg.w0 + len(sg);
+      const uint64_t b = (hi < e ? hi : e) - sg.w0;
+      if (a < b) body(sg, a, b);
+    }
   }
 }
 
@@ -159,37 +214,135 @@ __device__ __forceinline__ void copy_range(const unsigned char* __restrict__ src
   }
 }
 
-// Interleaved partition: CTA b takes quanta [q*b/G, q*(b+1)/G) of *every*
-// segment, so each CTA carries the same local/remote mix and finishes with
-// the others whatever the HBM:NVLink speed ratio.
-__device__ __forceinline__ bool cta_share(uint64_t n, uint64_t* a, uint64_t* b) {
-  const uint64_t q = (n + kQuantum - 1) / kQuantum;
-  *a = (q * blockIdx.x / gridDim.x) * kQuantum;
-  const uint64_t e = (q * (blockIdx.x + 1) / gridDim.x) * kQuantum;
-  *b = e < n ? e : n;
-  return *a < *b;
-}
+struct CopyLen {
+  __device__ uint64_t operator()(const CopySeg& s) const { return s.nbytes; }
+};
 
-__global__ void __launch_bounds__(512) copy_segments_kernel(const CopySeg* __restrict__ segs, int nseg,
+template <int MODE>
+__global__ void __launch_bounds__(512, 2) copy_segments_kernel(const CopySeg* __restrict__ segs, int nseg,
                                                             Partition part, SyncArgs sync) {
   uint32_t epoch;
   const bool ok = epoch_barrier(sync, &epoch);
-  if (ok && nseg > 0 && part.first_seg == nullptr) {
-    for (int s = 0; s < nseg; ++s) {
-      const CopySeg sg = segs[s];
-      uint64_t a, b;
-      if (cta_share(sg.nbytes, &a, &b)) copy_range(sg.src, sg.dst, a, b);
+  if (ok && nseg > 0)
+    for_each_share<MODE>(segs, nseg, part, sync.ctr + 3, CopyLen{},
+                   [](const CopySeg& sg, uint64_t a, uint64_t b) { copy_range(sg.src, sg.dst, a, b); });
+  epoch_finish(sync, epoch);
+}
+
+// ---- TMA bulk-copy engine ------------------------------------------------------
+
+constexpr int kTmaStages = 3;
+constexpr uint32_t kTmaStageBytes = 32 * 1024;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra W;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(smem)),
+      "l"(gmem), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_s2g(void* gmem, const void* smem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gmem), "r"(smem_u32(smem)),
+               "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+// One warp per CTA; lane 0 issues TMA bulk copies through a kTmaStages ring of
+// 32 KiB shared-memory stages: loads for the next stages are in flight while
+// the current stage is stored. Chunks (= one stage) come from the dynamic work
+// counter; unaligned runs fall back to the warp-wide LDG/STG path.
+__global__ void __launch_bounds__(32) copy_segments_tma_kernel(const CopySeg* __restrict__ segs, int nseg,
+                                                               Partition part, SyncArgs sync) {
+  extern __shared__ __align__(128) unsigned char stage_mem[];
+  __shared__ __align__(8) uint64_t full[kTmaStages];
+  uint32_t epoch;
+  const bool ok = epoch_barrier(sync, &epoch);
+  if (ok && nseg > 0) {
+    if (threadIdx.x == 0) {
+      for (int i = 0; i < kTmaStages; ++i) mbar_init(&full[i]);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-  } else if (ok && nseg > 0) {
-    const uint64_t lo = blockIdx.x * part.per_cta, hi = lo + part.per_cta;
-    for (int s = part.first_seg[blockIdx.x]; s < nseg; ++s) {
-      const CopySeg sg = segs[s];
-      if (sg.w0 >= hi) break;
-      const uint64_t a = (lo > sg.w0 ? lo : sg.w0) - sg.w0;
-      const uint64_t e = sg.w0 + sg.nbytes;
-      const uint64_t b = (hi < e ? hi : e) - sg.w0;
-      if (a < b) copy_range(sg.src, sg.dst, a, b);
+    __syncwarp();
+    if (threadIdx.x == 0) {
+      // chunk k lives in stage k % kTmaStages; its barrier phase is (k / kTmaStages) & 1
+      unsigned char* pend_dst[kTmaStages];
+      uint32_t pend_bytes[kTmaStages];
+      int s = 0;
+      uint32_t issued = 0;
+      bool more = true;
+      auto issue = [&]() {  // claim the next chunk and start its global->smem load
+        while (more) {
+          const uint32_t c = atomicAdd(sync.ctr + 3, 1u);
+          if (c >= part.total_chunks) {
+            more = false;
+            return;
+          }
+          const uint64_t w = static_cast<uint64_t>(c) * part.chunk;
+          while (segs[s].w0 + segs[s].nbytes <= w) ++s;
+          const CopySeg sg = segs[s];
+          const uint64_t a = w - sg.w0;
+          const uint64_t e = a + part.chunk < sg.nbytes ? a + part.chunk : sg.nbytes;
+          const uint32_t bytes = static_cast<uint32_t>(e - a);
+          const uint64_t al =
+              reinterpret_cast<uint64_t>(sg.src + a) | reinterpret_cast<uint64_t>(sg.dst + a) | bytes;
+          if (al & 15) {  // rare unaligned run: plain byte copy by this lane
+            for (uint64_t i = a; i < e; ++i) sg.dst[i] = sg.src[i];
+            continue;
+          }
+          const int st = issued % kTmaStages;
+          mbar_expect(&full[st], bytes);
+          bulk_g2s(stage_mem + st * kTmaStageBytes, sg.src + a, bytes, &full[st]);
+          pend_dst[st] = sg.dst + a;
+          pend_bytes[st] = bytes;
+          ++issued;
+          return;
+        }
+      };
+      for (int i = 0; i < kTmaStages; ++i) issue();
+      for (uint32_t k = 0; k < issued; ++k) {
+        const int st = k % kTmaStages;
+        mbar_wait(&full[st], (k / kTmaStages) & 1u);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        bulk_s2g(pend_dst[st], stage_mem + st * kTmaStageBytes, pend_bytes[st]);
+        if (k >= 1 && more) {
+          bulk_wait_read<1>();  // store k-1 has finished reading its stage
+          issue();              // chunk k-1+kTmaStages reuses stage (k-1) % kTmaStages
+        }
+      }
+      bulk_wait_all();
     }
+    __syncwarp();
   }
   epoch_finish(sync, epoch);
 }
@@ -293,33 +446,23 @@ __device__ __forceinline__ void reduce_range(TOut* __restrict__ dst, const TIn* 
   }
 }
 
-template <class TIn, class TOut>
-__global__ void __launch_bounds__(512) reduce_segments_kernel(const ReduceSeg* __restrict__ segs, int nseg,
+struct ReduceLen {
+  __device__ uint64_t operator()(const ReduceSeg& s) const { return s.nelem; }
+};
+
+template <class TIn, class TOut, int MODE>
+__global__ void __launch_bounds__(512, 2) reduce_segments_kernel(const ReduceSeg* __restrict__ segs, int nseg,
                                                               const void* const* __restrict__ terms,
                                                               Partition part, float beta, SyncArgs sync) {
   uint32_t epoch;
   const bool ok = epoch_barrier(sync, &epoch);
-  if (ok && nseg > 0 && part.first_seg == nullptr) {
-    for (int s = 0; s < nseg; ++s) {
-      const ReduceSeg sg = segs[s];
-      uint64_t a, b;
-      if (cta_share(sg.nelem, &a, &b))
-        reduce_range<TIn, TOut>(static_cast<TOut*>(sg.dst),
-                                reinterpret_cast<const TIn* const*>(terms + sg.term0), sg.nterms, a, b, beta);
-    }
-  } else if (ok && nseg > 0) {
-    const uint64_t lo = blockIdx.x * part.per_cta, hi = lo + part.per_cta;
-    for (int s = part.first_seg[blockIdx.x]; s < nseg; ++s) {
-      const ReduceSeg sg = segs[s];
-      if (sg.w0 >= hi) break;
-      const uint64_t a = (lo > sg.w0 ? lo : sg.w0) - sg.w0;
-      const uint64_t e = sg.w0 + sg.nelem;
-      const uint64_t b = (hi < e ? hi : e) - sg.w0;
-      if (a < b)
-        reduce_range<TIn, TOut>(static_cast<TOut*>(sg.dst),
-                                reinterpret_cast<const TIn* const*>(terms + sg.term0), sg.nterms, a, b, beta);
-    }
-  }
+  if (ok && nseg > 0)
+    for_each_share<MODE>(segs, nseg, part, sync.ctr + 3, ReduceLen{},
+                   [&](const ReduceSeg& sg, uint64_t a, uint64_t b) {
+                     reduce_range<TIn, TOut>(static_cast<TOut*>(sg.dst),
+                                             reinterpret_cast<const TIn* const*>(terms + sg.term0), sg.nterms,
+                                             a, b, beta);
+                   });
   epoch_finish(sync, epoch);
 }
 
@@ -334,25 +477,53 @@ int device_sm_count() {
 
 int copy_blocks_per_sm(int threads) {
   int n = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, copy_segments_kernel, threads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, copy_segments_kernel<kPartContiguous>, threads, 0);
   return n > 0 ? n : 1;
 }
 
+int tma_blocks_per_sm() {
+  static int n = -1;
+  if (n < 0) {
+    const int smem = kTmaStages * kTmaStageBytes;
+    cudaFuncSetAttribute(copy_segments_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, copy_segments_tma_kernel, 32, smem);
+    if (n < 1) n = 1;
+  }
+  return n;
+}
+
+uint64_t tma_chunk_bytes() { return kTmaStageBytes; }
+
 void launch_copy(const CopySeg* segs, int nseg, Partition part, const SyncArgs& sync, LaunchCfg cfg,
                  void* stream) {
-  copy_segments_kernel<<<cfg.grid, cfg.block, 0, static_cast<cudaStream_t>(stream)>>>(segs, nseg, part, sync);
+  auto st = static_cast<cudaStream_t>(stream);
+  if (part.mode == kPartTma) {
+    tma_blocks_per_sm();
+    copy_segments_tma_kernel<<<cfg.grid, 32, kTmaStages * kTmaStageBytes, st>>>(segs, nseg, part, sync);
+  } else if (part.mode == kPartInterleaved) {
+    copy_segments_kernel<kPartInterleaved><<<cfg.grid, cfg.block, 0, st>>>(segs, nseg, part, sync);
+  } else if (part.mode == kPartDynamic) {
+    copy_segments_kernel<kPartDynamic><<<cfg.grid, cfg.block, 0, st>>>(segs, nseg, part, sync);
+  } else {
+    copy_segments_kernel<kPartContiguous><<<cfg.grid, cfg.block, 0, st>>>(segs, nseg, part, sync);
+  }
 }
 
 template <class TIn, class TOut>
 static void launch_reduce_t(const ReduceSeg* segs, int nseg, const void* const* terms, Partition part,
                             float beta, const SyncArgs& sync, int grid, int block, cudaStream_t st) {
-  reduce_segments_kernel<TIn, TOut><<<grid, block, 0, st>>>(segs, nseg, terms, part, beta, sync);
+  if (part.mode == kPartInterleaved)
+    reduce_segments_kernel<TIn, TOut, kPartInterleaved><<<grid, block, 0, st>>>(segs, nseg, terms, part, beta, sync);
+  else if (part.mode == kPartDynamic)
+    reduce_segments_kernel<TIn, TOut, kPartDynamic><<<grid, block, 0, st>>>(segs, nseg, terms, part, beta, sync);
+  else
+    reduce_segments_kernel<TIn, TOut, kPartContiguous><<<grid, block, 0, st>>>(segs, nseg, terms, part, beta, sync);
 }
 
 template <class TIn, class TOut>
 static int occ_t(int threads) {
   int n = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, reduce_segments_kernel<TIn, TOut>, threads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, reduce_segments_kernel<TIn, TOut, kPartContiguous>, threads, 0);
   return n > 0 ? n : 1;
 }
 

@@ -33,11 +33,20 @@ struct ReduceSeg {
   int32_t term0;
 };
 
-// first_seg == nullptr selects the interleaved partition (every CTA takes an
-// equal quantum-aligned share of every segment).
+// How a launch's work space is split over CTAs.
+enum PartMode : int {
+  kPartContiguous = 0,   // CTA b owns [b*per_cta, (b+1)*per_cta); first_seg[b] precomputed
+  kPartInterleaved = 1,  // every CTA takes an equal quantum-aligned share of every segment
+  kPartDynamic = 2,      // `chunk`-sized pieces handed out by an atomic counter (ctr[3])
+  kPartTma = 3,          // dynamic chunks moved by TMA bulk copies (copy kernel only)
+};
+
 struct Partition {
-  const int32_t* first_seg;  // [grid]
-  uint64_t per_cta;          // work units per CTA (multiple of kQuantum)
+  const int32_t* first_seg;  // [grid] (contiguous mode)
+  uint64_t per_cta;          // work units per CTA (contiguous mode; multiple of kQuantum)
+  int mode;
+  uint32_t total_chunks;     // dynamic / TMA modes
+  uint64_t chunk;            // dynamic / TMA chunk size (segments are padded to it)
 };
 
 // Cross-GPU epoch barrier over peer-mapped flag words. Every GPU of an exec
@@ -69,6 +78,8 @@ void launch_reduce(const ReduceSeg* segs, int nseg, const void* const* terms, Pa
                    void* stream);
 int device_sm_count();
 int copy_blocks_per_sm(int threads);
+int tma_blocks_per_sm();
+uint64_t tma_chunk_bytes();
 int reduce_blocks_per_sm(int threads, int in_dtype, int out_dtype);
 
 }  // namespace hb::dev

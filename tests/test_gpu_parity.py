@@ -35,7 +35,7 @@ def o_layout(l):
     return O.Layout(l.name, l.tp, l.cp, l.pp, l.dp, l.rank_offset)
 
 
-def run_case(cfg, seed=0, beta=0.0, perturb=True):
+def run_case(cfg, seed=0, beta=0.0, perturb=True, partition=0):
     """Fill every resident rank's inputs, run fwd+bwd on the device, compare with the oracle."""
     _require_gpu()
     rng = np.random.default_rng(seed)
@@ -46,7 +46,7 @@ def run_case(cfg, seed=0, beta=0.0, perturb=True):
         s = cfg.splice
         sp = hbb.SpliceSpec(s["Q"], s["S"], cfg.hidden, cfg.tokens, s["codes"], s["text_mode"])
     rt = hbb.BridgeRuntime(plan, sp, act_dtype=TDT[cfg.act], grad_in_dtype=TDT[cfg.grad_in],
-                           grad_out_dtype=TDT[cfg.grad_out])
+                           grad_out_dtype=TDT[cfg.grad_out], partition=partition)
     src, dst = o_layout(cfg.src), o_layout(cfg.dst)
     B = cfg.batch
     SI, DI = O.intervals(B, src.dp), O.intervals(B, dst.dp)
@@ -141,6 +141,21 @@ def run_case(cfg, seed=0, beta=0.0, perturb=True):
 @pytest.mark.parametrize("beta", [0.0, 1.0])
 def test_configs_scaled_vs_oracle(name, beta):
     run_case(configs.get(name, scale=64), seed=hash(name) % 1000, beta=beta)
+
+
+@pytest.mark.parametrize("partition", [1, 2, 3, 4])
+@pytest.mark.parametrize("name", ["c2", "c4", "c5"])
+def test_partition_modes_vs_oracle(name, partition):
+    """Every CTA work split (contiguous, interleaved, dynamic, TMA bulk) gives identical results."""
+    run_case(configs.get(name, scale=64), seed=7, beta=1.0, partition=partition)
+
+
+def test_odd_width_all_partition_modes():
+    for partition in (1, 2, 3, 4):
+        cfg = configs.get("c2", scale=64)
+        cfg.tokens, cfg.hidden = 1, 3
+        cfg.act = cfg.grad_in = cfg.grad_out = "fp32"
+        run_case(cfg, seed=3, beta=1.0, partition=partition)
 
 
 def test_reference_layout_splice_vs_oracle():
