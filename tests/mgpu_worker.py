@@ -45,7 +45,8 @@ def run(name, rank, N, dev, steps=3):
     local = [r for r in range(plan.world) if r2g[r] == rank]
     rt = hbb.BridgeRuntime(plan, sp, n_gpus=N, my_gpu=rank, rank_to_gpu=r2g, act_dtype=torch.bfloat16,
                            grad_in_dtype=torch.bfloat16, grad_out_dtype=torch.float32, timeout_s=30.0,
-                           fwd_mode=int(os.environ.get("HB_FWD_MODE", "0")))
+                           fwd_mode=int(os.environ.get("HB_FWD_MODE", "0")),
+                           partition=int(os.environ.get("HB_PARTITION", "0")))
     rt.exchange_handles()
     src, dst = o_layout(cfg.src), o_layout(cfg.dst)
     B, W = cfg.batch, cfg.width
