@@ -132,6 +132,7 @@ Exec::~Exec() {
   }
   cudaFree(fwd_part_.first_seg);
   cudaFree(fwd2_part_.first_seg);
+  for (auto* p : {&fwd_part_, &fwd2_part_, &bwd_part_}) cudaFree(p->chunks);
   for (auto& t : tables_) cudaFree(t.copy2);
   cudaFree(ctr2_);
   cudaFree(bwd_part_.first_seg);
@@ -248,6 +249,28 @@ void Exec::build_partition(const std::vector<uint64_t>& w0, const std::vector<ui
   out->chunk = unit;
   out->total_chunks = static_cast<uint32_t>((total + unit - 1) / unit);
   out->per_cta = 0;
+  cudaFree(out->chunks);
+  out->chunks = nullptr;
+  if (mode == dev::kPartDynamic || mode == dev::kPartTma) {
+    // Hand-out order: chunk j of segment s gets key (j + 0.5) / chunks(s), so all
+    // segments advance at the same fractional pace; ties keep segment order.
+    std::vector<std::pair<double, uint2>> order;
+    for (size_t s = 0; s < n.size(); ++s) {
+      const uint64_t k = (n[s] + unit - 1) / unit;
+      for (uint64_t j = 0; j < k; ++j)
+        order.push_back({(j + 0.5) / static_cast<double>(k), make_uint2(static_cast<unsigned>(s), static_cast<unsigned>(j))});
+    }
+    std::stable_sort(order.begin(), order.end(),
+                     [](const auto& a, const auto& b) { return a.first < b.first; });
+    std::vector<uint2> table(order.size());
+    for (size_t i = 0; i < order.size(); ++i) table[i] = order[i].second;
+    out->total_chunks = static_cast<uint32_t>(table.size());
+    if (!table.empty()) {
+      ck(cudaMalloc(&out->chunks, table.size() * sizeof(uint2)), "cudaMalloc(chunk table)");
+      ck(cudaMemcpy(out->chunks, table.data(), table.size() * sizeof(uint2), cudaMemcpyHostToDevice), "upload");
+    }
+    return;
+  }
   if (mode != dev::kPartContiguous) return;
   const uint64_t per = std::max<uint64_t>(dev::kQuantum, pad_to((total + grid - 1) / grid, dev::kQuantum));
   std::vector<int32_t> first(grid, static_cast<int32_t>(w0.size()));

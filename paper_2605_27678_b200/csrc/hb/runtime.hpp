@@ -115,7 +115,8 @@ class Exec {
     int mode = 0;
     uint32_t total_chunks = 0;
     uint64_t chunk = 0;
-    dev::Partition dev() const { return {first_seg, per_cta, mode, total_chunks, chunk}; }
+    uint2* chunks = nullptr;
+    dev::Partition dev() const { return {first_seg, per_cta, mode, total_chunks, chunk, chunks}; }
   };
   DevPartition fwd_part_, fwd2_part_, bwd_part_;
   uint32_t* ctr2_ = nullptr;  // phase-2 counters (local-only launch)

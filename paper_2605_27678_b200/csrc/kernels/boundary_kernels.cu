@@ -154,14 +154,12 @@ __device__ __forceinline__ void for_each_share(const S* __restrict__ segs, int n
     if (threadIdx.x == 0) next = atomicAdd(work_ctr, 1u);
     __syncthreads();
     uint32_t c = next;
-    int s = 0;
     while (c < part.total_chunks) {
       __syncthreads();
       if (threadIdx.x == 0) next = atomicAdd(work_ctr, 1u);  // prefetch the next chunk index
-      const uint64_t w = static_cast<uint64_t>(c) * part.chunk;
-      while (segs[s].w0 + len(segs[s]) <= w) ++s;  // chunks are handed out in increasing order
-      const S sg = segs[s];
-      const uint64_t a = w - sg.w0, e = a + part.chunk, n = len(sg);
+      const uint2 t = part.chunks[c];                         // (segment, chunk within segment)
+      const S sg = segs[t.x];
+      const uint64_t a = static_cast<uint64_t>(t.y) * part.chunk, e = a + part.chunk, n = len(sg);
       body(sg, a, e < n ? e : n);
       __syncthreads();
       c = next;
@@ -298,7 +296,6 @@ __global__ void __launch_bounds__(32) copy_segments_tma_kernel(const CopySeg* __
       // chunk k lives in stage k % kTmaStages; its barrier phase is (k / kTmaStages) & 1
       unsigned char* pend_dst[kTmaStages];
       uint32_t pend_bytes[kTmaStages];
-      int s = 0;
       uint32_t issued = 0;
       bool more = true;
       auto issue = [&]() {  // claim the next chunk and start its global->smem load
@@ -308,10 +305,9 @@ __global__ void __launch_bounds__(32) copy_segments_tma_kernel(const CopySeg* __
             more = false;
             return;
           }
-          const uint64_t w = static_cast<uint64_t>(c) * part.chunk;
-          while (segs[s].w0 + segs[s].nbytes <= w) ++s;
-          const CopySeg sg = segs[s];
-          const uint64_t a = w - sg.w0;
+          const uint2 t = part.chunks[c];
+          const CopySeg sg = segs[t.x];
+          const uint64_t a = static_cast<uint64_t>(t.y) * part.chunk;
           const uint64_t e = a + part.chunk < sg.nbytes ? a + part.chunk : sg.nbytes;
           const uint32_t bytes = static_cast<uint32_t>(e - a);
           const uint64_t al =

@@ -3,6 +3,8 @@
 
 #include <cstdint>
 
+#include <vector_types.h>
+
 namespace hb::dev {
 
 enum Dtype : int { kBF16 = 0, kFP16 = 1, kFP32 = 2, kFP64 = 3 };
@@ -37,7 +39,9 @@ struct ReduceSeg {
 enum PartMode : int {
   kPartContiguous = 0,   // CTA b owns [b*per_cta, (b+1)*per_cta); first_seg[b] precomputed
   kPartInterleaved = 1,  // every CTA takes an equal quantum-aligned share of every segment
-  kPartDynamic = 2,      // `chunk`-sized pieces handed out by an atomic counter (ctr[3])
+  kPartDynamic = 2,      // `chunk`-sized pieces handed out by an atomic counter (ctr[3]) in the
+                         // order of a host-built table that advances every segment at the
+                         // same fractional pace (local HBM and remote NVLink runs overlap)
   kPartTma = 3,          // dynamic chunks moved by TMA bulk copies (copy kernel only)
 };
 
@@ -46,7 +50,8 @@ struct Partition {
   uint64_t per_cta;          // work units per CTA (contiguous mode; multiple of kQuantum)
   int mode;
   uint32_t total_chunks;     // dynamic / TMA modes
-  uint64_t chunk;            // dynamic / TMA chunk size (segments are padded to it)
+  uint64_t chunk;            // dynamic / TMA chunk size
+  const uint2* chunks;       // [total_chunks] (segment, chunk within segment), in hand-out order
 };
 
 // Cross-GPU epoch barrier over peer-mapped flag words. Every GPU of an exec
