@@ -40,7 +40,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--config", default="c2")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--blocks-per-sm", type=int, default=0)
@@ -80,9 +80,27 @@ def make_splice(cfg):
     return hbb.SpliceSpec(s["Q"], s["S"], cfg.hidden, cfg.tokens, s["codes"], s["text_mode"])
 
 
+def _union_len(ivs):
+    tot, cur_s, cur_e = 0, None, None
+    for s, e in sorted(ivs):
+        if cur_e is None or s > cur_e:
+            if cur_e is not None:
+                tot += cur_e - cur_s
+            cur_s, cur_e = s, e
+        else:
+            cur_e = max(cur_e, e)
+    return tot + (cur_e - cur_s if cur_e is not None else 0)
+
+
 def traffic_model(cfg, n_gpus):
-    """Per-GPU algorithmic bytes from the index map: HBM reads+writes (incl. bytes
-    served to peers and the fp32 accumulator read-modify-write) and NVLink ingress."""
+    """Per-GPU *minimum* bytes from the index map (the roofline's algorithmic bytes).
+
+    HBM(g) = destination writes on g (x2 for the beta=1 fp32 read-modify-write)
+           + each distinct source element read once per consuming GPU (by the owner,
+             whether the consumer is local or a peer).
+    NVL(g) = distinct remote source elements consumed by g (NVLink ingress).
+    A kernel that re-reads the same source for several consumers on one GPU is
+    charged against this minimum, never credited for it."""
     from paper_2605_27678_b200 import bridge as hbb
     from paper_2605_27678_b200 import configs
 
@@ -91,27 +109,28 @@ def traffic_model(cfg, n_gpus):
     r2g = configs.rank_to_gpu(plan.world, n_gpus)
     a, gi, go = DT_SIZE[cfg.act], DT_SIZE[cfg.grad_in], DT_SIZE[cfg.grad_out]
     z = lambda: [0] * n_gpus  # noqa: E731
-    f_hbm, f_nvl, b_hbm, b_nvl = z(), z(), z(), z()
-    seen = set()  # remote runs cross NVLink once per consuming GPU, then fan out locally
+    out = {"fwd_hbm": z(), "fwd_nvl": z(), "bwd_hbm": z(), "bwd_nvl": z()}
+
+    def account(kind, reads, esize):
+        # reads: {(reader_gpu, src_rank, src_slot): [(start, end), ...]} in elements
+        for (g_rd, sr, ss), ivs in reads.items():
+            nbytes = _union_len(ivs) * esize
+            out[kind + "_hbm"][r2g[sr]] += nbytes
+            if r2g[sr] != g_rd:
+                out[kind + "_nvl"][g_rd] += nbytes
+
+    reads = {}
     for (sr, ss, so, dr, ds, do, n) in hbb.index_forward(plan, sp):
-        g_src, g_dst = r2g[sr], r2g[dr]
-        f_hbm[g_dst] += n * a            # write
-        key = (sr, ss, so, n, g_dst)
-        if g_src != g_dst and key in seen:
-            f_hbm[g_dst] += n * a        # local re-read of the first consumer's copy
-            continue
-        seen.add(key)
-        f_hbm[g_src] += n * a            # read at the owner (local or served to a peer)
-        if g_src != g_dst:
-            f_nvl[g_dst] += n * a
+        out["fwd_hbm"][r2g[dr]] += n * a  # write
+        reads.setdefault((r2g[dr], sr, ss), []).append((so, so + n))
+    account("fwd", reads, a)
+    reads = {}
     for (dr, ds, do, n, terms) in hbb.index_backward(plan, sp):
-        g_dst = r2g[dr]
-        b_hbm[g_dst] += n * go * (2 if cfg.beta else 1)
+        out["bwd_hbm"][r2g[dr]] += n * go * (2 if cfg.beta else 1)
         for (tr, ts, to) in terms:
-            b_hbm[r2g[tr]] += n * gi
-            if r2g[tr] != g_dst:
-                b_nvl[g_dst] += n * gi
-    return {"fwd_hbm": f_hbm, "fwd_nvl": f_nvl, "bwd_hbm": b_hbm, "bwd_nvl": b_nvl}
+            reads.setdefault((r2g[dr], tr, ts), []).append((to, to + n))
+    account("bwd", reads, gi)
+    return out
 
 
 def peaks():
@@ -303,6 +322,8 @@ def main():
     tm = traffic_model(cfg, N)
     per_gpu_step = tm["fwd_hbm"][rank] + tm["bwd_hbm"][rank]
     slots = args.slots or max(1, min(8, math.ceil(3 * L2_BYTES / max(per_gpu_step, 1))))
+    if not args.no_e2e:
+        slots = max(slots, 2)  # the pipelined e2e leg alternates two buffer sets
 
     rt = hbb.BridgeRuntime(plan, sp, n_gpus=N, my_gpu=rank, rank_to_gpu=r2g, act_dtype=tdt[cfg.act],
                            grad_in_dtype=tdt[cfg.grad_in], grad_out_dtype=tdt[cfg.grad_out],
@@ -497,46 +518,89 @@ def _cpu_model():
 
 def run_e2e(args, cfg, rt, local, stream, N, dev, barrier, payload, slots):
     """Same metric through the public API with pinned HOST buffers: every step
-    copies its inputs host->device (source shards, destination gradients, text),
-    runs forward+backward, and reads the outputs back (destination shards and
-    source gradients), all inside the timed region."""
+    copies its inputs host->device (source shards, text, destination gradients),
+    runs forward+backward, and reads both outputs back (destination shards and
+    source gradients), all inside the timed region.
+
+    Steps are software-pipelined over 3 streams (H2D, boundary, D2H) and 2 buffer
+    sets so PCIe runs full duplex. Reuse rules: inputs of a
+    set are overwritten only after this GPU's *next* boundary op completed (its
+    epoch barrier proves every peer finished reading them); outputs are
+    overwritten only after their D2H copy finished."""
     import torch
 
     from paper_2605_27678_b200 import bridge as hbb
 
-    ins, outs = [], []
-    for r in local:
-        for slot in (hbb.SLOT_SRC_ACT, hbb.SLOT_TEXT, hbb.SLOT_DST_GRAD):
-            b = rt.buffer(r, slot, 0)
-            if b is not None:
-                ins.append((slot, b, torch.empty(b.shape, dtype=b.dtype, pin_memory=True).copy_(b.cpu())))
-        for slot in (hbb.SLOT_DST_ACT, hbb.SLOT_SRC_GRAD):
-            b = rt.buffer(r, slot, 0)
-            if b is not None:
-                outs.append((b, torch.empty(b.shape, dtype=b.dtype, pin_memory=True)))
-    h2d = sum(h.numel() * h.element_size() for _, _, h in ins)
-    d2h = sum(h.numel() * h.element_size() for _, h in outs)
-    K = max(1, args.e2e_steps)
-    mb = 10_000_000
-    slot_mb = lambda m: m - (m % slots)  # noqa: E731  (always buffer set 0)
+    S = 2 if slots >= 2 else 1
+    fwd_in, bwd_in, outs = [], [], []
+    host_in = {}
+    for k in range(S):
+        fi, bi, oo = [], [], []
+        for r in local:
+            for slot in (hbb.SLOT_SRC_ACT, hbb.SLOT_TEXT, hbb.SLOT_DST_GRAD):
+                b = rt.buffer(r, slot, k)
+                if b is None:
+                    continue
+                key = (r, slot)
+                if key not in host_in:
+                    host_in[key] = torch.empty(b.shape, dtype=b.dtype, pin_memory=True).copy_(b.cpu())
+                (bi if slot == hbb.SLOT_DST_GRAD else fi).append((b, host_in[key]))
+            for slot in (hbb.SLOT_DST_ACT, hbb.SLOT_SRC_GRAD):
+                b = rt.buffer(r, slot, k)
+                if b is not None:
+                    oo.append((b, torch.empty(b.shape, dtype=b.dtype, pin_memory=True)))
+        fwd_in.append(fi)
+        bwd_in.append(bi)
+        outs.append(oo)
+    h2d = sum(h.numel() * h.element_size() for _, h in fwd_in[0] + bwd_in[0])
+    d2h = sum(h.numel() * h.element_size() for _, h in outs[0])
+    K = max(2, args.e2e_steps)
+    s_h2d, s_d2h = torch.cuda.Stream(), torch.cuda.Stream()
+    ev = lambda: torch.cuda.Event()  # noqa: E731
+    fwd_done = [None] * K
+    bwd_done = [None] * K
+    d2h_done = [None] * K
+    base = 20_000_000
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with torch.cuda.stream(stream):
-        e0.record(stream)
-        for i in range(K):
-            m = slot_mb(mb + i * slots)
-            for slot, b, h in ins:
-                if slot != hbb.SLOT_DST_GRAD:
-                    b.copy_(h, non_blocking=True)
-            rt.forward(m, stream)
-            for slot, b, h in ins:
-                if slot == hbb.SLOT_DST_GRAD:
-                    b.copy_(h, non_blocking=True)
-            rt.backward(m, cfg.beta, stream)
-            for b, h in outs:
+    e0.record(s_h2d)
+    stream.wait_stream(s_h2d)
+    s_d2h.wait_stream(s_h2d)
+    for i in range(K):
+        k = i % S
+        mb = base + i  # base % S == 0, so mb % S == k selects buffer set k
+        h_src, h_grad = ev(), ev()
+        with torch.cuda.stream(s_h2d):
+            if i >= S:
+                s_h2d.wait_event(bwd_done[i - S])   # op after fwd_{i-S}: everyone read set k's sources
+            for b, h in fwd_in[k]:
+                b.copy_(h, non_blocking=True)
+            h_src.record(s_h2d)
+            if i >= S:
+                s_h2d.wait_event(fwd_done[i - S + 1])  # op after bwd_{i-S}: everyone read set k's grads
+            for b, h in bwd_in[k]:
+                b.copy_(h, non_blocking=True)
+            h_grad.record(s_h2d)
+        stream.wait_event(h_src)
+        if i >= S:
+            stream.wait_event(d2h_done[i - S])      # outputs of set k already read back
+        rt.forward(mb, stream)
+        fwd_done[i] = ev()
+        fwd_done[i].record(stream)
+        stream.wait_event(h_grad)
+        rt.backward(mb, cfg.beta, stream)
+        bwd_done[i] = ev()
+        bwd_done[i].record(stream)
+        with torch.cuda.stream(s_d2h):
+            s_d2h.wait_event(bwd_done[i])
+            for b, h in outs[k]:
                 h.copy_(b, non_blocking=True)
-        e1.record(stream)
-    stream.synchronize()
+            d2h_done[i] = ev()
+            d2h_done[i].record(s_d2h)
+    s_d2h.wait_stream(stream)
+    s_d2h.wait_stream(s_h2d)
+    e1.record(s_d2h)
+    torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / K
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if N > 1:
@@ -546,8 +610,9 @@ def run_e2e(args, cfg, rt, local, stream, N, dev, barrier, payload, slots):
     ms = t.item()
     barrier()
     return {"value": round(payload / (ms * 1e-3) / 1e9, 3), "unit": "GB/s", "ms_per_step": round(ms, 3),
-            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": K,
-            "path": "BridgeRuntime.forward/backward (C-ABI hb_exec_*) with pinned host buffers"}
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": K, "buffer_sets": S,
+            "path": "BridgeRuntime.forward/backward (C-ABI hb_exec_*) with pinned host buffers; "
+                    "H2D / boundary / D2H streams pipelined over buffer sets"}
 
 
 if __name__ == "__main__":
