@@ -36,7 +36,7 @@ DT_SIZE = {"bf16": 2, "fp16": 2, "fp32": 4, "fp64": 8}
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--config", default="c2")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -47,7 +47,7 @@ def parse():
     ap.add_argument("--threads", type=int, default=0)
     ap.add_argument("--slots", type=int, default=0, help="buffer sets rotated across steps (0=auto)")
     ap.add_argument("--no-clocks", action="store_true", help="skip nvidia-smi sampling")
-    ap.add_argument("--clock-ms", type=int, default=200)
+    ap.add_argument("--clock-ms", type=int, default=100)
     ap.add_argument("--fwd-mode", type=int, default=0, help="forward: 0 auto, 1 pull, 2 push")
     ap.add_argument("--partition", type=int, default=0, help="0 auto, 1 contiguous, 2 interleaved")
     return ap.parse_args()
