@@ -291,3 +291,57 @@ def test_mb_slots_rotate_buffers():
         out0 = rt.buffer(0, hbb.SLOT_DST_ACT, s).float().view(4, -1)
         assert torch.equal(out0[:, 0].cpu(), torch.tensor([10.0 * s + i for i in range(4)]))
     rt.close()
+
+
+# ---------------------------------------------------------------- golden fixtures
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5", "spec_fanin2_nc"])
+def test_device_matches_golden_fixture(name):
+    """Device path vs the committed oracle fixtures (no oracle library needed at run time)."""
+    _require_gpu()
+    import json
+    import os
+
+    gold = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    with open(os.path.join(gold, name + ".json")) as f:
+        meta = json.load(f)
+    arr = dict(np.load(os.path.join(gold, name + ".npz")))
+    src, dst = O.Layout(*meta["src"]), O.Layout(*meta["dst"])
+    B, W = meta["B"], meta["W"]
+    plan = hbb.plan_bridge(hbg.BoundaryEdge(to_hb(src), to_hb(dst), B, W))
+    sp = None
+    if "splice" in meta:
+        s = meta["splice"]
+        sp = hbb.SpliceSpec(s["Q"], s["S"], meta["hidden"], meta["tokens"], s["codes"], s["text_mode"])
+    rt = hbb.BridgeRuntime(plan, sp, act_dtype=torch.float32, grad_in_dtype=torch.float32,
+                           grad_out_dtype=torch.float32)
+    SI = O.intervals(B, src.dp)
+    X = torch.from_numpy(arr["X"]).to(DEV)
+    for r in src.stage_ranks(src.pp - 1):
+        d = src.coord(r)[3]
+        rt.buffer(r, hbb.SLOT_SRC_ACT).copy_(X[SI[d][0]:SI[d][0] + SI[d][1]].reshape(-1))
+    if sp is not None:
+        codes = np.asarray(meta["splice"]["codes"])
+        L = meta["splice"]["S"] // dst.cp
+        for r in dst.stage_ranks(0):
+            c = dst.coord(r)[1]
+            sl = codes.reshape(-1, meta["splice"]["S"])[:, c * L:(c + 1) * L].reshape(-1)
+            rows = [-1 - int(x) for x in sl if x < 0]
+            if meta["splice"]["text_mode"] != 1:
+                rows = list(range(len(arr["text"])))
+            b = rt.buffer(r, hbb.SLOT_TEXT)
+            b.copy_(torch.from_numpy(arr["text"][rows].reshape(-1)).to(DEV)[: b.numel()])
+    for r in dst.stage_ranks(0):
+        rt.buffer(r, hbb.SLOT_DST_GRAD).copy_(torch.from_numpy(arr[f"grad_r{r}"].reshape(-1)).to(DEV))
+    rt.forward(0)
+    rt.backward(0, 0.0)
+    torch.cuda.synchronize()
+    for r in dst.stage_ranks(0):
+        got = rt.buffer(r, hbb.SLOT_DST_ACT).cpu().numpy()
+        np.testing.assert_array_equal(got, arr[f"fwd_r{r}"].reshape(-1), err_msg=f"{name} fwd rank {r}")
+    for r in src.stage_ranks(src.pp - 1):
+        got = rt.buffer(r, hbb.SLOT_SRC_GRAD).cpu().numpy()
+        np.testing.assert_allclose(got, arr[f"bwd_r{r}"].reshape(-1), rtol=1e-6, atol=1e-6,
+                                   err_msg=f"{name} bwd rank {r}")
+    rt.close()

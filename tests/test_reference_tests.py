@@ -1,0 +1,30 @@
+"""The reference's own unit tests, built unmodified from /root/reference with a
+doctest shim (oracle/Makefile target `refcheck`):
+
+* test_grid.cpp against the reference grid.cpp      -> pins the oracle's layer
+* test_grid.cpp against the PRODUCT's hb::grid       -> the product passes the
+  reference's known-answer tests (16 cases, 1613 assertions)
+* test_simnet.cpp against the reference simnet.cpp   -> the fabric the oracle
+  executes over behaves as its own tests require
+"""
+import os
+import subprocess
+
+import pytest
+
+from helpers import ROOT
+
+BIN = os.path.join(ROOT, "oracle", "_ref")
+
+
+@pytest.mark.parametrize("name,cases", [("test_grid_ref", 16), ("test_grid_product", 16), ("test_simnet_ref", 18)])
+def test_reference_unit_tests_pass(name, cases):
+    exe = os.path.join(BIN, name)
+    if not os.path.exists(exe):
+        if os.path.isdir("/root/reference/proj"):
+            subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "refcheck"], check=True)
+        else:
+            pytest.skip("reference tests not built and /root/reference absent")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert f"test cases: {cases} | 0 failed" in r.stdout
