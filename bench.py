@@ -49,7 +49,9 @@ def parse():
     ap.add_argument("--no-clocks", action="store_true", help="skip nvidia-smi sampling")
     ap.add_argument("--clock-ms", type=int, default=100)
     ap.add_argument("--fwd-mode", type=int, default=0, help="forward: 0 auto, 1 pull, 2 push")
-    ap.add_argument("--partition", type=int, default=0, help="0 auto, 1 contiguous, 2 interleaved")
+    ap.add_argument("--partition", type=int, default=0,
+                    help="0 auto, 1 contiguous, 2 interleaved, 3 dynamic, 4 TMA bulk copy")
+    ap.add_argument("--no-nccl", action="store_true", help="skip the NCCL comparison leg (N == world)")
     return ap.parse_args()
 
 
@@ -472,6 +474,10 @@ def main():
     if not args.no_e2e:
         e2e = run_e2e(args, cfg, rt, local, stream, N, dev, barrier, fwd_b + bwd_b, slots)
 
+    nccl = None
+    if N > 1 and N == plan.world and not args.no_nccl:
+        nccl = run_nccl_comparison(args, cfg, plan, sp, rt, rank, dev, barrier, fwd_b + bwd_b, stream)
+
     cpu = None
     if rank == 0 and N == 1 and not args.no_cpu:
         try:
@@ -498,6 +504,7 @@ def main():
             "payload_bytes_per_step": {"fwd": fwd_b, "bwd": bwd_b},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clocks,
+            "nccl_comparison": nccl,
         }
         print(json.dumps(line), flush=True)
     rt.close()
@@ -613,6 +620,69 @@ def run_e2e(args, cfg, rt, local, stream, N, dev, barrier, payload, slots):
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": K, "buffer_sets": S,
             "path": "BridgeRuntime.forward/backward (C-ABI hb_exec_*) with pinned host buffers; "
                     "H2D / boundary / D2H streams pipelined over buffer sets"}
+
+
+def run_nccl_comparison(args, cfg, plan, sp, rt, rank, dev, barrier, payload, stream):
+    """The same step executed literally as the reference plan with NCCL
+    (send/recv, broadcast, all-gather, all-reduce on per-step subgroups), one
+    process per logical rank; parity-checked against the hetbridge result."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_27678_b200 import bridge as hbb
+    from paper_2605_27678_b200.nccl_path import NcclPlanExecutor
+
+    tdt = {"bf16": torch.bfloat16, "fp16": torch.float16, "fp32": torch.float32}
+    ex = NcclPlanExecutor(plan, sp, dev, act_dtype=tdt[cfg.act], grad_dtype=tdt[cfg.grad_in])
+    r = rank
+    if ex.src is not None:
+        ex.src.view(-1).copy_(rt.buffer(r, hbb.SLOT_SRC_ACT, 0))
+    g_in = rt.buffer(r, hbb.SLOT_DST_GRAD, 0)
+    if sp is not None:
+        if g_in is not None:
+            ex.token_grad.view(-1).copy_(g_in)
+        t = rt.buffer(r, hbb.SLOT_TEXT, 0)
+        if t is not None:
+            ex.text.view(-1)[: t.numel()].copy_(t)
+    elif g_in is not None:
+        ex.dst_grad.view(-1).copy_(g_in.float())
+    # reference result of hetbridge for set 0 with beta=0
+    mb = 40_000_000
+    rt.forward(mb, stream)
+    rt.backward(mb, 0.0, stream)
+    torch.cuda.synchronize()
+    barrier()
+    ex.forward()
+    ex.backward()
+    torch.cuda.synchronize()
+    ok = True
+    out = rt.buffer(r, hbb.SLOT_DST_ACT, 0)
+    if out is not None:
+        mine = ex.tokens if sp is not None else ex.dst
+        ok &= bool(torch.equal(mine.reshape(-1), out))
+    sg = rt.buffer(r, hbb.SLOT_SRC_GRAD, 0)
+    if sg is not None:
+        ref = sg.float()
+        ok &= bool(((ex.src_grad.reshape(-1) - ref).abs() <= 1e-6 * ref.abs().clamp(min=1.0)).all())
+    if sp is not None and g_in is not None:  # NCCL path re-splits its token grad every step
+        ex.token_grad.view(-1).copy_(g_in)
+    K = max(3, min(args.steps, 20))
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(K):
+        ex.forward()
+        ex.backward()
+    e1.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) / K, 0.0 if ok else 1.0], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = t[0].item()
+    barrier()
+    return {"ms_per_step": round(ms, 4), "value": round(payload / (ms * 1e-3) / 1e9, 2), "unit": "GB/s",
+            "parity_vs_hetbridge": t[1].item() == 0.0, "steps": K,
+            "path": "reference plan replayed with NCCL (torch.distributed send/recv, broadcast, all_gather, "
+                    "all_reduce on per-step subgroups); splice as bridge + local assemble"}
 
 
 if __name__ == "__main__":

@@ -82,6 +82,8 @@ int hb_leader_rank(const hb_layout* l, int pp, int dp, int* rank);       /* grid
 int hb_placement_of_edge(const hb_edge* e, int* placement);              /* grid.hpp:78 */
 int hb_ranks_of_stage(const hb_layout* l, int pp, int* out, int cap, int* n); /* grid.hpp:82 */
 int hb_replica_group(const hb_layout* l, int pp, int dp, int* out, int cap, int* n); /* :86 */
+/* per-module process groups of `rank`: kind 0 TP, 1 CP, 2 PP, 3 DP (runtime rank-group setup) */
+int hb_module_group(const hb_layout* l, int rank, int kind, int* out, int cap, int* n);
 
 /* ---- plan (bridge.hpp:137-142) ----------------------------------------------- */
 int hb_classify_dp_relation(const hb_edge* e, int* kind, int* factor); /* bridge.hpp:137 */

@@ -25,7 +25,7 @@ ERROR_NAMES = [
 EXPORTS = [
     "hb_last_error", "hb_error_name", "hb_abi_version",
     "hb_coord_of_rank", "hb_rank_of_coord", "hb_partition_batch", "hb_leader_rank",
-    "hb_placement_of_edge", "hb_ranks_of_stage", "hb_replica_group",
+    "hb_placement_of_edge", "hb_ranks_of_stage", "hb_replica_group", "hb_module_group",
     "hb_classify_dp_relation", "hb_plan_create", "hb_plan_destroy", "hb_plan_export", "hb_plan_info",
     "hb_cp_token_slice", "hb_splice_create", "hb_splice_destroy",
     "hb_index_forward", "hb_index_backward", "hb_index_buffer_elems",
@@ -95,6 +95,7 @@ def _declare(L):
         "hb_placement_of_edge": (I, [P(Edge), P(I)]),
         "hb_ranks_of_stage": (I, [P(Layout), I, P(I), I, P(I)]),
         "hb_replica_group": (I, [P(Layout), I, I, P(I), I, P(I)]),
+        "hb_module_group": (I, [P(Layout), I, I, P(I), I, P(I)]),
         "hb_classify_dp_relation": (I, [P(Edge), P(I), P(I)]),
         "hb_plan_create": (I, [P(Edge), P(V)]),
         "hb_plan_destroy": (None, [V]),

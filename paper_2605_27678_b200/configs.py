@@ -83,6 +83,28 @@ def get(name: str, scale: int = 1) -> BoundaryConfig:
         return BoundaryConfig("c5", "non-colocated vit{dp2}@0-1 -> llm{tp2,pp3}@2-7, bf16 h4096, 16 img x 576",
                               ModuleLayout("vit", dp=2), ModuleLayout("llm", tp=2, pp=3, rank_offset=2), 16,
                               576, h(4096))
+    # 4-rank variants of the same relations (one process per logical rank on a
+    # 4-GPU box; used to exercise the NCCL comparison path and N == world runs).
+    if name == "c2w4":
+        return BoundaryConfig("c2w4", "fan-in colocated vit{dp4} -> llm{tp2,dp2}, bf16 h4096, 32 img x 576",
+                              ModuleLayout("vit", dp=4), ModuleLayout("llm", tp=2, dp=2), 32, 576, h(4096),
+                              logical_world=4)
+    if name == "c3w4":
+        return BoundaryConfig("c3w4", "fan-out colocated enc{tp2,dp2} -> llm{dp4}, bf16 h5120, 32 img x 576",
+                              ModuleLayout("encoder", tp=2, dp=2), ModuleLayout("llm", dp=4), 32, 576, h(5120),
+                              logical_world=4)
+    if name == "c4w4":
+        base = get("c4", scale)
+        base.name = "c4w4"
+        base.description = "CP splice vit{dp4} -> llm{tp2,cp2}, 16 img x 576 at placeholders"
+        base.src = ModuleLayout("vit", dp=4)
+        base.dst = ModuleLayout("llm", tp=2, cp=2)
+        base.logical_world = 4
+        return base
+    if name == "c5w4":
+        return BoundaryConfig("c5w4", "non-colocated vit{dp1}@0 -> llm{tp1,pp3}@1-3, bf16 h4096, 8 img x 576",
+                              ModuleLayout("vit", dp=1), ModuleLayout("llm", pp=3, rank_offset=1), 8, 576,
+                              h(4096), logical_world=4)
     raise KeyError(name)
 
 

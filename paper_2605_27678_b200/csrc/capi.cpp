@@ -137,6 +137,13 @@ int hb_replica_group(const hb_layout* l, int pp, int dp, int* out, int cap, int*
   return guard([&] { fill(hb::grid::replica_group(layout(l), pp, dp), out, cap, n); });
 }
 
+int hb_module_group(const hb_layout* l, int rank, int kind, int* out, int cap, int* n) {
+  return guard([&] {
+    if (kind < 0 || kind > 3) hb::raise(hb::ErrorCode::InvalidArgument, "group kind must be 0..3");
+    fill(hb::grid::module_group(layout(l), rank, static_cast<hb::grid::GroupKind>(kind)), out, cap, n);
+  });
+}
+
 int hb_classify_dp_relation(const hb_edge* e, int* kind, int* factor) {
   return guard([&] {
     need(kind, "kind");

@@ -100,6 +100,20 @@ std::vector<int> replica_group(const ModuleLayout& l, int pp_idx, int dp_idx) {
   return v;
 }
 
+std::vector<int> module_group(const ModuleLayout& l, int rank, GroupKind kind) {
+  const GridCoord c = coord_of_rank(l, rank);
+  const int n = kind == GroupKind::TP ? l.tp : kind == GroupKind::CP ? l.cp : kind == GroupKind::PP ? l.pp : l.dp;
+  std::vector<int> v;
+  v.reserve(n);
+  for (int i = 0; i < n; ++i) {
+    GridCoord x = c;
+    (kind == GroupKind::TP ? x.tp_idx : kind == GroupKind::CP ? x.cp_idx : kind == GroupKind::PP ? x.pp_idx : x.dp_idx) = i;
+    v.push_back(rank_of_coord(l, x));
+  }
+  std::sort(v.begin(), v.end());
+  return v;
+}
+
 std::string to_string(const BatchInterval& iv) {
   return "[" + std::to_string(iv.start) + "," + std::to_string(iv.end()) + ")";
 }

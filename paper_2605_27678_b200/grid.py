@@ -119,6 +119,27 @@ def replica_group(layout: ModuleLayout, pp_idx: int, dp_idx: int) -> list[int]:
     return _list(lib().hb_replica_group, ctypes.byref(layout._c()), pp_idx, dp_idx)
 
 
+GROUP_KINDS = {"tp": 0, "cp": 1, "pp": 2, "dp": 3}
+
+
+def module_group(layout: ModuleLayout, rank: int, kind: str) -> list[int]:
+    """Ranks of `rank`'s TP / CP / PP / DP group inside its module (ascending)."""
+    return _list(lib().hb_module_group, ctypes.byref(layout._c()), rank, GROUP_KINDS[kind])
+
+
+def module_groups(layout: ModuleLayout) -> dict:
+    """Every distinct TP/CP/PP/DP group of a module: {kind: [sorted rank lists]}."""
+    out = {}
+    for kind in GROUP_KINDS:
+        seen = []
+        for r in range(layout.rank_begin(), layout.rank_end()):
+            g = module_group(layout, r, kind)
+            if g not in seen:
+                seen.append(g)
+        out[kind] = seen
+    return out
+
+
 def replica_position(layout: ModuleLayout, c: GridCoord) -> int:
     return c.cp_idx * layout.tp + c.tp_idx
 

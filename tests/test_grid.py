@@ -181,3 +181,22 @@ def test_cross_check_reference_placement():
         except HetBridgeError as e:
             got = e.code
         assert got == ref
+
+
+def test_module_groups_partition_the_module():
+    l = ModuleLayout("llm", 2, 2, 3, 2, 5)
+    for kind, size in (("tp", 2), ("cp", 2), ("pp", 3), ("dp", 2)):
+        groups = G.module_groups(l)[kind]
+        flat = sorted(r for g in groups for r in g)
+        assert flat == list(range(l.rank_begin(), l.rank_end()))
+        assert all(len(g) == size for g in groups)
+        for g in groups:  # members differ from each other only in that axis
+            cs = [G.coord_of_rank(l, r) for r in g]
+            for attr in ("tp_idx", "cp_idx", "pp_idx", "dp_idx"):
+                if not attr.startswith(kind):
+                    assert len({getattr(c, attr) for c in cs}) == 1
+    # the replica group of a (pp, dp) cell is the union of tp x cp around its leader
+    assert sorted(set(G.module_group(l, 5, "tp")) | set(G.module_group(l, 5, "cp")) |
+                  set(G.module_group(l, 8, "tp"))) == G.replica_group(l, 0, 0)
+    # C5: LLM stage-to-stage partners of rank 2 are its PP group
+    assert G.module_group(ModuleLayout("llm", tp=2, pp=3, rank_offset=2), 2, "pp") == [2, 4, 6]
