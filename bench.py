@@ -322,7 +322,8 @@ def main():
     tdt = {"bf16": torch.bfloat16, "fp16": torch.float16, "fp32": torch.float32}
 
     tm = traffic_model(cfg, N)
-    per_gpu_step = tm["fwd_hbm"][rank] + tm["bwd_hbm"][rank]
+    # rank-independent (every process must allocate the same number of buffer sets)
+    per_gpu_step = max(f + b for f, b in zip(tm["fwd_hbm"], tm["bwd_hbm"]))
     slots = args.slots or max(1, min(8, math.ceil(3 * L2_BYTES / max(per_gpu_step, 1))))
     if not args.no_e2e:
         slots = max(slots, 2)  # the pipelined e2e leg alternates two buffer sets

@@ -76,6 +76,10 @@ class BridgePlan:
             self._h = None
 
 
+def hbb_fingerprint(plan: BridgePlan) -> str:
+    return export_plan(plan, 8)
+
+
 def plan_bridge(edge: BoundaryEdge) -> BridgePlan:
     return BridgePlan(edge)
 
@@ -241,6 +245,17 @@ class BridgeRuntime:
         import torch
         import torch.distributed as dist
 
+        # every process must build the same buffer layout (same plan, map, dtypes, mb slots)
+        import hashlib
+
+        sp_fp = hashlib.sha256(self.splice.codes.tobytes()).hexdigest() if self.splice is not None else ""
+        fp = hashlib.sha256(repr((hbb_fingerprint(self.plan), sp_fp, self.rank_to_gpu, str(self.act_dtype),
+                                  str(self.grad_in_dtype), str(self.grad_out_dtype), self.mb_slots,
+                                  self.n_gpus)).encode()).digest()
+        fps = [None] * dist.get_world_size(group)
+        dist.all_gather_object(fps, fp, group=group)
+        if any(f != fp for f in fps):
+            raise HetBridgeError(24, "BridgeRuntime configuration differs across processes")
         mine = torch.frombuffer(bytearray(self.ipc_handle()), dtype=torch.uint8)
         dev = torch.device("cuda", torch.cuda.current_device())
         backend = dist.get_backend(group)
