@@ -39,6 +39,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--config", default="c2")
+    ap.add_argument("--scale", type=int, default=1, help="divide the hidden width (diagnostics only)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--no-e2e", action="store_true")
@@ -314,7 +315,7 @@ def main():
     if world_size > 1:
         dist.init_process_group("nccl", device_id=dev)
     N = world_size
-    cfg = configs.get(args.config)
+    cfg = configs.get(args.config, scale=args.scale)
     plan = hbb.plan_bridge(cfg.edge())
     sp = make_splice(cfg)
     r2g = configs.rank_to_gpu(plan.world, N)
@@ -398,11 +399,15 @@ def main():
         raise RuntimeError("device flag wait timed out")
 
     # isolated per-kernel timing (for the roofline of each kernel; not the headline)
+    align = torch.zeros(1, device=dev)
     iso = []
     for i in range(min(K, 20)):
         row = []
         for op in ("fwd", "bwd"):
             barrier()
+            if N > 1:  # align the GPUs on the device so launch skew is not timed
+                with torch.cuda.stream(stream):
+                    dist.all_reduce(align)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             if op == "fwd":
@@ -495,7 +500,7 @@ def main():
             "value": round(value, 2), "unit": "GB/s", "n_gpus": N, "steps": K, "warmup": args.warmup,
             "ms_per_step": round(ms_step, 5), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": cfg.act, "data": "synthetic",
-            "config": {"workload": cfg.description, "name": cfg.name, "global_batch": cfg.batch,
+            "config": {"workload": cfg.description + (f" (hidden /{args.scale})" if args.scale > 1 else ""), "name": cfg.name, "global_batch": cfg.batch,
                        "tokens_per_sample": cfg.tokens, "hidden": cfg.hidden,
                        "logical_ranks": plan.world, "rank_to_gpu": r2g,
                        "grad_in": cfg.grad_in, "grad_out": cfg.grad_out, "beta": cfg.beta,

@@ -54,32 +54,27 @@ def main():
     dist.barrier()
     W = nbytes // 2  # bf16 elements of one sample
     cases = []
-    for push in (False, True):
-        tag = "push" if push else "pull"
-        cases += [
-            (tag + "_one_way", hbg.ModuleLayout("enc", dp=1), hbg.ModuleLayout("llm", dp=1, rank_offset=1), [1, 0], push),
-            (tag + "_bidir", hbg.ModuleLayout("enc", dp=2), hbg.ModuleLayout("llm", tp=2, dp=1), [0, 1], push),
-        ]
-    for name, src, dst, r2g, push in cases:
+    for part in (1, 4):
+        for push in (False, True):
+            tag = ("push" if push else "pull") + ("_tma" if part == 4 else "_ldg")
+            cases += [
+                (tag + "_one_way", hbg.ModuleLayout("enc", dp=1), hbg.ModuleLayout("llm", dp=1, rank_offset=1), [1, 0], push, part),
+                (tag + "_bidir", hbg.ModuleLayout("enc", dp=2), hbg.ModuleLayout("llm", tp=2, dp=1), [0, 1], push, part),
+            ]
+    for name, src, dst, r2g, push, part in cases:
         B = src.dp
         plan = hbb.plan_bridge(hbg.BoundaryEdge(src, dst, B, W))
-        rt = hbb.BridgeRuntime(plan, n_gpus=N, my_gpu=rank, rank_to_gpu=r2g, fwd_mode=2 if push else 1)
+        rt = hbb.BridgeRuntime(plan, n_gpus=N, my_gpu=rank, rank_to_gpu=r2g, fwd_mode=2 if push else 1,
+                               partition=part)
         rt.exchange_handles()
         mb = [0]
-
-        def step():
-            rt.forward(mb[0])
-            rt.backward(mb[0], 0.0)
-            mb[0] += 1
 
         def fwd_only():
             rt.forward(mb[0])
             mb[0] += 1
 
         fwd_ms = timeit(fwd_only)
-        ms = timeit(step)
-        moved = W * 2  # bytes crossing NVLink into each consumer GPU per forward
-        out[name] = {"fwd_ms": fwd_ms, "fwd_pull_gbs_per_gpu": moved / fwd_ms / 1e6, "fwd_bwd_ms": ms}
+        out[name] = {"fwd_ms": round(fwd_ms, 4), "gbs_per_gpu": round(W * 2 / fwd_ms / 1e6, 1)}
         rt.close()
     if rank == 0:
         print(json.dumps(out))
