@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--partition", type=int, default=0,
                     help="0 auto, 1 contiguous, 2 interleaved, 3 dynamic, 4 TMA bulk copy")
     ap.add_argument("--no-nccl", action="store_true", help="skip the NCCL comparison leg (N == world)")
+    ap.add_argument("--no-graph", action="store_true", help="timed loop: per-op launches instead of CUDA graphs")
     return ap.parse_args()
 
 
@@ -371,15 +372,25 @@ def main():
     K = args.steps
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
            torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    use_graph = not args.no_graph
+    if use_graph:  # one CUDA graph per buffer set: forward + backward(beta)
+        for k in range(slots):
+            rt.capture_step(k, cfg.beta, True, stream)
+        for k in range(slots):
+            rt.replay_step(k, stream)
+        barrier()
     launches0 = rt.stats()["launches"]
     barrier()
     sampler.mark(True)
     for i in range(K):
         e0, e1, e2 = ev[i]
         e0.record(stream)
-        rt.forward(mb, stream)
-        e1.record(stream)
-        rt.backward(mb, cfg.beta, stream)
+        if use_graph:
+            rt.replay_step(mb % slots, stream)
+        else:
+            rt.forward(mb, stream)
+            e1.record(stream)
+            rt.backward(mb, cfg.beta, stream)
         e2.record(stream)
         mb += 1
     stream.synchronize()
@@ -387,8 +398,8 @@ def main():
     barrier()
     launches = rt.stats()["launches"] - launches0
     total_ms = ev[0][0].elapsed_time(ev[-1][2])
-    fwd_ms = sum(e[0].elapsed_time(e[1]) for e in ev) / K
-    bwd_ms = sum(e[1].elapsed_time(e[2]) for e in ev) / K
+    fwd_ms = 0.0 if use_graph else sum(e[0].elapsed_time(e[1]) for e in ev) / K
+    bwd_ms = 0.0 if use_graph else sum(e[1].elapsed_time(e[2]) for e in ev) / K
     t = torch.tensor([total_ms, fwd_ms, bwd_ms], dtype=torch.float64, device=dev)
     if N > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -408,6 +419,8 @@ def main():
             if N > 1:  # align the GPUs on the device so launch skew is not timed
                 with torch.cuda.stream(stream):
                     dist.all_reduce(align)
+            with torch.cuda.stream(stream):  # keep the GPU busy while the host enqueues: no host gap timed
+                torch.cuda._sleep(100_000)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             if op == "fwd":
@@ -504,6 +517,7 @@ def main():
                        "tokens_per_sample": cfg.tokens, "hidden": cfg.hidden,
                        "logical_ranks": plan.world, "rank_to_gpu": r2g,
                        "grad_in": cfg.grad_in, "grad_out": cfg.grad_out, "beta": cfg.beta,
+                       "launch": "one CUDA graph (fwd+bwd) per step" if use_graph else "per-op C-ABI launches",
                        "l2": f"inputs rotate over {slots} buffer set(s); per-GPU bytes per step "
                              f"{per_gpu_step / 1e6:.1f} MB x {slots} sets > 126 MB L2"},
             "per_gpu_gbs": round(value / N, 2), "tokens_per_s": round(tokens_s, 1),

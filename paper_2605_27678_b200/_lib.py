@@ -31,7 +31,8 @@ EXPORTS = [
     "hb_index_forward", "hb_index_backward", "hb_index_buffer_elems",
     "hb_exec_config_default", "hb_exec_create", "hb_exec_destroy", "hb_exec_ipc_handle",
     "hb_exec_open_peers", "hb_exec_buffer", "hb_exec_bind", "hb_exec_forward", "hb_exec_backward",
-    "hb_exec_seed_forward_record", "hb_exec_status", "hb_exec_stats",
+    "hb_exec_seed_forward_record", "hb_exec_status", "hb_exec_stats", "hb_exec_graph_capture",
+    "hb_exec_graph_launch",
 ]
 
 
@@ -117,6 +118,8 @@ def _declare(L):
         "hb_exec_forward": (I, [V, I, V]),
         "hb_exec_backward": (I, [V, I, ctypes.c_float, V]),
         "hb_exec_seed_forward_record": (I, [V, I]),
+        "hb_exec_graph_capture": (I, [V, I, I, ctypes.c_float, V]),
+        "hb_exec_graph_launch": (I, [V, I, V]),
         "hb_exec_status": (I, [V, P(U)]),
         "hb_exec_stats": (I, [V, P(LL), P(LL), P(LL), P(LL), P(LL)]),
     }

@@ -302,6 +302,14 @@ class BridgeRuntime:
     def backward(self, mb: int = 0, beta: float = 0.0, stream=None):
         check(lib().hb_exec_backward(self._h, mb, ctypes.c_float(beta), self._stream(stream)))
 
+    def capture_step(self, mb_slot: int = 0, beta: float = 1.0, with_backward: bool = True, stream=None):
+        """Capture forward (+ backward) of one buffer set into a CUDA graph."""
+        check(lib().hb_exec_graph_capture(self._h, mb_slot, 1 if with_backward else 0, ctypes.c_float(beta),
+                                          self._stream(stream)))
+
+    def replay_step(self, mb_slot: int = 0, stream=None):
+        check(lib().hb_exec_graph_launch(self._h, mb_slot, self._stream(stream)))
+
     def seed_forward_record(self, mb: int):
         check(lib().hb_exec_seed_forward_record(self._h, mb))
 

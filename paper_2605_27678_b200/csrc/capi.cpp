@@ -360,6 +360,20 @@ int hb_exec_backward(hb_exec* x, int mb, float beta, void* stream) {
   });
 }
 
+int hb_exec_graph_capture(hb_exec* x, int mb_slot, int with_bwd, float beta, void* stream) {
+  return guard([&] {
+    need(x, "exec");
+    x->x->graph_capture(mb_slot, with_bwd != 0, beta, stream);
+  });
+}
+
+int hb_exec_graph_launch(hb_exec* x, int mb_slot, void* stream) {
+  return guard([&] {
+    need(x, "exec");
+    x->x->graph_launch(mb_slot, stream);
+  });
+}
+
 int hb_exec_seed_forward_record(hb_exec* x, int mb) {
   return guard([&] {
     need(x, "exec");

@@ -125,6 +125,8 @@ Exec::Exec(const bridge::BridgePlan& plan, const index::SpliceSpec* splice, int 
 }
 
 Exec::~Exec() {
+  for (void* g : graphs_)
+    if (g) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(g));
   for (auto& t : tables_) {
     cudaFree(t.copy);
     cudaFree(t.reduce);
@@ -393,11 +395,8 @@ dev::SyncArgs Exec::make_sync_args() const {
   return s;
 }
 
-void Exec::forward(int mb, void* stream) {
-  if (fwd_done_.count(mb))
-    raise(ErrorCode::InvalidArgument, "microbatch " + std::to_string(mb) + " forwarded twice without backward");
-  prepare_fwd();
-  const DevTables& T = tables_[mb % cfg_.mb_slots];
+void Exec::launch_forward(int mb_slot, void* stream) {
+  const DevTables& T = tables_[mb_slot];
   dev::launch_copy(T.copy, static_cast<int>(fwd_local_.size()), fwd_part_.dev(),
                    fwd_push_ && n_gpus_ > 1 ? sync_push_ : sync_, {fwd_part_.grid, cfg_.threads}, stream);
   ck(cudaGetLastError(), "copy_segments launch");
@@ -406,11 +405,26 @@ void Exec::forward(int mb, void* stream) {
     dev::SyncArgs local{};
     local.ctr = ctr2_;
     local.my_gpu = my_gpu_;
-    dev::launch_copy(T.copy2, static_cast<int>(fwd_second_local_.size()),
-                     fwd2_part_.dev(), local, {fwd2_part_.grid, cfg_.threads}, stream);
+    dev::launch_copy(T.copy2, static_cast<int>(fwd_second_local_.size()), fwd2_part_.dev(), local,
+                     {fwd2_part_.grid, cfg_.threads}, stream);
     ck(cudaGetLastError(), "copy_segments (phase 2) launch");
     ++launches_;
   }
+}
+
+void Exec::launch_backward(int mb_slot, float beta, void* stream) {
+  const DevTables& T = tables_[mb_slot];
+  dev::launch_reduce(T.reduce, static_cast<int>(bwd_local_.size()), T.terms, bwd_part_.dev(), cfg_.grad_in_dtype,
+                     cfg_.grad_out_dtype, beta, sync_, {bwd_part_.grid, cfg_.threads}, stream);
+  ck(cudaGetLastError(), "reduce_segments launch");
+  ++launches_;
+}
+
+void Exec::forward(int mb, void* stream) {
+  if (fwd_done_.count(mb))
+    raise(ErrorCode::InvalidArgument, "microbatch " + std::to_string(mb) + " forwarded twice without backward");
+  prepare_fwd();
+  launch_forward(mb % cfg_.mb_slots, stream);
   fwd_done_.insert(mb);
 }
 
@@ -418,13 +432,42 @@ void Exec::backward(int mb, float beta, void* stream) {
   if (!fwd_done_.count(mb))
     raise(ErrorCode::UnknownMicrobatch, "no forward record for microbatch " + std::to_string(mb));
   prepare_bwd();
-  const DevTables& T = tables_[mb % cfg_.mb_slots];
-  dev::launch_reduce(T.reduce, static_cast<int>(bwd_local_.size()), T.terms,
-                     bwd_part_.dev(), cfg_.grad_in_dtype, cfg_.grad_out_dtype, beta,
-                     sync_, {bwd_part_.grid, cfg_.threads}, stream);
-  ck(cudaGetLastError(), "reduce_segments launch");
-  ++launches_;
+  launch_backward(mb % cfg_.mb_slots, beta, stream);
   fwd_done_.erase(mb);
+}
+
+void Exec::graph_capture(int mb_slot, bool with_bwd, float beta, void* stream) {
+  if (mb_slot < 0 || mb_slot >= cfg_.mb_slots) raise(ErrorCode::InvalidArgument, "mb slot out of range");
+  if (!stream) raise(ErrorCode::InvalidArgument, "graph capture needs a non-default stream");
+  prepare_fwd();
+  if (with_bwd) prepare_bwd();
+  graphs_.resize(cfg_.mb_slots, nullptr);
+  graph_kernels_.resize(cfg_.mb_slots, 0);
+  if (graphs_[mb_slot]) {
+    cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(graphs_[mb_slot]));
+    graphs_[mb_slot] = nullptr;
+  }
+  auto st = static_cast<cudaStream_t>(stream);
+  const int before = launches_;
+  ck(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
+  launch_forward(mb_slot, stream);
+  if (with_bwd) launch_backward(mb_slot, beta, stream);
+  cudaGraph_t g = nullptr;
+  ck(cudaStreamEndCapture(st, &g), "cudaStreamEndCapture");
+  cudaGraphExec_t ge = nullptr;
+  ck(cudaGraphInstantiate(&ge, g, 0), "cudaGraphInstantiate");
+  cudaGraphDestroy(g);
+  graphs_[mb_slot] = ge;
+  graph_kernels_[mb_slot] = launches_ - before;
+  launches_ = before;  // captured launches are counted when replayed
+}
+
+void Exec::graph_launch(int mb_slot, void* stream) {
+  if (mb_slot < 0 || mb_slot >= static_cast<int>(graphs_.size()) || !graphs_[mb_slot])
+    raise(ErrorCode::InvalidArgument, "no graph captured for this mb slot");
+  ck(cudaGraphLaunch(static_cast<cudaGraphExec_t>(graphs_[mb_slot]), static_cast<cudaStream_t>(stream)),
+     "cudaGraphLaunch");
+  launches_ += graph_kernels_[mb_slot];
 }
 
 void Exec::seed_forward_record(int mb) { fwd_done_.insert(mb); }

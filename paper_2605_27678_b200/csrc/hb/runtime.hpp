@@ -59,6 +59,12 @@ class Exec {
   void forward(int mb, void* stream);
   void backward(int mb, float beta, void* stream);
   void seed_forward_record(int mb);
+
+  // CUDA-graph capture of one buffer set's forward (+ backward with `beta`):
+  // the step is replayed with one graph launch (no per-kernel host overhead).
+  // Replays bypass the microbatch records (a replay is a complete fwd+bwd).
+  void graph_capture(int mb_slot, bool with_bwd, float beta, void* stream);
+  void graph_launch(int mb_slot, void* stream);
   uint32_t device_error() const;  // synchronises
 
   const index::IndexMap& map() const { return map_; }
@@ -135,6 +141,10 @@ class Exec {
   int sm_count_ = 0;
   int launches_ = 0;
   std::set<int> fwd_done_;
+  std::vector<void*> graphs_;       // cudaGraphExec_t per mb slot
+  std::vector<int> graph_kernels_;  // kernels per replay
+  void launch_forward(int mb_slot, void* stream);
+  void launch_backward(int mb_slot, float beta, void* stream);
 };
 
 }  // namespace hb::rt

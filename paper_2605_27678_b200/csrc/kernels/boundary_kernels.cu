@@ -482,6 +482,7 @@ int tma_blocks_per_sm() {
   if (n < 0) {
     const int smem = kTmaStages * kTmaStageBytes;
     cudaFuncSetAttribute(copy_segments_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(copy_segments_tma_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, copy_segments_tma_kernel, 32, smem);
     if (n < 1) n = 1;
   }

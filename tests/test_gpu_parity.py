@@ -345,3 +345,40 @@ def test_device_matches_golden_fixture(name):
         np.testing.assert_allclose(got, arr[f"bwd_r{r}"].reshape(-1), rtol=1e-6, atol=1e-6,
                                    err_msg=f"{name} bwd rank {r}")
     rt.close()
+
+
+def test_cuda_graph_replay_matches_direct_calls():
+    _require_gpu()
+    cfg = configs.get("c4", scale=64)
+    plan = hbb.plan_bridge(cfg.edge())
+    s = cfg.splice
+    sp = hbb.SpliceSpec(s["Q"], s["S"], cfg.hidden, cfg.tokens, s["codes"], s["text_mode"])
+    outs = []
+    for use_graph in (False, True):
+        rt = hbb.BridgeRuntime(plan, sp, mb_slots=2)
+        g = torch.Generator(device=DEV)
+        g.manual_seed(3)
+        for k in range(2):
+            for r in range(8):
+                for slot in (hbb.SLOT_SRC_ACT, hbb.SLOT_TEXT, hbb.SLOT_DST_GRAD):
+                    b = rt.buffer(r, slot, k)
+                    if b is not None:
+                        b.copy_(torch.randn(b.numel(), generator=g, device=DEV).to(b.dtype))
+                rt.buffer(r, hbb.SLOT_SRC_GRAD, k).zero_()
+        st = torch.cuda.Stream()
+        if use_graph:
+            for k in range(2):
+                rt.capture_step(k, 1.0, True, st)
+            for i in range(4):
+                rt.replay_step(i % 2, st)
+        else:
+            for i in range(4):
+                rt.forward(i, st)
+                rt.backward(i, 1.0, st)
+        st.synchronize()
+        outs.append([rt.buffer(r, sl, k).clone() for k in range(2) for r in range(8)
+                     for sl in (hbb.SLOT_DST_ACT, hbb.SLOT_SRC_GRAD)])
+        assert rt.stats()["launches"] == 8
+        rt.close()
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
