@@ -101,7 +101,12 @@ __device__ void epoch_finish(const SyncArgs& s, uint32_t e) {
   __shared__ int last;
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence_system();
+    // Push mode must make this CTA's remote stores visible before "done" is
+    // posted (system scope). Otherwise outputs are local and kernel completion
+    // already publishes them to peers, so a GPU-scope fence suffices (a
+    // system-scope fence in every CTA measurably lengthens short launches).
+    if (s.end_sync) __threadfence_system();
+    else __threadfence();
     last = atomicAdd(s.ctr + 1, 1u) == gridDim.x - 1;
   }
   __syncthreads();
