@@ -70,10 +70,13 @@ class BridgePlan:
         return self._xmsgs
 
     def __del__(self):
-        h = getattr(self, "_h", None)
-        if h and _lib._lib is not None:
-            _lib._lib.hb_plan_destroy(h)
-            self._h = None
+        try:
+            h = getattr(self, "_h", None)
+            if h and _lib._lib is not None:
+                _lib._lib.hb_plan_destroy(h)
+                self._h = None
+        except Exception:  # interpreter shutdown
+            pass
 
 
 def hbb_fingerprint(plan: BridgePlan) -> str:
@@ -127,10 +130,13 @@ class SpliceSpec:
         return SpliceSpec(n, S, d_h, S_v, codes, TEXT_FULL)
 
     def __del__(self):
-        h = getattr(self, "_h", None)
-        if h and _lib._lib is not None:
-            _lib._lib.hb_splice_destroy(h)
-            self._h = None
+        try:
+            h = getattr(self, "_h", None)
+            if h and _lib._lib is not None:
+                _lib._lib.hb_splice_destroy(h)
+                self._h = None
+        except Exception:  # interpreter shutdown
+            pass
 
 
 def index_forward(plan: BridgePlan, splice: SpliceSpec | None = None):
