@@ -134,7 +134,10 @@ Exec::~Exec() {
   }
   cudaFree(fwd_part_.first_seg);
   cudaFree(fwd2_part_.first_seg);
-  for (auto* p : {&fwd_part_, &fwd2_part_, &bwd_part_}) cudaFree(p->chunks);
+  for (auto* p : {&fwd_part_, &fwd2_part_, &bwd_part_}) {
+    cudaFree(p->chunks);
+    cudaFree(p->rchunks);
+  }
   for (auto& t : tables_) cudaFree(t.copy2);
   cudaFree(ctr2_);
   cudaFree(bwd_part_.first_seg);
@@ -241,35 +244,53 @@ uint64_t Exec::pad_unit(int mode, bool copy) const {
   return dev::kQuantum;
 }
 
-void Exec::build_partition(const std::vector<uint64_t>& w0, const std::vector<uint64_t>& n, int grid, int mode,
-                           uint64_t unit, DevPartition* out) {
+void Exec::build_partition(const std::vector<uint64_t>& w0, const std::vector<uint64_t>& n,
+                           const std::vector<char>& remote, double local_bytes, double remote_bytes, int grid,
+                           int mode, uint64_t unit, DevPartition* out) {
   const uint64_t total = w0.empty() ? 0 : w0.back() + n.back();
   cudaFree(out->first_seg);
+  cudaFree(out->chunks);
+  cudaFree(out->rchunks);
   out->first_seg = nullptr;
+  out->chunks = out->rchunks = nullptr;
   out->grid = grid;
   out->mode = mode;
   out->chunk = unit;
-  out->total_chunks = static_cast<uint32_t>((total + unit - 1) / unit);
+  out->total_chunks = out->rtotal_chunks = 0;
+  out->remote_ctas = 0;
   out->per_cta = 0;
-  cudaFree(out->chunks);
-  out->chunks = nullptr;
   if (mode == dev::kPartDynamic || mode == dev::kPartTma) {
-    // Hand-out order: chunk j of segment s gets key (j + 0.5) / chunks(s), so all
-    // segments advance at the same fractional pace; ties keep segment order.
-    std::vector<std::pair<double, uint2>> order;
-    for (size_t s = 0; s < n.size(); ++s) {
-      const uint64_t k = (n[s] + unit - 1) / unit;
-      for (uint64_t j = 0; j < k; ++j)
-        order.push_back({(j + 0.5) / static_cast<double>(k), make_uint2(static_cast<unsigned>(s), static_cast<unsigned>(j))});
+    // Two queues (local / remote). Hand-out order within a queue: chunk j of
+    // segment s gets key (j + 0.5) / chunks(s), so every segment advances at
+    // the same fractional pace; ties keep segment order.
+    for (int q = 0; q < 2; ++q) {
+      std::vector<std::pair<double, uint2>> order;
+      for (size_t s = 0; s < n.size(); ++s) {
+        if ((remote[s] != 0) != (q == 1)) continue;
+        const uint64_t k = (n[s] + unit - 1) / unit;
+        for (uint64_t j = 0; j < k; ++j)
+          order.push_back({(j + 0.5) / static_cast<double>(k),
+                           make_uint2(static_cast<unsigned>(s), static_cast<unsigned>(j))});
+      }
+      std::stable_sort(order.begin(), order.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+      std::vector<uint2> table(order.size());
+      for (size_t i = 0; i < order.size(); ++i) table[i] = order[i].second;
+      uint2** dst = q ? &out->rchunks : &out->chunks;
+      (q ? out->rtotal_chunks : out->total_chunks) = static_cast<uint32_t>(table.size());
+      if (!table.empty()) {
+        ck(cudaMalloc(dst, table.size() * sizeof(uint2)), "cudaMalloc(chunk table)");
+        ck(cudaMemcpy(*dst, table.data(), table.size() * sizeof(uint2), cudaMemcpyHostToDevice), "upload");
+      }
     }
-    std::stable_sort(order.begin(), order.end(),
-                     [](const auto& a, const auto& b) { return a.first < b.first; });
-    std::vector<uint2> table(order.size());
-    for (size_t i = 0; i < order.size(); ++i) table[i] = order[i].second;
-    out->total_chunks = static_cast<uint32_t>(table.size());
-    if (!table.empty()) {
-      ck(cudaMalloc(&out->chunks, table.size() * sizeof(uint2)), "cudaMalloc(chunk table)");
-      ck(cudaMemcpy(out->chunks, table.data(), table.size() * sizeof(uint2), cudaMemcpyHostToDevice), "upload");
+    // CTAs that start on the remote queue ~ the remote share of the time
+    // (NVLink ~770 GB/s vs HBM copy ~6.5 TB/s counted read+write).
+    if (out->rtotal_chunks == 0) {
+      out->remote_ctas = 0;
+    } else if (out->total_chunks == 0) {
+      out->remote_ctas = grid;
+    } else {
+      const double tr = remote_bytes / 770e9, tl = 2.0 * local_bytes / 6.5e12;
+      out->remote_ctas = std::clamp(static_cast<int>(grid * tr / (tr + tl) + 0.5), 1, grid - 1);
     }
     return;
   }
@@ -327,8 +348,17 @@ void Exec::prepare_fwd() {
     upload_copies(fwd_local_, mb, unit, &tables_[mb].copy, &w0s, &ns);
     upload_copies(fwd_second_local_, mb, unit, &tables_[mb].copy2, &w0s2, &ns2);
   }
-  build_partition(w0s, ns, copy_grid(), mode, unit, &fwd_part_);
-  if (!fwd_second_local_.empty()) build_partition(w0s2, ns2, copy_grid(), mode, unit, &fwd2_part_);
+  std::vector<char> rem;
+  double lb = 0, rb = 0;
+  for (size_t i = 0; i < fwd_local_.size(); ++i) {
+    const auto& sg = fwd_local_[i];
+    const bool r = gpu_of(fwd_push_ ? sg.dst.rank : sg.src.rank) != my_gpu_;
+    rem.push_back(r);
+    (r ? rb : lb) += static_cast<double>(ns[i]);
+  }
+  build_partition(w0s, ns, rem, lb, rb, copy_grid(), mode, unit, &fwd_part_);
+  if (!fwd_second_local_.empty())
+    build_partition(w0s2, ns2, std::vector<char>(ns2.size(), 0), 1.0, 0.0, copy_grid(), mode, unit, &fwd2_part_);
   dirty_fwd_ = false;
 }
 
@@ -375,7 +405,15 @@ void Exec::prepare_bwd() {
   }
   const int occ = dev::reduce_blocks_per_sm(cfg_.threads, cfg_.grad_in_dtype, cfg_.grad_out_dtype);
   const int bps = cfg_.blocks_per_sm > 0 ? std::min(cfg_.blocks_per_sm, occ) : occ;
-  build_partition(w0s, ns, sm_count_ * bps, mode, unit, &bwd_part_);
+  std::vector<char> rem;
+  double lb = 0, rb = 0;
+  for (size_t i = 0; i < bwd_local_.size(); ++i) {
+    bool r = false;
+    for (const auto& t : bwd_local_[i].terms) r |= gpu_of(t.rank) != my_gpu_;
+    rem.push_back(r);
+    (r ? rb : lb) += static_cast<double>(ns[i]) * (es_in + 2 * es_out);
+  }
+  build_partition(w0s, ns, rem, lb, rb, sm_count_ * bps, mode, unit, &bwd_part_);
   dirty_bwd_ = false;
 }
 

@@ -122,7 +122,12 @@ class Exec {
     uint32_t total_chunks = 0;
     uint64_t chunk = 0;
     uint2* chunks = nullptr;
-    dev::Partition dev() const { return {first_seg, per_cta, mode, total_chunks, chunk, chunks}; }
+    uint32_t rtotal_chunks = 0;
+    uint2* rchunks = nullptr;
+    int remote_ctas = 0;
+    dev::Partition dev() const {
+      return {first_seg, per_cta, mode, total_chunks, chunk, chunks, rtotal_chunks, rchunks, remote_ctas};
+    }
   };
   DevPartition fwd_part_, fwd2_part_, bwd_part_;
   uint32_t* ctr2_ = nullptr;  // phase-2 counters (local-only launch)
@@ -132,8 +137,10 @@ class Exec {
   int reduce_mode() const;
   uint64_t pad_unit(int mode, bool copy) const;
   int copy_grid() const;
-  void build_partition(const std::vector<uint64_t>& w0, const std::vector<uint64_t>& n, int grid, int mode,
-                       uint64_t unit, DevPartition* out);
+  // remote[s]: segment s reads (pull) or writes (push) a peer's buffer; cost_local/remote in bytes
+  void build_partition(const std::vector<uint64_t>& w0, const std::vector<uint64_t>& n,
+                       const std::vector<char>& remote, double local_bytes, double remote_bytes, int grid,
+                       int mode, uint64_t unit, DevPartition* out);
   bool dirty_fwd_ = true, dirty_bwd_ = true;
   uint32_t* ctr_ = nullptr;  // device counters
   dev::SyncArgs sync_{}, sync_push_{};

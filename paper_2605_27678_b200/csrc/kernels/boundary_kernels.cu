@@ -60,44 +60,70 @@ __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// Returns false if the barrier timed out (error flag set; caller skips work).
-__device__ bool epoch_barrier(const SyncArgs& s, uint32_t* target_out) {
-  __shared__ uint32_t target;
-  __shared__ int ok;
-  if (threadIdx.x == 0) {
-    target = *reinterpret_cast<volatile uint32_t*>(s.ctr) + 1;
-    ok = 1;
-  }
-  __syncthreads();
-  const uint32_t e = target;
-  *target_out = e;
-  if (s.wait_mask | s.post_mask) {
-    const int g = threadIdx.x;
-    if (blockIdx.x == 0 && g < kMaxGpus && ((s.post_mask >> g) & 1u)) {
-      __threadfence_system();
-      st_release_sys(s.peer_pad[g] + s.my_gpu, e);
+// Per-CTA view of the launch's epoch barrier (shared memory).
+struct CtaSync {
+  uint32_t e;  // this launch's epoch
+  int waited;  // peers' arrival at e confirmed
+  int ok;      // no timeout
+};
+
+// Bounded spin until *flag >= e; false on timeout (error word set).
+__device__ __forceinline__ bool spin_until(const SyncArgs& s, const uint32_t* flag, uint32_t e) {
+  const long long t0 = clock64();
+  while (static_cast<int32_t>(ld_acquire_sys(flag) - e) < 0) {
+    __nanosleep(64);
+    if (static_cast<uint64_t>(clock64() - t0) > s.timeout_cycles) {
+      atomicExch(s.ctr + 2, 1u);
+      return false;
     }
-    if (g < kMaxGpus && ((s.wait_mask >> g) & 1u)) {
-      const long long t0 = clock64();
-      while (static_cast<int32_t>(ld_acquire_sys(s.pad + g) - e) < 0) {
-        __nanosleep(64);
-        if (static_cast<uint64_t>(clock64() - t0) > s.timeout_cycles) {
-          atomicExch(s.ctr + 2, 1u);
-          ok = 0;
-          break;
-        }
-      }
-    }
-    __syncthreads();
   }
-  return ok != 0;
+  return true;
 }
 
-// Last CTA to finish bumps the local epoch (and resets the dynamic work
-// counter). In push mode it first publishes "my writes into your buffers are
-// done" (release, system scope) and waits for every writer into this GPU's
-// buffers, so kernel completion implies the outputs are complete.
-__device__ void epoch_finish(const SyncArgs& s, uint32_t e) {
+// Start of a launch: read the epoch, and (block 0) post arrival to every peer.
+// The post is a release store at system scope; earlier kernels' writes are
+// already complete at the kernel boundary.
+__device__ void sync_begin(const SyncArgs& s, CtaSync& cs) {
+  if (threadIdx.x == 0) {
+    cs.e = *reinterpret_cast<volatile uint32_t*>(s.ctr) + 1;
+    cs.waited = (s.wait_mask == 0);
+    cs.ok = 1;
+  }
+  __syncthreads();
+  const int g = threadIdx.x;
+  if (blockIdx.x == 0 && g < kMaxGpus && ((s.post_mask >> g) & 1u)) st_release_sys(s.peer_pad[g] + s.my_gpu, cs.e);
+}
+
+// Wait (once per CTA) until every peer arrived at this epoch: after that the
+// peers' buffers of this op may be read (pull) or written (push). Called by all
+// threads of the CTA. Returns false on timeout.
+__device__ bool sync_wait(const SyncArgs& s, CtaSync& cs) {
+  if (cs.waited) return cs.ok != 0;
+  __syncthreads();
+  const int g = threadIdx.x;
+  if (g < kMaxGpus && ((s.wait_mask >> g) & 1u))
+    if (!spin_until(s, s.pad + g, cs.e)) cs.ok = 0;
+  __syncthreads();
+  if (threadIdx.x == 0) cs.waited = 1;
+  __syncthreads();
+  return cs.ok != 0;
+}
+
+// Single-thread variant (TMA issuing lane).
+__device__ bool sync_wait_lane(const SyncArgs& s, CtaSync& cs) {
+  if (!cs.waited) {
+    for (int g = 0; g < kMaxGpus; ++g)
+      if (((s.wait_mask >> g) & 1u) && !spin_until(s, s.pad + g, cs.e)) cs.ok = 0;
+    cs.waited = 1;
+  }
+  return cs.ok != 0;
+}
+
+// Last CTA to finish: confirm every peer arrived at this epoch (so completion
+// of op e implies all peers completed op e-1, whatever work this GPU had), in
+// push mode publish "my writes into your buffers are done" and wait for every
+// writer into this GPU, then reset the work counters and bump the epoch.
+__device__ void epoch_finish(const SyncArgs& s, CtaSync& cs) {
   __shared__ int last;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -111,26 +137,19 @@ __device__ void epoch_finish(const SyncArgs& s, uint32_t e) {
   }
   __syncthreads();
   if (!last) return;
+  const int g = threadIdx.x;
+  if (g < kMaxGpus && ((s.wait_mask >> g) & 1u)) spin_until(s, s.pad + g, cs.e);
   if (s.end_sync) {
-    const int g = threadIdx.x;
-    if (g < kMaxGpus && ((s.post_mask >> g) & 1u)) st_release_sys(s.peer_pad[g] + kMaxGpus + s.my_gpu, e);
-    if (g < kMaxGpus && ((s.wait_mask >> g) & 1u)) {
-      const long long t0 = clock64();
-      while (static_cast<int32_t>(ld_acquire_sys(s.pad + kMaxGpus + g) - e) < 0) {
-        __nanosleep(64);
-        if (static_cast<uint64_t>(clock64() - t0) > s.timeout_cycles) {
-          atomicExch(s.ctr + 2, 1u);
-          break;
-        }
-      }
-    }
-    __syncthreads();
+    if (g < kMaxGpus && ((s.post_mask >> g) & 1u)) st_release_sys(s.peer_pad[g] + kMaxGpus + s.my_gpu, cs.e);
+    if (g < kMaxGpus && ((s.wait_mask >> g) & 1u)) spin_until(s, s.pad + kMaxGpus + g, cs.e);
   }
+  __syncthreads();
   if (threadIdx.x == 0) {
     s.ctr[1] = 0;
-    s.ctr[3] = 0;  // dynamic work counter
+    s.ctr[3] = 0;  // dynamic work counters (local / remote queues)
+    s.ctr[4] = 0;
     __threadfence();
-    atomicExch(s.ctr, e);
+    atomicExch(s.ctr, cs.e);
   }
 }
 
@@ -144,40 +163,55 @@ __device__ __forceinline__ bool cta_share(uint64_t n, uint64_t* a, uint64_t* b) 
 }
 
 // Drives `body(seg, a, b)` over this CTA's work under the partition's mode.
-// Segment fields used: w0 (work-space start) and a length accessor.
+// Dynamic mode keeps two queues: chunks whose data stays on this GPU (no peer
+// dependency: started immediately, hiding the barrier latency) and chunks that
+// touch a peer (handed out only after this CTA confirmed the peers' arrival).
+// The first `remote_ctas` CTAs drain the remote queue first, the rest the
+// local one; both then help with the other queue.
 template <int MODE, class S, class Len, class Body>
 __device__ __forceinline__ void for_each_share(const S* __restrict__ segs, int nseg, const Partition& part,
-                                               uint32_t* work_ctr, Len len, Body body) {
-  if constexpr (MODE == kPartInterleaved) {
-    for (int s = 0; s < nseg; ++s) {
-      const S sg = segs[s];
-      uint64_t a, b;
-      if (cta_share(len(sg), &a, &b)) body(sg, a, b);
-    }
-  } else if constexpr (MODE == kPartDynamic) {
+                                               const SyncArgs& sync, CtaSync& cs, Len len, Body body) {
+  if constexpr (MODE == kPartDynamic) {
     __shared__ uint32_t next;
-    if (threadIdx.x == 0) next = atomicAdd(work_ctr, 1u);
-    __syncthreads();
-    uint32_t c = next;
-    while (c < part.total_chunks) {
+    for (int pass = 0; pass < 2; ++pass) {
+      const bool remote = (pass == 0) == (static_cast<int>(blockIdx.x) < part.remote_ctas);
+      const uint2* table = remote ? part.rchunks : part.chunks;
+      const uint32_t total = remote ? part.rtotal_chunks : part.total_chunks;
+      uint32_t* ctr = sync.ctr + (remote ? 4 : 3);
+      if (total == 0) continue;
+      if (remote && !sync_wait(sync, cs)) return;
+      if (threadIdx.x == 0) next = atomicAdd(ctr, 1u);
       __syncthreads();
-      if (threadIdx.x == 0) next = atomicAdd(work_ctr, 1u);  // prefetch the next chunk index
-      const uint2 t = part.chunks[c];                         // (segment, chunk within segment)
-      const S sg = segs[t.x];
-      const uint64_t a = static_cast<uint64_t>(t.y) * part.chunk, e = a + part.chunk, n = len(sg);
-      body(sg, a, e < n ? e : n);
-      __syncthreads();
-      c = next;
+      uint32_t c = next;
+      while (c < total) {
+        __syncthreads();
+        if (threadIdx.x == 0) next = atomicAdd(ctr, 1u);  // prefetch the next chunk index
+        const uint2 t = table[c];                           // (segment, chunk within segment)
+        const S sg = segs[t.x];
+        const uint64_t a = static_cast<uint64_t>(t.y) * part.chunk, e = a + part.chunk, n = len(sg);
+        body(sg, a, e < n ? e : n);
+        __syncthreads();
+        c = next;
+      }
     }
   } else {
-    const uint64_t lo = blockIdx.x * part.per_cta, hi = lo + part.per_cta;
-    for (int s = part.first_seg[blockIdx.x]; s < nseg; ++s) {
-      const S sg = segs[s];
-      if (sg.w0 >= hi) break;
-      const uint64_t a = (lo > sg.w0 ? lo : sg.w0) - sg.w0;
-      const uint64_t e = sg.w0 + len(sg);
-      const uint64_t b = (hi < e ? hi : e) - sg.w0;
-      if (a < b) body(sg, a, b);
+    if (!sync_wait(sync, cs)) return;
+    if constexpr (MODE == kPartInterleaved) {
+      for (int s = 0; s < nseg; ++s) {
+        const S sg = segs[s];
+        uint64_t a, b;
+        if (cta_share(len(sg), &a, &b)) body(sg, a, b);
+      }
+    } else {
+      const uint64_t lo = blockIdx.x * part.per_cta, hi = lo + part.per_cta;
+      for (int s = part.first_seg[blockIdx.x]; s < nseg; ++s) {
+        const S sg = segs[s];
+        if (sg.w0 >= hi) break;
+        const uint64_t a = (lo > sg.w0 ? lo : sg.w0) - sg.w0;
+        const uint64_t e = sg.w0 + len(sg);
+        const uint64_t b = (hi < e ? hi : e) - sg.w0;
+        if (a < b) body(sg, a, b);
+      }
     }
   }
 }
@@ -224,12 +258,12 @@ struct CopyLen {
 template <int MODE>
 __global__ void __launch_bounds__(512, 2) copy_segments_kernel(const CopySeg* __restrict__ segs, int nseg,
                                                             Partition part, SyncArgs sync) {
-  uint32_t epoch;
-  const bool ok = epoch_barrier(sync, &epoch);
-  if (ok && nseg > 0)
-    for_each_share<MODE>(segs, nseg, part, sync.ctr + 3, CopyLen{},
-                   [](const CopySeg& sg, uint64_t a, uint64_t b) { copy_range(sg.src, sg.dst, a, b); });
-  epoch_finish(sync, epoch);
+  __shared__ CtaSync cs;
+  sync_begin(sync, cs);
+  if (nseg > 0)
+    for_each_share<MODE>(segs, nseg, part, sync, cs, CopyLen{},
+                         [](const CopySeg& sg, uint64_t a, uint64_t b) { copy_range(sg.src, sg.dst, a, b); });
+  epoch_finish(sync, cs);
 }
 
 // ---- TMA bulk-copy engine ------------------------------------------------------
@@ -289,9 +323,9 @@ __global__ void __launch_bounds__(32) copy_segments_tma_kernel(const CopySeg* __
                                                                Partition part, SyncArgs sync) {
   extern __shared__ __align__(128) unsigned char stage_mem[];
   __shared__ __align__(8) uint64_t full[kTmaStages];
-  uint32_t epoch;
-  const bool ok = epoch_barrier(sync, &epoch);
-  if (ok && nseg > 0) {
+  __shared__ CtaSync cs;
+  sync_begin(sync, cs);
+  if (nseg > 0) {
     if (threadIdx.x == 0) {
       for (int i = 0; i < kTmaStages; ++i) mbar_init(&full[i]);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -303,14 +337,26 @@ __global__ void __launch_bounds__(32) copy_segments_tma_kernel(const CopySeg* __
       uint32_t pend_bytes[kTmaStages];
       uint32_t issued = 0;
       bool more = true;
+      // queue order: remote-first CTAs start on peer chunks, the others on local ones
+      int q = static_cast<int>(blockIdx.x) < part.remote_ctas ? 1 : 0, passes = 0;
       auto issue = [&]() {  // claim the next chunk and start its global->smem load
         while (more) {
-          const uint32_t c = atomicAdd(sync.ctr + 3, 1u);
-          if (c >= part.total_chunks) {
+          const bool remote = q == 1;
+          const uint32_t total = remote ? part.rtotal_chunks : part.total_chunks;
+          const uint32_t c = total ? atomicAdd(sync.ctr + (remote ? 4 : 3), 1u) : total;
+          if (c >= total) {
+            if (++passes == 2) {
+              more = false;
+              return;
+            }
+            q ^= 1;
+            continue;
+          }
+          if (remote && !sync_wait_lane(sync, cs)) {
             more = false;
             return;
           }
-          const uint2 t = part.chunks[c];
+          const uint2 t = (remote ? part.rchunks : part.chunks)[c];
           const CopySeg sg = segs[t.x];
           const uint64_t a = static_cast<uint64_t>(t.y) * part.chunk;
           const uint64_t e = a + part.chunk < sg.nbytes ? a + part.chunk : sg.nbytes;
@@ -345,7 +391,7 @@ __global__ void __launch_bounds__(32) copy_segments_tma_kernel(const CopySeg* __
     }
     __syncwarp();
   }
-  epoch_finish(sync, epoch);
+  epoch_finish(sync, cs);
 }
 
 // ---- reduction ---------------------------------------------------------------
@@ -455,16 +501,16 @@ template <class TIn, class TOut, int MODE>
 __global__ void __launch_bounds__(512, 2) reduce_segments_kernel(const ReduceSeg* __restrict__ segs, int nseg,
                                                               const void* const* __restrict__ terms,
                                                               Partition part, float beta, SyncArgs sync) {
-  uint32_t epoch;
-  const bool ok = epoch_barrier(sync, &epoch);
-  if (ok && nseg > 0)
-    for_each_share<MODE>(segs, nseg, part, sync.ctr + 3, ReduceLen{},
-                   [&](const ReduceSeg& sg, uint64_t a, uint64_t b) {
-                     reduce_range<TIn, TOut>(static_cast<TOut*>(sg.dst),
-                                             reinterpret_cast<const TIn* const*>(terms + sg.term0), sg.nterms,
-                                             a, b, beta);
-                   });
-  epoch_finish(sync, epoch);
+  __shared__ CtaSync cs;
+  sync_begin(sync, cs);
+  if (nseg > 0)
+    for_each_share<MODE>(segs, nseg, part, sync, cs, ReduceLen{},
+                         [&](const ReduceSeg& sg, uint64_t a, uint64_t b) {
+                           reduce_range<TIn, TOut>(static_cast<TOut*>(sg.dst),
+                                                   reinterpret_cast<const TIn* const*>(terms + sg.term0),
+                                                   sg.nterms, a, b, beta);
+                         });
+  epoch_finish(sync, cs);
 }
 
 }  // namespace

@@ -49,9 +49,12 @@ struct Partition {
   const int32_t* first_seg;  // [grid] (contiguous mode)
   uint64_t per_cta;          // work units per CTA (contiguous mode; multiple of kQuantum)
   int mode;
-  uint32_t total_chunks;     // dynamic / TMA modes
+  uint32_t total_chunks;     // dynamic / TMA: chunks with no peer dependency
   uint64_t chunk;            // dynamic / TMA chunk size
   const uint2* chunks;       // [total_chunks] (segment, chunk within segment), in hand-out order
+  uint32_t rtotal_chunks;    // dynamic / TMA: chunks that read (pull) or write (push) a peer
+  const uint2* rchunks;      // [rtotal_chunks]
+  int remote_ctas;           // CTAs that start on the remote queue
 };
 
 // Cross-GPU epoch barrier over peer-mapped flag words. Every GPU of an exec
@@ -62,7 +65,7 @@ constexpr int kMaxGpus = 32;
 struct SyncArgs {
   uint32_t* pad;                  // local pad: pad[g] = last epoch posted by GPU g
   uint32_t* peer_pad[kMaxGpus];   // peers' pads (nullptr for self / non-members)
-  uint32_t* ctr;                  // local: [0] epoch, [1] finished-CTA count, [2] error flag
+  uint32_t* ctr;                  // local: [0] epoch, [1] finished CTAs, [2] error, [3]/[4] work queues
   uint32_t wait_mask;             // GPUs to wait for
   uint32_t post_mask;             // GPUs to post to
   int end_sync;                   // push mode: also post/wait "writes done" (pad[32+g]) before exit

@@ -1,5 +1,5 @@
 # full state sweep: N=${N}
-exec > gpurun_out/state_n${N}.log 2>&1
+exec > gpurun_out/state_n${N}${TAG}.log 2>&1
 for c in ${CONFIGS:-c2 c3 c4 c5}; do
   if [ "$N" = "1" ]; then timeout 300 python bench.py --config $c --steps 300 --warmup 10 --no-e2e --no-cpu --no-clocks $EXTRA;
   else timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29580 bench.py --gpus $N --config $c --steps 300 --warmup 10 --no-e2e --no-clocks $EXTRA 2>/dev/null; fi | tail -1 > gpurun_out/state_${c}_n${N}.json
