@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <tuple>
@@ -422,7 +423,12 @@ dev::SyncArgs Exec::make_sync_args() const {
   s.pad = reinterpret_cast<uint32_t*>(local_base_);
   s.ctr = ctr_;
   s.my_gpu = my_gpu_;
-  if (n_gpus_ > 1 && ((group_mask_ >> my_gpu_) & 1u)) {
+  // HB_DEBUG_NO_SYNC=1 drops the cross-GPU barrier (UNSAFE; overhead experiments only).
+  static const bool no_sync = [] {
+    const char* v = std::getenv("HB_DEBUG_NO_SYNC");
+    return v && v[0] == '1';
+  }();
+  if (n_gpus_ > 1 && !no_sync && ((group_mask_ >> my_gpu_) & 1u)) {
     const uint32_t peers = group_mask_ & ~(1u << my_gpu_);
     s.wait_mask = peers;
     s.post_mask = peers;
