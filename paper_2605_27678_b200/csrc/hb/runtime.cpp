@@ -221,7 +221,13 @@ const void* Exec::resolve(int rank, int slot, int mb_slot) const {
 
 namespace {
 constexpr uint64_t kDynCopyChunk = 128 * 1024;   // bytes per dynamic copy chunk
-constexpr uint64_t kDynReduceChunk = 32 * 1024;  // elements per dynamic reduce chunk
+uint64_t env_u64(const char* name, uint64_t dflt) {
+  const char* v = std::getenv(name);
+  return v && *v ? std::strtoull(v, nullptr, 10) : dflt;
+}
+// elements per dynamic reduce chunk; TMA stage size (tuning knobs, HB_RED_CHUNK / HB_TMA_CHUNK_KB)
+const uint64_t kDynReduceChunk = env_u64("HB_RED_CHUNK", 32 * 1024);
+const int kTmaChunkKiB = static_cast<int>(env_u64("HB_TMA_CHUNK_KB", 32));
 uint64_t pad_to(uint64_t x, uint64_t q) { return (x + q - 1) / q * q; }
 }  // namespace
 
@@ -240,7 +246,7 @@ int Exec::reduce_mode() const {
 }
 
 uint64_t Exec::pad_unit(int mode, bool copy) const {
-  if (mode == dev::kPartTma) return dev::tma_chunk_bytes();
+  if (mode == dev::kPartTma) return dev::tma_chunk_bytes(kTmaChunkKiB);
   if (mode == dev::kPartDynamic) return copy ? kDynCopyChunk : kDynReduceChunk;
   return dev::kQuantum;
 }
@@ -335,7 +341,7 @@ void Exec::upload_copies(const std::vector<index::CopySeg>& segs, int mb, uint64
 }
 
 int Exec::copy_grid() const {
-  if (copy_mode() == dev::kPartTma) return sm_count_ * dev::tma_blocks_per_sm();
+  if (copy_mode() == dev::kPartTma) return sm_count_ * dev::tma_blocks_per_sm(dev::tma_chunk_bytes(kTmaChunkKiB));
   const int occ = dev::copy_blocks_per_sm(cfg_.threads);
   return sm_count_ * (cfg_.blocks_per_sm > 0 ? std::min(cfg_.blocks_per_sm, occ) : occ);
 }

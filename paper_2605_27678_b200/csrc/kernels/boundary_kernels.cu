@@ -268,8 +268,8 @@ __global__ void __launch_bounds__(512, 2) copy_segments_kernel(const CopySeg* __
 
 // ---- TMA bulk-copy engine ------------------------------------------------------
 
-constexpr int kTmaStages = 3;
-constexpr uint32_t kTmaStageBytes = 32 * 1024;
+// Stage ring variants (chunk = one stage); selected by Partition::chunk.
+// 3 x 32 KiB (default), 6 x 16 KiB, 8 x 8 KiB: 96 / 96 / 64 KiB of smem.
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -319,6 +319,7 @@ __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wa
 // 32 KiB shared-memory stages: loads for the next stages are in flight while
 // the current stage is stored. Chunks (= one stage) come from the dynamic work
 // counter; unaligned runs fall back to the warp-wide LDG/STG path.
+template <int kTmaStages, uint32_t kTmaStageBytes>
 __global__ void __launch_bounds__(32) copy_segments_tma_kernel(const CopySeg* __restrict__ segs, int nseg,
                                                                Partition part, SyncArgs sync) {
   extern __shared__ __align__(128) unsigned char stage_mem[];
@@ -528,26 +529,38 @@ int copy_blocks_per_sm(int threads) {
   return n > 0 ? n : 1;
 }
 
-int tma_blocks_per_sm() {
+template <int ST, uint32_t SB>
+static int tma_occupancy() {
   static int n = -1;
   if (n < 0) {
-    const int smem = kTmaStages * kTmaStageBytes;
-    cudaFuncSetAttribute(copy_segments_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(copy_segments_tma_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, copy_segments_tma_kernel, 32, smem);
+    const int smem = ST * SB;
+    cudaFuncSetAttribute(copy_segments_tma_kernel<ST, SB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(copy_segments_tma_kernel<ST, SB>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, copy_segments_tma_kernel<ST, SB>, 32, smem);
     if (n < 1) n = 1;
   }
   return n;
 }
 
-uint64_t tma_chunk_bytes() { return kTmaStageBytes; }
+int tma_blocks_per_sm(uint64_t chunk) {
+  if (chunk == 16 * 1024) return tma_occupancy<6, 16 * 1024>();
+  if (chunk == 8 * 1024) return tma_occupancy<8, 8 * 1024>();
+  return tma_occupancy<3, 32 * 1024>();
+}
+
+uint64_t tma_chunk_bytes(int kib) { return (kib == 16 || kib == 8) ? kib * 1024ull : 32 * 1024ull; }
 
 void launch_copy(const CopySeg* segs, int nseg, Partition part, const SyncArgs& sync, LaunchCfg cfg,
                  void* stream) {
   auto st = static_cast<cudaStream_t>(stream);
   if (part.mode == kPartTma) {
-    tma_blocks_per_sm();
-    copy_segments_tma_kernel<<<cfg.grid, 32, kTmaStages * kTmaStageBytes, st>>>(segs, nseg, part, sync);
+    tma_blocks_per_sm(part.chunk);
+    if (part.chunk == 16 * 1024)
+      copy_segments_tma_kernel<6, 16 * 1024><<<cfg.grid, 32, 6 * 16 * 1024, st>>>(segs, nseg, part, sync);
+    else if (part.chunk == 8 * 1024)
+      copy_segments_tma_kernel<8, 8 * 1024><<<cfg.grid, 32, 8 * 8 * 1024, st>>>(segs, nseg, part, sync);
+    else
+      copy_segments_tma_kernel<3, 32 * 1024><<<cfg.grid, 32, 3 * 32 * 1024, st>>>(segs, nseg, part, sync);
   } else if (part.mode == kPartInterleaved) {
     copy_segments_kernel<kPartInterleaved><<<cfg.grid, cfg.block, 0, st>>>(segs, nseg, part, sync);
   } else if (part.mode == kPartDynamic) {

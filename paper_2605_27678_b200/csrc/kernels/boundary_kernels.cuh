@@ -86,8 +86,8 @@ void launch_reduce(const ReduceSeg* segs, int nseg, const void* const* terms, Pa
                    void* stream);
 int device_sm_count();
 int copy_blocks_per_sm(int threads);
-int tma_blocks_per_sm();
-uint64_t tma_chunk_bytes();
+int tma_blocks_per_sm(uint64_t chunk);
+uint64_t tma_chunk_bytes(int kib);  // 32 (default), 16 or 8 KiB stages
 int reduce_blocks_per_sm(int threads, int in_dtype, int out_dtype);
 
 }  // namespace hb::dev
