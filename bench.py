@@ -54,6 +54,7 @@ def parse():
                     help="0 auto, 1 contiguous, 2 interleaved, 3 dynamic, 4 TMA bulk copy")
     ap.add_argument("--no-nccl", action="store_true", help="skip the NCCL comparison leg (N == world)")
     ap.add_argument("--no-graph", action="store_true", help="timed loop: per-op launches instead of CUDA graphs")
+    ap.add_argument("--no-overlap", action="store_true", help="skip the boundary || PP-P2P overlap leg (C5)")
     return ap.parse_args()
 
 
@@ -497,6 +498,10 @@ def main():
     if N > 1 and N == plan.world and not args.no_nccl:
         nccl = run_nccl_comparison(args, cfg, plan, sp, rt, rank, dev, barrier, fwd_b + bwd_b, stream)
 
+    overlap = None
+    if N > 1 and cfg.dst.pp > 1 and cfg.src.rank_offset != cfg.dst.rank_offset and not args.no_overlap:
+        overlap = run_pp_overlap(args, cfg, plan, rt, r2g, rank, dev, barrier, stream, slots)
+
     cpu = None
     if rank == 0 and N == 1 and not args.no_cpu:
         try:
@@ -525,6 +530,7 @@ def main():
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clocks,
             "nccl_comparison": nccl,
+            "overlap_with_pp_p2p": overlap,
         }
         print(json.dumps(line), flush=True)
     rt.close()
@@ -640,6 +646,73 @@ def run_e2e(args, cfg, rt, local, stream, N, dev, barrier, payload, slots):
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": K, "buffer_sets": S,
             "path": "BridgeRuntime.forward/backward (C-ABI hb_exec_*) with pinned host buffers; "
                     "H2D / boundary / D2H streams pipelined over buffer sets"}
+
+
+def run_pp_overlap(args, cfg, plan, rt, r2g, rank, dev, barrier, stream, slots):
+    """C5: boundary traffic (high-priority stream) overlapped with the LLM's
+    pipeline P2P (NCCL send/recv of one microbatch's stage activations between
+    consecutive PP stages, on a normal-priority stream). Reports each alone and
+    both together; overlap = (t_b + t_p - t_both) / min(t_b, t_p)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_27678_b200 import grid as hbg
+
+    llm = cfg.dst
+    # PP hops: (stage p rank) -> (stage p+1 rank) with identical tp/cp/dp coordinates
+    hops = []
+    for r in range(llm.rank_begin(), llm.rank_end()):
+        c = hbg.coord_of_rank(llm, r)
+        if c.pp_idx + 1 < llm.pp:
+            nxt = hbg.rank_of_coord(llm, hbg.GridCoord(c.tp_idx, c.cp_idx, c.pp_idx + 1, c.dp_idx))
+            if r2g[r] != r2g[nxt]:
+                hops.append((r, nxt))
+    nbytes = plan.dest_intervals[0].length * cfg.width  # one microbatch of stage activations (elements)
+    bufs = {h: torch.empty(nbytes, dtype=torch.bfloat16, device=dev) for h in hops
+            if rank in (r2g[h[0]], r2g[h[1]])}
+    pp_stream = torch.cuda.Stream(priority=0)
+
+    def pp_p2p():
+        ops = []
+        for (a, b), t in bufs.items():
+            if r2g[a] == rank:
+                ops.append(dist.P2POp(dist.isend, t, r2g[b]))
+            if r2g[b] == rank:
+                ops.append(dist.P2POp(dist.irecv, t, r2g[a]))
+        if ops:
+            with torch.cuda.stream(pp_stream):
+                for w in dist.batch_isend_irecv(ops):
+                    w.wait()
+
+    def boundary(i):
+        rt.replay_step(i % slots, stream)
+
+    def timed(fn, reps=10):
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        pp_stream.wait_stream(stream)
+        for i in range(reps):
+            fn(i)
+        stream.wait_stream(pp_stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1) / reps], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.item()
+
+    pp_p2p()  # warm up NCCL connections
+    torch.cuda.synchronize()
+    t_b = timed(boundary)
+    t_p = timed(lambda i: pp_p2p())
+    t_both = timed(lambda i: (pp_p2p(), boundary(i)))
+    overlap = (t_b + t_p - t_both) / max(1e-9, min(t_b, t_p))
+    return {"boundary_ms": round(t_b, 4), "pp_p2p_ms": round(t_p, 4), "both_ms": round(t_both, 4),
+            "overlap": round(overlap, 3), "pp_hops": [[a, b] for a, b in hops],
+            "pp_bytes_per_hop": nbytes * 2,
+            "how": "boundary fwd+bwd CUDA graph on a high-priority stream; PP stage activations via NCCL "
+                   "send/recv on a normal-priority stream, issued together"}
 
 
 def run_nccl_comparison(args, cfg, plan, sp, rt, rank, dev, barrier, payload, stream):
