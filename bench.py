@@ -702,6 +702,8 @@ def run_pp_overlap(args, cfg, plan, rt, r2g, rank, dev, barrier, stream, slots):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return t.item()
 
+    for k in range(slots):  # (re)capture the boundary step graphs on this stream
+        rt.capture_step(k, cfg.beta, True, stream)
     pp_p2p()  # warm up NCCL connections
     torch.cuda.synchronize()
     t_b = timed(boundary)
