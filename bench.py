@@ -371,8 +371,6 @@ def main():
     sampler.start()
     time.sleep(0.1)
     K = args.steps
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
-           torch.cuda.Event(enable_timing=True)) for _ in range(K)]
     use_graph = not args.no_graph
     if use_graph:  # one CUDA graph per buffer set: forward + backward(beta)
         for k in range(slots):
@@ -383,61 +381,50 @@ def main():
     launches0 = rt.stats()["launches"]
     barrier()
     sampler.mark(True)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
     for i in range(K):
-        e0, e1, e2 = ev[i]
-        e0.record(stream)
         if use_graph:
             rt.replay_step(mb % slots, stream)
         else:
             rt.forward(mb, stream)
-            e1.record(stream)
             rt.backward(mb, cfg.beta, stream)
-        e2.record(stream)
         mb += 1
+    t1.record(stream)
     stream.synchronize()
     sampler.mark(False)
     barrier()
     launches = rt.stats()["launches"] - launches0
-    total_ms = ev[0][0].elapsed_time(ev[-1][2])
-    fwd_ms = 0.0 if use_graph else sum(e[0].elapsed_time(e[1]) for e in ev) / K
-    bwd_ms = 0.0 if use_graph else sum(e[1].elapsed_time(e[2]) for e in ev) / K
-    t = torch.tensor([total_ms, fwd_ms, bwd_ms], dtype=torch.float64, device=dev)
+    t = torch.tensor([t0.elapsed_time(t1)], dtype=torch.float64, device=dev)
     if N > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms, fwd_ms, bwd_ms = t.tolist()
-    ms_step = total_ms / K
+    ms_step = t.item() / K
     clocks = sampler.stop()
     if rt.status():
         raise RuntimeError("device flag wait timed out")
 
-    # isolated per-kernel timing (for the roofline of each kernel; not the headline)
-    align = torch.zeros(1, device=dev)
-    iso = []
-    for i in range(min(K, 20)):
-        row = []
-        for op in ("fwd", "bwd"):
-            barrier()
-            if N > 1:  # align the GPUs on the device so launch skew is not timed
-                with torch.cuda.stream(stream):
-                    dist.all_reduce(align)
-            with torch.cuda.stream(stream):  # keep the GPU busy while the host enqueues: no host gap timed
-                torch.cuda._sleep(100_000)
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            if op == "fwd":
-                rt.forward(mb, stream)
-            else:
-                rt.backward(mb, cfg.beta, stream)
-            e1.record(stream)
-            stream.synchronize()
-            row.append(e0.elapsed_time(e1))
-        mb += 1
-        iso.append(row)
-    t = torch.tensor([sum(r[0] for r in iso) / len(iso), sum(r[1] for r in iso) / len(iso)],
-                     dtype=torch.float64, device=dev)
+    # per-kernel steady state: each op alone, replayed back to back as a CUDA graph
+    # (includes its share of launch and barrier cost; the headline is the step above)
+    K2 = max(20, min(K, 200))
+    per = []
+    for what in (0, 2):
+        for k in range(slots):
+            rt.capture_step(k, cfg.beta, stream=stream, what=what)
+        for k in range(slots):
+            rt.replay_step(k, stream, what)
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for i in range(K2):
+            rt.replay_step(i % slots, stream, what)
+        b.record(stream)
+        stream.synchronize()
+        per.append(a.elapsed_time(b) / K2)
+    t = torch.tensor(per, dtype=torch.float64, device=dev)
     if N > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     iso_fwd_ms, iso_bwd_ms = t.tolist()
+    barrier()
 
     fwd_b, bwd_b = payload_bytes(cfg)
     value = (fwd_b + bwd_b) / (ms_step * 1e-3) / 1e9
@@ -478,8 +465,8 @@ def main():
         "traffic": traffic,
         "peak_source": pk["src"] if dom["bound"] == "hbm" else "measured peer copy 770 GB/s (B200_PROFILING.md)",
         "per_kernel": {"fwd": fk, "bwd": bk,
-                       "timing": "isolated: each kernel bracketed by a device+host barrier, CUDA events, "
-                                 "mean over steps, max over ranks"},
+                       "timing": "each op alone replayed back to back as a CUDA graph (steady state incl. "
+                                 "launch + barrier share), CUDA events, max over ranks"},
         "step_tstar_ms_measured_peaks": round(tstar_step, 4),
         "step_frac_of_tstar": round(tstar_step / ms_step, 4),
     }

@@ -156,10 +156,11 @@ int hb_exec_forward(hb_exec* x, int mb, void* cuda_stream);
 /* backward: BridgeRuntime::backward_* ; src_grad = beta*src_grad + returned gradient */
 int hb_exec_backward(hb_exec* x, int mb, float beta, void* cuda_stream);
 int hb_exec_seed_forward_record(hb_exec* x, int mb); /* bridge.hpp:165 */
-/* CUDA graph of one buffer set's forward (+ backward with beta when with_bwd):
- * one graph launch per step; replays bypass the microbatch records. */
-int hb_exec_graph_capture(hb_exec* x, int mb_slot, int with_bwd, float beta, void* cuda_stream);
-int hb_exec_graph_launch(hb_exec* x, int mb_slot, void* cuda_stream);
+/* CUDA graph of one buffer set's boundary ops; what: 0 forward, 1 forward +
+ * backward(beta), 2 backward(beta). One graph launch replays the ops; replays
+ * bypass the microbatch records. */
+int hb_exec_graph_capture(hb_exec* x, int mb_slot, int what, float beta, void* cuda_stream);
+int hb_exec_graph_launch(hb_exec* x, int mb_slot, int what, void* cuda_stream);
 int hb_exec_status(hb_exec* x, unsigned* device_error);
 int hb_exec_stats(hb_exec* x, long long* fwd_segments, long long* bwd_segments,
                   long long* fwd_bytes, long long* bwd_elems, long long* launches);

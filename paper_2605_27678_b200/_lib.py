@@ -119,7 +119,7 @@ def _declare(L):
         "hb_exec_backward": (I, [V, I, ctypes.c_float, V]),
         "hb_exec_seed_forward_record": (I, [V, I]),
         "hb_exec_graph_capture": (I, [V, I, I, ctypes.c_float, V]),
-        "hb_exec_graph_launch": (I, [V, I, V]),
+        "hb_exec_graph_launch": (I, [V, I, I, V]),
         "hb_exec_status": (I, [V, P(U)]),
         "hb_exec_stats": (I, [V, P(LL), P(LL), P(LL), P(LL), P(LL)]),
     }

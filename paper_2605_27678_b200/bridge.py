@@ -308,13 +308,16 @@ class BridgeRuntime:
     def backward(self, mb: int = 0, beta: float = 0.0, stream=None):
         check(lib().hb_exec_backward(self._h, mb, ctypes.c_float(beta), self._stream(stream)))
 
-    def capture_step(self, mb_slot: int = 0, beta: float = 1.0, with_backward: bool = True, stream=None):
-        """Capture forward (+ backward) of one buffer set into a CUDA graph."""
-        check(lib().hb_exec_graph_capture(self._h, mb_slot, 1 if with_backward else 0, ctypes.c_float(beta),
-                                          self._stream(stream)))
+    GRAPH_FWD, GRAPH_STEP, GRAPH_BWD = 0, 1, 2
 
-    def replay_step(self, mb_slot: int = 0, stream=None):
-        check(lib().hb_exec_graph_launch(self._h, mb_slot, self._stream(stream)))
+    def capture_step(self, mb_slot: int = 0, beta: float = 1.0, with_backward: bool = True, stream=None,
+                     what: int | None = None):
+        """Capture one buffer set's ops into a CUDA graph (what: 0 fwd, 1 fwd+bwd, 2 bwd)."""
+        what = (1 if with_backward else 0) if what is None else what
+        check(lib().hb_exec_graph_capture(self._h, mb_slot, what, ctypes.c_float(beta), self._stream(stream)))
+
+    def replay_step(self, mb_slot: int = 0, stream=None, what: int = 1):
+        check(lib().hb_exec_graph_launch(self._h, mb_slot, what, self._stream(stream)))
 
     def seed_forward_record(self, mb: int):
         check(lib().hb_exec_seed_forward_record(self._h, mb))

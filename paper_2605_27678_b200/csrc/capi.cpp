@@ -360,17 +360,17 @@ int hb_exec_backward(hb_exec* x, int mb, float beta, void* stream) {
   });
 }
 
-int hb_exec_graph_capture(hb_exec* x, int mb_slot, int with_bwd, float beta, void* stream) {
+int hb_exec_graph_capture(hb_exec* x, int mb_slot, int what, float beta, void* stream) {
   return guard([&] {
     need(x, "exec");
-    x->x->graph_capture(mb_slot, with_bwd != 0, beta, stream);
+    x->x->graph_capture(mb_slot, what, beta, stream);
   });
 }
 
-int hb_exec_graph_launch(hb_exec* x, int mb_slot, void* stream) {
+int hb_exec_graph_launch(hb_exec* x, int mb_slot, int what, void* stream) {
   return guard([&] {
     need(x, "exec");
-    x->x->graph_launch(mb_slot, stream);
+    x->x->graph_launch(mb_slot, what, stream);
   });
 }
 

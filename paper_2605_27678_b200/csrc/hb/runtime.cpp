@@ -126,8 +126,7 @@ Exec::Exec(const bridge::BridgePlan& plan, const index::SpliceSpec* splice, int 
 }
 
 Exec::~Exec() {
-  for (void* g : graphs_)
-    if (g) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(g));
+  for (auto& kv : graphs_) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(kv.second.first));
   for (auto& t : tables_) {
     cudaFree(t.copy);
     cudaFree(t.reduce);
@@ -486,38 +485,38 @@ void Exec::backward(int mb, float beta, void* stream) {
   fwd_done_.erase(mb);
 }
 
-void Exec::graph_capture(int mb_slot, bool with_bwd, float beta, void* stream) {
+void Exec::graph_capture(int mb_slot, int what, float beta, void* stream) {
   if (mb_slot < 0 || mb_slot >= cfg_.mb_slots) raise(ErrorCode::InvalidArgument, "mb slot out of range");
+  if (what < 0 || what > 2) raise(ErrorCode::InvalidArgument, "graph 'what' must be 0 (fwd), 1 (fwd+bwd), 2 (bwd)");
   if (!stream) raise(ErrorCode::InvalidArgument, "graph capture needs a non-default stream");
-  prepare_fwd();
-  if (with_bwd) prepare_bwd();
-  graphs_.resize(cfg_.mb_slots, nullptr);
-  graph_kernels_.resize(cfg_.mb_slots, 0);
-  if (graphs_[mb_slot]) {
-    cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(graphs_[mb_slot]));
-    graphs_[mb_slot] = nullptr;
+  if (what != 2) prepare_fwd();
+  if (what != 0) prepare_bwd();
+  const auto key = std::make_pair(mb_slot, what);
+  auto it = graphs_.find(key);
+  if (it != graphs_.end()) {
+    cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(it->second.first));
+    graphs_.erase(it);
   }
   auto st = static_cast<cudaStream_t>(stream);
   const int before = launches_;
   ck(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
-  launch_forward(mb_slot, stream);
-  if (with_bwd) launch_backward(mb_slot, beta, stream);
+  if (what != 2) launch_forward(mb_slot, stream);
+  if (what != 0) launch_backward(mb_slot, beta, stream);
   cudaGraph_t g = nullptr;
   ck(cudaStreamEndCapture(st, &g), "cudaStreamEndCapture");
   cudaGraphExec_t ge = nullptr;
   ck(cudaGraphInstantiate(&ge, g, 0), "cudaGraphInstantiate");
   cudaGraphDestroy(g);
-  graphs_[mb_slot] = ge;
-  graph_kernels_[mb_slot] = launches_ - before;
+  graphs_[key] = {ge, launches_ - before};
   launches_ = before;  // captured launches are counted when replayed
 }
 
-void Exec::graph_launch(int mb_slot, void* stream) {
-  if (mb_slot < 0 || mb_slot >= static_cast<int>(graphs_.size()) || !graphs_[mb_slot])
-    raise(ErrorCode::InvalidArgument, "no graph captured for this mb slot");
-  ck(cudaGraphLaunch(static_cast<cudaGraphExec_t>(graphs_[mb_slot]), static_cast<cudaStream_t>(stream)),
+void Exec::graph_launch(int mb_slot, int what, void* stream) {
+  auto it = graphs_.find(std::make_pair(mb_slot, what));
+  if (it == graphs_.end()) raise(ErrorCode::InvalidArgument, "no graph captured for this (mb slot, what)");
+  ck(cudaGraphLaunch(static_cast<cudaGraphExec_t>(it->second.first), static_cast<cudaStream_t>(stream)),
      "cudaGraphLaunch");
-  launches_ += graph_kernels_[mb_slot];
+  launches_ += it->second.second;
 }
 
 void Exec::seed_forward_record(int mb) { fwd_done_.insert(mb); }

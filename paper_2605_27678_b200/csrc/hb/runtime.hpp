@@ -16,6 +16,7 @@
 #pragma once
 
 #include <cstdint>
+#include <map>
 #include <memory>
 #include <set>
 #include <vector>
@@ -63,8 +64,9 @@ class Exec {
   // CUDA-graph capture of one buffer set's forward (+ backward with `beta`):
   // the step is replayed with one graph launch (no per-kernel host overhead).
   // Replays bypass the microbatch records (a replay is a complete fwd+bwd).
-  void graph_capture(int mb_slot, bool with_bwd, float beta, void* stream);
-  void graph_launch(int mb_slot, void* stream);
+  // what: 0 forward only, 1 forward + backward, 2 backward only.
+  void graph_capture(int mb_slot, int what, float beta, void* stream);
+  void graph_launch(int mb_slot, int what, void* stream);
   uint32_t device_error() const;  // synchronises
 
   const index::IndexMap& map() const { return map_; }
@@ -148,8 +150,7 @@ class Exec {
   int sm_count_ = 0;
   int launches_ = 0;
   std::set<int> fwd_done_;
-  std::vector<void*> graphs_;       // cudaGraphExec_t per mb slot
-  std::vector<int> graph_kernels_;  // kernels per replay
+  std::map<std::pair<int, int>, std::pair<void*, int>> graphs_;  // (slot, what) -> (cudaGraphExec_t, kernels)
   void launch_forward(int mb_slot, void* stream);
   void launch_backward(int mb_slot, float beta, void* stream);
 };

@@ -379,6 +379,13 @@ def test_cuda_graph_replay_matches_direct_calls():
         outs.append([rt.buffer(r, sl, k).clone() for k in range(2) for r in range(8)
                      for sl in (hbb.SLOT_DST_ACT, hbb.SLOT_SRC_GRAD)])
         assert rt.stats()["launches"] == 8
+        if use_graph:  # forward-only and backward-only graphs replay too
+            rt.capture_step(0, 1.0, stream=st, what=rt.GRAPH_FWD)
+            rt.capture_step(0, 1.0, stream=st, what=rt.GRAPH_BWD)
+            rt.replay_step(0, st, rt.GRAPH_FWD)
+            rt.replay_step(0, st, rt.GRAPH_BWD)
+            st.synchronize()
+            assert rt.stats()["launches"] == 10
         rt.close()
     for a, b in zip(*outs):
         assert torch.equal(a, b)
