@@ -7,6 +7,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <string>
 #include <tuple>
 
 namespace hb::rt {
@@ -240,12 +241,17 @@ int Exec::copy_mode() const {
 }
 
 int Exec::reduce_mode() const {
+  // HB_RED_ENGINE=ldg keeps the LDG/STG reduce under the TMA copy partition
+  static const bool ldg = [] {
+    const char* v = std::getenv("HB_RED_ENGINE");
+    return v && std::string(v) == "ldg";
+  }();
   const int m = copy_mode();
-  return m == dev::kPartTma ? dev::kPartDynamic : m;
+  return (m == dev::kPartTma && ldg) ? dev::kPartDynamic : m;
 }
 
 uint64_t Exec::pad_unit(int mode, bool copy) const {
-  if (mode == dev::kPartTma) return dev::tma_chunk_bytes(kTmaChunkKiB);
+  if (mode == dev::kPartTma) return copy ? dev::tma_chunk_bytes(kTmaChunkKiB) : dev::reduce_tma_chunk_elems();
   if (mode == dev::kPartDynamic) return copy ? kDynCopyChunk : kDynReduceChunk;
   return dev::kQuantum;
 }
@@ -409,7 +415,8 @@ void Exec::prepare_bwd() {
       ck(cudaMemcpy(T.terms, terms.data(), terms.size() * sizeof(void*), cudaMemcpyHostToDevice), "upload");
     }
   }
-  const int occ = dev::reduce_blocks_per_sm(cfg_.threads, cfg_.grad_in_dtype, cfg_.grad_out_dtype);
+  const int occ = mode == dev::kPartTma ? dev::reduce_tma_blocks_per_sm(cfg_.grad_in_dtype, cfg_.grad_out_dtype)
+                                        : dev::reduce_blocks_per_sm(cfg_.threads, cfg_.grad_in_dtype, cfg_.grad_out_dtype);
   const int bps = cfg_.blocks_per_sm > 0 ? std::min(cfg_.blocks_per_sm, occ) : occ;
   std::vector<char> rem;
   double lb = 0, rb = 0;

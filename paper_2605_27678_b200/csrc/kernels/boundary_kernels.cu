@@ -498,6 +498,172 @@ struct ReduceLen {
   __device__ uint64_t operator()(const ReduceSeg& s) const { return s.nelem; }
 };
 
+// ---- TMA reduce engine -----------------------------------------------------------
+//
+// One warp per CTA. Lane 0 streams (term chunk, accumulator chunk) pairs into a
+// ring of shared-memory stages with TMA bulk loads; the warp computes
+// acc = beta*acc + term in fp32 in shared memory and lane 0 bulk-stores the
+// accumulator chunk back. Remote (NVLink) term latency is hidden by the ring
+// instead of by thread count. Chunks with more than one term (cp sums of a
+// non-splice edge) or unaligned tails are reduced by the warp with plain loads.
+constexpr int kRedStages = 4;
+constexpr uint32_t kRedElems = 4096;  // elements per chunk (= one stage)
+
+template <class TIn, class TOut>
+__global__ void __launch_bounds__(32) reduce_segments_tma_kernel(const ReduceSeg* __restrict__ segs, int nseg,
+                                                                 const void* const* __restrict__ terms,
+                                                                 Partition part, float beta, SyncArgs sync) {
+  constexpr uint32_t kTB = kRedElems * sizeof(TIn), kDB = kRedElems * sizeof(TOut);
+  extern __shared__ __align__(128) unsigned char red_mem[];  // kRedStages x (term | acc)
+  __shared__ __align__(8) uint64_t full[kRedStages];
+  struct Pend {
+    TOut* dst;
+    const TIn* term;  // single term (nullptr: none)
+    const TIn* const* tp;
+    uint64_t off;  // chunk offset inside the segment (for the term pointers)
+    uint32_t n;
+    int nterms;
+    int tma;  // 1: staged through smem by TMA, 0: warp reduces from global
+  };
+  __shared__ Pend pend[kRedStages];
+  __shared__ CtaSync cs;
+  __shared__ uint32_t issued_sh;
+  sync_begin(sync, cs);
+  if (nseg > 0) {
+    if (threadIdx.x == 0) {
+      for (int i = 0; i < kRedStages; ++i) mbar_init(&full[i]);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    const int lane = threadIdx.x;
+    int q = static_cast<int>(blockIdx.x) < part.remote_ctas ? 1 : 0, passes = 0;
+    bool more = true;
+    uint32_t issued = 0;
+    // lane 0 claims the next chunk, records it in pend[], starts its TMA loads
+    auto issue = [&]() {
+      while (more) {
+        const bool remote = q == 1;
+        const uint32_t total = remote ? part.rtotal_chunks : part.total_chunks;
+        const uint32_t c = total ? atomicAdd(sync.ctr + (remote ? 4 : 3), 1u) : total;
+        if (c >= total) {
+          if (++passes == 2) {
+            more = false;
+            return;
+          }
+          q ^= 1;
+          continue;
+        }
+        if (remote && !sync_wait_lane(sync, cs)) {
+          more = false;
+          return;
+        }
+        const uint2 t = (remote ? part.rchunks : part.chunks)[c];
+        const ReduceSeg sg = segs[t.x];
+        const uint64_t a = static_cast<uint64_t>(t.y) * part.chunk;
+        const uint64_t e = a + part.chunk < sg.nelem ? a + part.chunk : sg.nelem;
+        const uint32_t n = static_cast<uint32_t>(e - a);
+        const int st = issued % kRedStages;
+        Pend p;
+        p.dst = static_cast<TOut*>(sg.dst) + a;
+        p.tp = reinterpret_cast<const TIn* const*>(terms + sg.term0);
+        p.nterms = sg.nterms;
+        p.term = sg.nterms == 1 ? p.tp[0] + a : nullptr;
+        p.off = a;
+        p.n = n;
+        const uint64_t al = reinterpret_cast<uint64_t>(p.dst) | reinterpret_cast<uint64_t>(p.term) |
+                            (static_cast<uint64_t>(n) * sizeof(TIn)) | (static_cast<uint64_t>(n) * sizeof(TOut));
+        p.tma = sg.nterms <= 1 && (al & 15) == 0;
+        if (p.tma) {
+          const uint32_t tb = p.term ? n * sizeof(TIn) : 0, db = beta != 0.0f ? n * sizeof(TOut) : 0;
+          unsigned char* base = red_mem + st * (kTB + kDB);
+          mbar_expect(&full[st], tb + db);
+          if (tb) bulk_g2s(base, p.term, tb, &full[st]);
+          if (db) bulk_g2s(base + kTB, p.dst, db, &full[st]);  // tb+db == 0: the arrive completes the phase
+        } else {
+          mbar_expect(&full[st], 0);  // keep the stage's phase count in step with k / kRedStages
+        }
+        pend[st] = p;
+        ++issued;
+        return;
+      }
+    };
+    if (lane == 0) {
+      for (int i = 0; i < kRedStages; ++i) issue();
+      issued_sh = issued;
+    }
+    __syncwarp();
+    uint32_t k = 0;
+    while (true) {
+      __syncwarp();
+      const uint32_t avail = issued_sh;
+      if (k >= avail) break;
+      const int st = k % kRedStages;
+      const Pend p = pend[st];
+      if (p.tma) {
+        mbar_wait(&full[st], (k / kRedStages) & 1u);
+        const TIn* T = reinterpret_cast<const TIn*>(red_mem + st * (kTB + kDB));
+        TOut* D = reinterpret_cast<TOut*>(red_mem + st * (kTB + kDB) + kTB);
+        for (uint32_t i = lane * 8; i < p.n; i += 32 * 8) {  // n is a multiple of 8 (16-B aligned bytes)
+          float acc[8];
+          if (p.term) {
+            const uint4* tv = reinterpret_cast<const uint4*>(T + i);
+            uint4 v[sizeof(TIn) * 8 / 16];
+#pragma unroll
+            for (int j = 0; j < static_cast<int>(sizeof(TIn) * 8 / 16); ++j) v[j] = tv[j];
+            const TIn* e = reinterpret_cast<const TIn*>(v);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[j] = 0.0f + Cvt<TIn>::to(e[j]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[j] = 0.0f;
+          }
+          if (beta != 0.0f) {
+            const uint4* dv = reinterpret_cast<const uint4*>(D + i);
+            uint4 v[sizeof(TOut) * 8 / 16];
+#pragma unroll
+            for (int j = 0; j < static_cast<int>(sizeof(TOut) * 8 / 16); ++j) v[j] = dv[j];
+            const TOut* o = reinterpret_cast<const TOut*>(v);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[j] = fmaf(beta, Cvt<TOut>::to(o[j]), acc[j]);
+          }
+          uint4 w[sizeof(TOut) * 8 / 16];
+          TOut* we = reinterpret_cast<TOut*>(w);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) we[j] = Cvt<TOut>::from(acc[j]);
+          uint4* dw = reinterpret_cast<uint4*>(D + i);
+#pragma unroll
+          for (int j = 0; j < static_cast<int>(sizeof(TOut) * 8 / 16); ++j) dw[j] = w[j];
+        }
+        __syncwarp();
+        if (lane == 0) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          bulk_s2g(p.dst, D, p.n * sizeof(TOut));
+        }
+      } else {  // multi-term or unaligned: the warp reduces straight from global memory
+        mbar_wait(&full[st], (k / kRedStages) & 1u);
+        for (uint32_t i = lane; i < p.n; i += 32) {
+          float acc = 0.0f;
+          for (int t = 0; t < p.nterms; ++t) acc += Cvt<TIn>::to(p.tp[t][p.off + i]);
+          if (beta != 0.0f) acc = fmaf(beta, Cvt<TOut>::to(p.dst[i]), acc);
+          p.dst[i] = Cvt<TOut>::from(acc);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        if (k >= 1 && more) {
+          bulk_wait_read<1>();  // the store of chunk k-1 has read its stage
+          issue();
+        }
+        issued_sh = issued;
+      }
+      ++k;
+    }
+    if (lane == 0) bulk_wait_all();
+    __syncwarp();
+  }
+  epoch_finish(sync, cs);
+}
+
 template <class TIn, class TOut, int MODE>
 __global__ void __launch_bounds__(512, 2) reduce_segments_kernel(const ReduceSeg* __restrict__ segs, int nseg,
                                                               const void* const* __restrict__ terms,
@@ -571,9 +737,26 @@ void launch_copy(const CopySeg* segs, int nseg, Partition part, const SyncArgs& 
 }
 
 template <class TIn, class TOut>
+static int red_tma_occupancy() {
+  static int n = -1;
+  if (n < 0) {
+    const int smem = kRedStages * kRedElems * (sizeof(TIn) + sizeof(TOut));
+    cudaFuncSetAttribute(reduce_segments_tma_kernel<TIn, TOut>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(reduce_segments_tma_kernel<TIn, TOut>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, reduce_segments_tma_kernel<TIn, TOut>, 32, smem);
+    if (n < 1) n = 1;
+  }
+  return n;
+}
+
+template <class TIn, class TOut>
 static void launch_reduce_t(const ReduceSeg* segs, int nseg, const void* const* terms, Partition part,
                             float beta, const SyncArgs& sync, int grid, int block, cudaStream_t st) {
-  if (part.mode == kPartInterleaved)
+  if (part.mode == kPartTma) {
+    red_tma_occupancy<TIn, TOut>();
+    const int smem = kRedStages * kRedElems * (sizeof(TIn) + sizeof(TOut));
+    reduce_segments_tma_kernel<TIn, TOut><<<grid, 32, smem, st>>>(segs, nseg, terms, part, beta, sync);
+  } else if (part.mode == kPartInterleaved)
     reduce_segments_kernel<TIn, TOut, kPartInterleaved><<<grid, block, 0, st>>>(segs, nseg, terms, part, beta, sync);
   else if (part.mode == kPartDynamic)
     reduce_segments_kernel<TIn, TOut, kPartDynamic><<<grid, block, 0, st>>>(segs, nseg, terms, part, beta, sync);
@@ -601,6 +784,16 @@ static int occ_t(int threads) {
     case kFP32 * 4 + kFP32: MACRO(float, float); break;                 \
     default: break;                                                   \
   }
+
+int reduce_tma_blocks_per_sm(int in_dtype, int out_dtype) {
+  int n = 1;
+#define HB_OCC2(TI, TO) n = red_tma_occupancy<TI, TO>()
+  HB_DISPATCH(in_dtype, out_dtype, HB_OCC2)
+#undef HB_OCC2
+  return n;
+}
+
+uint64_t reduce_tma_chunk_elems() { return kRedElems; }
 
 int reduce_blocks_per_sm(int threads, int in_dtype, int out_dtype) {
   int n = 1;

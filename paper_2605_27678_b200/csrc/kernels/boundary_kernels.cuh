@@ -42,7 +42,7 @@ enum PartMode : int {
   kPartDynamic = 2,      // `chunk`-sized pieces handed out by an atomic counter (ctr[3]) in the
                          // order of a host-built table that advances every segment at the
                          // same fractional pace (local HBM and remote NVLink runs overlap)
-  kPartTma = 3,          // dynamic chunks moved by TMA bulk copies (copy kernel only)
+  kPartTma = 3,          // dynamic chunks staged through shared memory by TMA bulk copies
 };
 
 struct Partition {
@@ -89,5 +89,7 @@ int copy_blocks_per_sm(int threads);
 int tma_blocks_per_sm(uint64_t chunk);
 uint64_t tma_chunk_bytes(int kib);  // 32 (default), 16 or 8 KiB stages
 int reduce_blocks_per_sm(int threads, int in_dtype, int out_dtype);
+int reduce_tma_blocks_per_sm(int in_dtype, int out_dtype);
+uint64_t reduce_tma_chunk_elems();
 
 }  // namespace hb::dev
