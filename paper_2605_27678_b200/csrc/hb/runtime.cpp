@@ -61,45 +61,41 @@ Exec::Exec(const bridge::BridgePlan& plan, const index::SpliceSpec* splice, int 
   }
   bound_.assign(map_.world * index::kNumSlots, std::vector<void*>(cfg.mb_slots, nullptr));
 
-  // Forward mode. Pull needs one barrier; push needs a second ("writes done")
-  // but its remote stores never stall the issuing warp. Auto picks push when
-  // the NVLink traffic is bidirectional (every GPU that receives also sends),
-  // pull when it is one-way (measured: one-way pull 755 GB/s vs push 701;
-  // bidirectional push 653 vs pull 613, scripts/nvl_probe.py).
-  if (cfg_.fwd_mode == 2) {
-    fwd_push_ = true;
-  } else if (cfg_.fwd_mode == 0 && n_gpus_ > 1) {
-    std::vector<uint64_t> sent(n_gpus_, 0), recv(n_gpus_, 0);
-    for (const auto& s : map_.fwd) {
-      const int gs = gpu_of(s.src.rank), gd = gpu_of(s.dst.rank);
-      if (gs != gd) {
-        sent[gs] += s.n;
-        recv[gd] += s.n;
-      }
-    }
-    bool any = false, bidir = true;
-    for (int g = 0; g < n_gpus_; ++g) {
-      any |= recv[g] > 0;
-      if ((sent[g] > 0) != (recv[g] > 0)) bidir = false;
-    }
-    fwd_push_ = any && bidir;
+  // Forward mode. Pull (consumers read the owners' HBM) needs one barrier;
+  // push (owners write the consumers' HBM) needs a second "writes done"
+  // barrier. Measured with the host out of the loop (scripts/sweep_probe.py,
+  // N=4, profiles/r01_n4_sweep.log) pull is faster for every config, one-way
+  // and bidirectional (c2w4 68 vs 72 us, c4w4 68 vs 81 us, c2 150 vs 168 us),
+  // so auto means pull; push stays selectable.
+  fwd_push_ = cfg_.fwd_mode == 2 && n_gpus_ > 1;
+  // Fan-out grouping: every destination of one source run that this GPU
+  // executes shares a single read of the run (decided per GPU; the symmetric
+  // layout means no process needs another's grouping).
+  std::map<std::tuple<int, int, int64_t, int64_t>, std::vector<size_t>> groups;
+  std::vector<std::tuple<int, int, int64_t, int64_t>> order;
+  for (size_t i = 0; i < map_.fwd.size(); ++i) {
+    const auto& s = map_.fwd[i];
+    if (gpu_of(fwd_push_ ? s.src.rank : s.dst.rank) != my_gpu_) continue;
+    const auto key = std::make_tuple(s.src.rank, s.src.slot, s.src.off, s.n);
+    auto& g = groups[key];
+    if (g.empty()) order.push_back(key);
+    g.push_back(i);
   }
-  // Dedup: a remote source run needed by several ranks of one GPU crosses
-  // NVLink once (to the first of them); the others copy it locally in phase 2.
-  // Decided on the global map so every process agrees.
-  std::map<std::tuple<int, int, int64_t, int64_t, int>, index::Ref> first_copy;
-  for (const auto& s : map_.fwd) {
-    const int gs = gpu_of(s.src.rank), gd = gpu_of(s.dst.rank);
-    if (gs != gd) {
-      const auto key = std::make_tuple(s.src.rank, s.src.slot, s.src.off, s.n, gd);
-      auto it = first_copy.find(key);
-      if (it != first_copy.end()) {
-        if (gd == my_gpu_) fwd_second_local_.push_back({it->second, s.dst, s.n});
-        continue;
+  for (const auto& key : order) {
+    const auto& idx = groups[key];
+    for (size_t k = 0; k < idx.size(); k += dev::kMaxFan) {
+      FanSeg f;
+      const auto& first = map_.fwd[idx[k]];
+      f.src = first.src;
+      f.n = first.n;
+      f.remote = !fwd_push_ && gpu_of(first.src.rank) != my_gpu_;
+      for (size_t j = k; j < std::min(idx.size(), k + dev::kMaxFan); ++j) {
+        const auto& d = map_.fwd[idx[j]].dst;
+        f.dsts.push_back(d);
+        if (fwd_push_ && gpu_of(d.rank) != my_gpu_) f.remote = true;
       }
-      first_copy.emplace(key, s.dst);
+      fwd_local_.push_back(std::move(f));
     }
-    if (gpu_of(fwd_push_ ? s.src.rank : s.dst.rank) == my_gpu_) fwd_local_.push_back(s);
   }
   for (const auto& s : map_.bwd)
     if (gpu_of(s.dst.rank) == my_gpu_) bwd_local_.push_back(s);
@@ -113,8 +109,6 @@ Exec::Exec(const bridge::BridgePlan& plan, const index::SpliceSpec* splice, int 
   }
   ck(cudaMalloc(&ctr_, 64), "cudaMalloc(ctr)");
   ck(cudaMemset(ctr_, 0, 64), "cudaMemset(ctr)");
-  ck(cudaMalloc(&ctr2_, 64), "cudaMalloc(ctr2)");
-  ck(cudaMemset(ctr2_, 0, 64), "cudaMemset(ctr2)");
   peer_base_.assign(n_gpus_, nullptr);
   peer_base_[my_gpu_] = local_base_;
   tables_.resize(cfg.mb_slots);
@@ -134,13 +128,10 @@ Exec::~Exec() {
     cudaFree(t.terms);
   }
   cudaFree(fwd_part_.first_seg);
-  cudaFree(fwd2_part_.first_seg);
-  for (auto* p : {&fwd_part_, &fwd2_part_, &bwd_part_}) {
+  for (auto* p : {&fwd_part_, &bwd_part_}) {
     cudaFree(p->chunks);
     cudaFree(p->rchunks);
   }
-  for (auto& t : tables_) cudaFree(t.copy2);
-  cudaFree(ctr2_);
   cudaFree(bwd_part_.first_seg);
   for (int g = 0; g < n_gpus_; ++g)
     if (g != my_gpu_ && peer_base_[g]) cudaIpcCloseMemHandle(peer_base_[g]);
@@ -241,13 +232,16 @@ int Exec::copy_mode() const {
 }
 
 int Exec::reduce_mode() const {
-  // HB_RED_ENGINE=ldg keeps the LDG/STG reduce under the TMA copy partition
-  static const bool ldg = [] {
+  // The backward reduce runs the LDG/STG engine over dynamic chunks under the
+  // TMA copy partition: measured at N=1 (C2-C5) it reaches 0.87-0.97 of HBM
+  // while the one-warp TMA-staged reduce reaches 0.29-0.34 (its in-smem fp32
+  // pass is issue-bound). HB_RED_ENGINE=tma selects the TMA reduce.
+  static const bool tma = [] {
     const char* v = std::getenv("HB_RED_ENGINE");
-    return v && std::string(v) == "ldg";
+    return v && std::string(v) == "tma";
   }();
   const int m = copy_mode();
-  return (m == dev::kPartTma && ldg) ? dev::kPartDynamic : m;
+  return (m == dev::kPartTma && !tma) ? dev::kPartDynamic : m;
 }
 
 uint64_t Exec::pad_unit(int mode, bool copy) const {
@@ -320,28 +314,33 @@ void Exec::build_partition(const std::vector<uint64_t>& w0, const std::vector<ui
   out->per_cta = per;
 }
 
-void Exec::upload_copies(const std::vector<index::CopySeg>& segs, int mb, uint64_t unit, dev::CopySeg** out,
-                         std::vector<uint64_t>* w0s, std::vector<uint64_t>* ns) {
+void Exec::upload_copies(int mb, uint64_t unit, std::vector<uint64_t>* w0s, std::vector<uint64_t>* ns) {
   std::vector<dev::CopySeg> cs;
   uint64_t w = 0;
   w0s->clear();
   ns->clear();
-  for (const auto& s : segs) {
-    const int es = dev::dtype_size(slot_dtype(s.src.slot));
-    const uint64_t nbytes = static_cast<uint64_t>(s.n) * es;
-    cs.push_back({static_cast<const unsigned char*>(resolve(s.src.rank, s.src.slot, mb)) + s.src.off * es,
-                  static_cast<unsigned char*>(const_cast<void*>(resolve(s.dst.rank, s.dst.slot, mb))) +
-                      s.dst.off * es,
-                  nbytes, w});
+  for (const auto& f : fwd_local_) {
+    const int es = dev::dtype_size(slot_dtype(f.src.slot));
+    const uint64_t nbytes = static_cast<uint64_t>(f.n) * es;
+    dev::CopySeg c{};
+    c.src = static_cast<const unsigned char*>(resolve(f.src.rank, f.src.slot, mb)) + f.src.off * es;
+    c.ndst = static_cast<int32_t>(f.dsts.size());
+    for (size_t d = 0; d < f.dsts.size(); ++d)
+      c.dst[d] = static_cast<unsigned char*>(const_cast<void*>(resolve(f.dsts[d].rank, f.dsts[d].slot, mb))) +
+                 f.dsts[d].off * es;
+    c.nbytes = nbytes;
+    c.w0 = w;
+    cs.push_back(c);
     w0s->push_back(w);
     ns->push_back(nbytes);
     w = pad_to(w + nbytes, unit);
   }
-  cudaFree(*out);
-  *out = nullptr;
+  dev::CopySeg*& out = tables_[mb].copy;
+  cudaFree(out);
+  out = nullptr;
   if (!cs.empty()) {
-    ck(cudaMalloc(out, cs.size() * sizeof(dev::CopySeg)), "cudaMalloc(copy table)");
-    ck(cudaMemcpy(*out, cs.data(), cs.size() * sizeof(dev::CopySeg), cudaMemcpyHostToDevice), "upload");
+    ck(cudaMalloc(&out, cs.size() * sizeof(dev::CopySeg)), "cudaMalloc(copy table)");
+    ck(cudaMemcpy(out, cs.data(), cs.size() * sizeof(dev::CopySeg), cudaMemcpyHostToDevice), "upload");
   }
 }
 
@@ -355,22 +354,21 @@ void Exec::prepare_fwd() {
   if (!dirty_fwd_) return;
   const int mode = copy_mode();
   const uint64_t unit = pad_unit(mode, true);
-  std::vector<uint64_t> w0s, ns, w0s2, ns2;
-  for (int mb = 0; mb < cfg_.mb_slots; ++mb) {
-    upload_copies(fwd_local_, mb, unit, &tables_[mb].copy, &w0s, &ns);
-    upload_copies(fwd_second_local_, mb, unit, &tables_[mb].copy2, &w0s2, &ns2);
-  }
+  std::vector<uint64_t> w0s, ns;
+  for (int mb = 0; mb < cfg_.mb_slots; ++mb) upload_copies(mb, unit, &w0s, &ns);
   std::vector<char> rem;
   double lb = 0, rb = 0;
   for (size_t i = 0; i < fwd_local_.size(); ++i) {
-    const auto& sg = fwd_local_[i];
-    const bool r = gpu_of(fwd_push_ ? sg.dst.rank : sg.src.rank) != my_gpu_;
-    rem.push_back(r);
-    (r ? rb : lb) += static_cast<double>(ns[i]);
+    const auto& f = fwd_local_[i];
+    rem.push_back(f.remote);
+    // time weights: NVLink bytes of a remote run (one read in pull, one write
+    // per peer destination in push); HBM read + writes of a local run
+    int peer_dsts = 0;
+    for (const auto& d : f.dsts) peer_dsts += gpu_of(d.rank) != my_gpu_;
+    if (f.remote) rb += static_cast<double>(ns[i]) * (fwd_push_ ? peer_dsts : 1);
+    else lb += static_cast<double>(ns[i]) * 0.5 * (1.0 + f.dsts.size());
   }
   build_partition(w0s, ns, rem, lb, rb, copy_grid(), mode, unit, &fwd_part_);
-  if (!fwd_second_local_.empty())
-    build_partition(w0s2, ns2, std::vector<char>(ns2.size(), 0), 1.0, 0.0, copy_grid(), mode, unit, &fwd2_part_);
   dirty_fwd_ = false;
 }
 
@@ -457,15 +455,6 @@ void Exec::launch_forward(int mb_slot, void* stream) {
                    fwd_push_ && n_gpus_ > 1 ? sync_push_ : sync_, {fwd_part_.grid, cfg_.threads}, stream);
   ck(cudaGetLastError(), "copy_segments launch");
   ++launches_;
-  if (!fwd_second_local_.empty()) {
-    dev::SyncArgs local{};
-    local.ctr = ctr2_;
-    local.my_gpu = my_gpu_;
-    dev::launch_copy(T.copy2, static_cast<int>(fwd_second_local_.size()), fwd2_part_.dev(), local,
-                     {fwd2_part_.grid, cfg_.threads}, stream);
-    ck(cudaGetLastError(), "copy_segments (phase 2) launch");
-    ++launches_;
-  }
 }
 
 void Exec::launch_backward(int mb_slot, float beta, void* stream) {
@@ -536,8 +525,8 @@ uint32_t Exec::device_error() const {
 
 uint64_t Exec::local_fwd_bytes() const {
   uint64_t b = 0;
-  for (const auto& s : fwd_local_) b += static_cast<uint64_t>(s.n) * dev::dtype_size(slot_dtype(s.src.slot));
-  for (const auto& s : fwd_second_local_) b += static_cast<uint64_t>(s.n) * dev::dtype_size(slot_dtype(s.src.slot));
+  for (const auto& f : fwd_local_)
+    b += static_cast<uint64_t>(f.n) * f.dsts.size() * dev::dtype_size(slot_dtype(f.src.slot));
   return b;
 }
 

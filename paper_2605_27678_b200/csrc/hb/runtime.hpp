@@ -70,7 +70,7 @@ class Exec {
   uint32_t device_error() const;  // synchronises
 
   const index::IndexMap& map() const { return map_; }
-  int local_fwd_segments() const { return static_cast<int>(fwd_local_.size() + fwd_second_local_.size()); }
+  int local_fwd_segments() const { return static_cast<int>(fwd_local_.size()); }
   int local_bwd_segments() const { return static_cast<int>(bwd_local_.size()); }
   uint64_t local_fwd_bytes() const;
   uint64_t local_bwd_elems() const;
@@ -102,15 +102,20 @@ class Exec {
   std::vector<unsigned char*> peer_base_;
   std::vector<std::vector<void*>> bound_;  // [rank*kNumSlots+slot][mb] external binding
 
-  std::vector<index::CopySeg> fwd_local_;
-  // Phase 2 of the forward: copies of rows a remote owner already delivered to
-  // another rank on this GPU (dedup of repeated remote fetches; local HBM only).
-  std::vector<index::CopySeg> fwd_second_local_;
+  // Forward work of this GPU: source runs with every destination that needs
+  // them (pull: destinations resident here; push: sources resident here), so a
+  // run crosses NVLink / leaves HBM once however many replicas consume it.
+  struct FanSeg {
+    index::Ref src;
+    std::vector<index::Ref> dsts;
+    int64_t n = 0;
+    bool remote = false;  // reads (pull) or writes (push) a peer's buffer
+  };
+  std::vector<FanSeg> fwd_local_;
   std::vector<index::ReduceSeg> bwd_local_;
 
   struct DevTables {
     dev::CopySeg* copy = nullptr;
-    dev::CopySeg* copy2 = nullptr;
     dev::ReduceSeg* reduce = nullptr;
     const void** terms = nullptr;
   };
@@ -131,10 +136,8 @@ class Exec {
       return {first_seg, per_cta, mode, total_chunks, chunk, chunks, rtotal_chunks, rchunks, remote_ctas};
     }
   };
-  DevPartition fwd_part_, fwd2_part_, bwd_part_;
-  uint32_t* ctr2_ = nullptr;  // phase-2 counters (local-only launch)
-  void upload_copies(const std::vector<index::CopySeg>& segs, int mb, uint64_t unit, dev::CopySeg** out,
-                     std::vector<uint64_t>* w0s, std::vector<uint64_t>* ns);
+  DevPartition fwd_part_, bwd_part_;
+  void upload_copies(int mb, uint64_t unit, std::vector<uint64_t>* w0s, std::vector<uint64_t>* ns);
   int copy_mode() const;
   int reduce_mode() const;
   uint64_t pad_unit(int mode, bool copy) const;

@@ -217,19 +217,24 @@ __device__ __forceinline__ void for_each_share(const S* __restrict__ segs, int n
 }
 
 template <class T>
-__device__ __forceinline__ void copy_scalar(const unsigned char* src, unsigned char* dst, uint64_t lo,
-                                            uint64_t hi) {
+__device__ __forceinline__ void copy_scalar(const unsigned char* src, unsigned char* const* dst, int ndst,
+                                            uint64_t lo, uint64_t hi) {
   const T* s = reinterpret_cast<const T*>(src);
-  T* d = reinterpret_cast<T*>(dst);
-  for (uint64_t i = lo / sizeof(T) + threadIdx.x; i < hi / sizeof(T); i += blockDim.x) d[i] = s[i];
+  for (uint64_t i = lo / sizeof(T) + threadIdx.x; i < hi / sizeof(T); i += blockDim.x) {
+    const T v = s[i];
+    for (int d = 0; d < ndst; ++d) reinterpret_cast<T*>(dst[d])[i] = v;
+  }
 }
 
 constexpr int kUnroll = 8;
 
-// Copies bytes [a, b) of one segment with the whole CTA.
-__device__ __forceinline__ void copy_range(const unsigned char* __restrict__ src,
-                                           unsigned char* __restrict__ dst, uint64_t a, uint64_t b) {
-  const uint64_t align = reinterpret_cast<uint64_t>(src) | reinterpret_cast<uint64_t>(dst) | a;
+// Copies bytes [a, b) of one segment to each of its destinations with the
+// whole CTA: every 16 B of the source is loaded once and stored ndst times.
+__device__ __forceinline__ void copy_range(const CopySeg& sg, uint64_t a, uint64_t b) {
+  const unsigned char* __restrict__ src = sg.src;
+  const int nd = sg.ndst;
+  uint64_t align = reinterpret_cast<uint64_t>(src) | a;
+  for (int d = 0; d < nd; ++d) align |= reinterpret_cast<uint64_t>(sg.dst[d]);
   if ((align & 15) == 0) {
     const uint64_t vend = a + ((b - a) & ~uint64_t(15));
     const uint64_t step = static_cast<uint64_t>(blockDim.x) * 16;
@@ -238,16 +243,23 @@ __device__ __forceinline__ void copy_range(const unsigned char* __restrict__ src
       uint4 v[kUnroll];
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) v[u] = ld_stream(src + i + u * step);
+      for (int d = 0; d < nd; ++d) {
+        unsigned char* dst = sg.dst[d];
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) st_vec(dst + i + u * step, v[u]);
+        for (int u = 0; u < kUnroll; ++u) st_vec(dst + i + u * step, v[u]);
+      }
     }
-    for (; i < vend; i += step) st_vec(dst + i, ld_stream(src + i));
-    for (uint64_t j = vend + threadIdx.x; j < b; j += blockDim.x) dst[j] = src[j];
+    for (; i < vend; i += step) {
+      const uint4 v = ld_stream(src + i);
+      for (int d = 0; d < nd; ++d) st_vec(sg.dst[d] + i, v);
+    }
+    for (uint64_t j = vend + threadIdx.x; j < b; j += blockDim.x)
+      for (int d = 0; d < nd; ++d) sg.dst[d][j] = src[j];
   } else {
     const uint64_t al = align | b;
-    if ((al & 3) == 0) copy_scalar<uint32_t>(src, dst, a, b);
-    else if ((al & 1) == 0) copy_scalar<uint16_t>(src, dst, a, b);
-    else copy_scalar<unsigned char>(src, dst, a, b);
+    if ((al & 3) == 0) copy_scalar<uint32_t>(src, sg.dst, nd, a, b);
+    else if ((al & 1) == 0) copy_scalar<uint16_t>(src, sg.dst, nd, a, b);
+    else copy_scalar<unsigned char>(src, sg.dst, nd, a, b);
   }
 }
 
@@ -262,7 +274,7 @@ __global__ void __launch_bounds__(512, 2) copy_segments_kernel(const CopySeg* __
   sync_begin(sync, cs);
   if (nseg > 0)
     for_each_share<MODE>(segs, nseg, part, sync, cs, CopyLen{},
-                         [](const CopySeg& sg, uint64_t a, uint64_t b) { copy_range(sg.src, sg.dst, a, b); });
+                         [](const CopySeg& sg, uint64_t a, uint64_t b) { copy_range(sg, a, b); });
   epoch_finish(sync, cs);
 }
 
@@ -301,11 +313,17 @@ __device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, uint32_t 
       : "memory");
 }
 
-__device__ __forceinline__ void bulk_s2g(void* gmem, const void* smem, uint32_t bytes) {
+__device__ __forceinline__ void bulk_store(void* gmem, const void* smem, uint32_t bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gmem), "r"(smem_u32(smem)),
                "r"(bytes)
                : "memory");
-  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+
+__device__ __forceinline__ void bulk_s2g(void* gmem, const void* smem, uint32_t bytes) {
+  bulk_store(gmem, smem, bytes);
+  bulk_commit();
 }
 
 template <int N>
@@ -334,8 +352,9 @@ __global__ void __launch_bounds__(32) copy_segments_tma_kernel(const CopySeg* __
     __syncwarp();
     if (threadIdx.x == 0) {
       // chunk k lives in stage k % kTmaStages; its barrier phase is (k / kTmaStages) & 1
-      unsigned char* pend_dst[kTmaStages];
+      uint32_t pend_seg[kTmaStages];
       uint32_t pend_bytes[kTmaStages];
+      uint64_t pend_off[kTmaStages];
       uint32_t issued = 0;
       bool more = true;
       // queue order: remote-first CTAs start on peer chunks, the others on local ones
@@ -362,16 +381,18 @@ __global__ void __launch_bounds__(32) copy_segments_tma_kernel(const CopySeg* __
           const uint64_t a = static_cast<uint64_t>(t.y) * part.chunk;
           const uint64_t e = a + part.chunk < sg.nbytes ? a + part.chunk : sg.nbytes;
           const uint32_t bytes = static_cast<uint32_t>(e - a);
-          const uint64_t al =
-              reinterpret_cast<uint64_t>(sg.src + a) | reinterpret_cast<uint64_t>(sg.dst + a) | bytes;
+          uint64_t al = reinterpret_cast<uint64_t>(sg.src + a) | bytes;
+          for (int d = 0; d < sg.ndst; ++d) al |= reinterpret_cast<uint64_t>(sg.dst[d] + a);
           if (al & 15) {  // rare unaligned run: plain byte copy by this lane
-            for (uint64_t i = a; i < e; ++i) sg.dst[i] = sg.src[i];
+            for (uint64_t i = a; i < e; ++i)
+              for (int d = 0; d < sg.ndst; ++d) sg.dst[d][i] = sg.src[i];
             continue;
           }
           const int st = issued % kTmaStages;
           mbar_expect(&full[st], bytes);
           bulk_g2s(stage_mem + st * kTmaStageBytes, sg.src + a, bytes, &full[st]);
-          pend_dst[st] = sg.dst + a;
+          pend_seg[st] = t.x;
+          pend_off[st] = a;
           pend_bytes[st] = bytes;
           ++issued;
           return;
@@ -382,7 +403,11 @@ __global__ void __launch_bounds__(32) copy_segments_tma_kernel(const CopySeg* __
         const int st = k % kTmaStages;
         mbar_wait(&full[st], (k / kTmaStages) & 1u);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        bulk_s2g(pend_dst[st], stage_mem + st * kTmaStageBytes, pend_bytes[st]);
+        // one bulk group per chunk: a store to every destination of the run
+        const CopySeg& sg = segs[pend_seg[st]];
+        const int nd = sg.ndst;
+        for (int d = 0; d < nd; ++d) bulk_store(sg.dst[d] + pend_off[st], stage_mem + st * kTmaStageBytes, pend_bytes[st]);
+        bulk_commit();
         if (k >= 1 && more) {
           bulk_wait_read<1>();  // store k-1 has finished reading its stage
           issue();              // chunk k-1+kTmaStages reuses stage (k-1) % kTmaStages
@@ -634,11 +659,11 @@ __global__ void __launch_bounds__(32) reduce_segments_tma_kernel(const ReduceSeg
 #pragma unroll
           for (int j = 0; j < static_cast<int>(sizeof(TOut) * 8 / 16); ++j) dw[j] = w[j];
         }
+        // every writing lane orders its generic-proxy smem writes before the
+        // async-proxy (TMA) store that reads them
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
-        if (lane == 0) {
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          bulk_s2g(p.dst, D, p.n * sizeof(TOut));
-        }
+        if (lane == 0) bulk_s2g(p.dst, D, p.n * sizeof(TOut));
       } else {  // multi-term or unaligned: the warp reduces straight from global memory
         mbar_wait(&full[st], (k / kRedStages) & 1u);
         for (uint32_t i = lane; i < p.n; i += 32) {
@@ -651,7 +676,11 @@ __global__ void __launch_bounds__(32) reduce_segments_tma_kernel(const ReduceSeg
       __syncwarp();
       if (lane == 0) {
         if (k >= 1 && more) {
-          bulk_wait_read<1>();  // the store of chunk k-1 has read its stage
+          // the store of chunk k-1 must have read its stage before chunk k-1+S
+          // reloads it: with chunk k's own store committed that store may stay
+          // pending; a warp-reduced chunk k committed nothing, so wait for all
+          if (p.tma) bulk_wait_read<1>();
+          else bulk_wait_read<0>();
           issue();
         }
         issued_sh = issued;

@@ -18,11 +18,17 @@ inline int dtype_size(int dt) { return dt == kFP32 ? 4 : dt == kFP64 ? 8 : 2; }
 // first_seg[b] (precomputed on the host): no per-chunk searches.
 constexpr uint64_t kQuantum = 4096;
 
+// One source run copied to up to kMaxFan destinations: the run is read once
+// (HBM or NVLink) and stored to every destination (the TP/CP replicas that
+// hold the same rows on this GPU in pull mode; every consumer of a local run
+// in push mode).
+constexpr int kMaxFan = 8;
 struct CopySeg {
   const unsigned char* src;
-  unsigned char* dst;
+  unsigned char* dst[kMaxFan];
   uint64_t nbytes;
   uint64_t w0;
+  int32_t ndst;
 };
 
 // dst[i] = beta*dst[i] + sum_t term_t[i], fp32 accumulation, terms summed in
