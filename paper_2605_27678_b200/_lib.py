@@ -10,7 +10,8 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libhetbridge.so")
+# HB_LIB_PATH: an alternative in-tree build (A/B experiments only)
+LIB_PATH = os.environ.get("HB_LIB_PATH") or os.path.join(HERE, "libhetbridge.so")
 
 ERROR_NAMES = [
     "RankOutOfModule", "CoordOutOfBounds", "IndivisibleBatch", "PartialOverlap", "NonIntegerFan",

@@ -105,19 +105,18 @@ Exec::Exec(const bridge::BridgePlan& plan, const index::SpliceSpec* splice, int 
   if (cfg_.internal_alloc || n_gpus_ > 1) {
     ck(cudaMalloc(&local_base_, region_bytes_), "cudaMalloc(region)");
     ck(cudaMemset(local_base_, 0, kPadBytes), "cudaMemset(pad)");
-    static_assert(2 * dev::kMaxGpus * sizeof(uint32_t) <= kPadBytes, "pad holds start and done flags");
+    static_assert(4 * dev::kMaxGpus * sizeof(uint32_t) <= kPadBytes, "pad holds start and done flags of both kinds");
   }
-  ck(cudaMalloc(&ctr_, 64), "cudaMalloc(ctr)");
-  ck(cudaMemset(ctr_, 0, 64), "cudaMemset(ctr)");
+  ck(cudaMalloc(&ctr_, 2 * dev::kCtrBytes), "cudaMalloc(ctr)");
+  ck(cudaMemset(ctr_, 0, 2 * dev::kCtrBytes), "cudaMemset(ctr)");
   peer_base_.assign(n_gpus_, nullptr);
   peer_base_[my_gpu_] = local_base_;
   tables_.resize(cfg.mb_slots);
   int khz = 0;
   cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, device_);
   clock_khz_ = khz > 0 ? khz : 2000000;
-  sync_ = make_sync_args();
-  sync_push_ = sync_;
-  sync_push_.end_sync = 1;
+  sync_fwd_ = make_sync_args(kFwdKind, fwd_push_);
+  sync_bwd_ = make_sync_args(kBwdKind, false);
 }
 
 Exec::~Exec() {
@@ -174,9 +173,8 @@ void Exec::open_peers(const void* handles) {
     ck(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
     peer_base_[g] = static_cast<unsigned char*>(p);
   }
-  sync_ = make_sync_args();
-  sync_push_ = sync_;
-  sync_push_.end_sync = 1;
+  sync_fwd_ = make_sync_args(kFwdKind, fwd_push_);
+  sync_bwd_ = make_sync_args(kBwdKind, false);
   dirty_fwd_ = dirty_bwd_ = true;
 }
 
@@ -233,19 +231,15 @@ int Exec::copy_mode() const {
 
 int Exec::reduce_mode() const {
   // The backward reduce runs the LDG/STG engine over dynamic chunks under the
-  // TMA copy partition: measured at N=1 (C2-C5) it reaches 0.87-0.97 of HBM
-  // while the one-warp TMA-staged reduce reaches 0.29-0.34 (its in-smem fp32
-  // pass is issue-bound). HB_RED_ENGINE=tma selects the TMA reduce.
-  static const bool tma = [] {
-    const char* v = std::getenv("HB_RED_ENGINE");
-    return v && std::string(v) == "tma";
-  }();
+  // TMA copy partition (measured at N=1, C2-C5: 0.87-0.97 of HBM; a one-warp
+  // TMA-staged reduce reached only 0.29-0.34, its in-smem fp32 pass being
+  // issue-bound, and was dropped).
   const int m = copy_mode();
-  return (m == dev::kPartTma && !tma) ? dev::kPartDynamic : m;
+  return m == dev::kPartTma ? dev::kPartDynamic : m;
 }
 
 uint64_t Exec::pad_unit(int mode, bool copy) const {
-  if (mode == dev::kPartTma) return copy ? dev::tma_chunk_bytes(kTmaChunkKiB) : dev::reduce_tma_chunk_elems();
+  if (mode == dev::kPartTma) return dev::tma_chunk_bytes(kTmaChunkKiB);
   if (mode == dev::kPartDynamic) return copy ? kDynCopyChunk : kDynReduceChunk;
   return dev::kQuantum;
 }
@@ -264,6 +258,7 @@ void Exec::build_partition(const std::vector<uint64_t>& w0, const std::vector<ui
   out->chunk = unit;
   out->total_chunks = out->rtotal_chunks = 0;
   out->remote_ctas = 0;
+  out->lstatic = out->rstatic = 0;
   out->per_cta = 0;
   if (mode == dev::kPartDynamic || mode == dev::kPartTma) {
     // Two queues (local / remote). Hand-out order within a queue: chunk j of
@@ -298,6 +293,8 @@ void Exec::build_partition(const std::vector<uint64_t>& w0, const std::vector<ui
       const double tr = remote_bytes / 770e9, tl = 2.0 * local_bytes / 6.5e12;
       out->remote_ctas = std::clamp(static_cast<int>(grid * tr / (tr + tl) + 0.5), 1, grid - 1);
     }
+    out->rstatic = std::min<uint32_t>(out->remote_ctas, out->rtotal_chunks);
+    out->lstatic = std::min<uint32_t>(grid - out->remote_ctas, out->total_chunks);
     return;
   }
   if (mode != dev::kPartContiguous) return;
@@ -413,8 +410,7 @@ void Exec::prepare_bwd() {
       ck(cudaMemcpy(T.terms, terms.data(), terms.size() * sizeof(void*), cudaMemcpyHostToDevice), "upload");
     }
   }
-  const int occ = mode == dev::kPartTma ? dev::reduce_tma_blocks_per_sm(cfg_.grad_in_dtype, cfg_.grad_out_dtype)
-                                        : dev::reduce_blocks_per_sm(cfg_.threads, cfg_.grad_in_dtype, cfg_.grad_out_dtype);
+  const int occ = dev::reduce_blocks_per_sm(cfg_.threads, cfg_.grad_in_dtype, cfg_.grad_out_dtype);
   const int bps = cfg_.blocks_per_sm > 0 ? std::min(cfg_.blocks_per_sm, occ) : occ;
   std::vector<char> rem;
   double lb = 0, rb = 0;
@@ -428,11 +424,21 @@ void Exec::prepare_bwd() {
   dirty_bwd_ = false;
 }
 
-dev::SyncArgs Exec::make_sync_args() const {
+// Forward and backward launches keep separate counters and pad slots: each
+// kind's launch count stays in lockstep across the group's GPUs (every GPU
+// issues the same op sequence), and a kind's queue counters advance by a fixed
+// amount per launch of that kind (boundary_kernels.cuh).
+dev::SyncArgs Exec::make_sync_args(int kind, bool push) const {
   dev::SyncArgs s{};
-  s.pad = reinterpret_cast<uint32_t*>(local_base_);
-  s.ctr = ctr_;
+  const uint64_t pad_off = static_cast<uint64_t>(kind) * 2 * dev::kMaxGpus;  // u32 words
+  uint32_t* c = ctr_ + kind * (dev::kCtrBytes / 4);
+  s.pad = reinterpret_cast<uint32_t*>(local_base_) + (local_base_ ? pad_off : 0);
+  s.arrive = reinterpret_cast<unsigned long long*>(c);
+  s.queue = reinterpret_cast<unsigned long long*>(c + dev::kCtrLine);
+  s.fin = c + 3 * dev::kCtrLine;
+  s.err = ctr_ + 3 * dev::kCtrLine + 1;  // one error word per exec
   s.my_gpu = my_gpu_;
+  s.end_sync = push && n_gpus_ > 1;
   // HB_DEBUG_NO_SYNC=1 drops the cross-GPU barrier (UNSAFE; overhead experiments only).
   static const bool no_sync = [] {
     const char* v = std::getenv("HB_DEBUG_NO_SYNC");
@@ -443,7 +449,7 @@ dev::SyncArgs Exec::make_sync_args() const {
     s.wait_mask = peers;
     s.post_mask = peers;
     for (int g = 0; g < n_gpus_; ++g)
-      if ((peers >> g) & 1u) s.peer_pad[g] = reinterpret_cast<uint32_t*>(peer_base_[g]);
+      if ((peers >> g) & 1u) s.peer_pad[g] = reinterpret_cast<uint32_t*>(peer_base_[g]) + pad_off;
   }
   s.timeout_cycles = static_cast<uint64_t>(cfg_.timeout_s * clock_khz_ * 1e3);
   return s;
@@ -452,7 +458,7 @@ dev::SyncArgs Exec::make_sync_args() const {
 void Exec::launch_forward(int mb_slot, void* stream) {
   const DevTables& T = tables_[mb_slot];
   dev::launch_copy(T.copy, static_cast<int>(fwd_local_.size()), fwd_part_.dev(),
-                   fwd_push_ && n_gpus_ > 1 ? sync_push_ : sync_, {fwd_part_.grid, cfg_.threads}, stream);
+                   sync_fwd_, {fwd_part_.grid, cfg_.threads}, stream);
   ck(cudaGetLastError(), "copy_segments launch");
   ++launches_;
 }
@@ -460,7 +466,7 @@ void Exec::launch_forward(int mb_slot, void* stream) {
 void Exec::launch_backward(int mb_slot, float beta, void* stream) {
   const DevTables& T = tables_[mb_slot];
   dev::launch_reduce(T.reduce, static_cast<int>(bwd_local_.size()), T.terms, bwd_part_.dev(), cfg_.grad_in_dtype,
-                     cfg_.grad_out_dtype, beta, sync_, {bwd_part_.grid, cfg_.threads}, stream);
+                     cfg_.grad_out_dtype, beta, sync_bwd_, {bwd_part_.grid, cfg_.threads}, stream);
   ck(cudaGetLastError(), "reduce_segments launch");
   ++launches_;
 }
@@ -518,9 +524,9 @@ void Exec::graph_launch(int mb_slot, int what, void* stream) {
 void Exec::seed_forward_record(int mb) { fwd_done_.insert(mb); }
 
 uint32_t Exec::device_error() const {
-  uint32_t v[3] = {0, 0, 0};
-  ck(cudaMemcpy(v, ctr_, sizeof(v), cudaMemcpyDeviceToHost), "read status");
-  return v[2];
+  uint32_t v = 0;
+  ck(cudaMemcpy(&v, ctr_ + 3 * dev::kCtrLine + 1, sizeof(v), cudaMemcpyDeviceToHost), "read status");
+  return v;
 }
 
 uint64_t Exec::local_fwd_bytes() const {

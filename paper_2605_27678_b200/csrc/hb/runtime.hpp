@@ -84,7 +84,8 @@ class Exec {
   const void* resolve(int rank, int slot, int mb_slot) const;
   void prepare_fwd();  // resolve pointers, upload descriptors (after bind/open)
   void prepare_bwd();
-  dev::SyncArgs make_sync_args() const;
+  static constexpr int kFwdKind = 0, kBwdKind = 1;
+  dev::SyncArgs make_sync_args(int kind, bool push) const;
 
   bridge::BridgePlan plan_;
   index::IndexMap map_;
@@ -132,8 +133,10 @@ class Exec {
     uint32_t rtotal_chunks = 0;
     uint2* rchunks = nullptr;
     int remote_ctas = 0;
+    uint32_t lstatic = 0, rstatic = 0;
     dev::Partition dev() const {
-      return {first_seg, per_cta, mode, total_chunks, chunk, chunks, rtotal_chunks, rchunks, remote_ctas};
+      return {first_seg, per_cta, mode, total_chunks, chunk, chunks, rtotal_chunks, rchunks, remote_ctas,
+              lstatic, rstatic};
     }
   };
   DevPartition fwd_part_, bwd_part_;
@@ -148,7 +151,7 @@ class Exec {
                        int mode, uint64_t unit, DevPartition* out);
   bool dirty_fwd_ = true, dirty_bwd_ = true;
   uint32_t* ctr_ = nullptr;  // device counters
-  dev::SyncArgs sync_{}, sync_push_{};
+  dev::SyncArgs sync_fwd_{}, sync_bwd_{};
   int clock_khz_ = 2000000;
   int sm_count_ = 0;
   int launches_ = 0;

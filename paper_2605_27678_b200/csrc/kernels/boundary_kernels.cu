@@ -29,6 +29,7 @@
 
 #include "kernels/boundary_kernels.cuh"
 
+
 namespace hb::dev {
 
 namespace {
@@ -56,13 +57,22 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
   return v;
 }
 
-__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+// "+1" to this GPU's slot in every peer's pad (`word` = 0: started, kMaxGpus:
+// finished pushing). Called by every thread of a warp: lane g posts to peer g,
+// so the posts to several peers go out in parallel.
+__device__ __forceinline__ void post_peers_warp(const SyncArgs& s, int word) {
+  const int g = threadIdx.x & 31;
+  if ((s.post_mask >> g) & 1u) {
+    asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(s.peer_pad[g] + word + s.my_gpu), "r"(1u)
+                 : "memory");
+  }
 }
 
-// Per-CTA view of the launch's epoch barrier (shared memory).
+constexpr uint32_t kNoChunk = 0xffffffffu;
+
+// Per-CTA view of the launch (shared memory).
 struct CtaSync {
-  uint32_t e;  // this launch's epoch
+  uint32_t e;  // this launch's epoch (valid after cta_arrive_finish)
   int waited;  // peers' arrival at e confirmed
   int ok;      // no timeout
 };
@@ -73,43 +83,31 @@ __device__ __forceinline__ bool spin_until(const SyncArgs& s, const uint32_t* fl
   while (static_cast<int32_t>(ld_acquire_sys(flag) - e) < 0) {
     __nanosleep(64);
     if (static_cast<uint64_t>(clock64() - t0) > s.timeout_cycles) {
-      atomicExch(s.ctr + 2, 1u);
+      atomicExch(s.err, 1u);
       return false;
     }
   }
   return true;
 }
 
-// Start of a launch: read the epoch, and (block 0) post arrival to every peer.
-// The post is a release store at system scope; earlier kernels' writes are
-// already complete at the kernel boundary.
-__device__ void sync_begin(const SyncArgs& s, CtaSync& cs) {
-  if (threadIdx.x == 0) {
-    cs.e = *reinterpret_cast<volatile uint32_t*>(s.ctr) + 1;
-    cs.waited = (s.wait_mask == 0);
-    cs.ok = 1;
-  }
-  __syncthreads();
-  const int g = threadIdx.x;
-  if (blockIdx.x == 0 && g < kMaxGpus && ((s.post_mask >> g) & 1u)) st_release_sys(s.peer_pad[g] + s.my_gpu, cs.e);
+// Start of a launch, one thread per CTA: count this CTA in (CTA 0's first
+// warp posts "started" to every peer with post_peers_warp). Returns the raw arrival word; its latency overlaps
+// the CTA's first (static, local) chunk and is consumed by cta_arrive_finish.
+__device__ __forceinline__ unsigned long long cta_arrive_issue(const SyncArgs& s) {
+  return atomicAdd(s.arrive, 1ull);
 }
 
-// Wait (once per CTA) until every peer arrived at this epoch: after that the
-// peers' buffers of this op may be read (pull) or written (push). Called by all
-// threads of the CTA. Returns false on timeout.
-__device__ bool sync_wait(const SyncArgs& s, CtaSync& cs) {
-  if (cs.waited) return cs.ok != 0;
-  __syncthreads();
-  const int g = threadIdx.x;
-  if (g < kMaxGpus && ((s.wait_mask >> g) & 1u))
-    if (!spin_until(s, s.pad + g, cs.e)) cs.ok = 0;
-  __syncthreads();
-  if (threadIdx.x == 0) cs.waited = 1;
-  __syncthreads();
-  return cs.ok != 0;
+__device__ __forceinline__ void cta_arrive_finish(const SyncArgs& s, CtaSync& cs, unsigned long long old) {
+  cs.e = static_cast<uint32_t>(old >> 32) + 1;
+  cs.waited = (s.wait_mask == 0);
+  cs.ok = 1;
+  // last CTA in: advance the epoch, zero the arrivals (every CTA of this
+  // launch has read the word; the next launch starts after this one ends)
+  if ((old & 0xffffffffull) == gridDim.x - 1) atomicAdd(s.arrive, (1ull << 32) - gridDim.x);
 }
 
-// Single-thread variant (TMA issuing lane).
+// Wait (once per CTA, one thread) until every peer started op e: after that
+// the peers' buffers of this op may be read (pull) or written (push).
 __device__ bool sync_wait_lane(const SyncArgs& s, CtaSync& cs) {
   if (!cs.waited) {
     for (int g = 0; g < kMaxGpus; ++g)
@@ -119,39 +117,84 @@ __device__ bool sync_wait_lane(const SyncArgs& s, CtaSync& cs) {
   return cs.ok != 0;
 }
 
-// Last CTA to finish: confirm every peer arrived at this epoch (so completion
-// of op e implies all peers completed op e-1, whatever work this GPU had), in
-// push mode publish "my writes into your buffers are done" and wait for every
-// writer into this GPU, then reset the work counters and bump the epoch.
-__device__ void epoch_finish(const SyncArgs& s, CtaSync& cs) {
-  __shared__ int last;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    // Push mode must make this CTA's remote stores visible before "done" is
-    // posted (system scope). Otherwise outputs are local and kernel completion
-    // already publishes them to peers, so a GPU-scope fence suffices (a
-    // system-scope fence in every CTA measurably lengthens short launches).
-    if (s.end_sync) __threadfence_system();
-    else __threadfence();
-    last = atomicAdd(s.ctr + 1, 1u) == gridDim.x - 1;
-  }
-  __syncthreads();
-  if (!last) return;
-  const int g = threadIdx.x;
-  if (g < kMaxGpus && ((s.wait_mask >> g) & 1u)) spin_until(s, s.pad + g, cs.e);
-  if (s.end_sync) {
-    if (g < kMaxGpus && ((s.post_mask >> g) & 1u)) st_release_sys(s.peer_pad[g] + kMaxGpus + s.my_gpu, cs.e);
-    if (g < kMaxGpus && ((s.wait_mask >> g) & 1u)) spin_until(s, s.pad + kMaxGpus + g, cs.e);
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    s.ctr[1] = 0;
-    s.ctr[3] = 0;  // dynamic work counters (local / remote queues)
-    s.ctr[4] = 0;
-    __threadfence();
-    atomicExch(s.ctr, cs.e);
-  }
+// End of a launch, one thread per CTA. CTA 0 confirms every peer started op e,
+// so completion of op e implies every peer completed op e-1 (the buffer-reuse
+// contract), whatever work this GPU had. Push mode: the last CTA done writing
+// publishes "my writes into your buffers are done" and waits for every writer
+// into this GPU.
+__device__ void launch_end_lane(const SyncArgs& s, CtaSync& cs) {
+  if (blockIdx.x == 0) sync_wait_lane(s, cs);
+  if (!s.end_sync) return;
+  __threadfence_system();  // this CTA's remote stores before "done"
+  if (atomicAdd(s.fin, 1u) != gridDim.x - 1) return;
+  *s.fin = 0;
+  __threadfence_system();
+  for (int g = 0; g < kMaxGpus; ++g)
+    if ((s.post_mask >> g) & 1u) atomicAdd_system(s.peer_pad[g] + kMaxGpus + s.my_gpu, 1u);
+  for (int g = 0; g < kMaxGpus; ++g)
+    if ((s.wait_mask >> g) & 1u) spin_until(s, s.pad + kMaxGpus + g, cs.e);
 }
+
+// Work queues (dynamic / TMA partitions). One thread per CTA drives them.
+// A claim is issued (atomic in flight) before the current chunk is processed
+// and resolved after it, so the claim round trip overlaps the copy.
+struct Claimer {
+  int q;           // current queue: 1 remote, 0 local
+  int passes;      // queues finished
+  uint32_t first;  // static first chunk of the home queue (kNoChunk: none)
+  unsigned long long pre;  // raw value of the claim in flight (valid if has_pre)
+  int pre_q;
+  bool has_pre;
+
+  __device__ void init(const Partition& p) {
+    const int b = static_cast<int>(blockIdx.x);
+    q = b < p.remote_ctas ? 1 : 0;
+    passes = 0;
+    has_pre = false;
+    const uint32_t idx = q ? static_cast<uint32_t>(b) : static_cast<uint32_t>(b - p.remote_ctas);
+    first = idx < (q ? p.rstatic : p.lstatic) ? idx : kNoChunk;
+    if ((q ? p.rtotal_chunks : p.total_chunks) == 0) advance_queue(p);
+  }
+  __device__ void advance_queue(const Partition& p) {  // next non-empty queue, or done
+    while (++passes < 2) {
+      q ^= 1;
+      if ((q ? p.rtotal_chunks : p.total_chunks) != 0) return;
+    }
+  }
+  __device__ bool done() const { return passes >= 2; }
+  __device__ void issue(const SyncArgs& s) {  // start a claim in the current queue
+    pre = atomicAdd(s.queue + q * (kCtrLine / 2), 1ull);
+    pre_q = q;
+    has_pre = true;
+  }
+  __device__ uint32_t resolve(const Partition& p, uint32_t e, unsigned long long raw, int qq) const {
+    const uint32_t total = qq ? p.rtotal_chunks : p.total_chunks;
+    const uint32_t stat = qq ? p.rstatic : p.lstatic;
+    const unsigned long long adv = static_cast<unsigned long long>(total - stat) + gridDim.x;
+    const unsigned long long idx = raw - static_cast<unsigned long long>(e - 1) * adv + stat;
+    return idx < total ? static_cast<uint32_t>(idx) : kNoChunk;
+  }
+  // Next chunk (kNoChunk: this CTA is done); *remote = its queue. Consumes the
+  // claim in flight, claims synchronously across a queue switch, and starts
+  // the following claim.
+  __device__ uint32_t next(const Partition& p, const SyncArgs& s, uint32_t e, int* remote) {
+    uint32_t c = kNoChunk;
+    if (has_pre) {
+      has_pre = false;
+      c = resolve(p, e, pre, pre_q);
+      if (c == kNoChunk) advance_queue(p);
+    }
+    while (c == kNoChunk && !done()) {
+      issue(s);
+      has_pre = false;
+      c = resolve(p, e, pre, pre_q);
+      if (c == kNoChunk) advance_queue(p);
+    }
+    *remote = q;
+    if (c != kNoChunk) issue(s);
+    return c;
+  }
+};
 
 // Interleaved partition: CTA b takes quanta [q*b/G, q*(b+1)/G) of a segment.
 __device__ __forceinline__ bool cta_share(uint64_t n, uint64_t* a, uint64_t* b) {
@@ -162,57 +205,90 @@ __device__ __forceinline__ bool cta_share(uint64_t n, uint64_t* a, uint64_t* b) 
   return *a < *b;
 }
 
-// Drives `body(seg, a, b)` over this CTA's work under the partition's mode.
-// Dynamic mode keeps two queues: chunks whose data stays on this GPU (no peer
-// dependency: started immediately, hiding the barrier latency) and chunks that
-// touch a peer (handed out only after this CTA confirmed the peers' arrival).
-// The first `remote_ctas` CTAs drain the remote queue first, the rest the
-// local one; both then help with the other queue.
+// Drives `body(seg, a, b)` over this CTA's work under the partition's mode,
+// between the launch's arrival and end protocol. Dynamic mode keeps two
+// queues: chunks whose data stays on this GPU (no peer dependency: started
+// immediately, hiding the barrier latency) and chunks that touch a peer
+// (handed out only after this CTA confirmed the peers' arrival). The first
+// `remote_ctas` CTAs drain the remote queue first, the rest the local one;
+// both then help with the other queue. A CTA's first chunk is static; the
+// arrival round trip overlaps it.
 template <int MODE, class S, class Len, class Body>
-__device__ __forceinline__ void for_each_share(const S* __restrict__ segs, int nseg, const Partition& part,
-                                               const SyncArgs& sync, CtaSync& cs, Len len, Body body) {
+__device__ __forceinline__ void run_shares(const S* __restrict__ segs, int nseg, const Partition& part,
+                                           const SyncArgs& sync, Len len, Body body) {
+  __shared__ CtaSync cs;
+  __shared__ uint32_t cur;  // chunk being processed (kNoChunk: none)
+  __shared__ int cur_remote;
+  unsigned long long arr = 0;
+  if (blockIdx.x == 0 && threadIdx.x < 32) {
+    post_peers_warp(sync, 0);
+    __syncwarp();
+  }
+  if (threadIdx.x == 0) arr = cta_arrive_issue(sync);
   if constexpr (MODE == kPartDynamic) {
-    __shared__ uint32_t next;
-    for (int pass = 0; pass < 2; ++pass) {
-      const bool remote = (pass == 0) == (static_cast<int>(blockIdx.x) < part.remote_ctas);
-      const uint2* table = remote ? part.rchunks : part.chunks;
-      const uint32_t total = remote ? part.rtotal_chunks : part.total_chunks;
-      uint32_t* ctr = sync.ctr + (remote ? 4 : 3);
-      if (total == 0) continue;
-      if (remote && !sync_wait(sync, cs)) return;
-      if (threadIdx.x == 0) next = atomicAdd(ctr, 1u);
-      __syncthreads();
-      uint32_t c = next;
-      while (c < total) {
-        __syncthreads();
-        if (threadIdx.x == 0) next = atomicAdd(ctr, 1u);  // prefetch the next chunk index
-        const uint2 t = table[c];                           // (segment, chunk within segment)
+    Claimer cl;
+    if (threadIdx.x == 0) {
+      cl.init(part);
+      cur = cl.done() ? kNoChunk : cl.first;
+      cur_remote = cl.q;
+      if (!cl.done()) cl.issue(sync);  // the claim after the static chunk, in flight
+      if (cur != kNoChunk && cl.q == 1) {  // a remote first chunk needs the peers first
+        cta_arrive_finish(sync, cs, arr);
+        arr = ~0ull;
+        sync_wait_lane(sync, cs);
+      }
+    }
+    __syncthreads();
+    bool first = true;
+    while (true) {
+      const uint32_t c = cur;
+      // a remote chunk after a timed-out wait is claimed but not executed
+      if (c != kNoChunk && (!cur_remote || cs.ok)) {
+        const uint2 t = (cur_remote ? part.rchunks : part.chunks)[c];
         const S sg = segs[t.x];
         const uint64_t a = static_cast<uint64_t>(t.y) * part.chunk, e = a + part.chunk, n = len(sg);
         body(sg, a, e < n ? e : n);
-        __syncthreads();
-        c = next;
       }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        if (first && arr != ~0ull) cta_arrive_finish(sync, cs, arr);
+        first = false;
+        int rq = 0;
+        cur = cl.next(part, sync, cs.e, &rq);
+        cur_remote = rq;
+        if (cur != kNoChunk && rq) sync_wait_lane(sync, cs);
+      }
+      __syncthreads();
+      if (cur == kNoChunk) break;
     }
+    if (threadIdx.x == 0) launch_end_lane(sync, cs);
   } else {
-    if (!sync_wait(sync, cs)) return;
-    if constexpr (MODE == kPartInterleaved) {
-      for (int s = 0; s < nseg; ++s) {
-        const S sg = segs[s];
-        uint64_t a, b;
-        if (cta_share(len(sg), &a, &b)) body(sg, a, b);
-      }
-    } else {
-      const uint64_t lo = blockIdx.x * part.per_cta, hi = lo + part.per_cta;
-      for (int s = part.first_seg[blockIdx.x]; s < nseg; ++s) {
-        const S sg = segs[s];
-        if (sg.w0 >= hi) break;
-        const uint64_t a = (lo > sg.w0 ? lo : sg.w0) - sg.w0;
-        const uint64_t e = sg.w0 + len(sg);
-        const uint64_t b = (hi < e ? hi : e) - sg.w0;
-        if (a < b) body(sg, a, b);
+    if (threadIdx.x == 0) {
+      cta_arrive_finish(sync, cs, arr);
+      sync_wait_lane(sync, cs);
+    }
+    __syncthreads();
+    if (cs.ok && nseg > 0) {
+      if constexpr (MODE == kPartInterleaved) {
+        for (int s = 0; s < nseg; ++s) {
+          const S sg = segs[s];
+          uint64_t a, b;
+          if (cta_share(len(sg), &a, &b)) body(sg, a, b);
+        }
+      } else {
+        const uint64_t lo = blockIdx.x * part.per_cta, hi = lo + part.per_cta;
+        for (int s = part.first_seg[blockIdx.x]; s < nseg; ++s) {
+          const S sg = segs[s];
+          if (sg.w0 >= hi) break;
+          const uint64_t a = (lo > sg.w0 ? lo : sg.w0) - sg.w0;
+          const uint64_t e = sg.w0 + len(sg);
+          const uint64_t b = (hi < e ? hi : e) - sg.w0;
+          if (a < b) body(sg, a, b);
+        }
       }
     }
+    __syncthreads();
+    if (threadIdx.x == 0) launch_end_lane(sync, cs);
   }
 }
 
@@ -270,12 +346,8 @@ struct CopyLen {
 template <int MODE>
 __global__ void __launch_bounds__(512, 2) copy_segments_kernel(const CopySeg* __restrict__ segs, int nseg,
                                                             Partition part, SyncArgs sync) {
-  __shared__ CtaSync cs;
-  sync_begin(sync, cs);
-  if (nseg > 0)
-    for_each_share<MODE>(segs, nseg, part, sync, cs, CopyLen{},
-                         [](const CopySeg& sg, uint64_t a, uint64_t b) { copy_range(sg, a, b); });
-  epoch_finish(sync, cs);
+  run_shares<MODE>(segs, nseg, part, sync, CopyLen{},
+                   [](const CopySeg& sg, uint64_t a, uint64_t b) { copy_range(sg, a, b); });
 }
 
 // ---- TMA bulk-copy engine ------------------------------------------------------
@@ -321,11 +393,6 @@ __device__ __forceinline__ void bulk_store(void* gmem, const void* smem, uint32_
 
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 
-__device__ __forceinline__ void bulk_s2g(void* gmem, const void* smem, uint32_t bytes) {
-  bulk_store(gmem, smem, bytes);
-  bulk_commit();
-}
-
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() {
   asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
@@ -334,90 +401,101 @@ __device__ __forceinline__ void bulk_wait_read() {
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 // One warp per CTA; lane 0 issues TMA bulk copies through a kTmaStages ring of
-// 32 KiB shared-memory stages: loads for the next stages are in flight while
-// the current stage is stored. Chunks (= one stage) come from the dynamic work
-// counter; unaligned runs fall back to the warp-wide LDG/STG path.
+// shared-memory stages: loads for the next stages are in flight while the
+// current stage is stored (once per destination of the run). Chunks (= one
+// stage) come from the work queues; unaligned runs are copied by lane 0.
 template <int kTmaStages, uint32_t kTmaStageBytes>
 __global__ void __launch_bounds__(32) copy_segments_tma_kernel(const CopySeg* __restrict__ segs, int nseg,
                                                                Partition part, SyncArgs sync) {
   extern __shared__ __align__(128) unsigned char stage_mem[];
   __shared__ __align__(8) uint64_t full[kTmaStages];
   __shared__ CtaSync cs;
-  sync_begin(sync, cs);
-  if (nseg > 0) {
-    if (threadIdx.x == 0) {
-      for (int i = 0; i < kTmaStages; ++i) mbar_init(&full[i]);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncwarp();
-    if (threadIdx.x == 0) {
-      // chunk k lives in stage k % kTmaStages; its barrier phase is (k / kTmaStages) & 1
-      uint32_t pend_seg[kTmaStages];
-      uint32_t pend_bytes[kTmaStages];
-      uint64_t pend_off[kTmaStages];
-      uint32_t issued = 0;
-      bool more = true;
-      // queue order: remote-first CTAs start on peer chunks, the others on local ones
-      int q = static_cast<int>(blockIdx.x) < part.remote_ctas ? 1 : 0, passes = 0;
-      auto issue = [&]() {  // claim the next chunk and start its global->smem load
-        while (more) {
-          const bool remote = q == 1;
-          const uint32_t total = remote ? part.rtotal_chunks : part.total_chunks;
-          const uint32_t c = total ? atomicAdd(sync.ctr + (remote ? 4 : 3), 1u) : total;
-          if (c >= total) {
-            if (++passes == 2) {
-              more = false;
-              return;
-            }
-            q ^= 1;
-            continue;
-          }
-          if (remote && !sync_wait_lane(sync, cs)) {
-            more = false;
-            return;
-          }
-          const uint2 t = (remote ? part.rchunks : part.chunks)[c];
-          const CopySeg sg = segs[t.x];
-          const uint64_t a = static_cast<uint64_t>(t.y) * part.chunk;
-          const uint64_t e = a + part.chunk < sg.nbytes ? a + part.chunk : sg.nbytes;
-          const uint32_t bytes = static_cast<uint32_t>(e - a);
-          uint64_t al = reinterpret_cast<uint64_t>(sg.src + a) | bytes;
-          for (int d = 0; d < sg.ndst; ++d) al |= reinterpret_cast<uint64_t>(sg.dst[d] + a);
-          if (al & 15) {  // rare unaligned run: plain byte copy by this lane
-            for (uint64_t i = a; i < e; ++i)
-              for (int d = 0; d < sg.ndst; ++d) sg.dst[d][i] = sg.src[i];
-            continue;
-          }
-          const int st = issued % kTmaStages;
-          mbar_expect(&full[st], bytes);
-          bulk_g2s(stage_mem + st * kTmaStageBytes, sg.src + a, bytes, &full[st]);
-          pend_seg[st] = t.x;
-          pend_off[st] = a;
-          pend_bytes[st] = bytes;
-          ++issued;
-          return;
-        }
-      };
-      for (int i = 0; i < kTmaStages; ++i) issue();
-      for (uint32_t k = 0; k < issued; ++k) {
-        const int st = k % kTmaStages;
-        mbar_wait(&full[st], (k / kTmaStages) & 1u);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        // one bulk group per chunk: a store to every destination of the run
-        const CopySeg& sg = segs[pend_seg[st]];
-        const int nd = sg.ndst;
-        for (int d = 0; d < nd; ++d) bulk_store(sg.dst[d] + pend_off[st], stage_mem + st * kTmaStageBytes, pend_bytes[st]);
-        bulk_commit();
-        if (k >= 1 && more) {
-          bulk_wait_read<1>();  // store k-1 has finished reading its stage
-          issue();              // chunk k-1+kTmaStages reuses stage (k-1) % kTmaStages
-        }
-      }
-      bulk_wait_all();
-    }
+  if (blockIdx.x == 0) {
+    post_peers_warp(sync, 0);
     __syncwarp();
   }
-  epoch_finish(sync, cs);
+  if (threadIdx.x != 0) return;  // one issuing lane; the rest of the warp has nothing to do
+  const unsigned long long arr = cta_arrive_issue(sync);
+  for (int i = 0; i < kTmaStages; ++i) mbar_init(&full[i]);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  // chunk k lives in stage k % kTmaStages; its barrier phase is (k / kTmaStages) & 1
+  uint32_t pend_seg[kTmaStages];
+  uint32_t pend_bytes[kTmaStages];
+  uint64_t pend_off[kTmaStages];
+  uint32_t issued = 0;
+  bool more = true, arrived = false;
+  Claimer cl;
+  cl.init(part);
+  bool use_first = !cl.done();
+  if (!cl.done()) cl.issue(sync);  // the claim after the static chunk, in flight
+  auto arrive = [&]() {
+    if (!arrived) {
+      cta_arrive_finish(sync, cs, arr);
+      arrived = true;
+    }
+  };
+  auto issue = [&]() {  // next chunk: start its global->smem load
+    while (more) {
+      uint32_t c;
+      int rq;
+      if (use_first) {
+        use_first = false;
+        c = cl.first;
+        rq = cl.q;
+      } else {
+        arrive();
+        c = cl.next(part, sync, cs.e, &rq);
+        if (c == kNoChunk) {
+          more = false;
+          return;
+        }
+      }
+      if (c == kNoChunk) continue;
+      if (rq == 1) {
+        arrive();
+        if (!sync_wait_lane(sync, cs)) continue;  // timed out: claimed, not executed
+      }
+      const uint2 t = (rq ? part.rchunks : part.chunks)[c];
+      const CopySeg& sg = segs[t.x];
+      const uint64_t a = static_cast<uint64_t>(t.y) * part.chunk;
+      const uint64_t e = a + part.chunk < sg.nbytes ? a + part.chunk : sg.nbytes;
+      const uint32_t bytes = static_cast<uint32_t>(e - a);
+      const int nd = sg.ndst;
+      uint64_t al = reinterpret_cast<uint64_t>(sg.src + a) | bytes;
+      for (int d = 0; d < nd; ++d) al |= reinterpret_cast<uint64_t>(sg.dst[d] + a);
+      if (al & 15) {  // rare unaligned run: plain byte copy by this lane
+        for (uint64_t i = a; i < e; ++i)
+          for (int d = 0; d < nd; ++d) sg.dst[d][i] = sg.src[i];
+        continue;
+      }
+      const int st = issued % kTmaStages;
+      mbar_expect(&full[st], bytes);
+      bulk_g2s(stage_mem + st * kTmaStageBytes, sg.src + a, bytes, &full[st]);
+      pend_seg[st] = t.x;
+      pend_off[st] = a;
+      pend_bytes[st] = bytes;
+      ++issued;
+      return;
+    }
+  };
+  for (int i = 0; i < kTmaStages; ++i) issue();
+  for (uint32_t k = 0; k < issued; ++k) {
+    const int st = k % kTmaStages;
+    mbar_wait(&full[st], (k / kTmaStages) & 1u);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    // one bulk group per chunk: a store to every destination of the run
+    const CopySeg& sg = segs[pend_seg[st]];
+    const int nd = sg.ndst;
+    for (int d = 0; d < nd; ++d) bulk_store(sg.dst[d] + pend_off[st], stage_mem + st * kTmaStageBytes, pend_bytes[st]);
+    bulk_commit();
+    if (k >= 1 && more) {
+      bulk_wait_read<1>();  // store k-1 has finished reading its stage
+      issue();              // chunk k-1+kTmaStages reuses stage (k-1) % kTmaStages
+    }
+  }
+  bulk_wait_all();
+  arrive();
+  launch_end_lane(sync, cs);
 }
 
 // ---- reduction ---------------------------------------------------------------
@@ -523,190 +601,14 @@ struct ReduceLen {
   __device__ uint64_t operator()(const ReduceSeg& s) const { return s.nelem; }
 };
 
-// ---- TMA reduce engine -----------------------------------------------------------
-//
-// One warp per CTA. Lane 0 streams (term chunk, accumulator chunk) pairs into a
-// ring of shared-memory stages with TMA bulk loads; the warp computes
-// acc = beta*acc + term in fp32 in shared memory and lane 0 bulk-stores the
-// accumulator chunk back. Remote (NVLink) term latency is hidden by the ring
-// instead of by thread count. Chunks with more than one term (cp sums of a
-// non-splice edge) or unaligned tails are reduced by the warp with plain loads.
-constexpr int kRedStages = 4;
-constexpr uint32_t kRedElems = 4096;  // elements per chunk (= one stage)
-
-template <class TIn, class TOut>
-__global__ void __launch_bounds__(32) reduce_segments_tma_kernel(const ReduceSeg* __restrict__ segs, int nseg,
-                                                                 const void* const* __restrict__ terms,
-                                                                 Partition part, float beta, SyncArgs sync) {
-  constexpr uint32_t kTB = kRedElems * sizeof(TIn), kDB = kRedElems * sizeof(TOut);
-  extern __shared__ __align__(128) unsigned char red_mem[];  // kRedStages x (term | acc)
-  __shared__ __align__(8) uint64_t full[kRedStages];
-  struct Pend {
-    TOut* dst;
-    const TIn* term;  // single term (nullptr: none)
-    const TIn* const* tp;
-    uint64_t off;  // chunk offset inside the segment (for the term pointers)
-    uint32_t n;
-    int nterms;
-    int tma;  // 1: staged through smem by TMA, 0: warp reduces from global
-  };
-  __shared__ Pend pend[kRedStages];
-  __shared__ CtaSync cs;
-  __shared__ uint32_t issued_sh;
-  sync_begin(sync, cs);
-  if (nseg > 0) {
-    if (threadIdx.x == 0) {
-      for (int i = 0; i < kRedStages; ++i) mbar_init(&full[i]);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncwarp();
-    const int lane = threadIdx.x;
-    int q = static_cast<int>(blockIdx.x) < part.remote_ctas ? 1 : 0, passes = 0;
-    bool more = true;
-    uint32_t issued = 0;
-    // lane 0 claims the next chunk, records it in pend[], starts its TMA loads
-    auto issue = [&]() {
-      while (more) {
-        const bool remote = q == 1;
-        const uint32_t total = remote ? part.rtotal_chunks : part.total_chunks;
-        const uint32_t c = total ? atomicAdd(sync.ctr + (remote ? 4 : 3), 1u) : total;
-        if (c >= total) {
-          if (++passes == 2) {
-            more = false;
-            return;
-          }
-          q ^= 1;
-          continue;
-        }
-        if (remote && !sync_wait_lane(sync, cs)) {
-          more = false;
-          return;
-        }
-        const uint2 t = (remote ? part.rchunks : part.chunks)[c];
-        const ReduceSeg sg = segs[t.x];
-        const uint64_t a = static_cast<uint64_t>(t.y) * part.chunk;
-        const uint64_t e = a + part.chunk < sg.nelem ? a + part.chunk : sg.nelem;
-        const uint32_t n = static_cast<uint32_t>(e - a);
-        const int st = issued % kRedStages;
-        Pend p;
-        p.dst = static_cast<TOut*>(sg.dst) + a;
-        p.tp = reinterpret_cast<const TIn* const*>(terms + sg.term0);
-        p.nterms = sg.nterms;
-        p.term = sg.nterms == 1 ? p.tp[0] + a : nullptr;
-        p.off = a;
-        p.n = n;
-        const uint64_t al = reinterpret_cast<uint64_t>(p.dst) | reinterpret_cast<uint64_t>(p.term) |
-                            (static_cast<uint64_t>(n) * sizeof(TIn)) | (static_cast<uint64_t>(n) * sizeof(TOut));
-        p.tma = sg.nterms <= 1 && (al & 15) == 0;
-        if (p.tma) {
-          const uint32_t tb = p.term ? n * sizeof(TIn) : 0, db = beta != 0.0f ? n * sizeof(TOut) : 0;
-          unsigned char* base = red_mem + st * (kTB + kDB);
-          mbar_expect(&full[st], tb + db);
-          if (tb) bulk_g2s(base, p.term, tb, &full[st]);
-          if (db) bulk_g2s(base + kTB, p.dst, db, &full[st]);  // tb+db == 0: the arrive completes the phase
-        } else {
-          mbar_expect(&full[st], 0);  // keep the stage's phase count in step with k / kRedStages
-        }
-        pend[st] = p;
-        ++issued;
-        return;
-      }
-    };
-    if (lane == 0) {
-      for (int i = 0; i < kRedStages; ++i) issue();
-      issued_sh = issued;
-    }
-    __syncwarp();
-    uint32_t k = 0;
-    while (true) {
-      __syncwarp();
-      const uint32_t avail = issued_sh;
-      if (k >= avail) break;
-      const int st = k % kRedStages;
-      const Pend p = pend[st];
-      if (p.tma) {
-        mbar_wait(&full[st], (k / kRedStages) & 1u);
-        const TIn* T = reinterpret_cast<const TIn*>(red_mem + st * (kTB + kDB));
-        TOut* D = reinterpret_cast<TOut*>(red_mem + st * (kTB + kDB) + kTB);
-        for (uint32_t i = lane * 8; i < p.n; i += 32 * 8) {  // n is a multiple of 8 (16-B aligned bytes)
-          float acc[8];
-          if (p.term) {
-            const uint4* tv = reinterpret_cast<const uint4*>(T + i);
-            uint4 v[sizeof(TIn) * 8 / 16];
-#pragma unroll
-            for (int j = 0; j < static_cast<int>(sizeof(TIn) * 8 / 16); ++j) v[j] = tv[j];
-            const TIn* e = reinterpret_cast<const TIn*>(v);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) acc[j] = 0.0f + Cvt<TIn>::to(e[j]);
-          } else {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) acc[j] = 0.0f;
-          }
-          if (beta != 0.0f) {
-            const uint4* dv = reinterpret_cast<const uint4*>(D + i);
-            uint4 v[sizeof(TOut) * 8 / 16];
-#pragma unroll
-            for (int j = 0; j < static_cast<int>(sizeof(TOut) * 8 / 16); ++j) v[j] = dv[j];
-            const TOut* o = reinterpret_cast<const TOut*>(v);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) acc[j] = fmaf(beta, Cvt<TOut>::to(o[j]), acc[j]);
-          }
-          uint4 w[sizeof(TOut) * 8 / 16];
-          TOut* we = reinterpret_cast<TOut*>(w);
-#pragma unroll
-          for (int j = 0; j < 8; ++j) we[j] = Cvt<TOut>::from(acc[j]);
-          uint4* dw = reinterpret_cast<uint4*>(D + i);
-#pragma unroll
-          for (int j = 0; j < static_cast<int>(sizeof(TOut) * 8 / 16); ++j) dw[j] = w[j];
-        }
-        // every writing lane orders its generic-proxy smem writes before the
-        // async-proxy (TMA) store that reads them
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) bulk_s2g(p.dst, D, p.n * sizeof(TOut));
-      } else {  // multi-term or unaligned: the warp reduces straight from global memory
-        mbar_wait(&full[st], (k / kRedStages) & 1u);
-        for (uint32_t i = lane; i < p.n; i += 32) {
-          float acc = 0.0f;
-          for (int t = 0; t < p.nterms; ++t) acc += Cvt<TIn>::to(p.tp[t][p.off + i]);
-          if (beta != 0.0f) acc = fmaf(beta, Cvt<TOut>::to(p.dst[i]), acc);
-          p.dst[i] = Cvt<TOut>::from(acc);
-        }
-      }
-      __syncwarp();
-      if (lane == 0) {
-        if (k >= 1 && more) {
-          // the store of chunk k-1 must have read its stage before chunk k-1+S
-          // reloads it: with chunk k's own store committed that store may stay
-          // pending; a warp-reduced chunk k committed nothing, so wait for all
-          if (p.tma) bulk_wait_read<1>();
-          else bulk_wait_read<0>();
-          issue();
-        }
-        issued_sh = issued;
-      }
-      ++k;
-    }
-    if (lane == 0) bulk_wait_all();
-    __syncwarp();
-  }
-  epoch_finish(sync, cs);
-}
-
 template <class TIn, class TOut, int MODE>
 __global__ void __launch_bounds__(512, 2) reduce_segments_kernel(const ReduceSeg* __restrict__ segs, int nseg,
                                                               const void* const* __restrict__ terms,
                                                               Partition part, float beta, SyncArgs sync) {
-  __shared__ CtaSync cs;
-  sync_begin(sync, cs);
-  if (nseg > 0)
-    for_each_share<MODE>(segs, nseg, part, sync, cs, ReduceLen{},
-                         [&](const ReduceSeg& sg, uint64_t a, uint64_t b) {
-                           reduce_range<TIn, TOut>(static_cast<TOut*>(sg.dst),
-                                                   reinterpret_cast<const TIn* const*>(terms + sg.term0),
-                                                   sg.nterms, a, b, beta);
-                         });
-  epoch_finish(sync, cs);
+  run_shares<MODE>(segs, nseg, part, sync, ReduceLen{}, [&](const ReduceSeg& sg, uint64_t a, uint64_t b) {
+    reduce_range<TIn, TOut>(static_cast<TOut*>(sg.dst), reinterpret_cast<const TIn* const*>(terms + sg.term0),
+                            sg.nterms, a, b, beta);
+  });
 }
 
 }  // namespace
@@ -766,26 +668,9 @@ void launch_copy(const CopySeg* segs, int nseg, Partition part, const SyncArgs& 
 }
 
 template <class TIn, class TOut>
-static int red_tma_occupancy() {
-  static int n = -1;
-  if (n < 0) {
-    const int smem = kRedStages * kRedElems * (sizeof(TIn) + sizeof(TOut));
-    cudaFuncSetAttribute(reduce_segments_tma_kernel<TIn, TOut>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(reduce_segments_tma_kernel<TIn, TOut>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, reduce_segments_tma_kernel<TIn, TOut>, 32, smem);
-    if (n < 1) n = 1;
-  }
-  return n;
-}
-
-template <class TIn, class TOut>
 static void launch_reduce_t(const ReduceSeg* segs, int nseg, const void* const* terms, Partition part,
                             float beta, const SyncArgs& sync, int grid, int block, cudaStream_t st) {
-  if (part.mode == kPartTma) {
-    red_tma_occupancy<TIn, TOut>();
-    const int smem = kRedStages * kRedElems * (sizeof(TIn) + sizeof(TOut));
-    reduce_segments_tma_kernel<TIn, TOut><<<grid, 32, smem, st>>>(segs, nseg, terms, part, beta, sync);
-  } else if (part.mode == kPartInterleaved)
+  if (part.mode == kPartInterleaved)
     reduce_segments_kernel<TIn, TOut, kPartInterleaved><<<grid, block, 0, st>>>(segs, nseg, terms, part, beta, sync);
   else if (part.mode == kPartDynamic)
     reduce_segments_kernel<TIn, TOut, kPartDynamic><<<grid, block, 0, st>>>(segs, nseg, terms, part, beta, sync);
@@ -813,16 +698,6 @@ static int occ_t(int threads) {
     case kFP32 * 4 + kFP32: MACRO(float, float); break;                 \
     default: break;                                                   \
   }
-
-int reduce_tma_blocks_per_sm(int in_dtype, int out_dtype) {
-  int n = 1;
-#define HB_OCC2(TI, TO) n = red_tma_occupancy<TI, TO>()
-  HB_DISPATCH(in_dtype, out_dtype, HB_OCC2)
-#undef HB_OCC2
-  return n;
-}
-
-uint64_t reduce_tma_chunk_elems() { return kRedElems; }
 
 int reduce_blocks_per_sm(int threads, int in_dtype, int out_dtype) {
   int n = 1;

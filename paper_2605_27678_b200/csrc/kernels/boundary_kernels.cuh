@@ -48,7 +48,7 @@ enum PartMode : int {
   kPartDynamic = 2,      // `chunk`-sized pieces handed out by an atomic counter (ctr[3]) in the
                          // order of a host-built table that advances every segment at the
                          // same fractional pace (local HBM and remote NVLink runs overlap)
-  kPartTma = 3,          // dynamic chunks staged through shared memory by TMA bulk copies
+  kPartTma = 3,          // dynamic chunks moved by TMA bulk copies through shared memory (copy kernel)
 };
 
 struct Partition {
@@ -61,23 +61,46 @@ struct Partition {
   uint32_t rtotal_chunks;    // dynamic / TMA: chunks that read (pull) or write (push) a peer
   const uint2* rchunks;      // [rtotal_chunks]
   int remote_ctas;           // CTAs that start on the remote queue
+  // Static first chunks: CTA b < remote_ctas starts on remote chunk b, CTA
+  // b >= remote_ctas on local chunk b - remote_ctas (no claim round trip);
+  // the rest is claimed from the queue counters.
+  uint32_t lstatic;          // = min(grid - remote_ctas, total_chunks)
+  uint32_t rstatic;          // = min(remote_ctas, rtotal_chunks)
 };
 
 // Cross-GPU epoch barrier over peer-mapped flag words. Every GPU of an exec
 // group launches exactly one kernel per boundary op, so the per-exec op
-// counters stay in lockstep: at op e each GPU posts e to every peer's pad and
-// waits until every peer posted e to its own pad.
+// counts stay in lockstep: at its op e each GPU adds 1 to its slot in every
+// peer's pad (so pad[g] = ops GPU g has started) and, before touching a
+// peer's buffers, waits until pad[g] >= e for every peer g.
+//
+// Device counters (one 128-B line each, no false sharing between them):
+//   arrive : (epoch << 32) | CTAs arrived in this launch. Each CTA adds 1 once
+//            at start and learns e = epoch + 1; the last to arrive advances the
+//            epoch and zeroes the arrivals (no CTA of this launch reads it after).
+//   queue[2]: monotone 64-bit claim counters of the local / remote work queue.
+//            Every CTA claims until one claim fails in each non-empty queue, so a
+//            launch advances queue q by exactly (total_q - static_q) + grid and
+//            launch e's chunk index is raw - (e-1)*advance + static_q: no reset,
+//            no end-of-launch counter, no fence.
+//   fin    : push mode only — CTAs done writing (last CTA posts "writes done").
+//   err    : error word (1 = a flag wait timed out; the exec is unusable after).
 constexpr int kMaxGpus = 32;
+constexpr int kCtrLine = 32;  // u32 words per 128-B line
 struct SyncArgs {
-  uint32_t* pad;                  // local pad: pad[g] = last epoch posted by GPU g
+  uint32_t* pad;                  // local pad: pad[g] = ops GPU g started, pad[32+g] = ops it finished pushing
   uint32_t* peer_pad[kMaxGpus];   // peers' pads (nullptr for self / non-members)
-  uint32_t* ctr;                  // local: [0] epoch, [1] finished CTAs, [2] error, [3]/[4] work queues
+  unsigned long long* arrive;
+  unsigned long long* queue;      // [0] local, [kCtrLine/2] remote
+  uint32_t* fin;
+  uint32_t* err;
   uint32_t wait_mask;             // GPUs to wait for
   uint32_t post_mask;             // GPUs to post to
   int end_sync;                   // push mode: also post/wait "writes done" (pad[32+g]) before exit
   int my_gpu;
   uint64_t timeout_cycles;
 };
+constexpr int kCtrBytes = 4 * 128;  // arrive | queues | fin | err lines
 
 struct LaunchCfg {
   int grid;
@@ -95,7 +118,5 @@ int copy_blocks_per_sm(int threads);
 int tma_blocks_per_sm(uint64_t chunk);
 uint64_t tma_chunk_bytes(int kib);  // 32 (default), 16 or 8 KiB stages
 int reduce_blocks_per_sm(int threads, int in_dtype, int out_dtype);
-int reduce_tma_blocks_per_sm(int in_dtype, int out_dtype);
-uint64_t reduce_tma_chunk_elems();
 
 }  // namespace hb::dev
