@@ -121,6 +121,10 @@ typedef struct {
 int hb_index_forward(const hb_plan* p, const hb_splice* s, hb_copy_seg* out, size_t cap, size_t* n);
 int hb_index_backward(const hb_plan* p, const hb_splice* s, hb_reduce_seg* out, size_t cap,
                       size_t* n, hb_ref* terms, size_t tcap, size_t* tn);
+/* The backward map the device runtime executes by default (hb_exec_config.
+ * strict_provenance = 0): terms read from the holder's tp replicas in turn. */
+int hb_index_backward_balanced(const hb_plan* p, const hb_splice* s, hb_reduce_seg* out, size_t cap,
+                               size_t* n, hb_ref* terms, size_t tcap, size_t* tn);
 int hb_index_buffer_elems(const hb_plan* p, const hb_splice* s, int rank, int slot,
                           long long* elems);
 
@@ -137,6 +141,12 @@ typedef struct {
   double timeout_s; /* cross-GPU flag wait timeout                            */
   int fwd_mode;     /* forward: 0 auto, 1 consumers pull, 2 owners push         */
   int partition;    /* CTA work split: 0 auto, 1 contiguous, 2 interleaved      */
+  /* 0 (default): the backward reads each gradient term from one of the holder's
+   * tp replicas (the source rank itself if it is one, else replica j % tp), which
+   * spreads NVLink egress; identical sums when tp replicas hold identical
+   * gradients, the contract of bridge.hpp:33-36. 1: always the tp=0 copy, the
+   * reference data path replica for replica (strict provenance). */
+  int strict_provenance;
 } hb_exec_config;
 void hb_exec_config_default(hb_exec_config* c);
 

@@ -29,7 +29,7 @@ EXPORTS = [
     "hb_placement_of_edge", "hb_ranks_of_stage", "hb_replica_group", "hb_module_group",
     "hb_classify_dp_relation", "hb_plan_create", "hb_plan_destroy", "hb_plan_export", "hb_plan_info",
     "hb_cp_token_slice", "hb_splice_create", "hb_splice_destroy",
-    "hb_index_forward", "hb_index_backward", "hb_index_buffer_elems",
+    "hb_index_forward", "hb_index_backward", "hb_index_backward_balanced", "hb_index_buffer_elems",
     "hb_exec_config_default", "hb_exec_create", "hb_exec_destroy", "hb_exec_ipc_handle",
     "hb_exec_open_peers", "hb_exec_buffer", "hb_exec_bind", "hb_exec_forward", "hb_exec_backward",
     "hb_exec_seed_forward_record", "hb_exec_status", "hb_exec_stats", "hb_exec_graph_capture",
@@ -76,7 +76,7 @@ class ExecConfig(ctypes.Structure):
                 ("grad_out_dtype", ctypes.c_int), ("mb_slots", ctypes.c_int),
                 ("internal_alloc", ctypes.c_int), ("blocks_per_sm", ctypes.c_int),
                 ("threads", ctypes.c_int), ("timeout_s", ctypes.c_double), ("fwd_mode", ctypes.c_int),
-                ("partition", ctypes.c_int)]
+                ("partition", ctypes.c_int), ("strict_provenance", ctypes.c_int)]
 
 
 _lib = None
@@ -108,6 +108,7 @@ def _declare(L):
         "hb_splice_destroy": (None, [V]),
         "hb_index_forward": (I, [V, V, P(CopySeg), Sz, P(Sz)]),
         "hb_index_backward": (I, [V, V, P(ReduceSeg), Sz, P(Sz), P(Ref), Sz, P(Sz)]),
+        "hb_index_backward_balanced": (I, [V, V, P(ReduceSeg), Sz, P(Sz), P(Ref), Sz, P(Sz)]),
         "hb_index_buffer_elems": (I, [V, V, I, I, P(LL)]),
         "hb_exec_config_default": (None, [P(ExecConfig)]),
         "hb_exec_create": (I, [V, V, I, I, P(I), I, P(ExecConfig), P(V)]),

@@ -150,15 +150,18 @@ def index_forward(plan: BridgePlan, splice: SpliceSpec | None = None):
             for s in arr[: n.value]]
 
 
-def index_backward(plan: BridgePlan, splice: SpliceSpec | None = None):
-    """Backward map: list of (dst_rank, dst_slot, dst_off, n, [(rank, slot, off), ...])."""
+def index_backward(plan: BridgePlan, splice: SpliceSpec | None = None, balanced: bool = False):
+    """Backward map: list of (dst_rank, dst_slot, dst_off, n, [(rank, slot, off), ...]).
+
+    balanced=False is the reference data path (tp=0 copies); True is the map the
+    device runtime executes by default (terms read from the holder's tp replicas)."""
     n, tn = ctypes.c_size_t(), ctypes.c_size_t()
     sh = splice._h if splice else None
-    check(lib().hb_index_backward(plan._h, sh, None, 0, ctypes.byref(n), None, 0, ctypes.byref(tn)))
+    fn = lib().hb_index_backward_balanced if balanced else lib().hb_index_backward
+    check(fn(plan._h, sh, None, 0, ctypes.byref(n), None, 0, ctypes.byref(tn)))
     arr = (_lib.ReduceSeg * max(n.value, 1))()
     terms = (_lib.Ref * max(tn.value, 1))()
-    check(lib().hb_index_backward(plan._h, sh, arr, n.value, ctypes.byref(n), terms, tn.value,
-                                  ctypes.byref(tn)))
+    check(fn(plan._h, sh, arr, n.value, ctypes.byref(n), terms, tn.value, ctypes.byref(tn)))
     out = []
     for s in arr[: n.value]:
         ts = [(t.rank, t.slot, t.off) for t in terms[s.term0: s.term0 + s.nterms]]
@@ -206,7 +209,7 @@ class BridgeRuntime:
                  my_gpu: int = 0, rank_to_gpu=None, act_dtype=None, grad_in_dtype=None,
                  grad_out_dtype=None, mb_slots: int = 1, internal_alloc: bool = True,
                  blocks_per_sm: int = 0, threads: int = 0, timeout_s: float = 0.0,
-                 fwd_mode: int = 0, partition: int = 0):
+                 fwd_mode: int = 0, partition: int = 0, strict_provenance: bool = False):
         import torch
 
         self.plan, self.splice = plan, splice
@@ -228,6 +231,7 @@ class BridgeRuntime:
         cfg.timeout_s = timeout_s
         cfg.fwd_mode = fwd_mode  # 0 auto, 1 pull, 2 push
         cfg.partition = partition
+        cfg.strict_provenance = 1 if strict_provenance else 0
         if not torch.cuda.is_available():
             raise HetBridgeError(25, "BridgeRuntime needs a CUDA device (no CPU fallback)")
         m = (ctypes.c_int * len(self.rank_to_gpu))(*self.rank_to_gpu)

@@ -105,6 +105,17 @@ def get(name: str, scale: int = 1) -> BoundaryConfig:
         return BoundaryConfig("c5w4", "non-colocated vit{dp1}@0 -> llm{tp1,pp3}@1-3, bf16 h4096, 8 img x 576",
                               ModuleLayout("vit", dp=1), ModuleLayout("llm", pp=3, rank_offset=1), 8, 576,
                               h(4096), logical_world=4)
+    # 4-GPU stand-ins for the per-GPU traffic of the 8-GPU runs (one rank per
+    # GPU, every GPU exchanging with three peers): C2's 4-member all-gather,
+    # C3's 4-member gradient gather (diagnostics; N=8 runs only in the driver).
+    if name == "c2x4":
+        return BoundaryConfig("c2x4", "fan-in colocated vit{dp4} -> llm{tp4}, bf16 h4096, 32 img x 576",
+                              ModuleLayout("vit", dp=4), ModuleLayout("llm", tp=4), 32, 576, h(4096),
+                              logical_world=4)
+    if name == "c3x4":
+        return BoundaryConfig("c3x4", "fan-out colocated enc{tp4} -> llm{dp4}, bf16 h5120, 32 img x 576",
+                              ModuleLayout("encoder", tp=4), ModuleLayout("llm", dp=4), 32, 576, h(5120),
+                              logical_world=4)
     raise KeyError(name)
 
 

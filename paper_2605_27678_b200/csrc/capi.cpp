@@ -84,7 +84,7 @@ const char* hb_error_name(int status) {
   return hb::error_code_name(static_cast<hb::ErrorCode>(status - 1));
 }
 
-int hb_abi_version(void) { return 4; }
+int hb_abi_version(void) { return 5; }
 
 int hb_coord_of_rank(const hb_layout* l, int rank, int coord4[4]) {
   return guard([&] {
@@ -237,12 +237,13 @@ int hb_index_forward(const hb_plan* p, const hb_splice* s, hb_copy_seg* out, siz
   });
 }
 
-int hb_index_backward(const hb_plan* p, const hb_splice* s, hb_reduce_seg* out, size_t cap, size_t* n,
-                      hb_ref* terms, size_t tcap, size_t* tn) {
+namespace {
+int index_backward(const hb_plan* p, const hb_splice* s, bool balanced, hb_reduce_seg* out, size_t cap, size_t* n,
+                   hb_ref* terms, size_t tcap, size_t* tn) {
   return guard([&] {
     need(p, "plan");
     need(n, "count");
-    const auto m = hb::index::build_index_map(p->plan, spec(s));
+    const auto m = hb::index::build_index_map(p->plan, spec(s), balanced);
     *n = m.bwd.size();
     size_t t = 0;
     for (size_t i = 0; i < m.bwd.size(); ++i) {
@@ -256,6 +257,17 @@ int hb_index_backward(const hb_plan* p, const hb_splice* s, hb_reduce_seg* out, 
     }
     if (tn) *tn = t;
   });
+}
+}  // namespace
+
+int hb_index_backward(const hb_plan* p, const hb_splice* s, hb_reduce_seg* out, size_t cap, size_t* n,
+                      hb_ref* terms, size_t tcap, size_t* tn) {
+  return index_backward(p, s, false, out, cap, n, terms, tcap, tn);
+}
+
+int hb_index_backward_balanced(const hb_plan* p, const hb_splice* s, hb_reduce_seg* out, size_t cap, size_t* n,
+                               hb_ref* terms, size_t tcap, size_t* tn) {
+  return index_backward(p, s, true, out, cap, n, terms, tcap, tn);
 }
 
 int hb_index_buffer_elems(const hb_plan* p, const hb_splice* s, int rank, int slot, long long* elems) {
@@ -282,6 +294,7 @@ void hb_exec_config_default(hb_exec_config* c) {
   c->timeout_s = d.timeout_s;
   c->fwd_mode = d.fwd_mode;
   c->partition = d.partition;
+  c->strict_provenance = d.strict_provenance;
 }
 
 int hb_exec_create(const hb_plan* p, const hb_splice* s, int n_gpus, int my_gpu, const int* rank_to_gpu,
@@ -302,6 +315,7 @@ int hb_exec_create(const hb_plan* p, const hb_splice* s, int n_gpus, int my_gpu,
       c.timeout_s = cfg->timeout_s > 0 ? cfg->timeout_s : c.timeout_s;
       c.fwd_mode = cfg->fwd_mode;
       c.partition = cfg->partition;
+      c.strict_provenance = cfg->strict_provenance;
     }
     std::vector<int> map;
     if (rank_to_gpu) map.assign(rank_to_gpu, rank_to_gpu + n_ranks);

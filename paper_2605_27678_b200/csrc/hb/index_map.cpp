@@ -149,7 +149,37 @@ void push_reduce(std::vector<ReduceSeg>& v, ReduceSeg&& s) {
 
 }  // namespace
 
-IndexMap build_index_map(const BridgePlan& p, const SpliceSpec* sp) {
+namespace {
+
+// Chooses which tensor-parallel replica of a gradient holder serves a term:
+// the source rank itself when it is one of the replicas (no transfer), else
+// the replica that has served the fewest elements so far (ties: lowest tp).
+// Decided per (source sample, holder) so a sample's rows stay one run.
+struct ReplicaChooser {
+  const BridgePlan& p;
+  std::vector<int64_t> load;
+  int operator()(int h, int r, int64_t weight) {
+    const auto& L = p.edge.dest;
+    if (L.tp == 1) return h;
+    grid::GridCoord c = grid::coord_of_rank(L, h);
+    int best = -1;
+    for (int k = 0; k < L.tp; ++k) {
+      c.tp_idx = k;
+      const int cand = grid::rank_of_coord(L, c);
+      if (cand == r) {
+        best = cand;
+        break;
+      }
+      if (best < 0 || load[cand] < load[best]) best = cand;
+    }
+    load[best] += weight;
+    return best;
+  }
+};
+
+}  // namespace
+
+IndexMap build_index_map(const BridgePlan& p, const SpliceSpec* sp, bool balance_replicas) {
   if (sp) sp->validate(p);
   IndexMap m;
   m.world = std::max(p.edge.source.rank_end(), p.edge.dest.rank_end());
@@ -163,6 +193,7 @@ IndexMap build_index_map(const BridgePlan& p, const SpliceSpec* sp) {
     m.elems[r][kSrcGrad] = n;
   }
 
+  ReplicaChooser choose{p, std::vector<int64_t>(m.world, 0)};
   if (!sp) {
     for (int r : Rd) {
       const auto& DI = p.dest_intervals[p.dest_shard_of(r)];
@@ -176,7 +207,8 @@ IndexMap build_index_map(const BridgePlan& p, const SpliceSpec* sp) {
       const auto& SI = p.src_intervals[p.source_shard_of(r)];
       for (int j = SI.start; j < SI.end(); ++j) {
         ReduceSeg s{{r, kSrcGrad, (j - SI.start) * W}, W, {}};
-        for (const RowRef& t : backward_origin(p, r, j)) s.terms.push_back({t.rank, kDstGrad, t.row * W});
+        for (const RowRef& t : backward_origin(p, r, j))
+          s.terms.push_back({balance_replicas ? choose(t.rank, r, W) : t.rank, kDstGrad, t.row * W});
         m.max_terms = std::max<int>(m.max_terms, s.terms.size());
         push_reduce(m.bwd, std::move(s));
       }
@@ -219,7 +251,19 @@ IndexMap build_index_map(const BridgePlan& p, const SpliceSpec* sp) {
   for (int r : Rs) {
     const auto& SI = p.src_intervals[p.source_shard_of(r)];
     for (int j = SI.start; j < SI.end(); ++j) {
-      const auto origin = backward_origin(p, r, j);
+      auto origin = backward_origin(p, r, j);
+      if (balance_replicas)
+        for (RowRef& o : origin) {
+          // weight: the rows of sample j that lie inside the holder's slice
+          const int c = grid::coord_of_rank(p.edge.dest, o.rank).cp_idx;
+          int64_t rows = 0;
+          for (int t = 0; t < sp->S_v; ++t) {
+            const int64_t at = pos_of[static_cast<int64_t>(o.row) * sp->S_v + t];
+            const int pos = at < 0 ? -1 : static_cast<int>(at % sp->S);
+            rows += pos >= c * L && pos < (c + 1) * L;
+          }
+          if (rows) o.rank = choose(o.rank, r, rows * dh);
+        }
       for (int t = 0; t < sp->S_v; ++t) {
         ReduceSeg s{{r, kSrcGrad, (j - SI.start) * W + t * dh}, dh, {}};
         for (const RowRef& o : origin) {

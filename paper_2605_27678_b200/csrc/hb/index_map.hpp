@@ -74,7 +74,15 @@ struct IndexMap {
   int max_terms = 0;
 };
 
-IndexMap build_index_map(const bridge::BridgePlan& plan, const SpliceSpec* splice);
+/// balance_replicas: the backward reads each destination-gradient term from
+/// one of the holder's tensor-parallel replicas instead of always the tp=0
+/// copy (bridge.hpp:33-36: tp replicas hand back identical gradients), chosen
+/// as the source rank itself when it is one of them, else replica j % tp for
+/// global sample j. The sums are unchanged for inputs that honour the
+/// contract, and the NVLink egress of a gradient return is spread over the tp
+/// replicas instead of concentrating on the tp=0 rank. false reproduces the
+/// reference data path replica for replica (strict provenance).
+IndexMap build_index_map(const bridge::BridgePlan& plan, const SpliceSpec* splice, bool balance_replicas = false);
 
 /// Row-level provenance, exposed for tests: source rank/row that feeds
 /// destination rank `r`'s global sample j in forward, and the ordered

@@ -32,7 +32,7 @@ Exec::Exec(const bridge::BridgePlan& plan, const index::SpliceSpec* splice, int 
     if (dt < dev::kBF16 || dt > dev::kFP64) raise(ErrorCode::InvalidArgument, "unknown dtype");
   if (cfg.grad_in_dtype == dev::kFP64 || cfg.grad_out_dtype == dev::kFP64)
     raise(ErrorCode::InvalidArgument, "fp64 gradients are not supported on the device path");
-  map_ = index::build_index_map(plan_, splice);
+  map_ = index::build_index_map(plan_, splice, cfg.strict_provenance == 0);
   if (static_cast<int>(rank_to_gpu_.size()) < map_.world)
     raise(ErrorCode::InvalidArgument, "rank_to_gpu must cover every logical rank of the edge");
   for (int r = 0; r < map_.world; ++r)
@@ -291,7 +291,10 @@ void Exec::build_partition(const std::vector<uint64_t>& w0, const std::vector<ui
       out->remote_ctas = grid;
     } else {
       const double tr = remote_bytes / 770e9, tl = 2.0 * local_bytes / 6.5e12;
-      out->remote_ctas = std::clamp(static_cast<int>(grid * tr / (tr + tl) + 0.5), 1, grid - 1);
+      // HB_REMOTE_PCT overrides the remote share of the grid (tuning knob)
+      static const double frac = static_cast<double>(env_u64("HB_REMOTE_PCT", 0)) / 100.0;
+      const double f = frac > 0 ? frac : tr / (tr + tl);
+      out->remote_ctas = std::clamp(static_cast<int>(grid * f + 0.5), 1, grid - 1);
     }
     out->rstatic = std::min<uint32_t>(out->remote_ctas, out->rtotal_chunks);
     out->lstatic = std::min<uint32_t>(grid - out->remote_ctas, out->total_chunks);
@@ -421,6 +424,7 @@ void Exec::prepare_bwd() {
     (r ? rb : lb) += static_cast<double>(ns[i]) * (es_in + 2 * es_out);
   }
   build_partition(w0s, ns, rem, lb, rb, sm_count_ * bps, mode, unit, &bwd_part_);
+  bwd_part_.ring = static_cast<int>(env_u64("HB_RED_RING", 1));  // A/B knob: 0 = LDG for remote chunks too
   dirty_bwd_ = false;
 }
 

@@ -38,6 +38,7 @@ struct ExecConfig {
   double timeout_s = 20.0;          // flag-wait timeout
   int fwd_mode = 0;                 // forward: 0 auto, 1 consumers pull from owners, 2 owners push
   int partition = 0;                // 0 auto, 1 contiguous, 2 interleaved, 3 dynamic, 4 TMA bulk (copy)
+  int strict_provenance = 0;        // 1: backward reads tp=0 copies only (index_map.hpp balance_replicas)
 };
 
 class Exec {
@@ -134,9 +135,10 @@ class Exec {
     uint2* rchunks = nullptr;
     int remote_ctas = 0;
     uint32_t lstatic = 0, rstatic = 0;
+    int ring = 1;
     dev::Partition dev() const {
       return {first_seg, per_cta, mode, total_chunks, chunk, chunks, rtotal_chunks, rchunks, remote_ctas,
-              lstatic, rstatic};
+              lstatic, rstatic, ring};
     }
   };
   DevPartition fwd_part_, bwd_part_;

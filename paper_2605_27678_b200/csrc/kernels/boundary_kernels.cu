@@ -247,7 +247,7 @@ __device__ __forceinline__ void run_shares(const S* __restrict__ segs, int nseg,
         const uint2 t = (cur_remote ? part.rchunks : part.chunks)[c];
         const S sg = segs[t.x];
         const uint64_t a = static_cast<uint64_t>(t.y) * part.chunk, e = a + part.chunk, n = len(sg);
-        body(sg, a, e < n ? e : n);
+        body(sg, a, e < n ? e : n, cur_remote != 0);
       }
       __syncthreads();
       if (threadIdx.x == 0) {
@@ -273,7 +273,7 @@ __device__ __forceinline__ void run_shares(const S* __restrict__ segs, int nseg,
         for (int s = 0; s < nseg; ++s) {
           const S sg = segs[s];
           uint64_t a, b;
-          if (cta_share(len(sg), &a, &b)) body(sg, a, b);
+          if (cta_share(len(sg), &a, &b)) body(sg, a, b, false);
         }
       } else {
         const uint64_t lo = blockIdx.x * part.per_cta, hi = lo + part.per_cta;
@@ -283,7 +283,7 @@ __device__ __forceinline__ void run_shares(const S* __restrict__ segs, int nseg,
           const uint64_t a = (lo > sg.w0 ? lo : sg.w0) - sg.w0;
           const uint64_t e = sg.w0 + len(sg);
           const uint64_t b = (hi < e ? hi : e) - sg.w0;
-          if (a < b) body(sg, a, b);
+          if (a < b) body(sg, a, b, false);
         }
       }
     }
@@ -347,7 +347,7 @@ template <int MODE>
 __global__ void __launch_bounds__(512, 2) copy_segments_kernel(const CopySeg* __restrict__ segs, int nseg,
                                                             Partition part, SyncArgs sync) {
   run_shares<MODE>(segs, nseg, part, sync, CopyLen{},
-                   [](const CopySeg& sg, uint64_t a, uint64_t b) { copy_range(sg, a, b); });
+                   [](const CopySeg& sg, uint64_t a, uint64_t b, bool) { copy_range(sg, a, b); });
 }
 
 // ---- TMA bulk-copy engine ------------------------------------------------------
@@ -514,78 +514,148 @@ template <> struct Cvt<__half> {
   __device__ static __half from(float x) { return __float2half_rn(x); }
 };
 
-// 8 elements of T through 16 B vector accesses (1 x uint4 for 2-byte T, 2 for fp32).
+// 8 elements of T <-> 8 floats through 16 B vector accesses (1 x uint4 for
+// 2-byte T, 2 for fp32). Conversions work on the 32-bit words with bit ops
+// and packed cvt instructions, so nothing is type-punned through memory (a
+// punned uint4 array ends up in local memory under the 64-register cap).
+template <class T> struct Pack8;
+template <> struct Pack8<float> {
+  static constexpr int NV = 2;
+  __device__ static void unpack(const uint4 (&v)[NV], float (&f)[8]) {
+    f[0] = __uint_as_float(v[0].x); f[1] = __uint_as_float(v[0].y);
+    f[2] = __uint_as_float(v[0].z); f[3] = __uint_as_float(v[0].w);
+    f[4] = __uint_as_float(v[1].x); f[5] = __uint_as_float(v[1].y);
+    f[6] = __uint_as_float(v[1].z); f[7] = __uint_as_float(v[1].w);
+  }
+  __device__ static void pack(const float (&f)[8], uint4 (&v)[NV]) {
+    v[0] = make_uint4(__float_as_uint(f[0]), __float_as_uint(f[1]), __float_as_uint(f[2]), __float_as_uint(f[3]));
+    v[1] = make_uint4(__float_as_uint(f[4]), __float_as_uint(f[5]), __float_as_uint(f[6]), __float_as_uint(f[7]));
+  }
+};
+__device__ __forceinline__ uint32_t cvt_bf16x2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+__device__ __forceinline__ uint32_t cvt_f16x2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+__device__ __forceinline__ float f16_lo(uint32_t w) { return __half2float(__ushort_as_half(static_cast<unsigned short>(w & 0xffffu))); }
+__device__ __forceinline__ float f16_hi(uint32_t w) { return __half2float(__ushort_as_half(static_cast<unsigned short>(w >> 16))); }
+template <> struct Pack8<__nv_bfloat16> {
+  static constexpr int NV = 1;
+  __device__ static void unpack(const uint4 (&v)[NV], float (&f)[8]) {
+    const uint32_t w[4] = {v[0].x, v[0].y, v[0].z, v[0].w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      f[2 * i] = __uint_as_float(w[i] << 16);
+      f[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+    }
+  }
+  __device__ static void pack(const float (&f)[8], uint4 (&v)[NV]) {
+    v[0] = make_uint4(cvt_bf16x2(f[0], f[1]), cvt_bf16x2(f[2], f[3]), cvt_bf16x2(f[4], f[5]), cvt_bf16x2(f[6], f[7]));
+  }
+};
+template <> struct Pack8<__half> {
+  static constexpr int NV = 1;
+  __device__ static void unpack(const uint4 (&v)[NV], float (&f)[8]) {
+    const uint32_t w[4] = {v[0].x, v[0].y, v[0].z, v[0].w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      f[2 * i] = f16_lo(w[i]);
+      f[2 * i + 1] = f16_hi(w[i]);
+    }
+  }
+  __device__ static void pack(const float (&f)[8], uint4 (&v)[NV]) {
+    v[0] = make_uint4(cvt_f16x2(f[0], f[1]), cvt_f16x2(f[2], f[3]), cvt_f16x2(f[4], f[5]), cvt_f16x2(f[6], f[7]));
+  }
+};
+
 template <class T>
 __device__ __forceinline__ void load8(const T* p, float (&f)[8]) {
-  constexpr int NV = sizeof(T) * 8 / 16;
-  uint4 v[NV];
+  uint4 v[Pack8<T>::NV];
 #pragma unroll
-  for (int i = 0; i < NV; ++i) v[i] = ld_stream(reinterpret_cast<const uint4*>(p) + i);
-  const T* e = reinterpret_cast<const T*>(v);
-#pragma unroll
-  for (int i = 0; i < 8; ++i) f[i] = Cvt<T>::to(e[i]);
+  for (int i = 0; i < Pack8<T>::NV; ++i) v[i] = ld_stream(reinterpret_cast<const uint4*>(p) + i);
+  Pack8<T>::unpack(v, f);
 }
 
 template <class T>
 __device__ __forceinline__ void load8_coherent(const T* p, float (&f)[8]) {
-  constexpr int NV = sizeof(T) * 8 / 16;
-  uint4 v[NV];
+  uint4 v[Pack8<T>::NV];
 #pragma unroll
-  for (int i = 0; i < NV; ++i) v[i] = *(reinterpret_cast<const uint4*>(p) + i);
-  const T* e = reinterpret_cast<const T*>(v);
-#pragma unroll
-  for (int i = 0; i < 8; ++i) f[i] = Cvt<T>::to(e[i]);
+  for (int i = 0; i < Pack8<T>::NV; ++i) v[i] = *(reinterpret_cast<const uint4*>(p) + i);
+  Pack8<T>::unpack(v, f);
 }
 
 template <class T>
 __device__ __forceinline__ void store8(T* p, const float (&f)[8]) {
-  constexpr int NV = sizeof(T) * 8 / 16;
-  uint4 v[NV];
-  T* e = reinterpret_cast<T*>(v);
+  uint4 v[Pack8<T>::NV];
+  Pack8<T>::pack(f, v);
 #pragma unroll
-  for (int i = 0; i < 8; ++i) e[i] = Cvt<T>::from(f[i]);
-#pragma unroll
-  for (int i = 0; i < NV; ++i) st_vec(reinterpret_cast<uint4*>(p) + i, v[i]);
+  for (int i = 0; i < Pack8<T>::NV; ++i) st_vec(reinterpret_cast<uint4*>(p) + i, v[i]);
 }
 
+// acc[] (+)= the n terms' 8 elements at offset i (acc starts at +0.0f: terms
+// are summed in order from +0.0, as simnet's all_reduce does).
+template <class TIn>
+__device__ __forceinline__ void sum_terms8(const TIn* const* __restrict__ tp, int nterms, uint64_t i,
+                                           float (&acc)[8]) {
+  load8(tp[0] + i, acc);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) acc[k] = 0.0f + acc[k];
+  for (int t = 1; t < nterms; ++t) {
+    float v[8];
+    load8(tp[t] + i, v);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc[k] += v[k];
+  }
+}
+
+template <class TOut>
+__device__ __forceinline__ void finish8(TOut* __restrict__ dst, uint64_t i, float beta, float (&acc)[8]) {
+  if (beta != 0.0f) {
+    float o[8];
+    load8_coherent(dst + i, o);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc[k] = fmaf(beta, o[k], acc[k]);
+  }
+  store8(dst + i, acc);
+}
+
+// dst[a, b) = beta*dst + sum of the terms, whole CTA, two 8-element groups per
+// thread per iteration (their loads are issued together).
 template <class TIn, class TOut>
 __device__ __forceinline__ void reduce_range(TOut* __restrict__ dst, const TIn* const* __restrict__ tp, int nterms,
                                              uint64_t a, uint64_t b, float beta) {
   uint64_t align = reinterpret_cast<uint64_t>(dst + a);
   for (int t = 0; t < nterms; ++t) align |= reinterpret_cast<uint64_t>(tp[t] + a);
   uint64_t i = a;
-  if ((align & 15) == 0) {
+  if ((align & 15) == 0 && nterms > 0) {
     const uint64_t vend = a + ((b - a) & ~uint64_t(7));
     const uint64_t step = static_cast<uint64_t>(blockDim.x) * 8;
-    for (i = a + threadIdx.x * 8; i < vend; i += 2 * step) {
-      const bool two = i + step < vend;
+    for (i = a + threadIdx.x * 8; i + step < vend; i += 2 * step) {
       float acc0[8], acc1[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) acc0[k] = acc1[k] = 0.0f;
-      for (int t = 0; t < nterms; ++t) {
-        float v0[8], v1[8];
-        load8(tp[t] + i, v0);
-        if (two) load8(tp[t] + i + step, v1);
-#pragma unroll
-        for (int k = 0; k < 8; ++k) acc0[k] += v0[k];
-        if (two) {
-#pragma unroll
-          for (int k = 0; k < 8; ++k) acc1[k] += v1[k];
-        }
-      }
-      if (beta != 0.0f) {
+      sum_terms8(tp, nterms, i, acc0);
+      sum_terms8(tp, nterms, i + step, acc1);
+      if (beta != 0.0f) {  // both accumulator loads in flight before either store
         float o0[8], o1[8];
         load8_coherent(dst + i, o0);
-        if (two) load8_coherent(dst + i + step, o1);
+        load8_coherent(dst + i + step, o1);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) acc0[k] = fmaf(beta, o0[k], acc0[k]);
-        if (two) {
-#pragma unroll
-          for (int k = 0; k < 8; ++k) acc1[k] = fmaf(beta, o1[k], acc1[k]);
+        for (int k = 0; k < 8; ++k) {
+          acc0[k] = fmaf(beta, o0[k], acc0[k]);
+          acc1[k] = fmaf(beta, o1[k], acc1[k]);
         }
       }
       store8(dst + i, acc0);
-      if (two) store8(dst + i + step, acc1);
+      store8(dst + i + step, acc1);
+    }
+    if (i < vend) {
+      float acc[8];
+      sum_terms8(tp, nterms, i, acc);
+      finish8(dst, i, beta, acc);
     }
     i = vend;
   }
@@ -601,13 +671,102 @@ struct ReduceLen {
   __device__ uint64_t operator()(const ReduceSeg& s) const { return s.nelem; }
 };
 
+// Remote single-term chunks (the gradient-return pulls of the dynamic
+// partition) stream their term through a ring of shared-memory stages filled by
+// TMA bulk loads from the peer (one issuing thread, kRedRingBytes in flight per
+// CTA), so NVLink latency is hidden by the ring rather than by per-thread loads;
+// every thread reads its 8-element groups from smem and does the fp32
+// read-modify-write of the local accumulator (its dst loads are issued before
+// it waits for the stage). Everything else uses reduce_range.
+constexpr uint32_t kRedSub = 4096;                 // elements per stage
+constexpr uint32_t kRedRingBytes = 64 * 1024;      // per CTA
+template <class TIn>
+__host__ __device__ constexpr int red_stages() { return static_cast<int>(kRedRingBytes / (kRedSub * sizeof(TIn))); }
+
+template <class TIn, class TOut>
+struct RedRing {
+  uint64_t* full;            // [stages] mbarriers (shared)
+  unsigned char* mem;        // stages x kRedSub x sizeof(TIn) (dynamic shared)
+  uint32_t used;             // stages consumed so far (uniform across the CTA)
+
+  __device__ void issue(const TIn* src, uint32_t k, uint32_t nelem) {  // sub-load k of the ring's lifetime
+    constexpr int S = red_stages<TIn>();
+    const int st = k % S;
+    const uint32_t bytes = nelem * sizeof(TIn);
+    mbar_expect(&full[st], bytes);
+    bulk_g2s(mem + st * (kRedSub * sizeof(TIn)), src, bytes, &full[st]);
+  }
+
+  // dst[0, n) = beta*dst + term[0, n); n a multiple of 8, 16-B aligned pointers
+  __device__ void run(TOut* __restrict__ dst, const TIn* __restrict__ term, uint64_t n, float beta) {
+    constexpr int S = red_stages<TIn>();
+    const uint32_t nsub = static_cast<uint32_t>((n + kRedSub - 1) / kRedSub);
+    auto sub_len = [&](uint32_t i) {
+      const uint64_t r = n - static_cast<uint64_t>(i) * kRedSub;
+      return static_cast<uint32_t>(r < kRedSub ? r : kRedSub);
+    };
+    if (threadIdx.x == 0)
+      for (uint32_t i = 0; i < nsub && i < static_cast<uint32_t>(S); ++i)
+        issue(term + static_cast<uint64_t>(i) * kRedSub, used + i, sub_len(i));
+    for (uint32_t i = 0; i < nsub; ++i) {
+      const uint32_t k = used + i, len = sub_len(i);
+      const int st = k % S;
+      TOut* d = dst + static_cast<uint64_t>(i) * kRedSub;
+      const TIn* T = reinterpret_cast<const TIn*>(mem + st * (kRedSub * sizeof(TIn)));
+      // the first group's accumulator load goes out before the stage wait
+      const uint32_t j0 = threadIdx.x * 8;
+      float o[8];
+      if (beta != 0.0f && j0 < len) load8_coherent(d + j0, o);
+      mbar_wait(&full[st], (k / S) & 1u);
+      for (uint32_t j = j0; j < len; j += blockDim.x * 8) {
+        if (j != j0 && beta != 0.0f) load8_coherent(d + j, o);
+        float acc[8];
+        load8_coherent(T + j, acc);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q] = beta != 0.0f ? fmaf(beta, o[q], 0.0f + acc[q]) : 0.0f + acc[q];
+        store8(d + j, acc);
+      }
+      __syncthreads();  // stage st fully read
+      if (threadIdx.x == 0 && i + S < nsub) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(term + static_cast<uint64_t>(i + S) * kRedSub, k + S, sub_len(i + S));
+      }
+    }
+    used += nsub;
+  }
+};
+
 template <class TIn, class TOut, int MODE>
 __global__ void __launch_bounds__(512, 2) reduce_segments_kernel(const ReduceSeg* __restrict__ segs, int nseg,
                                                               const void* const* __restrict__ terms,
                                                               Partition part, float beta, SyncArgs sync) {
-  run_shares<MODE>(segs, nseg, part, sync, ReduceLen{}, [&](const ReduceSeg& sg, uint64_t a, uint64_t b) {
-    reduce_range<TIn, TOut>(static_cast<TOut*>(sg.dst), reinterpret_cast<const TIn* const*>(terms + sg.term0),
-                            sg.nterms, a, b, beta);
+  constexpr int S = red_stages<TIn>();
+  extern __shared__ __align__(128) unsigned char red_mem[];
+  __shared__ __align__(8) uint64_t full[S];
+  RedRing<TIn, TOut> ring{full, red_mem, 0};
+  if constexpr (MODE == kPartDynamic) {
+    if (threadIdx.x == 0) {
+      for (int i = 0; i < S; ++i) mbar_init(&full[i]);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    // (run_shares syncs the CTA before the first body)
+  }
+  run_shares<MODE>(segs, nseg, part, sync, ReduceLen{},
+                   [&](const ReduceSeg& sg, uint64_t a, uint64_t b, bool remote) {
+    const TIn* const* tp = reinterpret_cast<const TIn* const*>(terms + sg.term0);
+    TOut* dst = static_cast<TOut*>(sg.dst);
+    if constexpr (MODE == kPartDynamic) {
+      if (remote && sg.nterms == 1 && part.ring) {  // (remote chunks exist => the ring smem was allocated)
+        const uint64_t n8 = (b - a) & ~uint64_t(7);
+        const uint64_t al = reinterpret_cast<uint64_t>(dst + a) | reinterpret_cast<uint64_t>(tp[0] + a);
+        if ((al & 15) == 0 && n8 > 0) {
+          ring.run(dst + a, tp[0] + a, n8, beta);
+          if (a + n8 < b) reduce_range<TIn, TOut>(dst, tp, 1, a + n8, b, beta);
+          return;
+        }
+      }
+    }
+    reduce_range<TIn, TOut>(dst, tp, sg.nterms, a, b, beta);
   });
 }
 
@@ -668,12 +827,25 @@ void launch_copy(const CopySeg* segs, int nseg, Partition part, const SyncArgs& 
 }
 
 template <class TIn, class TOut>
+static int red_ring_smem() {
+  static const int smem = [] {
+    cudaFuncSetAttribute(reduce_segments_kernel<TIn, TOut, kPartDynamic>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kRedRingBytes);
+    return static_cast<int>(kRedRingBytes);
+  }();
+  return smem;
+}
+
+template <class TIn, class TOut>
 static void launch_reduce_t(const ReduceSeg* segs, int nseg, const void* const* terms, Partition part,
                             float beta, const SyncArgs& sync, int grid, int block, cudaStream_t st) {
   if (part.mode == kPartInterleaved)
     reduce_segments_kernel<TIn, TOut, kPartInterleaved><<<grid, block, 0, st>>>(segs, nseg, terms, part, beta, sync);
   else if (part.mode == kPartDynamic)
-    reduce_segments_kernel<TIn, TOut, kPartDynamic><<<grid, block, 0, st>>>(segs, nseg, terms, part, beta, sync);
+    // the ring's shared memory only when there are remote chunks to stage
+    reduce_segments_kernel<TIn, TOut, kPartDynamic>
+        <<<grid, block, part.ring && part.rtotal_chunks ? red_ring_smem<TIn, TOut>() : 0, st>>>(segs, nseg, terms,
+                                                                                           part, beta, sync);
   else
     reduce_segments_kernel<TIn, TOut, kPartContiguous><<<grid, block, 0, st>>>(segs, nseg, terms, part, beta, sync);
 }

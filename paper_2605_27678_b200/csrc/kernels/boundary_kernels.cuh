@@ -66,6 +66,7 @@ struct Partition {
   // the rest is claimed from the queue counters.
   uint32_t lstatic;          // = min(grid - remote_ctas, total_chunks)
   uint32_t rstatic;          // = min(remote_ctas, rtotal_chunks)
+  int ring;                  // reduce: stage remote single-term chunks through the TMA ring
 };
 
 // Cross-GPU epoch barrier over peer-mapped flag words. Every GPU of an exec

@@ -42,7 +42,9 @@ def source_shards(src: O.Layout, B: int, W: int, rng, perturb_replicas=True, dty
     return out
 
 
-def dest_grads(dst: O.Layout, B: int, W: int, rng, perturb_replicas=True):
+def dest_grads(dst: O.Layout, B: int, W: int, rng, perturb_replicas=True, contract=False):
+    """contract=True: gradients that honour bridge.hpp:33-36 — tp replicas of a
+    (cp, dp) cell identical, cp replicas different (they are summed)."""
     G = rng.standard_normal((B, W))
     DI = O.intervals(B, dst.dp)
     out = {}
@@ -50,7 +52,9 @@ def dest_grads(dst: O.Layout, B: int, W: int, rng, perturb_replicas=True):
         t, c, p, d = dst.coord(r)
         st, n = DI[d]
         a = G[st:st + n].copy()
-        if perturb_replicas and (t or c):
+        if contract:
+            a += 100.0 * c
+        elif perturb_replicas and (t or c):
             a += 1000.0 * (t + 1) + 100.0 * (c + 1)
         out[r] = a
     return out
@@ -67,9 +71,9 @@ def apply_forward(plan, bufs: dict, splice=None):
     return out
 
 
-def apply_backward(plan, bufs: dict, splice=None, prev: dict | None = None, beta=0.0):
+def apply_backward(plan, bufs: dict, splice=None, prev: dict | None = None, beta=0.0, balanced=False):
     out = {}
-    for (dr, ds, do, n, terms) in hbb.index_backward(plan, splice):
+    for (dr, ds, do, n, terms) in hbb.index_backward(plan, splice, balanced):
         key = (dr, ds)
         if key not in out:
             out[key] = np.full(hbb.buffer_elems(plan, dr, ds, splice), np.nan)

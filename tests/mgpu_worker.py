@@ -30,6 +30,9 @@ def o_layout(l):
     return O.Layout(l.name, l.tp, l.cp, l.pp, l.dp, l.rank_offset)
 
 
+STRICT = os.environ.get("HB_STRICT", "0") == "1"
+
+
 def bf16_round(a):
     return torch.from_numpy(a.astype(np.float32)).to(torch.bfloat16).double().numpy()
 
@@ -46,7 +49,7 @@ def run(name, rank, N, dev, steps=3):
     rt = hbb.BridgeRuntime(plan, sp, n_gpus=N, my_gpu=rank, rank_to_gpu=r2g, act_dtype=torch.bfloat16,
                            grad_in_dtype=torch.bfloat16, grad_out_dtype=torch.float32, timeout_s=30.0,
                            fwd_mode=int(os.environ.get("HB_FWD_MODE", "0")),
-                           partition=int(os.environ.get("HB_PARTITION", "0")))
+                           partition=int(os.environ.get("HB_PARTITION", "0")), strict_provenance=STRICT)
     rt.exchange_handles()
     src, dst = o_layout(cfg.src), o_layout(cfg.dst)
     B, W = cfg.batch, cfg.width
@@ -81,7 +84,10 @@ def run(name, rank, N, dev, steps=3):
         for r in dst.stage_ranks(0):
             t, c, p, d = dst.coord(r)
             n = (cfg.splice["Q"] * L * cfg.hidden) if sp else DI[d][1] * W
-            g = bf16_round(np.random.default_rng(100 * step + r).standard_normal(n))
+            # strict: every rank its own gradient (pins the tp=0 data path);
+            # default: contract gradients, tp replicas of a (cp, dp) cell equal
+            seed = 100 * step + (r if STRICT else 10 * c + d)
+            g = bf16_round(np.random.default_rng(seed).standard_normal(n))
             G[r] = g
             gg = g
             if sp:

@@ -30,6 +30,13 @@ def check_plain(src, dst, B, W, seed=0):
     assert {k[0] for k in gotb} == set(refb)
     for r, a in refb.items():
         np.testing.assert_allclose(gotb[(r, hbb.SLOT_SRC_GRAD)], a.reshape(-1), rtol=0, atol=1e-12)
+    # the runtime's default map (terms from the holder's tp replicas in turn) on
+    # gradients that honour the tp-replica contract
+    gc = dest_grads(dst, B, W, rng, contract=True)
+    refc, _, _ = O.bridge_backward(src, dst, B, W, gc)
+    gotc = apply_backward(plan, {(r, hbb.SLOT_DST_GRAD): a.reshape(-1) for r, a in gc.items()}, balanced=True)
+    for r, a in refc.items():
+        np.testing.assert_allclose(gotc[(r, hbb.SLOT_SRC_GRAD)], a.reshape(-1), rtol=0, atol=1e-12)
 
 
 def test_sweep_vs_oracle():
@@ -88,6 +95,20 @@ def splice_case(src, dst, B, S_v, d_h, Q, S, codes, text_mode, seed=0):
     gotb = apply_backward(plan, {(r, hbb.SLOT_DST_GRAD): a.reshape(-1) for r, a in tg.items()}, sp)
     for r, a in refb.items():
         np.testing.assert_array_equal(gotb[(r, hbb.SLOT_SRC_GRAD)], a.reshape(-1))
+    # balanced map on contract gradients: tp replicas of a (cp, dp) cell identical
+    cell = {}
+    tc = {}
+    for r in dst.stage_ranks(0):
+        t, c, p, d = dst.coord(r)
+        if (c, d) not in cell:
+            cell[(c, d)] = rng.standard_normal((Q * L, d_h))
+        tc[r] = cell[(c, d)]
+    vc = {r: O.splice_backward(codes, Q, S, d_h, dst.coord(r)[1] * L, L, tc[r], vrows).reshape(-1, W)
+          for r in dst.stage_ranks(0)}
+    refc, _, _ = O.bridge_backward(src, dst, B, W, vc)
+    gotc = apply_backward(plan, {(r, hbb.SLOT_DST_GRAD): a.reshape(-1) for r, a in tc.items()}, sp, balanced=True)
+    for r, a in refc.items():
+        np.testing.assert_array_equal(gotc[(r, hbb.SLOT_SRC_GRAD)], a.reshape(-1))
 
 
 @pytest.mark.parametrize("text_mode", [0, 1])
@@ -172,3 +193,32 @@ def test_splice_spec_validation():
     with pytest.raises(hbb.HetBridgeError) as ei:  # S % cp
         hbb.index_forward(plan, hbb.SpliceSpec(1, 3, 3, 2, [0, 1, -1]))
     assert ei.value.code == "DivisibilityViolation"
+
+
+@pytest.mark.parametrize("name", ["c4", "c5"])
+def test_balanced_backward_spreads_serving_ranks(name):
+    """Default runtime map: the gradient return of a tp>1 destination is served
+    by every tp replica, not only tp=0 (the reference reads tp=0 only)."""
+    cfg = configs.get(name, scale=256)
+    plan = hbb.plan_bridge(cfg.edge())
+    sp = None
+    if cfg.splice:
+        s = cfg.splice
+        sp = hbb.SpliceSpec(s["Q"], s["S"], cfg.hidden, cfg.tokens, s["codes"], s["text_mode"])
+    def served(balanced):
+        load = {}
+        for (_, _, _, n, terms) in hbb.index_backward(plan, sp, balanced):
+            for (r, _, _) in terms:
+                load[r] = load.get(r, 0) + n
+        return load
+    strict, bal = served(False), served(True)
+    assert sum(strict.values()) == sum(bal.values())
+    tp0 = {r for r in strict}
+    assert all(plan_coord_tp(cfg.dst, r) == 0 for r in tp0)
+    assert len(bal) == cfg.dst.tp * len(strict)
+    assert max(bal.values()) <= 0.6 * max(strict.values())
+
+
+def plan_coord_tp(layout, r):
+    from paper_2605_27678_b200 import grid as hbg
+    return hbg.coord_of_rank(layout, r).tp_idx
