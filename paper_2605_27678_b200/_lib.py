@@ -126,7 +126,11 @@ def _declare(L):
         "hb_exec_stats": (I, [V, P(LL), P(LL), P(LL), P(LL), P(LL)]),
     }
     for name, (res, args) in sig.items():
-        f = getattr(L, name)
+        f = getattr(L, name, None)
+        if f is None and os.environ.get("HB_LIB_PATH"):  # older A/B build: skip newer entry points
+            continue
+        if f is None:
+            raise ImportError(f"{LIB_PATH} does not export {name}")
         f.restype = res
         f.argtypes = args
 

@@ -573,6 +573,38 @@ template <> struct Pack8<__half> {
   }
 };
 
+#if HB_PUN_CONVERT  // A/B: element-wise conversion through a punned uint4 array
+template <class T>
+__device__ __forceinline__ void load8(const T* p, float (&f)[8]) {
+  constexpr int NV = sizeof(T) * 8 / 16;
+  uint4 v[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) v[i] = ld_stream(reinterpret_cast<const uint4*>(p) + i);
+  const T* e = reinterpret_cast<const T*>(v);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) f[i] = Cvt<T>::to(e[i]);
+}
+template <class T>
+__device__ __forceinline__ void load8_coherent(const T* p, float (&f)[8]) {
+  constexpr int NV = sizeof(T) * 8 / 16;
+  uint4 v[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) v[i] = *(reinterpret_cast<const uint4*>(p) + i);
+  const T* e = reinterpret_cast<const T*>(v);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) f[i] = Cvt<T>::to(e[i]);
+}
+template <class T>
+__device__ __forceinline__ void store8(T* p, const float (&f)[8]) {
+  constexpr int NV = sizeof(T) * 8 / 16;
+  uint4 v[NV];
+  T* e = reinterpret_cast<T*>(v);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) e[i] = Cvt<T>::from(f[i]);
+#pragma unroll
+  for (int i = 0; i < NV; ++i) st_vec(reinterpret_cast<uint4*>(p) + i, v[i]);
+}
+#else
 template <class T>
 __device__ __forceinline__ void load8(const T* p, float (&f)[8]) {
   uint4 v[Pack8<T>::NV];
@@ -596,6 +628,7 @@ __device__ __forceinline__ void store8(T* p, const float (&f)[8]) {
 #pragma unroll
   for (int i = 0; i < Pack8<T>::NV; ++i) st_vec(reinterpret_cast<uint4*>(p) + i, v[i]);
 }
+#endif
 
 // acc[] (+)= the n terms' 8 elements at offset i (acc starts at +0.0f: terms
 // are summed in order from +0.0, as simnet's all_reduce does).
@@ -610,6 +643,31 @@ __device__ __forceinline__ void sum_terms8(const TIn* const* __restrict__ tp, in
     load8(tp[t] + i, v);
 #pragma unroll
     for (int k = 0; k < 8; ++k) acc[k] += v[k];
+  }
+}
+
+// Two groups (offsets i and i + step) with every load of a term issued before
+// any of them is consumed (the loop over terms is data-dependent, so separate
+// per-group calls would serialise the groups' load latencies).
+template <class TIn>
+__device__ __forceinline__ void sum_terms8x2(const TIn* const* __restrict__ tp, int nterms, uint64_t i,
+                                             uint64_t step, float (&acc0)[8], float (&acc1)[8]) {
+  load8(tp[0] + i, acc0);
+  load8(tp[0] + i + step, acc1);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    acc0[k] = 0.0f + acc0[k];
+    acc1[k] = 0.0f + acc1[k];
+  }
+  for (int t = 1; t < nterms; ++t) {
+    float v0[8], v1[8];
+    load8(tp[t] + i, v0);
+    load8(tp[t] + i + step, v1);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      acc0[k] += v0[k];
+      acc1[k] += v1[k];
+    }
   }
 }
 
@@ -637,8 +695,7 @@ __device__ __forceinline__ void reduce_range(TOut* __restrict__ dst, const TIn* 
     const uint64_t step = static_cast<uint64_t>(blockDim.x) * 8;
     for (i = a + threadIdx.x * 8; i + step < vend; i += 2 * step) {
       float acc0[8], acc1[8];
-      sum_terms8(tp, nterms, i, acc0);
-      sum_terms8(tp, nterms, i + step, acc1);
+      sum_terms8x2(tp, nterms, i, step, acc0, acc1);
       if (beta != 0.0f) {  // both accumulator loads in flight before either store
         float o0[8], o1[8];
         load8_coherent(dst + i, o0);
