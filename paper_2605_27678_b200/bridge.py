@@ -298,6 +298,15 @@ class BridgeRuntime:
                                  tensor.numel() * tensor.element_size()))
         self._keep[(rank, slot, mb_slot)] = tensor
 
+    def buffer_numel(self, rank: int, slot: int) -> int:
+        """Elements of a logical rank's buffer (0: the rank has none in this slot)."""
+        return buffer_elems(self.plan, rank, slot, self.splice)
+
+    def local_ranks(self, slot: int) -> list[int]:
+        """Logical ranks resident on this GPU that own a buffer in ``slot``, ascending."""
+        return [r for r in range(self.plan.world)
+                if self.rank_to_gpu[r] == self.my_gpu and self.buffer_numel(r, slot) > 0]
+
     # -- ops
     @staticmethod
     def _stream(stream):
