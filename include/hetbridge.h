@@ -175,6 +175,17 @@ int hb_exec_status(hb_exec* x, unsigned* device_error);
 int hb_exec_stats(hb_exec* x, long long* fwd_segments, long long* bwd_segments,
                   long long* fwd_bytes, long long* bwd_elems, long long* launches);
 
+/* ---- projector GEMM with a boundary epilogue (the
+ *      encoder projector of tinymodel.hpp:62) ----------------------------------
+ * Y[M x N] = X[M x K] . W[N x K]^T on the sm_100a tensor cores (tcgen05, TMEM
+ * accumulators, TMA-fed), bf16 in/out, fp32 accumulation. Output row m is
+ * stored to every non-null row_dst[m*fan + f] (device array of pointers to N
+ * bf16, local or peer-mapped), so the projector writes straight into the
+ * boundary's destination rows. Needs N % 256 == 0, K % 64 == 0, 16-B aligned
+ * operands and leading dimensions. */
+int hb_projector_gemm(const void* x, long long ldx, const void* w, long long ldw, void* const* row_dst, int fan,
+                      int M, int N, int K, void* cuda_stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -10,6 +10,7 @@
 #include "hb/bridge.hpp"
 #include "hb/index_map.hpp"
 #include "hb/runtime.hpp"
+#include "kernels/projector_gemm.cuh"
 
 struct hb_plan {
   hb::bridge::BridgePlan plan;
@@ -412,6 +413,22 @@ int hb_exec_stats(hb_exec* x, long long* fs, long long* bs, long long* fb, long 
     if (fb) *fb = static_cast<long long>(x->x->local_fwd_bytes());
     if (be) *be = static_cast<long long>(x->x->local_bwd_elems());
     if (nl) *nl = x->x->launches();
+  });
+}
+
+int hb_projector_gemm(const void* x, long long ldx, const void* w, long long ldw, void* const* row_dst, int fan,
+                      int M, int N, int K, void* cuda_stream) {
+  return guard([&] {
+    need(x, "x");
+    need(w, "w");
+    need(row_dst, "row_dst");
+    if (fan < 1) hb::raise(hb::ErrorCode::InvalidArgument, "fan must be >= 1");
+    if (hb::dev::projector_check_shape(M, N, K))
+      hb::raise(hb::ErrorCode::ShapeMismatch, "projector GEMM needs N % 256 == 0 and K % 64 == 0");
+    hb::dev::ProjectorArgs a{M, N, K, reinterpret_cast<unsigned char* const*>(row_dst), fan};
+    const int st = hb::dev::launch_projector(x, ldx, w, ldw, a, hb::dev::device_sm_count(), cuda_stream);
+    if (st == 3) hb::raise(hb::ErrorCode::InvalidArgument, "projector operands must be 16-B aligned");
+    if (st) hb::raise(hb::ErrorCode::CudaError, "projector GEMM launch failed (" + std::to_string(st) + ")");
   });
 }
 

@@ -1,0 +1,3 @@
+exec > gpurun_out/s16.log 2>&1
+timeout 300 python -m pytest tests/test_projector.py -x -q 2>&1 | tail -25
+timeout 300 python scripts/proj_probe.py
