@@ -185,6 +185,14 @@ int hb_exec_stats(hb_exec* x, long long* fwd_segments, long long* bwd_segments,
  * operands and leading dimensions. */
 int hb_projector_gemm(const void* x, long long ldx, const void* w, long long ldw, void* const* row_dst, int fan,
                       int M, int N, int K, void* cuda_stream);
+/* Boundary forward with the projector fused in: x = the pre-projection token
+ * rows of every local source rank stacked in ascending rank order [rows x K],
+ * w = the projector weight [d_h x K]; each projected row is stored straight
+ * into every destination row of the plan (the source shards are never
+ * written). Replaces forward_* for that microbatch (records it like
+ * hb_exec_forward). One GPU, non-splice edges, bf16 activations. */
+int hb_exec_forward_projected(hb_exec* x, int mb, const void* act, long long ldx, const void* w, long long ldw,
+                              int d_h, int K, void* cuda_stream);
 
 #ifdef __cplusplus
 }

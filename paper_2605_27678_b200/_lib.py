@@ -33,6 +33,7 @@ EXPORTS = [
     "hb_exec_config_default", "hb_exec_create", "hb_exec_destroy", "hb_exec_ipc_handle",
     "hb_exec_open_peers", "hb_exec_buffer", "hb_exec_bind", "hb_exec_forward", "hb_exec_backward",
     "hb_exec_seed_forward_record", "hb_exec_status", "hb_exec_stats", "hb_exec_graph_capture", "hb_projector_gemm",
+    "hb_exec_forward_projected",
     "hb_exec_graph_launch",
 ]
 
@@ -125,6 +126,7 @@ def _declare(L):
         "hb_exec_status": (I, [V, P(U)]),
         "hb_exec_stats": (I, [V, P(LL), P(LL), P(LL), P(LL), P(LL)]),
         "hb_projector_gemm": (I, [V, LL, V, LL, V, I, I, I, I, V]),
+        "hb_exec_forward_projected": (I, [V, I, V, LL, V, LL, I, I, V]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name, None)

@@ -318,6 +318,19 @@ class BridgeRuntime:
     def forward(self, mb: int = 0, stream=None):
         check(lib().hb_exec_forward(self._h, mb, self._stream(stream)))
 
+    def forward_projected(self, mb: int, x, w, stream=None):
+        """Forward with the encoder projector fused in (hb_exec_forward_projected):
+        x [rows, K] bf16 = pre-projection token rows of the local source ranks
+        stacked in ascending rank order; w [d_h, K] bf16. Each projected row goes
+        straight to every destination row; SRC_ACT is not written."""
+        import torch
+
+        if x.dtype != torch.bfloat16 or w.dtype != torch.bfloat16 or x.stride(1) != 1 or w.stride(1) != 1:
+            raise HetBridgeError(24, "forward_projected takes row-major bf16 x and w")
+        check(lib().hb_exec_forward_projected(self._h, mb, ctypes.c_void_p(x.data_ptr()), x.stride(0),
+                                              ctypes.c_void_p(w.data_ptr()), w.stride(0), w.shape[0], w.shape[1],
+                                              self._stream(stream)))
+
     def backward(self, mb: int = 0, beta: float = 0.0, stream=None):
         check(lib().hb_exec_backward(self._h, mb, ctypes.c_float(beta), self._stream(stream)))
 

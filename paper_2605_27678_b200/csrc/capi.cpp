@@ -416,6 +416,16 @@ int hb_exec_stats(hb_exec* x, long long* fs, long long* bs, long long* fb, long 
   });
 }
 
+int hb_exec_forward_projected(hb_exec* x, int mb, const void* act, long long ldx, const void* w, long long ldw,
+                              int d_h, int K, void* cuda_stream) {
+  return guard([&] {
+    need(x, "exec");
+    need(act, "x");
+    need(w, "w");
+    x->x->forward_projected(mb, act, ldx, w, ldw, d_h, K, cuda_stream);
+  });
+}
+
 int hb_projector_gemm(const void* x, long long ldx, const void* w, long long ldw, void* const* row_dst, int fan,
                       int M, int N, int K, void* cuda_stream) {
   return guard([&] {

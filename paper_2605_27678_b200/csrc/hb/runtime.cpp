@@ -1,6 +1,8 @@
 // hetbridge — per-edge device runtime (see runtime.hpp).
 #include "hb/runtime.hpp"
 
+#include "kernels/projector_gemm.cuh"
+
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -112,6 +114,7 @@ Exec::Exec(const bridge::BridgePlan& plan, const index::SpliceSpec* splice, int 
   peer_base_.assign(n_gpus_, nullptr);
   peer_base_[my_gpu_] = local_base_;
   tables_.resize(cfg.mb_slots);
+  proj_.resize(cfg.mb_slots);
   int khz = 0;
   cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, device_);
   clock_khz_ = khz > 0 ? khz : 2000000;
@@ -121,6 +124,7 @@ Exec::Exec(const bridge::BridgePlan& plan, const index::SpliceSpec* splice, int 
 
 Exec::~Exec() {
   for (auto& kv : graphs_) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(kv.second.first));
+  for (auto& t : proj_) cudaFree(t.rows_dev);
   for (auto& t : tables_) {
     cudaFree(t.copy);
     cudaFree(t.reduce);
@@ -480,6 +484,64 @@ void Exec::forward(int mb, void* stream) {
     raise(ErrorCode::InvalidArgument, "microbatch " + std::to_string(mb) + " forwarded twice without backward");
   prepare_fwd();
   launch_forward(mb % cfg_.mb_slots, stream);
+  fwd_done_.insert(mb);
+}
+
+void Exec::forward_projected(int mb, const void* x, int64_t ldx, const void* w, int64_t ldw, int d_h, int K,
+                             void* stream) {
+  if (fwd_done_.count(mb))
+    raise(ErrorCode::InvalidArgument, "microbatch " + std::to_string(mb) + " forwarded twice without backward");
+  if (n_gpus_ != 1)
+    raise(ErrorCode::InvalidArgument, "the fused projector forward runs on one GPU (all ranks resident)");
+  if (cfg_.act_dtype != dev::kBF16) raise(ErrorCode::InvalidArgument, "the fused projector writes bf16 activations");
+  for (int r = 0; r < map_.world; ++r)
+    if (map_.elems[r][index::kText])
+      raise(ErrorCode::InvalidArgument, "fused projector forward on a splice edge: use forward()");
+  if (d_h <= 0 || plan_.edge.feature_width % d_h)
+    raise(ErrorCode::ShapeMismatch, "d_h must divide the feature width");
+  if (dev::projector_check_shape(1, d_h, K))
+    raise(ErrorCode::ShapeMismatch, "projector GEMM needs d_h % 256 == 0 and K % 64 == 0");
+  const int slot = mb % cfg_.mb_slots;
+  ProjTable& P = proj_[slot];
+  if (P.d_h != d_h || !P.rows_dev || dirty_fwd_) {
+    prepare_fwd();
+    // token row -> destination rows, from the forward map (every destination,
+    // in map order); rows are numbered over the local source ranks ascending
+    std::map<int, int64_t> row_base;  // source rank -> first stacked row
+    int64_t rows = 0;
+    for (int r = 0; r < map_.world; ++r)
+      if (map_.elems[r][index::kSrcAct] && gpu_of(r) == my_gpu_) {
+        row_base[r] = rows;
+        rows += map_.elems[r][index::kSrcAct] / d_h;
+      }
+    std::vector<std::vector<unsigned char*>> dst(rows);
+    const int es = dev::dtype_size(cfg_.act_dtype);
+    for (const auto& sg : map_.fwd) {
+      if (sg.src.slot != index::kSrcAct) continue;  // splice text rows are not projector output
+      if (sg.src.off % d_h || sg.dst.off % d_h || sg.n % d_h)
+        raise(ErrorCode::ShapeMismatch, "forward runs are not whole d_h rows");
+      auto* base = static_cast<unsigned char*>(const_cast<void*>(resolve(sg.dst.rank, sg.dst.slot, slot)));
+      for (int64_t i = 0; i < sg.n / d_h; ++i)
+        dst[row_base.at(sg.src.rank) + sg.src.off / d_h + i].push_back(base + (sg.dst.off + i * d_h) * es);
+    }
+    int fan = 1;
+    for (const auto& v : dst) fan = std::max<int>(fan, static_cast<int>(v.size()));
+    std::vector<unsigned char*> flat(static_cast<size_t>(rows) * fan, nullptr);
+    for (int64_t m = 0; m < rows; ++m)
+      for (size_t f = 0; f < dst[m].size(); ++f) flat[m * fan + f] = dst[m][f];
+    cudaFree(P.rows_dev);
+    P.rows_dev = nullptr;
+    ck(cudaMalloc(&P.rows_dev, flat.size() * sizeof(unsigned char*)), "cudaMalloc(projector rows)");
+    ck(cudaMemcpy(P.rows_dev, flat.data(), flat.size() * sizeof(unsigned char*), cudaMemcpyHostToDevice), "upload");
+    P.d_h = d_h;
+    P.fan = fan;
+    P.rows = static_cast<int>(rows);
+  }
+  const dev::ProjectorArgs a{P.rows, d_h, K, P.rows_dev, P.fan};
+  const int st = dev::launch_projector(x, ldx, w, ldw, a, sm_count_, stream);
+  if (st) raise(st == 3 ? ErrorCode::InvalidArgument : ErrorCode::CudaError,
+                "projector GEMM launch failed (" + std::to_string(st) + ")");
+  ++launches_;
   fwd_done_.insert(mb);
 }
 

@@ -59,6 +59,14 @@ class Exec {
   size_t buffer_bytes(int rank, int slot) const;
 
   void forward(int mb, void* stream);
+  // Forward with the encoder projector fused in: computes
+  // X . W^T for every local source rank (X: their token rows stacked in
+  // ascending rank order, [rows x K]; W: [d_h x K]) on the tensor cores and
+  // stores each output row straight into every destination row the plan maps
+  // it to; the source shards are never materialised. One GPU (all destinations
+  // resident) for now.
+  void forward_projected(int mb, const void* x, int64_t ldx, const void* w, int64_t ldw, int d_h, int K,
+                         void* stream);
   void backward(int mb, float beta, void* stream);
   void seed_forward_record(int mb);
 
@@ -122,6 +130,13 @@ class Exec {
     const void** terms = nullptr;
   };
   std::vector<DevTables> tables_;  // per mb slot
+  struct ProjTable {
+    int d_h = 0;
+    int fan = 0;
+    int rows = 0;
+    unsigned char** rows_dev = nullptr;  // [rows * fan]
+  };
+  std::vector<ProjTable> proj_;  // per mb slot
   // Static contiguous partition of each direction's work space over the grid.
   struct DevPartition {
     int32_t* first_seg = nullptr;

@@ -41,6 +41,7 @@ constexpr int kEpiWarps = 4;
 constexpr int kThreads = 32 * (2 + kEpiWarps);
 constexpr uint32_t kTmemCols = 2 * kBN;  // two accumulators
 constexpr size_t kSmemBytes = kStages * kStageBytes + 1024;  // + alignment slack
+constexpr int kEpiRowPitch = 80;  // staging row: 64 B of data + 16 B pad (bank spread)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -114,6 +115,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full[kStages], empty[kStages], tfull[2], tempty[2];
   __shared__ uint32_t tmem_base_sh;
+  __shared__ __align__(16) unsigned char epi_stage[kEpiWarps * 32 * kEpiRowPitch];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int tiles_m = (args.M + kBM - 1) / kBM, tiles_n = args.N / kBN, num_k = args.K / kBK;
@@ -189,8 +191,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_commit(&tfull[acc]);  // accumulator complete
       }
     }
-  } else {  // ---- epilogue warps: TMEM -> registers -> bf16 -> every destination of the row
+  } else {  // ---- epilogue warps: TMEM -> registers -> bf16 -> smem transpose -> every destination
     const int q = warp % 4;  // TMEM lane quarter this warp may access
+    // per warp: a 32-row x 64-B staging block, rows padded to 80 B so the
+    // 16-B writes of 8 consecutive lanes hit distinct banks
+    unsigned char* stage_w = epi_stage + (warp - 2) * (32 * kEpiRowPitch);
     int it = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
       const int acc = it & 1;
@@ -198,29 +203,40 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int m0 = (tile % tiles_m) * kBM, n0 = (tile / tiles_m) * kBN;
       mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
+      // this lane's row's destinations stay in registers; lanes fetch each
+      // other's with shuffles when they store
       const int row = m0 + q * 32 + lane;
-      const bool valid = row < args.M;
-      unsigned char* const* dst = args.row_dst + static_cast<size_t>(valid ? row : 0) * args.fan;
+      unsigned char* mine[kMaxProjFan];
+#pragma unroll
+      for (int f = 0; f < kMaxProjFan; ++f)
+        mine[f] = (row < args.M && f < args.fan) ? args.row_dst[static_cast<size_t>(row) * args.fan + f] : nullptr;
 #pragma unroll 1
       for (int c = 0; c < kBN / 32; ++c) {
         uint32_t v[32];
         HB_TMEM_LD32(tmem_base + acc * kBN + c * 32 + (static_cast<uint32_t>(q * 32) << 16), v);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (valid) {
-          uint4 o[4];
+        uint4* srow = reinterpret_cast<uint4*>(stage_w + lane * kEpiRowPitch);
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
-            o[i] = make_uint4(pack_bf16(v[8 * i], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
-                              pack_bf16(v[8 * i + 4], v[8 * i + 5]), pack_bf16(v[8 * i + 6], v[8 * i + 7]));
-          const size_t col_bytes = static_cast<size_t>(n0 + c * 32) * 2;
-          for (int f = 0; f < args.fan; ++f) {
-            unsigned char* p = dst[f];
-            if (!p) break;
-            uint4* out = reinterpret_cast<uint4*>(p + col_bytes);
+        for (int i = 0; i < 4; ++i)
+          srow[i] = make_uint4(pack_bf16(v[8 * i], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
+                               pack_bf16(v[8 * i + 4], v[8 * i + 5]), pack_bf16(v[8 * i + 6], v[8 * i + 7]));
+        __syncwarp();
+        // 4 lanes per row, 8 rows per instruction: every store writes whole
+        // 64-B row segments (two full sectors) instead of one 16-B piece per row
+        const size_t col_bytes = static_cast<size_t>(n0 + c * 32) * 2 + (lane & 3) * 16;
 #pragma unroll
-            for (int i = 0; i < 4; ++i) out[i] = o[i];
+        for (int k = 0; k < 4; ++k) {
+          const int r = 8 * k + (lane >> 2);
+          const uint4 val = *reinterpret_cast<const uint4*>(stage_w + r * kEpiRowPitch + (lane & 3) * 16);
+#pragma unroll
+          for (int f = 0; f < kMaxProjFan; ++f) {
+            if (f >= args.fan) break;
+            unsigned char* p = reinterpret_cast<unsigned char*>(
+                __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(mine[f]), r));
+            if (p) *reinterpret_cast<uint4*>(p + col_bytes) = val;
           }
         }
+        __syncwarp();
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
@@ -268,7 +284,7 @@ int projector_check_shape(int M, int N, int K) {
 
 int launch_projector(const void* x, int64_t ldx, const void* w, int64_t ldw, const ProjectorArgs& args,
                      int sm_count, void* stream) {
-  if (projector_check_shape(args.M, args.N, args.K)) return 1;
+  if (projector_check_shape(args.M, args.N, args.K) || args.fan < 1 || args.fan > kMaxProjFan) return 1;
   if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(w)) & 15) return 3;
   if ((ldx * 2) % 16 || (ldw * 2) % 16) return 3;
   CUtensorMap mx, mw;

@@ -8,6 +8,8 @@ namespace hb::dev {
 // Y[M x N] = X[M x K] . W[N x K]^T, bf16 in, fp32 accumulate (TMEM), bf16 out.
 // Output row m is stored to row_dst[m*fan + f] for every non-null f < fan
 // (each a pointer to N contiguous bf16 elements, 16-B aligned; local or peer).
+constexpr int kMaxProjFan = 8;  // destinations per output row
+
 struct ProjectorArgs {
   int M, N, K;
   unsigned char* const* row_dst;  // device array [M * fan]
