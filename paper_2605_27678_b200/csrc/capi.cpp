@@ -4,6 +4,10 @@
 #include "hetbridge.h"
 
 #include <cstring>
+#include <map>
+#include <mutex>
+
+#include <cuda_runtime.h>
 #include <memory>
 #include <string>
 
@@ -420,8 +424,7 @@ int hb_exec_forward_projected(hb_exec* x, int mb, const void* act, long long ldx
                               int d_h, int K, void* cuda_stream) {
   return guard([&] {
     need(x, "exec");
-    need(act, "x");
-    need(w, "w");
+    need(w, "w");  // act may be null when this GPU hosts no source rank
     x->x->forward_projected(mb, act, ldx, w, ldw, d_h, K, cuda_stream);
   });
 }
@@ -435,7 +438,29 @@ int hb_projector_gemm(const void* x, long long ldx, const void* w, long long ldw
     if (fan < 1) hb::raise(hb::ErrorCode::InvalidArgument, "fan must be >= 1");
     if (hb::dev::projector_check_shape(M, N, K))
       hb::raise(hb::ErrorCode::ShapeMismatch, "projector GEMM needs N % 256 == 0 and K % 64 == 0");
-    hb::dev::ProjectorArgs a{M, N, K, reinterpret_cast<unsigned char* const*>(row_dst), fan};
+    // standalone GEMM: no peers, no launch protocol (counters must still be valid)
+    static std::mutex mu;
+    static std::map<int, unsigned long long*> per_device;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    unsigned long long* scratch = nullptr;
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      auto& p = per_device[dev];
+      if (!p) {
+        void* q = nullptr;
+        if (cudaMalloc(&q, hb::dev::kCtrBytes) != cudaSuccess || cudaMemset(q, 0, hb::dev::kCtrBytes) != cudaSuccess)
+          hb::raise(hb::ErrorCode::CudaError, "projector scratch counters");
+        p = static_cast<unsigned long long*>(q);
+      }
+      scratch = p;
+    }
+    hb::dev::SyncArgs none{};
+    none.arrive = scratch;
+    none.queue = scratch + hb::dev::kCtrLine / 2;
+    none.fin = reinterpret_cast<uint32_t*>(scratch) + 3 * hb::dev::kCtrLine;
+    none.err = none.fin + 1;
+    hb::dev::ProjectorArgs a{M, N, K, reinterpret_cast<unsigned char* const*>(row_dst), fan, none};
     const int st = hb::dev::launch_projector(x, ldx, w, ldw, a, hb::dev::device_sm_count(), cuda_stream);
     if (st == 3) hb::raise(hb::ErrorCode::InvalidArgument, "projector operands must be 16-B aligned");
     if (st) hb::raise(hb::ErrorCode::CudaError, "projector GEMM launch failed (" + std::to_string(st) + ")");

@@ -107,10 +107,10 @@ Exec::Exec(const bridge::BridgePlan& plan, const index::SpliceSpec* splice, int 
   if (cfg_.internal_alloc || n_gpus_ > 1) {
     ck(cudaMalloc(&local_base_, region_bytes_), "cudaMalloc(region)");
     ck(cudaMemset(local_base_, 0, kPadBytes), "cudaMemset(pad)");
-    static_assert(4 * dev::kMaxGpus * sizeof(uint32_t) <= kPadBytes, "pad holds start and done flags of both kinds");
+    static_assert(2 * kNumKinds * dev::kMaxGpus * sizeof(uint32_t) <= kPadBytes, "pad holds start and done flags of every kind");
   }
-  ck(cudaMalloc(&ctr_, 2 * dev::kCtrBytes), "cudaMalloc(ctr)");
-  ck(cudaMemset(ctr_, 0, 2 * dev::kCtrBytes), "cudaMemset(ctr)");
+  ck(cudaMalloc(&ctr_, kNumKinds * dev::kCtrBytes), "cudaMalloc(ctr)");
+  ck(cudaMemset(ctr_, 0, kNumKinds * dev::kCtrBytes), "cudaMemset(ctr)");
   peer_base_.assign(n_gpus_, nullptr);
   peer_base_[my_gpu_] = local_base_;
   tables_.resize(cfg.mb_slots);
@@ -120,6 +120,7 @@ Exec::Exec(const bridge::BridgePlan& plan, const index::SpliceSpec* splice, int 
   clock_khz_ = khz > 0 ? khz : 2000000;
   sync_fwd_ = make_sync_args(kFwdKind, fwd_push_);
   sync_bwd_ = make_sync_args(kBwdKind, false);
+  sync_proj_ = make_sync_args(kProjKind, true);
 }
 
 Exec::~Exec() {
@@ -179,6 +180,7 @@ void Exec::open_peers(const void* handles) {
   }
   sync_fwd_ = make_sync_args(kFwdKind, fwd_push_);
   sync_bwd_ = make_sync_args(kBwdKind, false);
+  sync_proj_ = make_sync_args(kProjKind, true);
   dirty_fwd_ = dirty_bwd_ = true;
 }
 
@@ -491,8 +493,6 @@ void Exec::forward_projected(int mb, const void* x, int64_t ldx, const void* w, 
                              void* stream) {
   if (fwd_done_.count(mb))
     raise(ErrorCode::InvalidArgument, "microbatch " + std::to_string(mb) + " forwarded twice without backward");
-  if (n_gpus_ != 1)
-    raise(ErrorCode::InvalidArgument, "the fused projector forward runs on one GPU (all ranks resident)");
   if (cfg_.act_dtype != dev::kBF16) raise(ErrorCode::InvalidArgument, "the fused projector writes bf16 activations");
   for (int r = 0; r < map_.world; ++r)
     if (map_.elems[r][index::kText])
@@ -517,7 +517,8 @@ void Exec::forward_projected(int mb, const void* x, int64_t ldx, const void* w, 
     std::vector<std::vector<unsigned char*>> dst(rows);
     const int es = dev::dtype_size(cfg_.act_dtype);
     for (const auto& sg : map_.fwd) {
-      if (sg.src.slot != index::kSrcAct) continue;  // splice text rows are not projector output
+      // rows this GPU projects: its own source ranks' (pushed to local and peer destinations)
+      if (sg.src.slot != index::kSrcAct || gpu_of(sg.src.rank) != my_gpu_) continue;
       if (sg.src.off % d_h || sg.dst.off % d_h || sg.n % d_h)
         raise(ErrorCode::ShapeMismatch, "forward runs are not whole d_h rows");
       auto* base = static_cast<unsigned char*>(const_cast<void*>(resolve(sg.dst.rank, sg.dst.slot, slot)));
@@ -537,7 +538,8 @@ void Exec::forward_projected(int mb, const void* x, int64_t ldx, const void* w, 
     P.fan = fan;
     P.rows = static_cast<int>(rows);
   }
-  const dev::ProjectorArgs a{P.rows, d_h, K, P.rows_dev, P.fan};
+  if (P.rows > 0 && !x) raise(ErrorCode::InvalidArgument, "null projector input for the local source rows");
+  const dev::ProjectorArgs a{P.rows, d_h, K, P.rows_dev, P.fan, sync_proj_};
   const int st = dev::launch_projector(x, ldx, w, ldw, a, sm_count_, stream);
   if (st) raise(st == 3 ? ErrorCode::InvalidArgument : ErrorCode::CudaError,
                 "projector GEMM launch failed (" + std::to_string(st) + ")");

@@ -93,7 +93,7 @@ class Exec {
   const void* resolve(int rank, int slot, int mb_slot) const;
   void prepare_fwd();  // resolve pointers, upload descriptors (after bind/open)
   void prepare_bwd();
-  static constexpr int kFwdKind = 0, kBwdKind = 1;
+  static constexpr int kFwdKind = 0, kBwdKind = 1, kProjKind = 2, kNumKinds = 3;
   dev::SyncArgs make_sync_args(int kind, bool push) const;
 
   bridge::BridgePlan plan_;
@@ -168,7 +168,7 @@ class Exec {
                        int mode, uint64_t unit, DevPartition* out);
   bool dirty_fwd_ = true, dirty_bwd_ = true;
   uint32_t* ctr_ = nullptr;  // device counters
-  dev::SyncArgs sync_fwd_{}, sync_bwd_{};
+  dev::SyncArgs sync_fwd_{}, sync_bwd_{}, sync_proj_{};
   int clock_khz_ = 2000000;
   int sm_count_ = 0;
   int launches_ = 0;

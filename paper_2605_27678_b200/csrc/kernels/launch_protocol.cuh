@@ -1,0 +1,97 @@
+// hetbridge — the in-kernel launch protocol shared by every boundary kernel
+// (copy, reduce, fused projector): per-CTA arrival with the launch epoch,
+// "started" posts to peers, lazy peer waits, and the end-of-launch contract.
+// See boundary_kernels.cuh (SyncArgs) and DESIGN.md §4.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "kernels/boundary_kernels.cuh"
+
+namespace hb::dev {
+namespace {
+
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// "+1" to this GPU's slot in every peer's pad (`word` = 0: started, kMaxGpus:
+// finished pushing). Called by every thread of a warp: lane g posts to peer g,
+// so the posts to several peers go out in parallel.
+__device__ __forceinline__ void post_peers_warp(const SyncArgs& s, int word) {
+  const int g = threadIdx.x & 31;
+  if ((s.post_mask >> g) & 1u) {
+    asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(s.peer_pad[g] + word + s.my_gpu), "r"(1u)
+                 : "memory");
+  }
+}
+
+// Per-CTA view of the launch (shared memory).
+struct CtaSync {
+  uint32_t e;  // this launch's epoch (valid after cta_arrive_finish)
+  int waited;  // peers' arrival at e confirmed
+  int ok;      // no timeout
+};
+
+// Bounded spin until *flag >= e; false on timeout (error word set).
+__device__ __forceinline__ bool spin_until(const SyncArgs& s, const uint32_t* flag, uint32_t e) {
+  const long long t0 = clock64();
+  while (static_cast<int32_t>(ld_acquire_sys(flag) - e) < 0) {
+    __nanosleep(64);
+    if (static_cast<uint64_t>(clock64() - t0) > s.timeout_cycles) {
+      atomicExch(s.err, 1u);
+      return false;
+    }
+  }
+  return true;
+}
+
+// Start of a launch, one thread per CTA: count this CTA in (CTA 0's first
+// warp posts "started" to every peer with post_peers_warp). Returns the raw arrival word; its latency overlaps
+// the CTA's first (static, local) chunk and is consumed by cta_arrive_finish.
+__device__ __forceinline__ unsigned long long cta_arrive_issue(const SyncArgs& s) {
+  return atomicAdd(s.arrive, 1ull);
+}
+
+__device__ __forceinline__ void cta_arrive_finish(const SyncArgs& s, CtaSync& cs, unsigned long long old) {
+  cs.e = static_cast<uint32_t>(old >> 32) + 1;
+  cs.waited = (s.wait_mask == 0);
+  cs.ok = 1;
+  // last CTA in: advance the epoch, zero the arrivals (every CTA of this
+  // launch has read the word; the next launch starts after this one ends)
+  if ((old & 0xffffffffull) == gridDim.x - 1) atomicAdd(s.arrive, (1ull << 32) - gridDim.x);
+}
+
+// Wait (once per CTA, one thread) until every peer started op e: after that
+// the peers' buffers of this op may be read (pull) or written (push).
+__device__ bool sync_wait_lane(const SyncArgs& s, CtaSync& cs) {
+  if (!cs.waited) {
+    for (int g = 0; g < kMaxGpus; ++g)
+      if (((s.wait_mask >> g) & 1u) && !spin_until(s, s.pad + g, cs.e)) cs.ok = 0;
+    cs.waited = 1;
+  }
+  return cs.ok != 0;
+}
+
+// End of a launch, one thread per CTA. CTA 0 confirms every peer started op e,
+// so completion of op e implies every peer completed op e-1 (the buffer-reuse
+// contract), whatever work this GPU had. Push mode: the last CTA done writing
+// publishes "my writes into your buffers are done" and waits for every writer
+// into this GPU.
+__device__ void launch_end_lane(const SyncArgs& s, CtaSync& cs) {
+  if (blockIdx.x == 0) sync_wait_lane(s, cs);
+  if (!s.end_sync) return;
+  __threadfence_system();  // this CTA's remote stores before "done"
+  if (atomicAdd(s.fin, 1u) != gridDim.x - 1) return;
+  *s.fin = 0;
+  __threadfence_system();
+  for (int g = 0; g < kMaxGpus; ++g)
+    if ((s.post_mask >> g) & 1u) atomicAdd_system(s.peer_pad[g] + kMaxGpus + s.my_gpu, 1u);
+  for (int g = 0; g < kMaxGpus; ++g)
+    if ((s.wait_mask >> g) & 1u) spin_until(s, s.pad + kMaxGpus + g, cs.e);
+}
+
+}  // namespace
+}  // namespace hb::dev

@@ -27,6 +27,7 @@
 
 #include <cstdint>
 
+#include "kernels/launch_protocol.cuh"
 #include "kernels/projector_gemm.cuh"
 
 namespace hb::dev {
@@ -134,6 +135,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  // launch protocol: count in (epoch), CTA 0 posts "started" to the peers
+  // whose destinations this launch writes
+  __shared__ CtaSync cs;
+  if (blockIdx.x == 0 && warp == 0) post_peers_warp(args.sync, 0);
+  if (threadIdx.x == 0) cta_arrive_finish(args.sync, cs, cta_arrive_issue(args.sync));
   if (warp == 1) {  // one warp allocates (and later frees) the two accumulators
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
                  "r"(kTmemCols)
@@ -196,6 +202,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     // per warp: a 32-row x 64-B staging block, rows padded to 80 B so the
     // 16-B writes of 8 consecutive lanes hit distinct banks
     unsigned char* stage_w = epi_stage + (warp - 2) * (32 * kEpiRowPitch);
+    // before the first store: every peer has started this op, so its
+    // destination buffers of this set are no longer read
+    bool ok = true;
+    if (lane == 0)
+      for (int g = 0; g < kMaxGpus; ++g)
+        if (((args.sync.wait_mask >> g) & 1u) && !spin_until(args.sync, args.sync.pad + g, cs.e)) ok = false;
+    ok = __shfl_sync(0xffffffffu, ok, 0);
     int it = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
       const int acc = it & 1;
@@ -233,7 +246,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (f >= args.fan) break;
             unsigned char* p = reinterpret_cast<unsigned char*>(
                 __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(mine[f]), r));
-            if (p) *reinterpret_cast<uint4*>(p + col_bytes) = val;
+            if (p && ok) *reinterpret_cast<uint4*>(p + col_bytes) = val;
           }
         }
         __syncwarp();
@@ -248,6 +261,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols)
                  : "memory");
   }
+  // end: "writes done" to every peer written, wait for every writer into this GPU
+  if (threadIdx.x == 0) launch_end_lane(args.sync, cs);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -277,7 +292,7 @@ bool make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, ui
 }  // namespace
 
 int projector_check_shape(int M, int N, int K) {
-  if (M < 1 || N < kBN || K < kBK) return 1;
+  if (M < 0 || N < kBN || K < kBK) return 1;
   if (N % kBN || K % kBK) return 2;
   return 0;
 }
@@ -287,8 +302,10 @@ int launch_projector(const void* x, int64_t ldx, const void* w, int64_t ldw, con
   if (projector_check_shape(args.M, args.N, args.K) || args.fan < 1 || args.fan > kMaxProjFan) return 1;
   if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(w)) & 15) return 3;
   if ((ldx * 2) % 16 || (ldw * 2) % 16) return 3;
-  CUtensorMap mx, mw;
-  if (!make_map(&mx, x, args.M, args.K, ldx, kBM) || !make_map(&mw, w, args.N, args.K, ldw, kBN)) return 4;
+  CUtensorMap mx{}, mw{};
+  // M == 0: this GPU projects no rows but still takes part in the launch protocol
+  if (args.M > 0 && (!make_map(&mx, x, args.M, args.K, ldx, kBM) || !make_map(&mw, w, args.N, args.K, ldw, kBN)))
+    return 4;
   static bool attr = [] {
     cudaFuncSetAttribute(projector_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(kSmemBytes));
@@ -296,7 +313,7 @@ int launch_projector(const void* x, int64_t ldx, const void* w, int64_t ldw, con
   }();
   (void)attr;
   const int tiles = ((args.M + kBM - 1) / kBM) * (args.N / kBN);
-  const int grid = tiles < sm_count ? tiles : sm_count;
+  const int grid = tiles < 1 ? 1 : tiles < sm_count ? tiles : sm_count;
   projector_gemm_kernel<<<grid, kThreads, kSmemBytes, static_cast<cudaStream_t>(stream)>>>(mx, mw, args);
   return cudaGetLastError() == cudaSuccess ? 0 : 5;
 }

@@ -3,6 +3,8 @@
 
 #include <cstdint>
 
+#include "kernels/boundary_kernels.cuh"
+
 namespace hb::dev {
 
 // Y[M x N] = X[M x K] . W[N x K]^T, bf16 in, fp32 accumulate (TMEM), bf16 out.
@@ -14,6 +16,7 @@ struct ProjectorArgs {
   int M, N, K;
   unsigned char* const* row_dst;  // device array [M * fan]
   int fan;
+  SyncArgs sync;  // launch protocol (push: peers' destinations); empty masks on one GPU
 };
 
 // 0 OK; 1 shape (N % 256, K % 64), 3 alignment, 4 tensor map, 5 launch.

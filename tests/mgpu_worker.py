@@ -134,6 +134,61 @@ def run(name, rank, N, dev, steps=3):
     return flag.item() == 0, w.item(), r2g
 
 
+def run_projected(name, rank, N, dev):
+    """Fused projector forward (tcgen05 GEMM pushing rows to every destination,
+    local or peer) == GEMM into the source shards + the pulled forward reshard."""
+    from paper_2605_27678_b200.projector import projector_gemm
+
+    base = configs.get(name)
+    cfg = configs.get(name, scale=base.hidden // 256)
+    d_h, K = cfg.hidden, 128
+    plan = hbb.plan_bridge(cfg.edge())
+    r2g = configs.rank_to_gpu(plan.world, N)
+    rts = []
+    for _ in range(2):
+        rt = hbb.BridgeRuntime(plan, n_gpus=N, my_gpu=rank, rank_to_gpu=r2g, timeout_s=30.0)
+        rt.exchange_handles()
+        rts.append(rt)
+    rt_a, rt_b = rts
+    srcs = rt_a.local_ranks(hbb.SLOT_SRC_ACT)
+    g = torch.Generator(device=dev).manual_seed(11)
+    w = (torch.randn(d_h, K, device=dev, generator=g) / K ** 0.5).to(torch.bfloat16)
+    xs = []
+    for r in srcs:  # rows of source rank r: deterministic in r (tp replicas of a shard share them)
+        t, c, p, d = o_layout(cfg.src).coord(r)
+        n = rt_a.buffer_numel(r, hbb.SLOT_SRC_ACT) // d_h
+        xs.append(torch.randn(n, K, device=dev, generator=torch.Generator(device=dev).manual_seed(1000 + d))
+                  .to(torch.bfloat16))
+    x = torch.cat(xs) if xs else torch.zeros(0, K, device=dev, dtype=torch.bfloat16)
+    ok = True
+    for step in range(2):
+        torch.cuda.synchronize()
+        dist.barrier()
+        rt_a.forward_projected(step, x, w)  # no local source rank: protocol-only launch
+        y = projector_gemm(x, w) if x.shape[0] else x
+        o = 0
+        for r in srcs:
+            b = rt_b.buffer(r, hbb.SLOT_SRC_ACT)
+            n = b.numel() // d_h
+            b.copy_(y[o:o + n].reshape(-1))
+            o += n
+        rt_b.forward(step)
+        torch.cuda.synchronize()
+        for rt in rts:
+            rt.seed_forward_record(step)
+            rt.backward(step, 0.0)
+        torch.cuda.synchronize()
+        if rt_a.status() or rt_b.status():
+            raise RuntimeError("flag wait timed out")
+        for r in rt_a.local_ranks(hbb.SLOT_DST_ACT):
+            ok &= bool(torch.equal(rt_a.buffer(r, hbb.SLOT_DST_ACT), rt_b.buffer(r, hbb.SLOT_DST_ACT)))
+    flag = torch.tensor([0 if ok else 1], device=dev)
+    dist.all_reduce(flag)
+    for rt in rts:
+        rt.close()
+    return flag.item() == 0, 0.0, r2g
+
+
 def main():
     rank = int(os.environ["RANK"])
     N = int(os.environ["WORLD_SIZE"])
@@ -143,8 +198,9 @@ def main():
     dist.init_process_group("nccl", device_id=dev)
     names = sys.argv[1:] or ["c2", "c3", "c4", "c5", "c1"]
     all_ok = True
+    proj = os.environ.get("HB_PROJ", "0") == "1"
     for name in names:
-        ok, worst, r2g = run(name, rank, N, dev)
+        ok, worst, r2g = (run_projected if proj else run)(name, rank, N, dev)
         all_ok &= ok
         if rank == 0:
             print(json.dumps({"config": name, "n_gpus": N, "parity": ok, "bwd_max_rel": worst,
