@@ -9,15 +9,17 @@
 //
 // Structure (one CTA per SM, persistent over 128 x 256 output tiles):
 //   warp 0      TMA producer: cp.async.bulk.tensor 2-D loads of X and W tiles
-//               (128B-swizzled, 64-element K blocks) into a 4-stage smem ring
+//               (128B-swizzled, 64-element K blocks) into a 3-stage smem ring
 //   warp 1      MMA issuer: one lane issues tcgen05.mma.cta_group::1.kind::f16
 //               (M=128, N=256, K=16) into a TMEM accumulator; tcgen05.commit
 //               frees smem stages and publishes a finished accumulator
 //   warps 2..5  epilogue: tcgen05.ld 32x32b.x32 (warp w reads TMEM lanes
-//               32*(w%4)..+31 = its tile rows), fp32 -> bf16, 16-B stores to
-//               every destination of the row; the accumulator is double
-//               buffered in TMEM (2 x 256 columns) so the next tile's MMAs run
-//               under this tile's epilogue.
+//               32*(w%4)..+31 = its tile rows), fp32 -> bf16 into a per-lane
+//               512-B smem row, then one TMA bulk store of the row per
+//               destination (local HBM or a peer over NVSwitch). TMEM is
+//               released as soon as the tile sits in smem; the accumulator is
+//               double buffered (2 x 256 columns) so the next tile's MMAs run
+//               under this tile's stores.
 // Roofline: tensor (2*M*N*K flop) for K large; for the projector shapes the
 // output stores (M*N*2 B per destination) usually bind.
 #include <cuda.h>
@@ -35,14 +37,17 @@ namespace hb::dev {
 namespace {
 
 constexpr int kBM = 128, kBN = 256, kBK = 64;  // tile; kBK = one 128-B swizzle row of bf16
-constexpr int kStages = 4;
+constexpr int kStages = 3;
 constexpr uint32_t kABytes = kBM * kBK * 2, kBBytes = kBN * kBK * 2;  // 16 KiB, 32 KiB
 constexpr uint32_t kStageBytes = kABytes + kBBytes;
 constexpr int kEpiWarps = 4;
 constexpr int kThreads = 32 * (2 + kEpiWarps);
 constexpr uint32_t kTmemCols = 2 * kBN;  // two accumulators
-constexpr size_t kSmemBytes = kStages * kStageBytes + 1024;  // + alignment slack
-constexpr int kEpiRowPitch = 80;  // staging row: 64 B of data + 16 B pad (bank spread)
+// epilogue staging: per epilogue warp 32 tile rows of 512 B (256 bf16), rows
+// padded to 528 B so the lanes' 16-B writes of one chunk spread over all banks
+constexpr int kEpiRowPitch = kBN * 2 + 16;
+constexpr uint32_t kEpiBytes = kEpiWarps * 32 * kEpiRowPitch;
+constexpr size_t kSmemBytes = kStages * kStageBytes + kEpiBytes + 1024;  // + alignment slack
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -116,7 +121,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full[kStages], empty[kStages], tfull[2], tempty[2];
   __shared__ uint32_t tmem_base_sh;
-  __shared__ __align__(16) unsigned char epi_stage[kEpiWarps * 32 * kEpiRowPitch];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int tiles_m = (args.M + kBM - 1) / kBM, tiles_n = args.N / kBN, num_k = args.K / kBK;
@@ -197,11 +201,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_commit(&tfull[acc]);  // accumulator complete
       }
     }
-  } else {  // ---- epilogue warps: TMEM -> registers -> bf16 -> smem transpose -> every destination
+  } else {  // ---- epilogue warps: TMEM -> registers -> bf16 -> smem rows -> TMA bulk stores per destination
     const int q = warp % 4;  // TMEM lane quarter this warp may access
-    // per warp: a 32-row x 64-B staging block, rows padded to 80 B so the
-    // 16-B writes of 8 consecutive lanes hit distinct banks
-    unsigned char* stage_w = epi_stage + (warp - 2) * (32 * kEpiRowPitch);
+    unsigned char* stage_w = smem + kStages * kStageBytes + (warp - 2) * (32 * kEpiRowPitch);
+    unsigned char* my_row = stage_w + lane * kEpiRowPitch;
     // before the first store: every peer has started this op, so its
     // destination buffers of this set are no longer read
     bool ok = true;
@@ -214,46 +217,40 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int acc = it & 1;
       const uint32_t aphase = (it >> 1) & 1;
       const int m0 = (tile % tiles_m) * kBM, n0 = (tile / tiles_m) * kBN;
+      const int row = m0 + q * 32 + lane;
       mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
-      // this lane's row's destinations stay in registers; lanes fetch each
-      // other's with shuffles when they store
-      const int row = m0 + q * 32 + lane;
-      unsigned char* mine[kMaxProjFan];
-#pragma unroll
-      for (int f = 0; f < kMaxProjFan; ++f)
-        mine[f] = (row < args.M && f < args.fan) ? args.row_dst[static_cast<size_t>(row) * args.fan + f] : nullptr;
+      // this lane's staging row is free once its previous bulk stores have read it
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 #pragma unroll 1
       for (int c = 0; c < kBN / 32; ++c) {
         uint32_t v[32];
         HB_TMEM_LD32(tmem_base + acc * kBN + c * 32 + (static_cast<uint32_t>(q * 32) << 16), v);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        uint4* srow = reinterpret_cast<uint4*>(stage_w + lane * kEpiRowPitch);
+        uint4* dst = reinterpret_cast<uint4*>(my_row + c * 64);
 #pragma unroll
         for (int i = 0; i < 4; ++i)
-          srow[i] = make_uint4(pack_bf16(v[8 * i], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
-                               pack_bf16(v[8 * i + 4], v[8 * i + 5]), pack_bf16(v[8 * i + 6], v[8 * i + 7]));
-        __syncwarp();
-        // 4 lanes per row, 8 rows per instruction: every store writes whole
-        // 64-B row segments (two full sectors) instead of one 16-B piece per row
-        const size_t col_bytes = static_cast<size_t>(n0 + c * 32) * 2 + (lane & 3) * 16;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int r = 8 * k + (lane >> 2);
-          const uint4 val = *reinterpret_cast<const uint4*>(stage_w + r * kEpiRowPitch + (lane & 3) * 16);
-#pragma unroll
-          for (int f = 0; f < kMaxProjFan; ++f) {
-            if (f >= args.fan) break;
-            unsigned char* p = reinterpret_cast<unsigned char*>(
-                __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(mine[f]), r));
-            if (p && ok) *reinterpret_cast<uint4*>(p + col_bytes) = val;
-          }
-        }
-        __syncwarp();
+          dst[i] = make_uint4(pack_bf16(v[8 * i], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
+                              pack_bf16(v[8 * i + 4], v[8 * i + 5]), pack_bf16(v[8 * i + 6], v[8 * i + 7]));
       }
+      // the accumulator is in smem now: hand TMEM back to the MMA warp
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
+      // each lane stores its row (512 contiguous bytes) to every destination
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      if (row < args.M && ok) {
+        unsigned char* const* d = args.row_dst + static_cast<size_t>(row) * args.fan;
+        for (int f = 0; f < args.fan; ++f) {
+          unsigned char* p = d[f];
+          if (!p) break;
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(p + static_cast<size_t>(n0) * 2),
+                       "r"(smem_u32(my_row)), "r"(static_cast<uint32_t>(kBN * 2))
+                       : "memory");
+        }
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
     }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // every store complete before the end protocol
   }
   __syncthreads();
   if (warp == 1) {
