@@ -221,7 +221,7 @@ uint64_t env_u64(const char* name, uint64_t dflt) {
   return v && *v ? std::strtoull(v, nullptr, 10) : dflt;
 }
 // elements per dynamic reduce chunk; TMA stage size (tuning knobs, HB_RED_CHUNK / HB_TMA_CHUNK_KB)
-const uint64_t kDynReduceChunk = env_u64("HB_RED_CHUNK", 32 * 1024);
+const uint64_t kDynReduceChunk = env_u64("HB_RED_CHUNK", 0);  // 0: sized per launch (prepare_bwd)
 const int kTmaChunkKiB = static_cast<int>(env_u64("HB_TMA_CHUNK_KB", 32));
 uint64_t pad_to(uint64_t x, uint64_t q) { return (x + q - 1) / q * q; }
 }  // namespace
@@ -351,7 +351,10 @@ void Exec::upload_copies(int mb, uint64_t unit, std::vector<uint64_t>* w0s, std:
 }
 
 int Exec::copy_grid() const {
-  if (copy_mode() == dev::kPartTma) return sm_count_ * dev::tma_blocks_per_sm(dev::tma_chunk_bytes(kTmaChunkKiB));
+  if (copy_mode() == dev::kPartTma) {
+    const int occ = dev::tma_blocks_per_sm(dev::tma_chunk_bytes(kTmaChunkKiB));
+    return sm_count_ * (cfg_.blocks_per_sm > 0 ? std::min(cfg_.blocks_per_sm, occ) : occ);
+  }
   const int occ = dev::copy_blocks_per_sm(cfg_.threads);
   return sm_count_ * (cfg_.blocks_per_sm > 0 ? std::min(cfg_.blocks_per_sm, occ) : occ);
 }
@@ -381,7 +384,18 @@ void Exec::prepare_fwd() {
 void Exec::prepare_bwd() {
   if (!dirty_bwd_) return;
   const int mode = reduce_mode();
-  const uint64_t unit = pad_unit(mode, false);
+  uint64_t unit = pad_unit(mode, false);
+  if (mode == dev::kPartDynamic && unit == 0) {
+    // at least ~2 chunks per CTA, 8K..32K elements: large returns keep long
+    // streaming chunks, small ones spread over the whole grid (measured: c2x4
+    // at 1/8 width 12.5 -> 9.0 us with 8K chunks; C2 N=1 best at 32K)
+    uint64_t total = 0;
+    for (const auto& s : bwd_local_) total += static_cast<uint64_t>(s.n);
+    const uint64_t grid = static_cast<uint64_t>(sm_count_) *
+                          dev::reduce_blocks_per_sm(cfg_.threads, cfg_.grad_in_dtype, cfg_.grad_out_dtype);
+    unit = 8192;
+    while (unit < 32768 && total / (2 * unit) >= 2 * grid) unit *= 2;
+  }
   const int es_in = dev::dtype_size(cfg_.grad_in_dtype), es_out = dev::dtype_size(cfg_.grad_out_dtype);
   std::vector<uint64_t> w0s, ns;
   for (int mb = 0; mb < cfg_.mb_slots; ++mb) {

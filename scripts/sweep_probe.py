@@ -39,7 +39,8 @@ def main():
             tm = bench.traffic_model(cfg, N)
             for mode in MODES:
                 rt = hbb.BridgeRuntime(plan, sp, n_gpus=N, my_gpu=rank, rank_to_gpu=r2g, mb_slots=2,
-                                       fwd_mode=mode, partition=int(os.environ.get("PART", "0")))
+                                       fwd_mode=mode, partition=int(os.environ.get("PART", "0")),
+                                       blocks_per_sm=int(os.environ.get("BPS", "0")))
                 rt.exchange_handles()
                 mb = [0]
 
