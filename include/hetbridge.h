@@ -147,6 +147,12 @@ typedef struct {
    * gradients, the contract of bridge.hpp:33-36. 1: always the tp=0 copy, the
    * reference data path replica for replica (strict provenance). */
   int strict_provenance;
+  /* 1 (splice edges): the TEXT slot holds int32 token ids, one per text row, and
+   * the forward gathers each text row from the embedding table set with
+   * hb_exec_set_text_embedding (the LLM's embedding lookup fused into the
+   * splice). An id outside [0, vocab) makes hb_exec_status
+   * return InvalidArgument (device error 2). */
+  int text_embedding;
 } hb_exec_config;
 void hb_exec_config_default(hb_exec_config* c);
 
@@ -166,6 +172,8 @@ int hb_exec_forward(hb_exec* x, int mb, void* cuda_stream);
 /* backward: BridgeRuntime::backward_* ; src_grad = beta*src_grad + returned gradient */
 int hb_exec_backward(hb_exec* x, int mb, float beta, void* cuda_stream);
 int hb_exec_seed_forward_record(hb_exec* x, int mb); /* bridge.hpp:165 */
+/* Embedding table [vocab x d_h] (activation dtype, device memory of this GPU). */
+int hb_exec_set_text_embedding(hb_exec* x, const void* table, long long vocab);
 /* CUDA graph of one buffer set's boundary ops; what: 0 forward, 1 forward +
  * backward(beta), 2 backward(beta). One graph launch replays the ops; replays
  * bypass the microbatch records. */

@@ -33,7 +33,7 @@ EXPORTS = [
     "hb_exec_config_default", "hb_exec_create", "hb_exec_destroy", "hb_exec_ipc_handle",
     "hb_exec_open_peers", "hb_exec_buffer", "hb_exec_bind", "hb_exec_forward", "hb_exec_backward",
     "hb_exec_seed_forward_record", "hb_exec_status", "hb_exec_stats", "hb_exec_graph_capture", "hb_projector_gemm",
-    "hb_exec_forward_projected",
+    "hb_exec_forward_projected", "hb_exec_set_text_embedding",
     "hb_exec_graph_launch",
 ]
 
@@ -77,7 +77,8 @@ class ExecConfig(ctypes.Structure):
                 ("grad_out_dtype", ctypes.c_int), ("mb_slots", ctypes.c_int),
                 ("internal_alloc", ctypes.c_int), ("blocks_per_sm", ctypes.c_int),
                 ("threads", ctypes.c_int), ("timeout_s", ctypes.c_double), ("fwd_mode", ctypes.c_int),
-                ("partition", ctypes.c_int), ("strict_provenance", ctypes.c_int)]
+                ("partition", ctypes.c_int), ("strict_provenance", ctypes.c_int),
+                ("text_embedding", ctypes.c_int)]
 
 
 _lib = None
@@ -127,6 +128,7 @@ def _declare(L):
         "hb_exec_stats": (I, [V, P(LL), P(LL), P(LL), P(LL), P(LL)]),
         "hb_projector_gemm": (I, [V, LL, V, LL, V, I, I, I, I, V]),
         "hb_exec_forward_projected": (I, [V, I, V, LL, V, LL, I, I, V]),
+        "hb_exec_set_text_embedding": (I, [V, V, LL]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name, None)

@@ -209,7 +209,8 @@ class BridgeRuntime:
                  my_gpu: int = 0, rank_to_gpu=None, act_dtype=None, grad_in_dtype=None,
                  grad_out_dtype=None, mb_slots: int = 1, internal_alloc: bool = True,
                  blocks_per_sm: int = 0, threads: int = 0, timeout_s: float = 0.0,
-                 fwd_mode: int = 0, partition: int = 0, strict_provenance: bool = False):
+                 fwd_mode: int = 0, partition: int = 0, strict_provenance: bool = False,
+                 text_embedding: bool = False):
         import torch
 
         self.plan, self.splice = plan, splice
@@ -232,6 +233,8 @@ class BridgeRuntime:
         cfg.fwd_mode = fwd_mode  # 0 auto, 1 pull, 2 push
         cfg.partition = partition
         cfg.strict_provenance = 1 if strict_provenance else 0
+        cfg.text_embedding = 1 if text_embedding else 0
+        self.text_embedding = bool(text_embedding)
         if not torch.cuda.is_available():
             raise HetBridgeError(25, "BridgeRuntime needs a CUDA device (no CPU fallback)")
         m = (ctypes.c_int * len(self.rank_to_gpu))(*self.rank_to_gpu)
@@ -261,7 +264,7 @@ class BridgeRuntime:
         sp_fp = hashlib.sha256(self.splice.codes.tobytes()).hexdigest() if self.splice is not None else ""
         fp = hashlib.sha256(repr((hbb_fingerprint(self.plan), sp_fp, self.rank_to_gpu, str(self.act_dtype),
                                   str(self.grad_in_dtype), str(self.grad_out_dtype), self.mb_slots,
-                                  self.n_gpus)).encode()).digest()
+                                  self.n_gpus, self.text_embedding)).encode()).digest()
         fps = [None] * dist.get_world_size(group)
         dist.all_gather_object(fps, fp, group=group)
         if any(f != fp for f in fps):
@@ -276,7 +279,19 @@ class BridgeRuntime:
 
     # -- buffers
     def _dtype_of(self, slot):
+        import torch
+
+        if slot == SLOT_TEXT and self.text_embedding:
+            return torch.int32  # token ids, one per text row
         return {SLOT_DST_GRAD: self.grad_in_dtype, SLOT_SRC_GRAD: self.grad_out_dtype}.get(slot, self.act_dtype)
+
+    def set_text_embedding(self, table):
+        """Embedding table [vocab, d_h] (activation dtype, this GPU) that the
+        splice gathers its text rows from (``text_embedding=True``)."""
+        if not table.is_cuda or not table.is_contiguous() or table.dtype != self.act_dtype:
+            raise HetBridgeError(24, "embedding table must be a contiguous CUDA tensor of the activation dtype")
+        check(lib().hb_exec_set_text_embedding(self._h, ctypes.c_void_p(table.data_ptr()), table.shape[0]))
+        self._keep["embedding"] = table
 
     def buffer(self, rank: int, slot: int, mb_slot: int = 0):
         """Device tensor view (1-D, element dtype of the slot) of a resident rank's buffer."""

@@ -89,7 +89,7 @@ const char* hb_error_name(int status) {
   return hb::error_code_name(static_cast<hb::ErrorCode>(status - 1));
 }
 
-int hb_abi_version(void) { return 5; }
+int hb_abi_version(void) { return 6; }
 
 int hb_coord_of_rank(const hb_layout* l, int rank, int coord4[4]) {
   return guard([&] {
@@ -300,6 +300,7 @@ void hb_exec_config_default(hb_exec_config* c) {
   c->fwd_mode = d.fwd_mode;
   c->partition = d.partition;
   c->strict_provenance = d.strict_provenance;
+  c->text_embedding = d.text_embedding;
 }
 
 int hb_exec_create(const hb_plan* p, const hb_splice* s, int n_gpus, int my_gpu, const int* rank_to_gpu,
@@ -321,6 +322,7 @@ int hb_exec_create(const hb_plan* p, const hb_splice* s, int n_gpus, int my_gpu,
       c.fwd_mode = cfg->fwd_mode;
       c.partition = cfg->partition;
       c.strict_provenance = cfg->strict_provenance;
+      c.text_embedding = cfg->text_embedding;
     }
     std::vector<int> map;
     if (rank_to_gpu) map.assign(rank_to_gpu, rank_to_gpu + n_ranks);
@@ -405,6 +407,7 @@ int hb_exec_status(hb_exec* x, unsigned* device_error) {
     need(x, "exec");
     const unsigned e = x->x->device_error();
     if (device_error) *device_error = e;
+    if (e == hb::dev::kErrBadId) hb::raise(hb::ErrorCode::InvalidArgument, "text token id outside [0, vocab)");
     if (e) hb::raise(hb::ErrorCode::Timeout, "cross-GPU flag wait timed out on the device");
   });
 }
@@ -417,6 +420,13 @@ int hb_exec_stats(hb_exec* x, long long* fs, long long* bs, long long* fb, long 
     if (fb) *fb = static_cast<long long>(x->x->local_fwd_bytes());
     if (be) *be = static_cast<long long>(x->x->local_bwd_elems());
     if (nl) *nl = x->x->launches();
+  });
+}
+
+int hb_exec_set_text_embedding(hb_exec* x, const void* table, long long vocab) {
+  return guard([&] {
+    need(x, "exec");
+    x->x->set_text_embedding(table, vocab);
   });
 }
 

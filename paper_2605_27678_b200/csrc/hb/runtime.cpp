@@ -35,6 +35,9 @@ Exec::Exec(const bridge::BridgePlan& plan, const index::SpliceSpec* splice, int 
   if (cfg.grad_in_dtype == dev::kFP64 || cfg.grad_out_dtype == dev::kFP64)
     raise(ErrorCode::InvalidArgument, "fp64 gradients are not supported on the device path");
   map_ = index::build_index_map(plan_, splice, cfg.strict_provenance == 0);
+  splice_d_h_ = splice ? splice->d_h : 0;
+  if (cfg.text_embedding && !splice)
+    raise(ErrorCode::InvalidArgument, "text_embedding needs a splice edge (text rows to gather)");
   if (static_cast<int>(rank_to_gpu_.size()) < map_.world)
     raise(ErrorCode::InvalidArgument, "rank_to_gpu must cover every logical rank of the edge");
   for (int r = 0; r < map_.world; ++r)
@@ -55,7 +58,7 @@ Exec::Exec(const bridge::BridgePlan& plan, const index::SpliceSpec* splice, int 
       if (gpu_of(r) != g) continue;
       for (int s = 0; s < index::kNumSlots; ++s) {
         offsets_[g][r * index::kNumSlots + s] = off;
-        off += align_up(static_cast<uint64_t>(map_.elems[r][s]) * dev::dtype_size(slot_dtype(s)));
+        off += align_up(slot_bytes(r, s));
       }
     }
     mb_stride_[g] = off;
@@ -147,8 +150,18 @@ int Exec::slot_dtype(int slot) const {
   switch (slot) {
     case index::kDstGrad: return cfg_.grad_in_dtype;
     case index::kSrcGrad: return cfg_.grad_out_dtype;
+    case index::kText: return cfg_.text_embedding ? dev::kI32 : cfg_.act_dtype;
     default: return cfg_.act_dtype;
   }
+}
+
+int64_t Exec::text_row_elems() const { return splice_d_h_; }
+
+// Bytes of a rank's buffer: elements x dtype, except token ids (one per text row).
+uint64_t Exec::slot_bytes(int rank, int slot) const {
+  int64_t n = map_.elems[rank][slot];
+  if (slot == index::kText && cfg_.text_embedding) n /= splice_d_h_;
+  return static_cast<uint64_t>(n) * dev::dtype_size(slot_dtype(slot));
 }
 
 uint64_t Exec::offset_of(int gpu, int rank, int slot, int mb_slot) const {
@@ -158,7 +171,7 @@ uint64_t Exec::offset_of(int gpu, int rank, int slot, int mb_slot) const {
 size_t Exec::buffer_bytes(int rank, int slot) const {
   if (rank < 0 || rank >= map_.world || slot < 0 || slot >= index::kNumSlots)
     raise(ErrorCode::InvalidArgument, "buffer index out of range");
-  return static_cast<size_t>(map_.elems[rank][slot]) * dev::dtype_size(slot_dtype(slot));
+  return static_cast<size_t>(slot_bytes(rank, slot));
 }
 
 void Exec::ipc_handle(void* out64) const {
@@ -326,10 +339,19 @@ void Exec::upload_copies(int mb, uint64_t unit, std::vector<uint64_t>* w0s, std:
   w0s->clear();
   ns->clear();
   for (const auto& f : fwd_local_) {
-    const int es = dev::dtype_size(slot_dtype(f.src.slot));
+    const bool gather = f.src.slot == index::kText && cfg_.text_embedding;
+    const int es = dev::dtype_size(gather ? cfg_.act_dtype : slot_dtype(f.src.slot));
     const uint64_t nbytes = static_cast<uint64_t>(f.n) * es;
     dev::CopySeg c{};
-    c.src = static_cast<const unsigned char*>(resolve(f.src.rank, f.src.slot, mb)) + f.src.off * es;
+    if (gather) {  // rows table[ids[k]] for the run's text rows k
+      if (!embed_table_) raise(ErrorCode::InvalidArgument, "text_embedding: call set_text_embedding first");
+      c.src = embed_table_;
+      c.ids = static_cast<const int32_t*>(resolve(f.src.rank, f.src.slot, mb)) + f.src.off / splice_d_h_;
+      c.row_bytes = static_cast<uint32_t>(splice_d_h_ * es);
+      c.vocab = embed_vocab_;
+    } else {
+      c.src = static_cast<const unsigned char*>(resolve(f.src.rank, f.src.slot, mb)) + f.src.off * es;
+    }
     c.ndst = static_cast<int32_t>(f.dsts.size());
     for (size_t d = 0; d < f.dsts.size(); ++d)
       c.dst[d] = static_cast<unsigned char*>(const_cast<void*>(resolve(f.dsts[d].rank, f.dsts[d].slot, mb))) +
@@ -605,6 +627,14 @@ void Exec::graph_launch(int mb_slot, int what, void* stream) {
 
 void Exec::seed_forward_record(int mb) { fwd_done_.insert(mb); }
 
+void Exec::set_text_embedding(const void* table, int64_t vocab) {
+  if (!cfg_.text_embedding) raise(ErrorCode::InvalidArgument, "exec was created without text_embedding");
+  if (!table || vocab < 1) raise(ErrorCode::InvalidArgument, "embedding table must be non-null with vocab >= 1");
+  embed_table_ = static_cast<const unsigned char*>(table);
+  embed_vocab_ = vocab;
+  dirty_fwd_ = true;
+}
+
 uint32_t Exec::device_error() const {
   uint32_t v = 0;
   ck(cudaMemcpy(&v, ctr_ + 3 * dev::kCtrLine + 1, sizeof(v), cudaMemcpyDeviceToHost), "read status");
@@ -613,8 +643,7 @@ uint32_t Exec::device_error() const {
 
 uint64_t Exec::local_fwd_bytes() const {
   uint64_t b = 0;
-  for (const auto& f : fwd_local_)
-    b += static_cast<uint64_t>(f.n) * f.dsts.size() * dev::dtype_size(slot_dtype(f.src.slot));
+  for (const auto& f : fwd_local_) b += static_cast<uint64_t>(f.n) * f.dsts.size() * dev::dtype_size(cfg_.act_dtype);
   return b;
 }
 

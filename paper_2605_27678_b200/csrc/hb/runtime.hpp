@@ -39,6 +39,7 @@ struct ExecConfig {
   int fwd_mode = 0;                 // forward: 0 auto, 1 consumers pull from owners, 2 owners push
   int partition = 0;                // 0 auto, 1 contiguous, 2 interleaved, 3 dynamic, 4 TMA bulk (copy)
   int strict_provenance = 0;        // 1: backward reads tp=0 copies only (index_map.hpp balance_replicas)
+  int text_embedding = 0;           // splice: TEXT holds int32 token ids, rows gathered from an embedding table
 };
 
 class Exec {
@@ -69,6 +70,9 @@ class Exec {
                          void* stream);
   void backward(int mb, float beta, void* stream);
   void seed_forward_record(int mb);
+  // Embedding table [vocab x d_h] (act dtype, on this GPU) the splice gathers
+  // text rows from when cfg.text_embedding.
+  void set_text_embedding(const void* table, int64_t vocab);
 
   // CUDA-graph capture of one buffer set's forward (+ backward with `beta`):
   // the step is replayed with one graph launch (no per-kernel host overhead).
@@ -89,6 +93,11 @@ class Exec {
  private:
   int gpu_of(int rank) const { return rank_to_gpu_.at(rank); }
   int slot_dtype(int slot) const;
+  uint64_t slot_bytes(int rank, int slot) const;
+  int64_t text_row_elems() const;  // d_h of the splice (elements per text row)
+  int64_t splice_d_h_ = 0;
+  const unsigned char* embed_table_ = nullptr;
+  int64_t embed_vocab_ = 0;
   uint64_t offset_of(int gpu, int rank, int slot, int mb_slot) const;
   const void* resolve(int rank, int slot, int mb_slot) const;
   void prepare_fwd();  // resolve pointers, upload descriptors (after bind/open)

@@ -223,10 +223,38 @@ __device__ __forceinline__ void copy_scalar(const unsigned char* src, unsigned c
 
 constexpr int kUnroll = 8;
 
+__device__ __forceinline__ void copy_range_from(const CopySeg& sg, const unsigned char* __restrict__ src, uint64_t a,
+                                                uint64_t b);
+
+// Source address of byte `off` of a gather run (nullptr: bad id, error set).
+__device__ __forceinline__ const unsigned char* gather_src(const CopySeg& sg, uint64_t off, uint32_t* err) {
+  const int64_t id = sg.ids[off / sg.row_bytes];
+  if (id < 0 || id >= sg.vocab) {
+    atomicExch(err, kErrBadId);
+    return nullptr;
+  }
+  return sg.src + static_cast<uint64_t>(id) * sg.row_bytes + off % sg.row_bytes;
+}
+
 // Copies bytes [a, b) of one segment to each of its destinations with the
 // whole CTA: every 16 B of the source is loaded once and stored ndst times.
-__device__ __forceinline__ void copy_range(const CopySeg& sg, uint64_t a, uint64_t b) {
-  const unsigned char* __restrict__ src = sg.src;
+// Gather runs are copied row piece by row piece.
+__device__ __forceinline__ void copy_range(const CopySeg& sg, uint64_t a, uint64_t b, uint32_t* err) {
+  if (!sg.ids) {
+    copy_range_from(sg, sg.src, a, b);
+    return;
+  }
+  for (uint64_t off = a; off < b;) {
+    const uint64_t end = min(b, (off / sg.row_bytes + 1) * sg.row_bytes);
+    const unsigned char* p = gather_src(sg, off, err);
+    // copy_range_from indexes its source by the run offset: rebase the row piece
+    if (p) copy_range_from(sg, p - off, off, end);
+    off = end;
+  }
+}
+
+__device__ __forceinline__ void copy_range_from(const CopySeg& sg, const unsigned char* __restrict__ src, uint64_t a,
+                                                uint64_t b) {
   const int nd = sg.ndst;
   uint64_t align = reinterpret_cast<uint64_t>(src) | a;
   for (int d = 0; d < nd; ++d) align |= reinterpret_cast<uint64_t>(sg.dst[d]);
@@ -266,7 +294,7 @@ template <int MODE>
 __global__ void __launch_bounds__(512, 2) copy_segments_kernel(const CopySeg* __restrict__ segs, int nseg,
                                                             Partition part, SyncArgs sync) {
   run_shares<MODE>(segs, nseg, part, sync, CopyLen{},
-                   [](const CopySeg& sg, uint64_t a, uint64_t b, bool) { copy_range(sg, a, b); });
+                   [&](const CopySeg& sg, uint64_t a, uint64_t b, bool) { copy_range(sg, a, b, sync.err); });
 }
 
 // ---- TMA bulk-copy engine ------------------------------------------------------
@@ -380,16 +408,29 @@ __global__ void __launch_bounds__(32) copy_segments_tma_kernel(const CopySeg* __
       const uint64_t e = a + part.chunk < sg.nbytes ? a + part.chunk : sg.nbytes;
       const uint32_t bytes = static_cast<uint32_t>(e - a);
       const int nd = sg.ndst;
-      uint64_t al = reinterpret_cast<uint64_t>(sg.src + a) | bytes;
+      uint64_t al = reinterpret_cast<uint64_t>(sg.src + a) | bytes | (sg.ids ? sg.row_bytes : 0u);
       for (int d = 0; d < nd; ++d) al |= reinterpret_cast<uint64_t>(sg.dst[d] + a);
       if (al & 15) {  // rare unaligned run: plain byte copy by this lane
-        for (uint64_t i = a; i < e; ++i)
-          for (int d = 0; d < nd; ++d) sg.dst[d][i] = sg.src[i];
+        for (uint64_t i = a; i < e; ++i) {
+          const unsigned char* p = sg.ids ? gather_src(sg, i, sync.err) : sg.src + i;
+          if (p)
+            for (int d = 0; d < nd; ++d) sg.dst[d][i] = *p;
+        }
         continue;
       }
       const int st = issued % kTmaStages;
       mbar_expect(&full[st], bytes);
-      bulk_g2s(stage_mem + st * kTmaStageBytes, sg.src + a, bytes, &full[st]);
+      if (!sg.ids) {
+        bulk_g2s(stage_mem + st * kTmaStageBytes, sg.src + a, bytes, &full[st]);
+      } else {  // gather run: one bulk load per row piece (a bad id loads row 0, its stores are skipped below)
+        for (uint64_t off = a; off < e;) {
+          const uint64_t end = min(e, (off / sg.row_bytes + 1) * sg.row_bytes);
+          const unsigned char* p = gather_src(sg, off, sync.err);
+          bulk_g2s(stage_mem + st * kTmaStageBytes + (off - a), p ? p : sg.src + off % sg.row_bytes,
+                   static_cast<uint32_t>(end - off), &full[st]);
+          off = end;
+        }
+      }
       pend_seg[st] = t.x;
       pend_off[st] = a;
       pend_bytes[st] = bytes;

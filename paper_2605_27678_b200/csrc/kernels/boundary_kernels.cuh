@@ -7,9 +7,9 @@
 
 namespace hb::dev {
 
-enum Dtype : int { kBF16 = 0, kFP16 = 1, kFP32 = 2, kFP64 = 3 };
+enum Dtype : int { kBF16 = 0, kFP16 = 1, kFP32 = 2, kFP64 = 3, kI32 = 4 };
 
-inline int dtype_size(int dt) { return dt == kFP32 ? 4 : dt == kFP64 ? 8 : 2; }
+inline int dtype_size(int dt) { return (dt == kFP32 || dt == kI32) ? 4 : dt == kFP64 ? 8 : 2; }
 
 // Work space: every segment occupies [w0, w0 + n) of a padded linear work
 // space (bytes for copies, elements for reductions); w0 is rounded up to
@@ -23,13 +23,22 @@ constexpr uint64_t kQuantum = 4096;
 // hold the same rows on this GPU in pull mode; every consumer of a local run
 // in push mode).
 constexpr int kMaxFan = 8;
+//
+// Gather runs (text-embedding lookup fused into the splice): when `ids` is set,
+// the run is nbytes/row_bytes rows and row i comes from src + ids[i]*row_bytes
+// (src = the embedding table, `vocab` rows); an id outside [0, vocab) sets the
+// error word to kErrBadId (that row's contents are then unspecified).
 struct CopySeg {
   const unsigned char* src;
   unsigned char* dst[kMaxFan];
   uint64_t nbytes;
   uint64_t w0;
   int32_t ndst;
+  uint32_t row_bytes;  // gather runs only
+  const int32_t* ids;  // nullptr: contiguous run
+  int64_t vocab;
 };
+constexpr uint32_t kErrTimeout = 1, kErrBadId = 2;
 
 // dst[i] = beta*dst[i] + sum_t term_t[i], fp32 accumulation, terms summed in
 // order starting from +0.0f; term pointers live in a side array.

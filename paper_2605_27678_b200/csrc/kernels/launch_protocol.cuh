@@ -41,7 +41,7 @@ __device__ __forceinline__ bool spin_until(const SyncArgs& s, const uint32_t* fl
   while (static_cast<int32_t>(ld_acquire_sys(flag) - e) < 0) {
     __nanosleep(64);
     if (static_cast<uint64_t>(clock64() - t0) > s.timeout_cycles) {
-      atomicExch(s.err, 1u);
+      atomicExch(s.err, kErrTimeout);
       return false;
     }
   }

@@ -1,0 +1,78 @@
+"""Text-embedding lookup fused into the CP splice (
+tinymodel.hpp:97-101 builds the fused sequence from text embeddings and vision
+rows). With ``text_embedding=True`` the TEXT slot holds int32 token ids and the
+forward gathers each text row from the embedding table; the result must be
+bit-identical to splicing the pre-embedded rows table[ids]."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from helpers import hbb  # noqa: E402
+
+from paper_2605_27678_b200 import configs  # noqa: E402
+
+
+def _spec(cfg):
+    s = cfg.splice
+    return hbb.SpliceSpec(s["Q"], s["S"], cfg.hidden, cfg.tokens, s["codes"], s["text_mode"])
+
+
+@pytest.mark.parametrize("partition", [0, 1, 3])
+def test_embedding_gather_equals_pre_embedded_text(partition):
+    cfg = configs.get("c4", scale=64)
+    plan = hbb.plan_bridge(cfg.edge())
+    sp = _spec(cfg)
+    vocab, d_h = 997, cfg.hidden
+    table = torch.randn(vocab, d_h, device="cuda").to(torch.bfloat16)
+    rt_e = hbb.BridgeRuntime(plan, sp, text_embedding=True, partition=partition)
+    rt_p = hbb.BridgeRuntime(plan, sp, partition=partition)
+    rt_e.set_text_embedding(table)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    for r in rt_e.local_ranks(hbb.SLOT_SRC_ACT):
+        x = torch.randn(rt_e.buffer_numel(r, hbb.SLOT_SRC_ACT), device="cuda", generator=g).to(torch.bfloat16)
+        rt_e.buffer(r, hbb.SLOT_SRC_ACT).copy_(x)
+        rt_p.buffer(r, hbb.SLOT_SRC_ACT).copy_(x)
+    for r in rt_e.local_ranks(hbb.SLOT_TEXT):
+        ids_buf = rt_e.buffer(r, hbb.SLOT_TEXT)
+        assert ids_buf.dtype == torch.int32
+        ids = torch.randint(0, vocab, (ids_buf.numel(),), device="cuda", generator=g, dtype=torch.int32)
+        ids_buf.copy_(ids)
+        rt_p.buffer(r, hbb.SLOT_TEXT).copy_(table[ids.long()].reshape(-1))
+    rt_e.forward(0)
+    rt_p.forward(0)
+    torch.cuda.synchronize()
+    assert rt_e.status() == 0
+    for r in rt_e.local_ranks(hbb.SLOT_DST_ACT):
+        assert torch.equal(rt_e.buffer(r, hbb.SLOT_DST_ACT), rt_p.buffer(r, hbb.SLOT_DST_ACT)), f"rank {r}"
+    rt_e.close()
+    rt_p.close()
+
+
+def test_embedding_bad_token_id_reported():
+    cfg = configs.get("c4", scale=64)
+    plan = hbb.plan_bridge(cfg.edge())
+    rt = hbb.BridgeRuntime(plan, _spec(cfg), text_embedding=True)
+    table = torch.zeros(10, cfg.hidden, device="cuda", dtype=torch.bfloat16)
+    rt.set_text_embedding(table)
+    r = rt.local_ranks(hbb.SLOT_TEXT)[0]
+    rt.buffer(r, hbb.SLOT_TEXT).fill_(3)
+    rt.buffer(r, hbb.SLOT_TEXT)[5] = 10  # == vocab: out of range
+    rt.forward(0)
+    torch.cuda.synchronize()
+    with pytest.raises(hbb.HetBridgeError) as ei:
+        rt.status()
+    assert ei.value.code == "InvalidArgument"
+    rt.close()
+
+
+def test_embedding_requires_table_and_splice():
+    cfg = configs.get("c4", scale=64)
+    plan = hbb.plan_bridge(cfg.edge())
+    rt = hbb.BridgeRuntime(plan, _spec(cfg), text_embedding=True)
+    with pytest.raises(hbb.HetBridgeError):
+        rt.forward(0)  # no table set
+    rt.close()
+    with pytest.raises(hbb.HetBridgeError):
+        hbb.BridgeRuntime(hbb.plan_bridge(configs.get("c2", scale=64).edge()), text_embedding=True)
