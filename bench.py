@@ -691,11 +691,14 @@ def run_pp_overlap(args, cfg, plan, rt, r2g, rank, dev, barrier, stream, slots):
 
     for k in range(slots):  # (re)capture the boundary step graphs on this stream
         rt.capture_step(k, cfg.beta, True, stream)
-    pp_p2p()  # warm up NCCL connections
+    for _ in range(3):  # warm up NCCL connections and both paths together
+        pp_p2p()
+        boundary(0)
     torch.cuda.synchronize()
-    t_b = timed(boundary)
-    t_p = timed(lambda i: pp_p2p())
-    t_both = timed(lambda i: (pp_p2p(), boundary(i)))
+    # median of 3 trials of 20 reps each (NCCL P2P timing varies run to run)
+    trials = [(timed(boundary, 20), timed(lambda i: pp_p2p(), 20), timed(lambda i: (pp_p2p(), boundary(i)), 20))
+              for _ in range(3)]
+    t_b, t_p, t_both = (statistics.median(x) for x in zip(*trials))
     overlap = (t_b + t_p - t_both) / max(1e-9, min(t_b, t_p))
     return {"boundary_ms": round(t_b, 4), "pp_p2p_ms": round(t_p, 4), "both_ms": round(t_both, 4),
             "overlap": round(overlap, 3), "pp_hops": [[a, b] for a, b in hops],
