@@ -28,6 +28,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "kernels/launch_protocol.cuh"
 #include "kernels/projector_gemm.cuh"
@@ -77,6 +78,48 @@ __device__ __forceinline__ void tma_load_2d(void* smem, const CUtensorMap* map, 
       "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
 }
+// multicast variant: the W half this CTA loads lands in both CTAs of the pair
+__device__ __forceinline__ void tma_load_2d_mc(void* smem, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                               uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster [%0], "
+      "[%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(smem)),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+// Work items: single tiles (kCM = 1) or, for a CTA pair (kCM = 2), pairs of
+// M-adjacent tiles that share their W tile: CTA r of the pair takes m-tile
+// 2*i + r, and each CTA loads half of W and multicasts it to both.
+template <int kCM>
+struct TileMap {
+  int tiles_m, tiles_n, tiles_mp, rank;
+  __device__ TileMap(int M, int N, int r)
+      : tiles_m((M + kBM - 1) / kBM), tiles_n(N / kBN), tiles_mp((tiles_m + kCM - 1) / kCM), rank(r) {}
+  __device__ int items() const { return tiles_mp * tiles_n; }
+  __device__ int first() const { return static_cast<int>(blockIdx.x) / kCM; }
+  __device__ int step() const { return static_cast<int>(gridDim.x) / kCM; }
+  __device__ void coords(int item, int& m0, int& n0) const {
+    m0 = ((item % tiles_mp) * kCM + rank) * kBM;  // may lie beyond M in the last pair: rows are skipped
+    n0 = (item / tiles_mp) * kBN;
+  }
+};
+
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_commit(uint64_t* bar) {
@@ -115,6 +158,7 @@ __device__ __forceinline__ uint32_t pack_bf16(uint32_t lo, uint32_t hi) {
         "=r"(v[30]), "=r"(v[31])                                                                               \
       : "r"(addr))
 
+template <int kCM>
 __global__ void __launch_bounds__(kThreads, 1)
     projector_gemm_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_w,
                           ProjectorArgs args) {
@@ -123,15 +167,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ uint32_t tmem_base_sh;
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int tiles_m = (args.M + kBM - 1) / kBM, tiles_n = args.N / kBN, num_k = args.K / kBK;
-  const int num_tiles = tiles_m * tiles_n;
+  const int num_k = args.K / kBK;
+  const uint32_t crank = kCM > 1 ? cluster_rank() : 0;
+  const TileMap<kCM> tm(args.M, args.N, static_cast<int>(crank));
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&map_x) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&map_w) : "memory");
     for (int i = 0; i < kStages; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
+      mbar_init(&empty[i], kCM);  // both CTAs' MMAs read a stage the pair filled
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
@@ -152,6 +197,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (kCM > 1) cluster_sync_all();  // the peer's barriers exist before anything multicasts into them
   tc_fence_after();
   const uint32_t tmem_base = tmem_base_sh;
 
@@ -159,14 +205,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {  // ---- TMA producer
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int m0 = (tile % tiles_m) * kBM, n0 = (tile / tiles_m) * kBN;
+      for (int item = tm.first(); item < tm.items(); item += tm.step()) {
+        int m0, n0;
+        tm.coords(item, m0, n0);
         for (int kb = 0; kb < num_k; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           unsigned char* a = smem + stage * kStageBytes;
-          mbar_expect_tx(&full[stage], kStageBytes);
+          mbar_expect_tx(&full[stage], kStageBytes);  // own X tile + both W halves
           tma_load_2d(a, &map_x, &full[stage], kb * kBK, m0);
-          tma_load_2d(a + kABytes, &map_w, &full[stage], kb * kBK, n0);
+          if constexpr (kCM == 1) {
+            tma_load_2d(a + kABytes, &map_w, &full[stage], kb * kBK, n0);
+          } else {
+            constexpr int kHalf = kBN / kCM;
+            tma_load_2d_mc(a + kABytes + crank * (kBBytes / kCM), &map_w, &full[stage], kb * kBK,
+                           n0 + static_cast<int>(crank) * kHalf, static_cast<uint16_t>((1u << kCM) - 1));
+          }
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
@@ -179,7 +232,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+      for (int item = tm.first(); item < tm.items(); item += tm.step(), ++it) {
         const int acc = it & 1;
         const uint32_t aphase = (it >> 1) & 1;
         mbar_wait(&tempty[acc], aphase ^ 1);  // the epilogue drained this accumulator
@@ -192,7 +245,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k)  // K=16 per MMA: 32 B along the swizzled row
             umma_bf16(d, umma_desc_sw128(a + k * 32), umma_desc_sw128(b + k * 32), (kb | k) != 0);
-          tc_commit(&empty[stage]);  // frees the stage once these MMAs have read it
+          // frees the stage once these MMAs have read it (in both CTAs of a pair:
+          // each one's producer multicast into the other's stage)
+          if constexpr (kCM == 1) tc_commit(&empty[stage]);
+          else tc_commit_mc(&empty[stage], static_cast<uint16_t>((1u << kCM) - 1));
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
@@ -213,10 +269,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (((args.sync.wait_mask >> g) & 1u) && !spin_until(args.sync, args.sync.pad + g, cs.e)) ok = false;
     ok = __shfl_sync(0xffffffffu, ok, 0);
     int it = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+    for (int item = tm.first(); item < tm.items(); item += tm.step(), ++it) {
       const int acc = it & 1;
       const uint32_t aphase = (it >> 1) & 1;
-      const int m0 = (tile % tiles_m) * kBM, n0 = (tile / tiles_m) * kBN;
+      int m0, n0;
+      tm.coords(item, m0, n0);
       const int row = m0 + q * 32 + lane;
       mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
@@ -253,6 +310,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // every store complete before the end protocol
   }
   __syncthreads();
+  if constexpr (kCM > 1) cluster_sync_all();  // no CTA leaves while its peer may still arrive on its barriers
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols)
@@ -299,19 +357,45 @@ int launch_projector(const void* x, int64_t ldx, const void* w, int64_t ldw, con
   if (projector_check_shape(args.M, args.N, args.K) || args.fan < 1 || args.fan > kMaxProjFan) return 1;
   if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(w)) & 15) return 3;
   if ((ldx * 2) % 16 || (ldw * 2) % 16) return 3;
+  // CTA pairs sharing W tiles through TMA multicast (default), or single CTAs
+  static const int cm = [] {
+    const char* v = std::getenv("HB_PROJ_CLUSTER");
+    return (v && v[0] == '1') ? 1 : 2;
+  }();
   CUtensorMap mx{}, mw{};
   // M == 0: this GPU projects no rows but still takes part in the launch protocol
-  if (args.M > 0 && (!make_map(&mx, x, args.M, args.K, ldx, kBM) || !make_map(&mw, w, args.N, args.K, ldw, kBN)))
+  if (args.M > 0 && (!make_map(&mx, x, args.M, args.K, ldx, kBM) || !make_map(&mw, w, args.N, args.K, ldw, kBN / cm)))
     return 4;
   static bool attr = [] {
-    cudaFuncSetAttribute(projector_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(projector_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(kSmemBytes));
+    cudaFuncSetAttribute(projector_gemm_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(kSmemBytes));
+    cudaFuncSetAttribute(projector_gemm_kernel<2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
     return true;
   }();
   (void)attr;
-  const int tiles = ((args.M + kBM - 1) / kBM) * (args.N / kBN);
-  const int grid = tiles < 1 ? 1 : tiles < sm_count ? tiles : sm_count;
-  projector_gemm_kernel<<<grid, kThreads, kSmemBytes, static_cast<cudaStream_t>(stream)>>>(mx, mw, args);
+  const int items = ((args.M + kBM - 1) / kBM + cm - 1) / cm * (args.N / kBN);
+  int grid = items * cm < sm_count ? items * cm : sm_count - sm_count % cm;
+  if (grid < cm) grid = cm;
+  auto st = static_cast<cudaStream_t>(stream);
+  if (cm == 1) {
+    projector_gemm_kernel<1><<<grid, kThreads, kSmemBytes, st>>>(mx, mw, args);
+  } else {
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(grid);
+    lc.blockDim = dim3(kThreads);
+    lc.dynamicSmemBytes = kSmemBytes;
+    lc.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    if (cudaLaunchKernelEx(&lc, projector_gemm_kernel<2>, mx, mw, args) != cudaSuccess) return 5;
+  }
   return cudaGetLastError() == cudaSuccess ? 0 : 5;
 }
 
