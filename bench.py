@@ -48,7 +48,7 @@ def parse():
     ap.add_argument("--threads", type=int, default=0)
     ap.add_argument("--slots", type=int, default=0, help="buffer sets rotated across steps (0=auto)")
     ap.add_argument("--no-clocks", action="store_true", help="skip nvidia-smi sampling")
-    ap.add_argument("--clock-ms", type=int, default=100)
+    ap.add_argument("--clock-ms", type=int, default=50)
     ap.add_argument("--fwd-mode", type=int, default=0, help="forward: 0 auto, 1 pull, 2 push")
     ap.add_argument("--partition", type=int, default=0,
                     help="0 auto, 1 contiguous, 2 interleaved, 3 dynamic, 4 TMA bulk copy")
@@ -312,6 +312,10 @@ def main():
     world_size = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # nvidia-smi takes a while to start sampling: launch it now so the timed
+    # region (often well under a second) is covered by samples
+    sampler = ClockSampler(local_rank, args.clock_ms, not args.no_clocks)
+    sampler.start()
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     if world_size > 1:
@@ -367,8 +371,6 @@ def main():
     if rt.status():
         raise RuntimeError("device flag wait timed out during warm-up")
 
-    sampler = ClockSampler(local_rank, args.clock_ms, not args.no_clocks)
-    sampler.start()
     time.sleep(0.1)
     K = args.steps
     use_graph = not args.no_graph
