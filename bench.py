@@ -55,6 +55,10 @@ def parse():
     ap.add_argument("--no-nccl", action="store_true", help="skip the NCCL comparison leg (N == world)")
     ap.add_argument("--no-graph", action="store_true", help="timed loop: per-op launches instead of CUDA graphs")
     ap.add_argument("--no-overlap", action="store_true", help="skip the boundary || PP-P2P overlap leg (C5)")
+    ap.add_argument("--matrix", default="c2,c3,c4,c5",
+                    help="configs also measured (short) in the same run, so every N of the driver's scaling "
+                         "run records the fan-in / fan-out / CP-splice / non-colocated step ('' = none)")
+    ap.add_argument("--matrix-steps", type=int, default=200)
     return ap.parse_args()
 
 
@@ -148,6 +152,23 @@ def peaks():
         pass
     p["nvl_gbs"] = 770.0  # measured peer copy per direction (B200_PROFILING.md); 900 nominal
     return p
+
+
+def kernel_bound(tm, kind, ms, pk, N):
+    """T* of one kernel = max over GPUs of max(HBM/peak, NVLink ingress/peak); achieved
+    = the critical GPU's binding bytes / measured kernel time (max over ranks)."""
+    best = None
+    for g in range(N):
+        h, n = tm[kind + "_hbm"][g], tm[kind + "_nvl"][g]
+        t_h, t_n = h / (pk["hbm_gbs"] * 1e9), n / (pk["nvl_gbs"] * 1e9)
+        cand = ("nvlink", n, pk["nvl_gbs"], t_n, g) if t_n > t_h else ("hbm", h, pk["hbm_gbs"], t_h, g)
+        if best is None or cand[3] > best[3]:
+            best = cand
+    res, nbytes, peak, tstar, g = best
+    ach = nbytes / (ms * 1e-3) / 1e9 if ms > 0 else 0.0
+    return {"ms": round(ms, 4), "bound": res, "critical_gpu": g, "bytes": nbytes, "achieved_gbs": round(ach, 1),
+            "peak_gbs": peak, "frac": round(ach / peak, 4), "tstar_ms": round(tstar * 1e3, 4),
+            "hbm_bytes_per_gpu": tm[kind + "_hbm"], "nvl_in_bytes_per_gpu": tm[kind + "_nvl"]}
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -434,22 +455,7 @@ def main():
 
     # roofline of the dominant kernel on this GPU (bytes from the index map)
     pk = peaks()
-    def bound(kind, ms):
-        """T* of one kernel = max over GPUs of max(HBM/peak, NVLink ingress/peak); achieved
-        = the critical GPU's binding bytes / measured kernel time (max over ranks)."""
-        best = None
-        for g in range(N):
-            h, n = tm[kind + "_hbm"][g], tm[kind + "_nvl"][g]
-            t_h, t_n = h / (pk["hbm_gbs"] * 1e9), n / (pk["nvl_gbs"] * 1e9)
-            cand = ("nvlink", n, pk["nvl_gbs"], t_n, g) if t_n > t_h else ("hbm", h, pk["hbm_gbs"], t_h, g)
-            if best is None or cand[3] > best[3]:
-                best = cand
-        res, nbytes, peak, tstar, g = best
-        ach = nbytes / (ms * 1e-3) / 1e9 if ms > 0 else 0.0
-        return {"ms": round(ms, 4), "bound": res, "critical_gpu": g, "bytes": nbytes, "achieved_gbs": round(ach, 1),
-                "peak_gbs": peak, "frac": round(ach / peak, 4), "tstar_ms": round(tstar * 1e3, 4),
-                "hbm_bytes_per_gpu": tm[kind + "_hbm"], "nvl_in_bytes_per_gpu": tm[kind + "_nvl"]}
-    fk, bk = bound("fwd", iso_fwd_ms), bound("bwd", iso_bwd_ms)
+    fk, bk = kernel_bound(tm, "fwd", iso_fwd_ms, pk, N), kernel_bound(tm, "bwd", iso_bwd_ms, pk, N)
     dom_is_fwd = iso_fwd_ms >= iso_bwd_ms
     dom = fk if dom_is_fwd else bk
     traffic = None
@@ -491,6 +497,23 @@ def main():
     if N > 1 and cfg.dst.pp > 1 and cfg.src.rank_offset != cfg.dst.rank_offset and not args.no_overlap:
         overlap = run_pp_overlap(args, cfg, plan, rt, r2g, rank, dev, barrier, stream, slots)
 
+    matrix = None
+    names = [c for c in args.matrix.split(",") if c and c != cfg.name]
+    if names and args.scale == 1:
+        matrix = {cfg.name: {"ms_per_step": round(ms_step, 5), "value_gbs": round(value, 2),
+                             "tstar_ms": round(tstar_step, 4), "frac_of_tstar": round(tstar_step / ms_step, 4),
+                             "fwd_ms": fk["ms"], "fwd_tstar_ms": fk["tstar_ms"], "fwd_bound": fk["bound"],
+                             "bwd_ms": bk["ms"], "bwd_tstar_ms": bk["tstar_ms"], "bwd_bound": bk["bound"],
+                             "overlap_with_pp_p2p": overlap}}
+        rt.close()
+        rt = None
+        torch.cuda.synchronize()
+        for name in names:
+            try:
+                matrix[name] = run_matrix_config(args, name, N, rank, dev, barrier, stream, pk)
+            except Exception as exc:  # a diagnostic leg never voids the headline line
+                matrix[name] = {"error": f"{type(exc).__name__}: {exc}"}
+
     cpu = None
     if rank == 0 and N == 1 and not args.no_cpu:
         try:
@@ -520,11 +543,97 @@ def main():
             "clocks": clocks,
             "nccl_comparison": nccl,
             "overlap_with_pp_p2p": overlap,
+            "config_matrix": matrix,
         }
         print(json.dumps(line), flush=True)
-    rt.close()
+    if rt is not None:
+        rt.close()
     if N > 1:
         dist.destroy_process_group()
+
+
+def run_matrix_config(args, name, N, rank, dev, barrier, stream, pk):
+    """Short measurement of another BASELINE config in the same process group: the
+    same CUDA-graph step loop, per-op steady-state times and T* as the headline, at
+    args.matrix_steps steps (inputs rotate over buffer sets larger than L2)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_27678_b200 import bridge as hbb
+    from paper_2605_27678_b200 import configs
+
+    cfg = configs.get(name)
+    plan = hbb.plan_bridge(cfg.edge())
+    sp = make_splice(cfg)
+    r2g = configs.rank_to_gpu(plan.world, N)
+    local = [r for r in range(plan.world) if r2g[r] == rank]
+    tdt = {"bf16": torch.bfloat16, "fp16": torch.float16, "fp32": torch.float32}
+    tm = traffic_model(cfg, N)
+    per_gpu_step = max(f + b for f, b in zip(tm["fwd_hbm"], tm["bwd_hbm"]))
+    slots = max(2, min(8, math.ceil(3 * L2_BYTES / max(per_gpu_step, 1))))
+    rt = hbb.BridgeRuntime(plan, sp, n_gpus=N, my_gpu=rank, rank_to_gpu=r2g, act_dtype=tdt[cfg.act],
+                           grad_in_dtype=tdt[cfg.grad_in], grad_out_dtype=tdt[cfg.grad_out], mb_slots=slots)
+    try:
+        if N > 1:
+            rt.exchange_handles()
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(4321 + rank)
+        for s in range(slots):
+            for r in local:
+                for slot in (hbb.SLOT_SRC_ACT, hbb.SLOT_DST_GRAD, hbb.SLOT_TEXT, hbb.SLOT_SRC_GRAD):
+                    b = rt.buffer(r, slot, s)
+                    if b is None:
+                        continue
+                    if slot == hbb.SLOT_SRC_GRAD:
+                        b.zero_()
+                    else:
+                        b.copy_(torch.randn(b.numel(), generator=gen, device=dev).to(b.dtype))
+        for mb in range(3):
+            rt.forward(mb, stream)
+            rt.backward(mb, cfg.beta, stream)
+        barrier()
+
+        def timed(what, K):
+            for k in range(slots):
+                rt.capture_step(k, cfg.beta, True, stream, what=what)
+            for k in range(slots):
+                rt.replay_step(k, stream, what)
+            barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for i in range(K):
+                rt.replay_step(i % slots, stream, what)
+            b.record(stream)
+            stream.synchronize()
+            t = torch.tensor([a.elapsed_time(b) / K], dtype=torch.float64, device=dev)
+            if N > 1:
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            barrier()
+            return t.item()
+
+        K = max(20, args.matrix_steps)
+        ms_step = timed(1, K)
+        f_ms, b_ms = timed(0, K), timed(2, K)
+        if rt.status():
+            raise RuntimeError("device flag wait timed out")
+        fk, bk = kernel_bound(tm, "fwd", f_ms, pk, N), kernel_bound(tm, "bwd", b_ms, pk, N)
+        fwd_b, bwd_b = payload_bytes(cfg)
+        tstar = fk["tstar_ms"] + bk["tstar_ms"]
+        out = {"workload": cfg.description, "ms_per_step": round(ms_step, 5),
+               "value_gbs": round((fwd_b + bwd_b) / (ms_step * 1e-3) / 1e9, 2),
+               "tokens_per_s": round(cfg.batch * cfg.tokens / (ms_step * 1e-3), 1),
+               "tstar_ms": round(tstar, 4), "frac_of_tstar": round(tstar / ms_step, 4),
+               "fwd_ms": fk["ms"], "fwd_tstar_ms": fk["tstar_ms"], "fwd_bound": fk["bound"],
+               "bwd_ms": bk["ms"], "bwd_tstar_ms": bk["tstar_ms"], "bwd_bound": bk["bound"],
+               "steps": K, "buffer_sets": slots, "rank_to_gpu": r2g}
+        if N > 1 and cfg.dst.pp > 1 and cfg.src.rank_offset != cfg.dst.rank_offset and not args.no_overlap:
+            out["overlap_with_pp_p2p"] = run_pp_overlap(args, cfg, plan, rt, r2g, rank, dev, barrier, stream,
+                                                        slots)
+        return out
+    finally:
+        barrier()
+        rt.close()
+        torch.cuda.synchronize()
 
 
 def _cpu_model():

@@ -182,6 +182,13 @@ int hb_exec_graph_launch(hb_exec* x, int mb_slot, int what, void* cuda_stream);
 int hb_exec_status(hb_exec* x, unsigned* device_error);
 int hb_exec_stats(hb_exec* x, long long* fwd_segments, long long* bwd_segments,
                   long long* fwd_bytes, long long* bwd_elems, long long* launches);
+/* Diagnostics (no reference counterpart): with HB_TRACE=1 in the environment
+ * at hb_exec_create, every boundary launch records per-CTA %globaltimer stamps
+ * (8 x u64 per CTA: entry, arrival resolved, peers confirmed, first chunk
+ * landed, work done, exit, chunks, remote chunks). Copies the last launch of
+ * kind (0 forward, 1 backward) into out[max_ctas x 8]; *n_ctas = CTAs copied
+ * (0 when tracing is off), *grid = that launch's grid. Synchronises. */
+int hb_exec_trace(hb_exec* x, int kind, unsigned long long* out, int max_ctas, int* n_ctas, int* grid);
 
 /* ---- projector GEMM with a boundary epilogue (the
  *      encoder projector of tinymodel.hpp:62) ----------------------------------

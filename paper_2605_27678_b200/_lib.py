@@ -34,7 +34,7 @@ EXPORTS = [
     "hb_exec_open_peers", "hb_exec_buffer", "hb_exec_bind", "hb_exec_forward", "hb_exec_backward",
     "hb_exec_seed_forward_record", "hb_exec_status", "hb_exec_stats", "hb_exec_graph_capture", "hb_projector_gemm",
     "hb_exec_forward_projected", "hb_exec_set_text_embedding",
-    "hb_exec_graph_launch",
+    "hb_exec_graph_launch", "hb_exec_trace",
 ]
 
 
@@ -129,6 +129,7 @@ def _declare(L):
         "hb_projector_gemm": (I, [V, LL, V, LL, V, I, I, I, I, V]),
         "hb_exec_forward_projected": (I, [V, I, V, LL, V, LL, I, I, V]),
         "hb_exec_set_text_embedding": (I, [V, V, LL]),
+        "hb_exec_trace": (I, [V, I, V, I, P(I), P(I)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name, None)

@@ -374,6 +374,17 @@ class BridgeRuntime:
         keys = ["fwd_segments", "bwd_segments", "fwd_bytes", "bwd_elems", "launches"]
         return dict(zip(keys, (x.value for x in v)))
 
+    def trace(self, kind: int):
+        """HB_TRACE=1 diagnostics: per-CTA stamps of the last launch of `kind`
+        (0 fwd, 1 bwd) as a [ctas x 8] uint64 numpy array (empty when off)."""
+        import numpy as np
+
+        grid, n = ctypes.c_int(), ctypes.c_int()
+        check(lib().hb_exec_trace(self._h, kind, None, 0, ctypes.byref(n), ctypes.byref(grid)))
+        out = np.zeros((max(grid.value, 1), 8), dtype=np.uint64)
+        check(lib().hb_exec_trace(self._h, kind, out.ctypes.data, grid.value, ctypes.byref(n), ctypes.byref(grid)))
+        return out[:n.value]
+
     def close(self):
         h = getattr(self, "_h", None)
         if h and _lib._lib is not None:

@@ -423,6 +423,14 @@ int hb_exec_stats(hb_exec* x, long long* fs, long long* bs, long long* fb, long 
   });
 }
 
+int hb_exec_trace(hb_exec* x, int kind, unsigned long long* out, int max_ctas, int* n_ctas, int* grid) {
+  return guard([&] {
+    need(x, "exec");
+    const int n = x->x->read_trace(kind, out, max_ctas, grid);
+    if (n_ctas) *n_ctas = n;
+  });
+}
+
 int hb_exec_set_text_embedding(hb_exec* x, const void* table, long long vocab) {
   return guard([&] {
     need(x, "exec");

@@ -114,6 +114,11 @@ Exec::Exec(const bridge::BridgePlan& plan, const index::SpliceSpec* splice, int 
   }
   ck(cudaMalloc(&ctr_, kNumKinds * dev::kCtrBytes), "cudaMalloc(ctr)");
   ck(cudaMemset(ctr_, 0, kNumKinds * dev::kCtrBytes), "cudaMemset(ctr)");
+  if (const char* tr = std::getenv("HB_TRACE"); tr && tr[0] == '1') {  // diagnostics: per-CTA timestamps of the last launch of each kind
+    const size_t tb = kNumKinds * static_cast<size_t>(dev::kTraceMaxCtas) * dev::kTraceWords * 8;
+    ck(cudaMalloc(&trace_, tb), "cudaMalloc(trace)");
+    ck(cudaMemset(trace_, 0, tb), "cudaMemset(trace)");
+  }
   peer_base_.assign(n_gpus_, nullptr);
   peer_base_[my_gpu_] = local_base_;
   tables_.resize(cfg.mb_slots);
@@ -144,6 +149,7 @@ Exec::~Exec() {
     if (g != my_gpu_ && peer_base_[g]) cudaIpcCloseMemHandle(peer_base_[g]);
   cudaFree(local_base_);
   cudaFree(ctr_);
+  cudaFree(trace_);
 }
 
 int Exec::slot_dtype(int slot) const {
@@ -236,6 +242,8 @@ uint64_t env_u64(const char* name, uint64_t dflt) {
 // elements per dynamic reduce chunk; TMA stage size (tuning knobs, HB_RED_CHUNK / HB_TMA_CHUNK_KB)
 const uint64_t kDynReduceChunk = env_u64("HB_RED_CHUNK", 0);  // 0: sized per launch (prepare_bwd)
 const int kTmaChunkKiB = static_cast<int>(env_u64("HB_TMA_CHUNK_KB", 32));
+// HB_WAIT_ALL_PEERS=1: a remote chunk waits for every peer, not just its own (A/B knob)
+const bool kWaitAllPeers = env_u64("HB_WAIT_ALL_PEERS", 0) != 0;
 uint64_t pad_to(uint64_t x, uint64_t q) { return (x + q - 1) / q * q; }
 }  // namespace
 
@@ -315,6 +323,8 @@ void Exec::build_partition(const std::vector<uint64_t>& w0, const std::vector<ui
       const double f = frac > 0 ? frac : tr / (tr + tl);
       out->remote_ctas = std::clamp(static_cast<int>(grid * f + 0.5), 1, grid - 1);
     }
+    static const int prefetch = static_cast<int>(env_u64("HB_CLAIM_PREFETCH", 1));  // A/B knob
+    out->prefetch_other = prefetch;
     out->rstatic = std::min<uint32_t>(out->remote_ctas, out->rtotal_chunks);
     out->lstatic = std::min<uint32_t>(grid - out->remote_ctas, out->total_chunks);
     return;
@@ -358,6 +368,11 @@ void Exec::upload_copies(int mb, uint64_t unit, std::vector<uint64_t>* w0s, std:
                  f.dsts[d].off * es;
     c.nbytes = nbytes;
     c.w0 = w;
+    // the peers whose arrival this run waits for: a remote source (pull), remote destinations (push)
+    if (!gather && gpu_of(f.src.rank) != my_gpu_) c.peers |= 1u << gpu_of(f.src.rank);
+    for (const auto& d : f.dsts)
+      if (gpu_of(d.rank) != my_gpu_) c.peers |= 1u << gpu_of(d.rank);
+    if (c.peers && kWaitAllPeers) c.peers = ~0u;
     cs.push_back(c);
     w0s->push_back(w);
     ns->push_back(nbytes);
@@ -435,8 +450,11 @@ void Exec::prepare_bwd() {
       d.w0 = w;
       d.nterms = static_cast<int32_t>(s.terms.size());
       d.term0 = static_cast<int32_t>(terms.size());
-      for (const auto& t : s.terms)
+      for (const auto& t : s.terms) {
         terms.push_back(static_cast<const unsigned char*>(resolve(t.rank, t.slot, mb)) + t.off * es_in);
+        if (gpu_of(t.rank) != my_gpu_) d.peers |= 1u << gpu_of(t.rank);
+      }
+      if (d.peers && kWaitAllPeers) d.peers = ~0u;
       rs.push_back(d);
       w0s.push_back(w);
       ns.push_back(s.n);
@@ -498,6 +516,7 @@ dev::SyncArgs Exec::make_sync_args(int kind, bool push) const {
       if ((peers >> g) & 1u) s.peer_pad[g] = reinterpret_cast<uint32_t*>(peer_base_[g]) + pad_off;
   }
   s.timeout_cycles = static_cast<uint64_t>(cfg_.timeout_s * clock_khz_ * 1e3);
+  if (trace_) s.trace = trace_ + static_cast<size_t>(kind) * dev::kTraceMaxCtas * dev::kTraceWords;
   return s;
 }
 
@@ -633,6 +652,17 @@ void Exec::set_text_embedding(const void* table, int64_t vocab) {
   embed_table_ = static_cast<const unsigned char*>(table);
   embed_vocab_ = vocab;
   dirty_fwd_ = true;
+}
+
+int Exec::read_trace(int kind, unsigned long long* out, int max_ctas, int* grid) const {
+  if (kind < 0 || kind >= kNumKinds) raise(ErrorCode::InvalidArgument, "trace kind out of range");
+  const int g = kind == kFwdKind ? fwd_part_.grid : kind == kBwdKind ? bwd_part_.grid : 0;
+  if (grid) *grid = g;
+  if (!trace_ || !out) return 0;
+  const int n = std::min({g, max_ctas, dev::kTraceMaxCtas});
+  ck(cudaMemcpy(out, trace_ + static_cast<size_t>(kind) * dev::kTraceMaxCtas * dev::kTraceWords,
+                static_cast<size_t>(n) * dev::kTraceWords * 8, cudaMemcpyDeviceToHost), "read trace");
+  return n;
 }
 
 uint32_t Exec::device_error() const {

@@ -81,6 +81,9 @@ class Exec {
   void graph_capture(int mb_slot, int what, float beta, void* stream);
   void graph_launch(int mb_slot, int what, void* stream);
   uint32_t device_error() const;  // synchronises
+  // HB_TRACE=1 diagnostics: copies the last launch of `kind`'s per-CTA stamps
+  // (dev::kTraceWords u64 each) into out; returns CTAs copied (0: tracing off).
+  int read_trace(int kind, unsigned long long* out, int max_ctas, int* grid) const;
 
   const index::IndexMap& map() const { return map_; }
   int local_fwd_segments() const { return static_cast<int>(fwd_local_.size()); }
@@ -160,9 +163,10 @@ class Exec {
     int remote_ctas = 0;
     uint32_t lstatic = 0, rstatic = 0;
     int ring = 1;
+    int prefetch_other = 1;
     dev::Partition dev() const {
       return {first_seg, per_cta, mode, total_chunks, chunk, chunks, rtotal_chunks, rchunks, remote_ctas,
-              lstatic, rstatic, ring};
+              lstatic, rstatic, ring, prefetch_other};
     }
   };
   DevPartition fwd_part_, bwd_part_;
@@ -177,6 +181,7 @@ class Exec {
                        int mode, uint64_t unit, DevPartition* out);
   bool dirty_fwd_ = true, dirty_bwd_ = true;
   uint32_t* ctr_ = nullptr;  // device counters
+  unsigned long long* trace_ = nullptr;  // HB_TRACE diagnostics
   dev::SyncArgs sync_fwd_{}, sync_bwd_{}, sync_proj_{};
   int clock_khz_ = 2000000;
   int sm_count_ = 0;

@@ -56,62 +56,71 @@ constexpr uint32_t kNoChunk = 0xffffffffu;
 
 // Work queues (dynamic / TMA partitions). One thread per CTA drives them.
 // A claim is issued (atomic in flight) before the current chunk is processed
-// and resolved after it, so the claim round trip overlaps the copy.
+// and resolved after it, so the claim round trip overlaps the copy. Once the
+// current queue is within one grid of its end, the first claim of the other
+// queue is started too, so the switch costs no extra round trip (every CTA
+// still claims each non-empty queue until exactly one claim fails there).
 struct Claimer {
   int q;           // current queue: 1 remote, 0 local
   int passes;      // queues finished
   uint32_t first;  // static first chunk of the home queue (kNoChunk: none)
-  unsigned long long pre;  // raw value of the claim in flight (valid if has_pre)
-  int pre_q;
-  bool has_pre;
+  unsigned long long pre[2];  // raw value of the claim in flight per queue (valid if has[q])
+  bool has[2];
 
+  __device__ static uint32_t total_of(const Partition& p, int qq) { return qq ? p.rtotal_chunks : p.total_chunks; }
   __device__ void init(const Partition& p) {
     const int b = static_cast<int>(blockIdx.x);
     q = b < p.remote_ctas ? 1 : 0;
     passes = 0;
-    has_pre = false;
+    has[0] = has[1] = false;
     const uint32_t idx = q ? static_cast<uint32_t>(b) : static_cast<uint32_t>(b - p.remote_ctas);
     first = idx < (q ? p.rstatic : p.lstatic) ? idx : kNoChunk;
-    if ((q ? p.rtotal_chunks : p.total_chunks) == 0) advance_queue(p);
+    if (total_of(p, q) == 0) advance_queue(p);
   }
   __device__ void advance_queue(const Partition& p) {  // next non-empty queue, or done
     while (++passes < 2) {
       q ^= 1;
-      if ((q ? p.rtotal_chunks : p.total_chunks) != 0) return;
+      if (total_of(p, q) != 0) return;
     }
   }
   __device__ bool done() const { return passes >= 2; }
-  __device__ void issue(const SyncArgs& s) {  // start a claim in the current queue
-    pre = atomicAdd(s.queue + q * (kCtrLine / 2), 1ull);
-    pre_q = q;
-    has_pre = true;
+  __device__ void claim(const SyncArgs& s, int qq) {
+    pre[qq] = atomicAdd(s.queue + qq * (kCtrLine / 2), 1ull);
+    has[qq] = true;
+  }
+  // Start the claim after chunk `c` of the current queue (kNoChunk: none held)
+  // and, near the queue's end, the other queue's first claim.
+  __device__ void issue(const Partition& p, const SyncArgs& s, uint32_t c) {
+    claim(s, q);
+    const int o = q ^ 1;
+    if (p.prefetch_other && passes == 0 && !has[o] && total_of(p, o) != 0 &&
+        (c == kNoChunk || static_cast<unsigned long long>(c) + gridDim.x >= total_of(p, q)))
+      claim(s, o);
   }
   __device__ uint32_t resolve(const Partition& p, uint32_t e, unsigned long long raw, int qq) const {
-    const uint32_t total = qq ? p.rtotal_chunks : p.total_chunks;
+    const uint32_t total = total_of(p, qq);
     const uint32_t stat = qq ? p.rstatic : p.lstatic;
     const unsigned long long adv = static_cast<unsigned long long>(total - stat) + gridDim.x;
     const unsigned long long idx = raw - static_cast<unsigned long long>(e - 1) * adv + stat;
     return idx < total ? static_cast<uint32_t>(idx) : kNoChunk;
   }
   // Next chunk (kNoChunk: this CTA is done); *remote = its queue. Consumes the
-  // claim in flight, claims synchronously across a queue switch, and starts
-  // the following claim.
+  // claims in flight (claiming synchronously only if none is), and starts the
+  // following claim.
   __device__ uint32_t next(const Partition& p, const SyncArgs& s, uint32_t e, int* remote) {
-    uint32_t c = kNoChunk;
-    if (has_pre) {
-      has_pre = false;
-      c = resolve(p, e, pre, pre_q);
-      if (c == kNoChunk) advance_queue(p);
-    }
-    while (c == kNoChunk && !done()) {
-      issue(s);
-      has_pre = false;
-      c = resolve(p, e, pre, pre_q);
-      if (c == kNoChunk) advance_queue(p);
+    while (!done()) {
+      if (!has[q]) claim(s, q);
+      has[q] = false;
+      const uint32_t c = resolve(p, e, pre[q], q);
+      if (c != kNoChunk) {
+        *remote = q;
+        issue(p, s, c);
+        return c;
+      }
+      advance_queue(p);
     }
     *remote = q;
-    if (c != kNoChunk) issue(s);
-    return c;
+    return kNoChunk;
   }
 };
 
@@ -138,49 +147,70 @@ __device__ __forceinline__ void run_shares(const S* __restrict__ segs, int nseg,
   __shared__ CtaSync cs;
   __shared__ uint32_t cur;  // chunk being processed (kNoChunk: none)
   __shared__ int cur_remote;
+  __shared__ uint2 cur_t;   // its (segment, chunk within segment)
   unsigned long long arr = 0;
   if (blockIdx.x == 0 && threadIdx.x < 32) {
     post_peers_warp(sync, 0);
     __syncwarp();
   }
-  if (threadIdx.x == 0) arr = cta_arrive_issue(sync);
+  if (threadIdx.x == 0) {
+    trace_at(sync, kTrEntry);
+    arr = cta_arrive_issue(sync);
+  }
   if constexpr (MODE == kPartDynamic) {
     Claimer cl;
     if (threadIdx.x == 0) {
       cl.init(part);
       cur = cl.done() ? kNoChunk : cl.first;
       cur_remote = cl.q;
-      if (!cl.done()) cl.issue(sync);  // the claim after the static chunk, in flight
-      if (cur != kNoChunk && cl.q == 1) {  // a remote first chunk needs the peers first
-        cta_arrive_finish(sync, cs, arr);
-        arr = ~0ull;
-        sync_wait_lane(sync, cs);
+      if (!cl.done()) cl.issue(part, sync, cl.first);  // the claim after the static chunk, in flight
+      if (cur != kNoChunk) {
+        cur_t = (cl.q ? part.rchunks : part.chunks)[cur];
+        if (cl.q == 1) {  // a remote first chunk needs its peers first
+          cta_arrive_finish(sync, cs, arr);
+          arr = ~0ull;
+          sync_wait_peers(sync, cs, segs[cur_t.x].peers);
+        }
       }
     }
     __syncthreads();
     bool first = true;
+    uint32_t nch = 0, nrem = 0;
     while (true) {
       const uint32_t c = cur;
       // a remote chunk after a timed-out wait is claimed but not executed
       if (c != kNoChunk && (!cur_remote || cs.ok)) {
-        const uint2 t = (cur_remote ? part.rchunks : part.chunks)[c];
+        const uint2 t = cur_t;
         const S sg = segs[t.x];
         const uint64_t a = static_cast<uint64_t>(t.y) * part.chunk, e = a + part.chunk, n = len(sg);
         body(sg, a, e < n ? e : n, cur_remote != 0);
+        ++nch;
+        nrem += cur_remote != 0;
       }
       __syncthreads();
       if (threadIdx.x == 0) {
+        if (first) trace_at(sync, kTrFirst);
         if (first && arr != ~0ull) cta_arrive_finish(sync, cs, arr);
         first = false;
         int rq = 0;
-        cur = cl.next(part, sync, cs.e, &rq);
+        const uint32_t nc = cl.next(part, sync, cs.e, &rq);
+        if (nc != kNoChunk) {
+          cur_t = (rq ? part.rchunks : part.chunks)[nc];
+          if (rq) sync_wait_peers(sync, cs, segs[cur_t.x].peers);
+        }
+        cur = nc;
         cur_remote = rq;
-        if (cur != kNoChunk && rq) sync_wait_lane(sync, cs);
       }
       __syncthreads();
       if (cur == kNoChunk) break;
     }
-    if (threadIdx.x == 0) launch_end_lane(sync, cs);
+    if (threadIdx.x == 0) {
+      trace_at(sync, kTrDone);
+      launch_end_lane(sync, cs);
+      trace_at(sync, kTrExit);
+      trace_val(sync, kTrChunks, nch);
+      trace_val(sync, kTrRemote, nrem);
+    }
   } else {
     if (threadIdx.x == 0) {
       cta_arrive_finish(sync, cs, arr);
@@ -362,6 +392,7 @@ __global__ void __launch_bounds__(32) copy_segments_tma_kernel(const CopySeg* __
     __syncwarp();
   }
   if (threadIdx.x != 0) return;  // one issuing lane; the rest of the warp has nothing to do
+  trace_at(sync, kTrEntry);
   const unsigned long long arr = cta_arrive_issue(sync);
   for (int i = 0; i < kTmaStages; ++i) mbar_init(&full[i]);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -369,12 +400,12 @@ __global__ void __launch_bounds__(32) copy_segments_tma_kernel(const CopySeg* __
   uint32_t pend_seg[kTmaStages];
   uint32_t pend_bytes[kTmaStages];
   uint64_t pend_off[kTmaStages];
-  uint32_t issued = 0;
+  uint32_t issued = 0, nremote = 0;
   bool more = true, arrived = false;
   Claimer cl;
   cl.init(part);
   bool use_first = !cl.done();
-  if (!cl.done()) cl.issue(sync);  // the claim after the static chunk, in flight
+  if (!cl.done()) cl.issue(part, sync, cl.first);  // the claim after the static chunk, in flight
   auto arrive = [&]() {
     if (!arrived) {
       cta_arrive_finish(sync, cs, arr);
@@ -398,12 +429,12 @@ __global__ void __launch_bounds__(32) copy_segments_tma_kernel(const CopySeg* __
         }
       }
       if (c == kNoChunk) continue;
-      if (rq == 1) {
-        arrive();
-        if (!sync_wait_lane(sync, cs)) continue;  // timed out: claimed, not executed
-      }
       const uint2 t = (rq ? part.rchunks : part.chunks)[c];
       const CopySeg& sg = segs[t.x];
+      if (rq == 1) {
+        arrive();
+        if (!sync_wait_peers(sync, cs, sg.peers)) continue;  // timed out: claimed, not executed
+      }
       const uint64_t a = static_cast<uint64_t>(t.y) * part.chunk;
       const uint64_t e = a + part.chunk < sg.nbytes ? a + part.chunk : sg.nbytes;
       const uint32_t bytes = static_cast<uint32_t>(e - a);
@@ -435,6 +466,7 @@ __global__ void __launch_bounds__(32) copy_segments_tma_kernel(const CopySeg* __
       pend_off[st] = a;
       pend_bytes[st] = bytes;
       ++issued;
+      nremote += rq;
       return;
     }
   };
@@ -442,6 +474,7 @@ __global__ void __launch_bounds__(32) copy_segments_tma_kernel(const CopySeg* __
   for (uint32_t k = 0; k < issued; ++k) {
     const int st = k % kTmaStages;
     mbar_wait(&full[st], (k / kTmaStages) & 1u);
+    if (k == 0) trace_at(sync, kTrFirst);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     // one bulk group per chunk: a store to every destination of the run
     const CopySeg& sg = segs[pend_seg[st]];
@@ -453,9 +486,17 @@ __global__ void __launch_bounds__(32) copy_segments_tma_kernel(const CopySeg* __
       issue();              // chunk k-1+kTmaStages reuses stage (k-1) % kTmaStages
     }
   }
-  bulk_wait_all();
+  // Push mode publishes "writes done" to peers: the stores must be complete.
+  // Otherwise only the stage reads must be (the grid's completion makes the
+  // stores visible to the stream's next kernel, as a TMA-store epilogue does).
+  if (sync.end_sync) bulk_wait_all();
+  else bulk_wait_read<0>();
   arrive();
+  trace_at(sync, kTrDone);
   launch_end_lane(sync, cs);
+  trace_at(sync, kTrExit);
+  trace_val(sync, kTrChunks, issued);
+  trace_val(sync, kTrRemote, nremote);
 }
 
 // ---- reduction ---------------------------------------------------------------

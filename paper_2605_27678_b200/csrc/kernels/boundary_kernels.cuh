@@ -37,6 +37,8 @@ struct CopySeg {
   uint32_t row_bytes;  // gather runs only
   const int32_t* ids;  // nullptr: contiguous run
   int64_t vocab;
+  uint32_t peers;      // GPUs this run reads (pull) or writes (push) besides this one
+  uint32_t pad_;
 };
 constexpr uint32_t kErrTimeout = 1, kErrBadId = 2;
 
@@ -48,6 +50,8 @@ struct ReduceSeg {
   uint64_t w0;
   int32_t nterms;
   int32_t term0;
+  uint32_t peers;  // GPUs holding this segment's terms besides this one
+  uint32_t pad_;
 };
 
 // How a launch's work space is split over CTAs.
@@ -76,6 +80,7 @@ struct Partition {
   uint32_t lstatic;          // = min(grid - remote_ctas, total_chunks)
   uint32_t rstatic;          // = min(remote_ctas, rtotal_chunks)
   int ring;                  // reduce: stage remote single-term chunks through the TMA ring
+  int prefetch_other;        // start the other queue's first claim near the current queue's end
 };
 
 // Cross-GPU epoch barrier over peer-mapped flag words. Every GPU of an exec
@@ -109,7 +114,14 @@ struct SyncArgs {
   int end_sync;                   // push mode: also post/wait "writes done" (pad[32+g]) before exit
   int my_gpu;
   uint64_t timeout_cycles;
+  // Diagnostics (HB_TRACE=1; nullptr otherwise): per CTA kTraceWords u64 of
+  // %globaltimer stamps written by the CTA's driving thread — entry, arrival
+  // resolved, peers confirmed, first chunk landed, work done, exit — and the
+  // CTA's chunk counts (total, remote).
+  unsigned long long* trace;
 };
+constexpr int kTraceWords = 8;
+constexpr int kTraceMaxCtas = 4096;
 constexpr int kCtrBytes = 4 * 128;  // arrive | queues | fin | err lines
 
 struct LaunchCfg {

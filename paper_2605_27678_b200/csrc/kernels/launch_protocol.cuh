@@ -28,11 +28,27 @@ __device__ __forceinline__ void post_peers_warp(const SyncArgs& s, int word) {
   }
 }
 
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Trace stamp k of this CTA (no-op unless HB_TRACE set SyncArgs::trace).
+__device__ __forceinline__ void trace_at(const SyncArgs& s, int k) {
+  if (s.trace && blockIdx.x < kTraceMaxCtas) s.trace[blockIdx.x * kTraceWords + k] = global_ns();
+}
+__device__ __forceinline__ void trace_val(const SyncArgs& s, int k, unsigned long long v) {
+  if (s.trace && blockIdx.x < kTraceMaxCtas) s.trace[blockIdx.x * kTraceWords + k] = v;
+}
+enum TraceSlot : int { kTrEntry = 0, kTrArrived = 1, kTrPeers = 2, kTrFirst = 3, kTrDone = 4, kTrExit = 5,
+                       kTrChunks = 6, kTrRemote = 7 };
+
 // Per-CTA view of the launch (shared memory).
 struct CtaSync {
-  uint32_t e;  // this launch's epoch (valid after cta_arrive_finish)
-  int waited;  // peers' arrival at e confirmed
-  int ok;      // no timeout
+  uint32_t e;     // this launch's epoch (valid after cta_arrive_finish)
+  uint32_t have;  // GPUs whose arrival at e this CTA has confirmed
+  int ok;         // no timeout
 };
 
 // Bounded spin until *flag >= e; false on timeout (error word set).
@@ -56,23 +72,34 @@ __device__ __forceinline__ unsigned long long cta_arrive_issue(const SyncArgs& s
 }
 
 __device__ __forceinline__ void cta_arrive_finish(const SyncArgs& s, CtaSync& cs, unsigned long long old) {
+  trace_at(s, kTrArrived);
   cs.e = static_cast<uint32_t>(old >> 32) + 1;
-  cs.waited = (s.wait_mask == 0);
+  cs.have = 0;
   cs.ok = 1;
   // last CTA in: advance the epoch, zero the arrivals (every CTA of this
   // launch has read the word; the next launch starts after this one ends)
   if ((old & 0xffffffffull) == gridDim.x - 1) atomicAdd(s.arrive, (1ull << 32) - gridDim.x);
 }
 
-// Wait (once per CTA, one thread) until every peer started op e: after that
-// the peers' buffers of this op may be read (pull) or written (push).
-__device__ bool sync_wait_lane(const SyncArgs& s, CtaSync& cs) {
-  if (!cs.waited) {
-    for (int g = 0; g < kMaxGpus; ++g)
-      if (((s.wait_mask >> g) & 1u) && !spin_until(s, s.pad + g, cs.e)) cs.ok = 0;
-    cs.waited = 1;
+// Wait (one thread per CTA) until every GPU in `peers` started op e: after
+// that those peers' buffers of this op may be read (pull) or written (push).
+// Each peer is confirmed once per CTA, so a CTA whose chunk reads only early
+// peers proceeds while a late peer is still launching.
+__device__ bool sync_wait_peers(const SyncArgs& s, CtaSync& cs, uint32_t peers) {
+  uint32_t need = peers & s.wait_mask & ~cs.have;
+  if (need) {
+    while (need) {
+      const int g = __ffs(need) - 1;
+      need &= need - 1;
+      if (!spin_until(s, s.pad + g, cs.e)) cs.ok = 0;
+    }
+    cs.have |= peers & s.wait_mask;
+    if (cs.have == s.wait_mask) trace_at(s, kTrPeers);
   }
   return cs.ok != 0;
+}
+__device__ __forceinline__ bool sync_wait_lane(const SyncArgs& s, CtaSync& cs) {
+  return sync_wait_peers(s, cs, s.wait_mask);
 }
 
 // End of a launch, one thread per CTA. CTA 0 confirms every peer started op e,
