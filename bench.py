@@ -54,6 +54,8 @@ def parse():
                     help="0 auto, 1 contiguous, 2 interleaved, 3 dynamic, 4 TMA bulk copy")
     ap.add_argument("--no-nccl", action="store_true", help="skip the NCCL comparison leg (N == world)")
     ap.add_argument("--no-graph", action="store_true", help="timed loop: per-op launches instead of CUDA graphs")
+    ap.add_argument("--graph-per-step", action="store_true",
+                    help="timed loop: one graph launch per step instead of one per cycle of buffer sets")
     ap.add_argument("--no-overlap", action="store_true", help="skip the boundary || PP-P2P overlap leg (C5)")
     ap.add_argument("--matrix", default="c2,c3,c4,c5",
                     help="configs also measured (short) in the same run, so every N of the driver's scaling "
@@ -352,7 +354,8 @@ def main():
     tm = traffic_model(cfg, N)
     # rank-independent (every process must allocate the same number of buffer sets)
     per_gpu_step = max(f + b for f, b in zip(tm["fwd_hbm"], tm["bwd_hbm"]))
-    slots = args.slots or max(1, min(8, math.ceil(3 * L2_BYTES / max(per_gpu_step, 1))))
+    # >= 3x L2 of inputs across the rotation, and >= 4 sets so one cycle graph covers 4+ steps
+    slots = args.slots or max(4, min(8, math.ceil(3 * L2_BYTES / max(per_gpu_step, 1))))
     if not args.no_e2e:
         slots = max(slots, 2)  # the pipelined e2e leg alternates two buffer sets
 
@@ -395,9 +398,13 @@ def main():
     time.sleep(0.1)
     K = args.steps
     use_graph = not args.no_graph
+    cycle = use_graph and slots > 1 and not args.graph_per_step
     if use_graph:  # one CUDA graph per buffer set: forward + backward(beta)
         for k in range(slots):
             rt.capture_step(k, cfg.beta, True, stream)
+        if cycle:  # and one graph of a whole cycle: a step on every buffer set in turn
+            rt.capture_step(0, cfg.beta, True, stream, what=rt.GRAPH_CYCLE)
+            rt.replay_step(0, stream, rt.GRAPH_CYCLE)
         for k in range(slots):
             rt.replay_step(k, stream)
         barrier()
@@ -406,13 +413,20 @@ def main():
     sampler.mark(True)
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0.record(stream)
-    for i in range(K):
-        if use_graph:
-            rt.replay_step(mb % slots, stream)
-        else:
-            rt.forward(mb, stream)
-            rt.backward(mb, cfg.beta, stream)
-        mb += 1
+    if cycle:  # exactly K steps: K // slots cycles, then the remainder one step at a time
+        for _ in range(K // slots):
+            rt.replay_step(0, stream, rt.GRAPH_CYCLE)
+        for i in range(K % slots):
+            rt.replay_step(i, stream)
+        mb += K
+    else:
+        for i in range(K):
+            if use_graph:
+                rt.replay_step(mb % slots, stream)
+            else:
+                rt.forward(mb, stream)
+                rt.backward(mb, cfg.beta, stream)
+            mb += 1
     t1.record(stream)
     stream.synchronize()
     sampler.mark(False)
@@ -448,6 +462,24 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     iso_fwd_ms, iso_bwd_ms = t.tolist()
     barrier()
+    ms_graph_per_step = None
+    if cycle:  # the same steps with one graph launch per step (host launch cost per step)
+        for k in range(slots):
+            rt.capture_step(k, cfg.beta, True, stream)
+        for k in range(slots):
+            rt.replay_step(k, stream)
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for i in range(K2):
+            rt.replay_step(i % slots, stream)
+        b.record(stream)
+        stream.synchronize()
+        t = torch.tensor([a.elapsed_time(b) / K2], dtype=torch.float64, device=dev)
+        if N > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_graph_per_step = round(t.item(), 5)
+        barrier()
 
     fwd_b, bwd_b = payload_bytes(cfg)
     value = (fwd_b + bwd_b) / (ms_step * 1e-3) / 1e9
@@ -534,7 +566,10 @@ def main():
                        "tokens_per_sample": cfg.tokens, "hidden": cfg.hidden,
                        "logical_ranks": plan.world, "rank_to_gpu": r2g,
                        "grad_in": cfg.grad_in, "grad_out": cfg.grad_out, "beta": cfg.beta,
-                       "launch": "one CUDA graph (fwd+bwd) per step" if use_graph else "per-op C-ABI launches",
+                       "launch": (f"one CUDA graph per cycle of {slots} steps (fwd+bwd on each buffer set in "
+                                  f"turn; K % {slots} steps as one graph each)") if cycle else
+                                 ("one CUDA graph (fwd+bwd) per step" if use_graph else "per-op C-ABI launches"),
+                       "ms_per_step_one_graph_per_step": ms_graph_per_step,
                        "l2": f"inputs rotate over {slots} buffer set(s); per-GPU bytes per step "
                              f"{per_gpu_step / 1e6:.1f} MB x {slots} sets > 126 MB L2"},
             "per_gpu_gbs": round(value / N, 2), "tokens_per_s": round(tokens_s, 1),
@@ -570,7 +605,7 @@ def run_matrix_config(args, name, N, rank, dev, barrier, stream, pk):
     tdt = {"bf16": torch.bfloat16, "fp16": torch.float16, "fp32": torch.float32}
     tm = traffic_model(cfg, N)
     per_gpu_step = max(f + b for f, b in zip(tm["fwd_hbm"], tm["bwd_hbm"]))
-    slots = max(2, min(8, math.ceil(3 * L2_BYTES / max(per_gpu_step, 1))))
+    slots = max(4, min(8, math.ceil(3 * L2_BYTES / max(per_gpu_step, 1))))
     rt = hbb.BridgeRuntime(plan, sp, n_gpus=N, my_gpu=rank, rank_to_gpu=r2g, act_dtype=tdt[cfg.act],
                            grad_in_dtype=tdt[cfg.grad_in], grad_out_dtype=tdt[cfg.grad_out], mb_slots=slots)
     try:
@@ -612,7 +647,23 @@ def run_matrix_config(args, name, N, rank, dev, barrier, stream, pk):
             return t.item()
 
         K = max(20, args.matrix_steps)
-        ms_step = timed(1, K)
+        ms_step_pg = timed(1, K)  # one graph launch per step
+        ms_step = ms_step_pg
+        if not args.graph_per_step:  # one graph launch per cycle of buffer sets (the headline's loop)
+            rt.capture_step(0, cfg.beta, True, stream, what=rt.GRAPH_CYCLE)
+            rt.replay_step(0, stream, rt.GRAPH_CYCLE)
+            barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(max(1, K // slots)):
+                rt.replay_step(0, stream, rt.GRAPH_CYCLE)
+            b.record(stream)
+            stream.synchronize()
+            t = torch.tensor([a.elapsed_time(b) / (max(1, K // slots) * slots)], dtype=torch.float64, device=dev)
+            if N > 1:
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            barrier()
+            ms_step = t.item()
         f_ms, b_ms = timed(0, K), timed(2, K)
         if rt.status():
             raise RuntimeError("device flag wait timed out")
@@ -625,6 +676,7 @@ def run_matrix_config(args, name, N, rank, dev, barrier, stream, pk):
                "tstar_ms": round(tstar, 4), "frac_of_tstar": round(tstar / ms_step, 4),
                "fwd_ms": fk["ms"], "fwd_tstar_ms": fk["tstar_ms"], "fwd_bound": fk["bound"],
                "bwd_ms": bk["ms"], "bwd_tstar_ms": bk["tstar_ms"], "bwd_bound": bk["bound"],
+               "ms_per_step_one_graph_per_step": round(ms_step_pg, 5),
                "steps": K, "buffer_sets": slots, "rank_to_gpu": r2g}
         if N > 1 and cfg.dst.pp > 1 and cfg.src.rank_offset != cfg.dst.rank_offset and not args.no_overlap:
             out["overlap_with_pp_p2p"] = run_pp_overlap(args, cfg, plan, rt, r2g, rank, dev, barrier, stream,

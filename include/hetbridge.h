@@ -175,8 +175,9 @@ int hb_exec_seed_forward_record(hb_exec* x, int mb); /* bridge.hpp:165 */
 /* Embedding table [vocab x d_h] (activation dtype, device memory of this GPU). */
 int hb_exec_set_text_embedding(hb_exec* x, const void* table, long long vocab);
 /* CUDA graph of one buffer set's boundary ops; what: 0 forward, 1 forward +
- * backward(beta), 2 backward(beta). One graph launch replays the ops; replays
- * bypass the microbatch records. */
+ * backward(beta), 2 backward(beta), 3 forward + backward(beta) of every buffer
+ * set in order (one launch replays mb_slots steps; mb_slot ignored). One graph
+ * launch replays the ops; replays bypass the microbatch records. */
 int hb_exec_graph_capture(hb_exec* x, int mb_slot, int what, float beta, void* cuda_stream);
 int hb_exec_graph_launch(hb_exec* x, int mb_slot, int what, void* cuda_stream);
 int hb_exec_status(hb_exec* x, unsigned* device_error);

@@ -242,8 +242,11 @@ uint64_t env_u64(const char* name, uint64_t dflt) {
 // elements per dynamic reduce chunk; TMA stage size (tuning knobs, HB_RED_CHUNK / HB_TMA_CHUNK_KB)
 const uint64_t kDynReduceChunk = env_u64("HB_RED_CHUNK", 0);  // 0: sized per launch (prepare_bwd)
 const int kTmaChunkKiB = static_cast<int>(env_u64("HB_TMA_CHUNK_KB", 32));
-// HB_WAIT_ALL_PEERS=1: a remote chunk waits for every peer, not just its own (A/B knob)
-const bool kWaitAllPeers = env_u64("HB_WAIT_ALL_PEERS", 0) != 0;
+// A remote copy chunk waits for every peer's arrival by default; HB_WAIT_ALL_PEERS=0 waits
+// only for the GPUs the chunk touches. Measured at N=4 (one box, A/B): per-peer waits save
+// ~1 us on c4w4 but cost 6 us on c2x4's all-gather (early peers' links fill first, the
+// late peer's share becomes the tail).
+const bool kWaitAllPeers = env_u64("HB_WAIT_ALL_PEERS", 1) != 0;
 uint64_t pad_to(uint64_t x, uint64_t q) { return (x + q - 1) / q * q; }
 }  // namespace
 
@@ -434,6 +437,31 @@ void Exec::prepare_bwd() {
     while (unit < 32768 && total / (2 * unit) >= 2 * grid) unit *= 2;
   }
   const int es_in = dev::dtype_size(cfg_.grad_in_dtype), es_out = dev::dtype_size(cfg_.grad_out_dtype);
+  // Fan-out groups: segments with the same length and the same ordered terms
+  // (the TP replicas of one source shard on this GPU) become one device segment
+  // that reads the terms once and accumulates into each replica (<= kMaxFan).
+  // HB_RED_FAN=0 keeps one segment per accumulator (A/B knob).
+  std::vector<std::vector<size_t>> groups;
+  {
+    static const bool fan = env_u64("HB_RED_FAN", 1) != 0;
+    std::map<std::vector<int64_t>, size_t> open;  // key -> index of its group
+    for (size_t i = 0; i < bwd_local_.size(); ++i) {
+      const auto& sg = bwd_local_[i];
+      std::vector<int64_t> key{static_cast<int64_t>(sg.n)};
+      for (const auto& t : sg.terms) {
+        key.push_back(t.rank);
+        key.push_back(t.slot);
+        key.push_back(static_cast<int64_t>(t.off));
+      }
+      auto it = fan ? open.find(key) : open.end();
+      if (it != open.end() && groups[it->second].size() < static_cast<size_t>(dev::kMaxFan)) {
+        groups[it->second].push_back(i);
+      } else {
+        if (fan) open[key] = groups.size();
+        groups.push_back({i});
+      }
+    }
+  }
   std::vector<uint64_t> w0s, ns;
   for (int mb = 0; mb < cfg_.mb_slots; ++mb) {
     DevTables& T = tables_[mb];
@@ -442,10 +470,15 @@ void Exec::prepare_bwd() {
     uint64_t w = 0;
     w0s.clear();
     ns.clear();
-    for (const auto& s : bwd_local_) {
+    for (const auto& grp : groups) {
+      const auto& s = bwd_local_[grp[0]];
+      auto acc_ptr = [&](size_t k) {
+        const auto& g = bwd_local_[k];
+        return static_cast<unsigned char*>(const_cast<void*>(resolve(g.dst.rank, g.dst.slot, mb))) +
+               g.dst.off * es_out;
+      };
       dev::ReduceSeg d{};
-      d.dst = static_cast<unsigned char*>(const_cast<void*>(resolve(s.dst.rank, s.dst.slot, mb))) +
-              s.dst.off * es_out;
+      d.dst = acc_ptr(grp[0]);
       d.nelem = s.n;
       d.w0 = w;
       d.nterms = static_cast<int32_t>(s.terms.size());
@@ -454,7 +487,9 @@ void Exec::prepare_bwd() {
         terms.push_back(static_cast<const unsigned char*>(resolve(t.rank, t.slot, mb)) + t.off * es_in);
         if (gpu_of(t.rank) != my_gpu_) d.peers |= 1u << gpu_of(t.rank);
       }
-      if (d.peers && kWaitAllPeers) d.peers = ~0u;
+      d.ndst = static_cast<int32_t>(grp.size());
+      d.dst0 = static_cast<int32_t>(terms.size());
+      for (size_t k : grp) terms.push_back(acc_ptr(k));
       rs.push_back(d);
       w0s.push_back(w);
       ns.push_back(s.n);
@@ -477,14 +512,18 @@ void Exec::prepare_bwd() {
   const int bps = cfg_.blocks_per_sm > 0 ? std::min(cfg_.blocks_per_sm, occ) : occ;
   std::vector<char> rem;
   double lb = 0, rb = 0;
-  for (size_t i = 0; i < bwd_local_.size(); ++i) {
+  for (size_t i = 0; i < groups.size(); ++i) {
     bool r = false;
-    for (const auto& t : bwd_local_[i].terms) r |= gpu_of(t.rank) != my_gpu_;
+    for (const auto& t : bwd_local_[groups[i][0]].terms) r |= gpu_of(t.rank) != my_gpu_;
     rem.push_back(r);
-    (r ? rb : lb) += static_cast<double>(ns[i]) * (es_in + 2 * es_out);
+    (r ? rb : lb) += static_cast<double>(ns[i]) * (es_in + 2 * es_out * groups[i].size());
   }
+  bwd_groups_ = static_cast<int>(groups.size());
+  int fan = 0;
+  for (const auto& g : groups) fan |= g.size() > 1;
   build_partition(w0s, ns, rem, lb, rb, sm_count_ * bps, mode, unit, &bwd_part_);
   bwd_part_.ring = static_cast<int>(env_u64("HB_RED_RING", 1));  // A/B knob: 0 = LDG for remote chunks too
+  bwd_part_.fan = fan;
   dirty_bwd_ = false;
 }
 
@@ -530,7 +569,7 @@ void Exec::launch_forward(int mb_slot, void* stream) {
 
 void Exec::launch_backward(int mb_slot, float beta, void* stream) {
   const DevTables& T = tables_[mb_slot];
-  dev::launch_reduce(T.reduce, static_cast<int>(bwd_local_.size()), T.terms, bwd_part_.dev(), cfg_.grad_in_dtype,
+  dev::launch_reduce(T.reduce, bwd_groups_, T.terms, bwd_part_.dev(), cfg_.grad_in_dtype,
                      cfg_.grad_out_dtype, beta, sync_bwd_, {bwd_part_.grid, cfg_.threads}, stream);
   ck(cudaGetLastError(), "reduce_segments launch");
   ++launches_;
@@ -612,7 +651,9 @@ void Exec::backward(int mb, float beta, void* stream) {
 
 void Exec::graph_capture(int mb_slot, int what, float beta, void* stream) {
   if (mb_slot < 0 || mb_slot >= cfg_.mb_slots) raise(ErrorCode::InvalidArgument, "mb slot out of range");
-  if (what < 0 || what > 2) raise(ErrorCode::InvalidArgument, "graph 'what' must be 0 (fwd), 1 (fwd+bwd), 2 (bwd)");
+  if (what < 0 || what > 3)
+    raise(ErrorCode::InvalidArgument, "graph 'what' must be 0 (fwd), 1 (fwd+bwd), 2 (bwd), 3 (a step per buffer set)");
+  if (what == 3) mb_slot = 0;  // the cycle graph is keyed on slot 0
   if (!stream) raise(ErrorCode::InvalidArgument, "graph capture needs a non-default stream");
   if (what != 2) prepare_fwd();
   if (what != 0) prepare_bwd();
@@ -625,8 +666,15 @@ void Exec::graph_capture(int mb_slot, int what, float beta, void* stream) {
   auto st = static_cast<cudaStream_t>(stream);
   const int before = launches_;
   ck(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
-  if (what != 2) launch_forward(mb_slot, stream);
-  if (what != 0) launch_backward(mb_slot, beta, stream);
+  if (what == 3) {  // fwd + bwd of buffer set 0, then 1, ... : one launch replays a full cycle
+    for (int k = 0; k < cfg_.mb_slots; ++k) {
+      launch_forward(k, stream);
+      launch_backward(k, beta, stream);
+    }
+  } else {
+    if (what != 2) launch_forward(mb_slot, stream);
+    if (what != 0) launch_backward(mb_slot, beta, stream);
+  }
   cudaGraph_t g = nullptr;
   ck(cudaStreamEndCapture(st, &g), "cudaStreamEndCapture");
   cudaGraphExec_t ge = nullptr;
@@ -637,7 +685,7 @@ void Exec::graph_capture(int mb_slot, int what, float beta, void* stream) {
 }
 
 void Exec::graph_launch(int mb_slot, int what, void* stream) {
-  auto it = graphs_.find(std::make_pair(mb_slot, what));
+  auto it = graphs_.find(std::make_pair(what == 3 ? 0 : mb_slot, what));
   if (it == graphs_.end()) raise(ErrorCode::InvalidArgument, "no graph captured for this (mb slot, what)");
   ck(cudaGraphLaunch(static_cast<cudaGraphExec_t>(it->second.first), static_cast<cudaStream_t>(stream)),
      "cudaGraphLaunch");

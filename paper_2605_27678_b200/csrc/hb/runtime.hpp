@@ -164,9 +164,10 @@ class Exec {
     uint32_t lstatic = 0, rstatic = 0;
     int ring = 1;
     int prefetch_other = 1;
+    int fan = 0;
     dev::Partition dev() const {
       return {first_seg, per_cta, mode, total_chunks, chunk, chunks, rtotal_chunks, rchunks, remote_ctas,
-              lstatic, rstatic, ring, prefetch_other};
+              lstatic, rstatic, ring, prefetch_other, fan};
     }
   };
   DevPartition fwd_part_, bwd_part_;
@@ -180,6 +181,7 @@ class Exec {
                        const std::vector<char>& remote, double local_bytes, double remote_bytes, int grid,
                        int mode, uint64_t unit, DevPartition* out);
   bool dirty_fwd_ = true, dirty_bwd_ = true;
+  int bwd_groups_ = 0;  // device reduce segments (fan-out groups of bwd_local_)
   uint32_t* ctr_ = nullptr;  // device counters
   unsigned long long* trace_ = nullptr;  // HB_TRACE diagnostics
   dev::SyncArgs sync_fwd_{}, sync_bwd_{}, sync_proj_{};

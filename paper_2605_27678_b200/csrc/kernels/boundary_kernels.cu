@@ -147,7 +147,6 @@ __device__ __forceinline__ void run_shares(const S* __restrict__ segs, int nseg,
   __shared__ CtaSync cs;
   __shared__ uint32_t cur;  // chunk being processed (kNoChunk: none)
   __shared__ int cur_remote;
-  __shared__ uint2 cur_t;   // its (segment, chunk within segment)
   unsigned long long arr = 0;
   if (blockIdx.x == 0 && threadIdx.x < 32) {
     post_peers_warp(sync, 0);
@@ -158,34 +157,40 @@ __device__ __forceinline__ void run_shares(const S* __restrict__ segs, int nseg,
     arr = cta_arrive_issue(sync);
   }
   if constexpr (MODE == kPartDynamic) {
-    Claimer cl;
+    // Claim state lives in shared memory: only thread 0 touches it, between
+    // chunks, and keeping it out of registers across the body avoids spills
+    // in the 64-register reduce loop.
+    __shared__ Claimer cl;
+    __shared__ uint32_t nch, nrem;  // trace counters
     if (threadIdx.x == 0) {
+      nch = nrem = 0;
       cl.init(part);
       cur = cl.done() ? kNoChunk : cl.first;
       cur_remote = cl.q;
       if (!cl.done()) cl.issue(part, sync, cl.first);  // the claim after the static chunk, in flight
-      if (cur != kNoChunk) {
-        cur_t = (cl.q ? part.rchunks : part.chunks)[cur];
-        if (cl.q == 1) {  // a remote first chunk needs its peers first
-          cta_arrive_finish(sync, cs, arr);
-          arr = ~0ull;
-          sync_wait_peers(sync, cs, segs[cur_t.x].peers);
-        }
+      // a remote first chunk needs the peers first (all of them: a per-peer
+      // wait here would put two dependent table loads on thread 0's path
+      // between chunks; measured slower for the gradient return)
+      if (cur != kNoChunk && cl.q == 1) {
+        cta_arrive_finish(sync, cs, arr);
+        arr = ~0ull;
+        sync_wait_lane(sync, cs);
       }
     }
     __syncthreads();
     bool first = true;
-    uint32_t nch = 0, nrem = 0;
     while (true) {
       const uint32_t c = cur;
       // a remote chunk after a timed-out wait is claimed but not executed
       if (c != kNoChunk && (!cur_remote || cs.ok)) {
-        const uint2 t = cur_t;
+        const uint2 t = (cur_remote ? part.rchunks : part.chunks)[c];
         const S sg = segs[t.x];
         const uint64_t a = static_cast<uint64_t>(t.y) * part.chunk, e = a + part.chunk, n = len(sg);
         body(sg, a, e < n ? e : n, cur_remote != 0);
-        ++nch;
-        nrem += cur_remote != 0;
+        if (threadIdx.x == 0 && sync.trace) {
+          ++nch;
+          nrem += cur_remote != 0;
+        }
       }
       __syncthreads();
       if (threadIdx.x == 0) {
@@ -193,13 +198,9 @@ __device__ __forceinline__ void run_shares(const S* __restrict__ segs, int nseg,
         if (first && arr != ~0ull) cta_arrive_finish(sync, cs, arr);
         first = false;
         int rq = 0;
-        const uint32_t nc = cl.next(part, sync, cs.e, &rq);
-        if (nc != kNoChunk) {
-          cur_t = (rq ? part.rchunks : part.chunks)[nc];
-          if (rq) sync_wait_peers(sync, cs, segs[cur_t.x].peers);
-        }
-        cur = nc;
+        cur = cl.next(part, sync, cs.e, &rq);
         cur_remote = rq;
+        if (cur != kNoChunk && rq) sync_wait_lane(sync, cs);
       }
       __syncthreads();
       if (cur == kNoChunk) break;
@@ -725,6 +726,65 @@ __device__ __forceinline__ void reduce_range(TOut* __restrict__ dst, const TIn* 
   }
 }
 
+// reduce_range for a fan-out segment: the terms' sum is formed once per
+// 8-element group and read-modify-written into each of the nd accumulators.
+template <class TIn, class TOut>
+__device__ __forceinline__ void reduce_range_fan(TOut* const* __restrict__ dl, int nd, const TIn* const* __restrict__ tp,
+                                              int nterms, uint64_t a, uint64_t b, float beta) {
+  uint64_t align = 0;
+  for (int d = 0; d < nd; ++d) align |= reinterpret_cast<uint64_t>(dl[d] + a);
+  for (int t = 0; t < nterms; ++t) align |= reinterpret_cast<uint64_t>(tp[t] + a);
+  uint64_t i = a;
+  if ((align & 15) == 0 && nterms > 0) {
+    const uint64_t vend = a + ((b - a) & ~uint64_t(7));
+    const uint64_t step = static_cast<uint64_t>(blockDim.x) * 8;
+    for (i = a + threadIdx.x * 8; i + step < vend; i += 2 * step) {
+      float acc0[8], acc1[8];
+      sum_terms8x2(tp, nterms, i, step, acc0, acc1);
+      for (int d = 0; d < nd; ++d) {
+        TOut* dst = dl[d];
+        float o0[8], o1[8];
+        if (beta != 0.0f) {
+          load8_coherent(dst + i, o0);
+          load8_coherent(dst + i + step, o1);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            o0[k] = fmaf(beta, o0[k], acc0[k]);
+            o1[k] = fmaf(beta, o1[k], acc1[k]);
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            o0[k] = acc0[k];
+            o1[k] = acc1[k];
+          }
+        }
+        store8(dst + i, o0);
+        store8(dst + i + step, o1);
+      }
+    }
+    if (i < vend) {
+      float acc[8];
+      sum_terms8(tp, nterms, i, acc);
+      for (int d = 0; d < nd; ++d) {
+        float o[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) o[k] = acc[k];
+        finish8(dl[d], i, beta, o);
+      }
+    }
+    i = vend;
+  }
+  for (uint64_t e = i + threadIdx.x; e < b; e += blockDim.x) {  // tail / unaligned
+    float acc = 0.0f;
+    for (int t = 0; t < nterms; ++t) acc += Cvt<TIn>::to(tp[t][e]);
+    for (int d = 0; d < nd; ++d) {
+      const float v = beta != 0.0f ? fmaf(beta, Cvt<TOut>::to(dl[d][e]), acc) : acc;
+      dl[d][e] = Cvt<TOut>::from(v);
+    }
+  }
+}
+
 struct ReduceLen {
   __device__ uint64_t operator()(const ReduceSeg& s) const { return s.nelem; }
 };
@@ -753,6 +813,51 @@ struct RedRing {
     const uint32_t bytes = nelem * sizeof(TIn);
     mbar_expect(&full[st], bytes);
     bulk_g2s(mem + st * (kRedSub * sizeof(TIn)), src, bytes, &full[st]);
+  }
+
+  // dl[d][off, off + n) = beta*dl[d] + term[0, n) for each of the nd accumulators
+  // (a fan-out segment): the staged term is read from smem once per accumulator.
+  __device__ __forceinline__ void run_fan(TOut* const* dl, int nd, uint64_t off, const TIn* __restrict__ term, uint64_t n,
+                                       float beta) {
+    constexpr int S = red_stages<TIn>();
+    const uint32_t nsub = static_cast<uint32_t>((n + kRedSub - 1) / kRedSub);
+    auto sub_len = [&](uint32_t i) {
+      const uint64_t r = n - static_cast<uint64_t>(i) * kRedSub;
+      return static_cast<uint32_t>(r < kRedSub ? r : kRedSub);
+    };
+    if (threadIdx.x == 0)
+      for (uint32_t i = 0; i < nsub && i < static_cast<uint32_t>(S); ++i)
+        issue(term + static_cast<uint64_t>(i) * kRedSub, used + i, sub_len(i));
+    for (uint32_t i = 0; i < nsub; ++i) {
+      const uint32_t k = used + i, len = sub_len(i);
+      const int st = k % S;
+      const uint64_t base = off + static_cast<uint64_t>(i) * kRedSub;
+      const TIn* T = reinterpret_cast<const TIn*>(mem + st * (kRedSub * sizeof(TIn)));
+      mbar_wait(&full[st], (k / S) & 1u);
+      for (uint32_t j = threadIdx.x * 8; j < len; j += blockDim.x * 8) {
+        float acc[8];
+        load8_coherent(T + j, acc);
+        for (int d = 0; d < nd; ++d) {
+          TOut* p = dl[d] + base + j;
+          float o[8];
+          if (beta != 0.0f) {
+            load8_coherent(p, o);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) o[q] = fmaf(beta, o[q], 0.0f + acc[q]);
+          } else {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) o[q] = 0.0f + acc[q];
+          }
+          store8(p, o);
+        }
+      }
+      __syncthreads();  // stage st fully read
+      if (threadIdx.x == 0 && i + S < nsub) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(term + static_cast<uint64_t>(i + S) * kRedSub, k + S, sub_len(i + S));
+      }
+    }
+    used += nsub;
   }
 
   // dst[0, n) = beta*dst + term[0, n); n a multiple of 8, 16-B aligned pointers
@@ -794,7 +899,10 @@ struct RedRing {
   }
 };
 
-template <class TIn, class TOut, int MODE>
+// FAN: the launch has fan-out segments (ndst > 1); every segment then takes the
+// fan-out code path (a separate instantiation keeps the single-accumulator
+// kernel's register allocation untouched).
+template <class TIn, class TOut, int MODE, bool FAN>
 __global__ void __launch_bounds__(512, 2) reduce_segments_kernel(const ReduceSeg* __restrict__ segs, int nseg,
                                                               const void* const* __restrict__ terms,
                                                               Partition part, float beta, SyncArgs sync) {
@@ -813,6 +921,24 @@ __global__ void __launch_bounds__(512, 2) reduce_segments_kernel(const ReduceSeg
                    [&](const ReduceSeg& sg, uint64_t a, uint64_t b, bool remote) {
     const TIn* const* tp = reinterpret_cast<const TIn* const*>(terms + sg.term0);
     TOut* dst = static_cast<TOut*>(sg.dst);
+    if constexpr (FAN) {  // fan-out: one term read, several accumulators
+      // the side array holds the accumulator pointers too (written as const void*)
+      TOut* const* dl = reinterpret_cast<TOut* const*>(const_cast<void* const*>(terms + sg.dst0));
+      if constexpr (MODE == kPartDynamic) {
+        if (remote && sg.nterms == 1 && part.ring) {
+          const uint64_t n8 = (b - a) & ~uint64_t(7);
+          uint64_t al = reinterpret_cast<uint64_t>(tp[0] + a);
+          for (int d = 0; d < sg.ndst; ++d) al |= reinterpret_cast<uint64_t>(dl[d] + a);
+          if ((al & 15) == 0 && n8 > 0) {
+            ring.run_fan(dl, sg.ndst, a, tp[0] + a, n8, beta);
+            if (a + n8 < b) reduce_range_fan<TIn, TOut>(dl, sg.ndst, tp, 1, a + n8, b, beta);
+            return;
+          }
+        }
+      }
+      reduce_range_fan<TIn, TOut>(dl, sg.ndst, tp, sg.nterms, a, b, beta);
+      return;
+    }
     if constexpr (MODE == kPartDynamic) {
       if (remote && sg.nterms == 1 && part.ring) {  // (remote chunks exist => the ring smem was allocated)
         const uint64_t n8 = (b - a) & ~uint64_t(7);
@@ -884,34 +1010,43 @@ void launch_copy(const CopySeg* segs, int nseg, Partition part, const SyncArgs& 
   }
 }
 
-template <class TIn, class TOut>
+template <class TIn, class TOut, bool FAN>
 static int red_ring_smem() {
   static const int smem = [] {
-    cudaFuncSetAttribute(reduce_segments_kernel<TIn, TOut, kPartDynamic>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kRedRingBytes);
+    cudaFuncSetAttribute(reduce_segments_kernel<TIn, TOut, kPartDynamic, FAN>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, kRedRingBytes);
     return static_cast<int>(kRedRingBytes);
   }();
   return smem;
 }
 
+template <class TIn, class TOut, bool FAN>
+static void launch_reduce_f(const ReduceSeg* segs, int nseg, const void* const* terms, Partition part,
+                            float beta, const SyncArgs& sync, int grid, int block, cudaStream_t st) {
+  if (part.mode == kPartInterleaved)
+    reduce_segments_kernel<TIn, TOut, kPartInterleaved, FAN><<<grid, block, 0, st>>>(segs, nseg, terms, part, beta,
+                                                                                    sync);
+  else if (part.mode == kPartDynamic)
+    // the ring's shared memory only when there are remote chunks to stage
+    reduce_segments_kernel<TIn, TOut, kPartDynamic, FAN>
+        <<<grid, block, part.ring && part.rtotal_chunks ? red_ring_smem<TIn, TOut, FAN>() : 0, st>>>(
+            segs, nseg, terms, part, beta, sync);
+  else
+    reduce_segments_kernel<TIn, TOut, kPartContiguous, FAN><<<grid, block, 0, st>>>(segs, nseg, terms, part, beta,
+                                                                                   sync);
+}
+
 template <class TIn, class TOut>
 static void launch_reduce_t(const ReduceSeg* segs, int nseg, const void* const* terms, Partition part,
                             float beta, const SyncArgs& sync, int grid, int block, cudaStream_t st) {
-  if (part.mode == kPartInterleaved)
-    reduce_segments_kernel<TIn, TOut, kPartInterleaved><<<grid, block, 0, st>>>(segs, nseg, terms, part, beta, sync);
-  else if (part.mode == kPartDynamic)
-    // the ring's shared memory only when there are remote chunks to stage
-    reduce_segments_kernel<TIn, TOut, kPartDynamic>
-        <<<grid, block, part.ring && part.rtotal_chunks ? red_ring_smem<TIn, TOut>() : 0, st>>>(segs, nseg, terms,
-                                                                                           part, beta, sync);
-  else
-    reduce_segments_kernel<TIn, TOut, kPartContiguous><<<grid, block, 0, st>>>(segs, nseg, terms, part, beta, sync);
+  if (part.fan) launch_reduce_f<TIn, TOut, true>(segs, nseg, terms, part, beta, sync, grid, block, st);
+  else launch_reduce_f<TIn, TOut, false>(segs, nseg, terms, part, beta, sync, grid, block, st);
 }
 
 template <class TIn, class TOut>
 static int occ_t(int threads) {
   int n = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, reduce_segments_kernel<TIn, TOut, kPartContiguous>, threads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, reduce_segments_kernel<TIn, TOut, kPartContiguous, false>, threads, 0);
   return n > 0 ? n : 1;
 }
 

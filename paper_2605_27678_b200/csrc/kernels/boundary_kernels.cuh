@@ -43,7 +43,11 @@ struct CopySeg {
 constexpr uint32_t kErrTimeout = 1, kErrBadId = 2;
 
 // dst[i] = beta*dst[i] + sum_t term_t[i], fp32 accumulation, terms summed in
-// order starting from +0.0f; term pointers live in a side array.
+// order starting from +0.0f; term pointers live in a side array. A segment
+// with ndst > 1 applies the same sum to several accumulators (the TP replicas
+// of a source shard resident on this GPU): the terms are read once and each
+// accumulator gets its own read-modify-write; the ndst accumulator pointers
+// sit in the side array at dst0 (dst = the first of them).
 struct ReduceSeg {
   void* dst;
   uint64_t nelem;
@@ -51,7 +55,9 @@ struct ReduceSeg {
   int32_t nterms;
   int32_t term0;
   uint32_t peers;  // GPUs holding this segment's terms besides this one
-  uint32_t pad_;
+  int32_t ndst;
+  int32_t dst0;
+  int32_t pad_;
 };
 
 // How a launch's work space is split over CTAs.
@@ -81,6 +87,7 @@ struct Partition {
   uint32_t rstatic;          // = min(remote_ctas, rtotal_chunks)
   int ring;                  // reduce: stage remote single-term chunks through the TMA ring
   int prefetch_other;        // start the other queue's first claim near the current queue's end
+  int fan;                   // reduce: some segment has ndst > 1 (fan-out kernel variant)
 };
 
 // Cross-GPU epoch barrier over peer-mapped flag words. Every GPU of an exec

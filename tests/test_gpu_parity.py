@@ -367,7 +367,7 @@ def test_cuda_graph_replay_matches_direct_calls():
     s = cfg.splice
     sp = hbb.SpliceSpec(s["Q"], s["S"], cfg.hidden, cfg.tokens, s["codes"], s["text_mode"])
     outs = []
-    for use_graph in (False, True):
+    for use_graph in (False, True, "cycle"):
         rt = hbb.BridgeRuntime(plan, sp, mb_slots=2)
         g = torch.Generator(device=DEV)
         g.manual_seed(3)
@@ -379,7 +379,11 @@ def test_cuda_graph_replay_matches_direct_calls():
                         b.copy_(torch.randn(b.numel(), generator=g, device=DEV).to(b.dtype))
                 rt.buffer(r, hbb.SLOT_SRC_GRAD, k).zero_()
         st = torch.cuda.Stream()
-        if use_graph:
+        if use_graph == "cycle":  # one graph = a step on each buffer set in turn
+            rt.capture_step(0, 1.0, True, st, what=rt.GRAPH_CYCLE)
+            for i in range(2):
+                rt.replay_step(0, st, rt.GRAPH_CYCLE)
+        elif use_graph:
             for k in range(2):
                 rt.capture_step(k, 1.0, True, st)
             for i in range(4):
@@ -392,7 +396,7 @@ def test_cuda_graph_replay_matches_direct_calls():
         outs.append([rt.buffer(r, sl, k).clone() for k in range(2) for r in range(8)
                      for sl in (hbb.SLOT_DST_ACT, hbb.SLOT_SRC_GRAD)])
         assert rt.stats()["launches"] == 8
-        if use_graph:  # forward-only and backward-only graphs replay too
+        if use_graph is True:  # forward-only and backward-only graphs replay too
             rt.capture_step(0, 1.0, stream=st, what=rt.GRAPH_FWD)
             rt.capture_step(0, 1.0, stream=st, what=rt.GRAPH_BWD)
             rt.replay_step(0, st, rt.GRAPH_FWD)
@@ -400,5 +404,6 @@ def test_cuda_graph_replay_matches_direct_calls():
             st.synchronize()
             assert rt.stats()["launches"] == 10
         rt.close()
-    for a, b in zip(*outs):
-        assert torch.equal(a, b)
+    for other in outs[1:]:
+        for a, b in zip(outs[0], other):
+            assert torch.equal(a, b)
