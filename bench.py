@@ -41,7 +41,7 @@ def parse():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--scale", type=int, default=1, help="divide the hidden width (diagnostics only)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=8)
+    ap.add_argument("--e2e-steps", type=int, default=16)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--blocks-per-sm", type=int, default=0)

@@ -23,6 +23,8 @@
 //
 // Roofline (pure data movement; tensor cores not applicable): time >=
 // max(HBM bytes / HBM BW, NVLink ingress / NVLink BW); see DESIGN.md.
+#include <cstdlib>
+
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -1020,9 +1022,32 @@ static int red_ring_smem() {
   return smem;
 }
 
+// HB_RED_CARVEOUT (A/B knob, percent of the unified L1/smem given to shared
+// memory for the reduce kernels; 0 = driver default). Setting it to the TMA
+// copy kernel's 100 avoids an L1/smem reconfiguration between a forward and a
+// backward launch.
+template <class TIn, class TOut, bool FAN>
+static void red_carveout() {
+  static const bool done = [] {
+    const char* v = std::getenv("HB_RED_CARVEOUT");
+    const int pct = v && *v ? std::atoi(v) : 0;
+    if (pct > 0) {
+      cudaFuncSetAttribute(reduce_segments_kernel<TIn, TOut, kPartDynamic, FAN>,
+                           cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+      cudaFuncSetAttribute(reduce_segments_kernel<TIn, TOut, kPartContiguous, FAN>,
+                           cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+      cudaFuncSetAttribute(reduce_segments_kernel<TIn, TOut, kPartInterleaved, FAN>,
+                           cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    }
+    return true;
+  }();
+  (void)done;
+}
+
 template <class TIn, class TOut, bool FAN>
 static void launch_reduce_f(const ReduceSeg* segs, int nseg, const void* const* terms, Partition part,
                             float beta, const SyncArgs& sync, int grid, int block, cudaStream_t st) {
+  red_carveout<TIn, TOut, FAN>();
   if (part.mode == kPartInterleaved)
     reduce_segments_kernel<TIn, TOut, kPartInterleaved, FAN><<<grid, block, 0, st>>>(segs, nseg, terms, part, beta,
                                                                                     sync);
