@@ -93,6 +93,27 @@ int hb_plan_export(const hb_plan* p, int elem_bytes, char* buf, size_t cap, size
 int hb_plan_info(const hb_plan* p, int* placement, int* kind, int* factor,
                  int* cross_boundary_messages, int* world); /* BridgePlan fields, :122-135 */
 
+/* ---- configuration ingestion (SPEC cli module S:495-545: ExperimentConfig,
+ *      parse_config; paper Appendix B module_parallelisms) -------
+ * Grammar: `[module.<name>]` sections with tensor_model_parallel_size,
+ * context_parallel_size, pipeline_model_parallel_size, data_parallel_size,
+ * rank_offset; `[model]` and `[run]` sections (global_batch, num_microbatches,
+ * steps, seed, tolerance, ...); `#` comments; integer or decimal values only.
+ * Errors: 22 ParseError ("line N: ..."), 23 ValidationError (one "language"
+ * module and >= 1 encoder; IndivisibleBatch; PartialOverlap). */
+typedef struct hb_config hb_config;
+int hb_config_parse(const char* text, hb_config** out); /* parse_config */
+void hb_config_destroy(hb_config* c);
+int hb_config_num_modules(const hb_config* c, int* n);
+/* module i in file order; out->name stays valid while c lives */
+int hb_config_module(const hb_config* c, int i, hb_layout* out, int* is_language);
+int hb_config_run(const hb_config* c, int* global_batch, int* num_microbatches, int* steps,
+                  long long* seed, double* tolerance);
+/* encoder -> language edge of one microbatch (global_batch / num_microbatches samples) */
+int hb_config_edge(const hb_config* c, const char* encoder, int feature_width, hb_edge* out);
+/* canonical text (parse(render(c)) reproduces c) */
+int hb_config_render(const hb_config* c, char* buf, size_t cap, size_t* len);
+
 /* ---- splice (tinymodel.hpp:94-112) -------------------------------------------- */
 int hb_cp_token_slice(int seq_len, int cp, int cp_idx, int* start, int* length); /* :95 */
 /* codes[Q*S]: >= 0 vision row (local sample j)*S_v + token t; < 0 text row -1-code. */

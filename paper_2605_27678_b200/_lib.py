@@ -35,6 +35,8 @@ EXPORTS = [
     "hb_exec_seed_forward_record", "hb_exec_status", "hb_exec_stats", "hb_exec_graph_capture", "hb_projector_gemm",
     "hb_exec_forward_projected", "hb_exec_set_text_embedding",
     "hb_exec_graph_launch", "hb_exec_trace",
+    "hb_config_parse", "hb_config_destroy", "hb_config_num_modules", "hb_config_module", "hb_config_run",
+    "hb_config_edge", "hb_config_render",
 ]
 
 
@@ -130,6 +132,13 @@ def _declare(L):
         "hb_exec_forward_projected": (I, [V, I, V, LL, V, LL, I, I, V]),
         "hb_exec_set_text_embedding": (I, [V, V, LL]),
         "hb_exec_trace": (I, [V, I, V, I, P(I), P(I)]),
+        "hb_config_parse": (I, [C, P(V)]),
+        "hb_config_destroy": (None, [V]),
+        "hb_config_num_modules": (I, [V, P(I)]),
+        "hb_config_module": (I, [V, I, P(Layout), P(I)]),
+        "hb_config_run": (I, [V, P(I), P(I), P(I), P(LL), P(ctypes.c_double)]),
+        "hb_config_edge": (I, [V, C, I, P(Edge)]),
+        "hb_config_render": (I, [V, C, Sz, P(Sz)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name, None)

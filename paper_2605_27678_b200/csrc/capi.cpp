@@ -12,6 +12,7 @@
 #include <string>
 
 #include "hb/bridge.hpp"
+#include "hb/config.hpp"
 #include "hb/index_map.hpp"
 #include "hb/runtime.hpp"
 #include "kernels/projector_gemm.cuh"
@@ -24,6 +25,9 @@ struct hb_splice {
 };
 struct hb_exec {
   std::unique_ptr<hb::rt::Exec> x;
+};
+struct hb_config {
+  hb::config::ExperimentConfig c;
 };
 
 namespace {
@@ -176,6 +180,79 @@ int hb_plan_export(const hb_plan* p, int elem_bytes, char* buf, size_t cap, size
     need(p, "plan");
     if (elem_bytes < 1) hb::raise(hb::ErrorCode::InvalidArgument, "elem_bytes must be >= 1");
     const std::string s = hb::bridge::export_plan(p->plan, elem_bytes);
+    if (len) *len = s.size();
+    if (buf && cap) {
+      const size_t n = std::min(cap - 1, s.size());
+      std::memcpy(buf, s.data(), n);
+      buf[n] = 0;
+    }
+  });
+}
+
+int hb_config_parse(const char* text, hb_config** out) {
+  return guard([&] {
+    need(text, "text");
+    need(out, "out");
+    *out = nullptr;
+    auto c = std::make_unique<hb_config>();
+    c->c = hb::config::parse_config(text);
+    *out = c.release();
+  });
+}
+
+void hb_config_destroy(hb_config* c) { delete c; }
+
+int hb_config_num_modules(const hb_config* c, int* n) {
+  return guard([&] {
+    need(c, "config");
+    need(n, "n");
+    *n = static_cast<int>(c->c.modules.size());
+  });
+}
+
+int hb_config_module(const hb_config* c, int i, hb_layout* out, int* is_language) {
+  return guard([&] {
+    need(c, "config");
+    need(out, "out");
+    if (i < 0 || i >= static_cast<int>(c->c.modules.size()))
+      hb::raise(hb::ErrorCode::InvalidArgument, "module index out of range");
+    const auto& l = c->c.modules[i].layout;
+    *out = {l.name.c_str(), l.tp, l.cp, l.pp, l.dp, l.rank_offset};
+    if (is_language) *is_language = l.name == "language";
+  });
+}
+
+int hb_config_run(const hb_config* c, int* global_batch, int* num_microbatches, int* steps, long long* seed,
+                  double* tolerance) {
+  return guard([&] {
+    need(c, "config");
+    if (global_batch) *global_batch = c->c.global_batch;
+    if (num_microbatches) *num_microbatches = c->c.num_microbatches;
+    if (steps) *steps = c->c.steps;
+    if (seed) *seed = c->c.seed;
+    if (tolerance) *tolerance = c->c.tolerance;
+  });
+}
+
+int hb_config_edge(const hb_config* c, const char* encoder, int feature_width, hb_edge* out) {
+  return guard([&] {
+    need(c, "config");
+    need(encoder, "encoder");
+    need(out, "out");
+    const auto e = c->c.edge(encoder, feature_width);
+    const auto& s = c->c.module(e.source.name).layout;
+    const auto& d = c->c.language().layout;
+    *out = {{s.name.c_str(), s.tp, s.cp, s.pp, s.dp, s.rank_offset},
+            {d.name.c_str(), d.tp, d.cp, d.pp, d.dp, d.rank_offset},
+            e.global_batch,
+            e.feature_width};
+  });
+}
+
+int hb_config_render(const hb_config* c, char* buf, size_t cap, size_t* len) {
+  return guard([&] {
+    need(c, "config");
+    const std::string s = hb::config::render_config(c->c);
     if (len) *len = s.size();
     if (buf && cap) {
       const size_t n = std::min(cap - 1, s.size());

@@ -193,6 +193,30 @@ def test_dtype_matrix(act, gin, gout):
     run_case(cfg, seed=11, beta=1.0)
 
 
+@pytest.mark.parametrize("act,gin,gout", [("fp32", "fp32", "fp32"), ("bf16", "bf16", "bf16"),
+                                          ("fp16", "fp16", "fp32"), ("bf16", "fp32", "fp16")])
+def test_fan_out_return_dtypes(act, gin, gout):
+    """C3 on one GPU: the four encoder TP replicas of each source shard share one
+    fan-out reduce segment (terms read once, four accumulators)."""
+    cfg = configs.get("c3", scale=128)
+    cfg.act, cfg.grad_in, cfg.grad_out = act, gin, gout
+    run_case(cfg, seed=13, beta=1.0)
+
+
+@pytest.mark.parametrize("partition", [1, 2, 3, 4])
+@pytest.mark.parametrize("beta", [0.0, 1.0])
+def test_fan_out_return_partitions(partition, beta):
+    run_case(configs.get("c3", scale=64), seed=17, beta=beta, partition=partition)
+
+
+def test_fan_out_return_unaligned_rows():
+    """W=3 fp32 rows: the fan-out kernel's scalar tail path."""
+    cfg = configs.get("c3", scale=64)
+    cfg.tokens, cfg.hidden = 1, 3
+    cfg.act = cfg.grad_in = cfg.grad_out = "fp32"
+    run_case(cfg, seed=19, beta=1.0)
+
+
 def test_nc_cp_reduction_multi_term():
     """NC edge into an LLM with cp=2: backward sums two cp contributions (fp32, fixed order)."""
     cfg = configs.get("c5", scale=64)
