@@ -28,3 +28,18 @@ def test_reference_unit_tests_pass(name, cases):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     assert f"test cases: {cases} | 0 failed" in r.stdout
+
+
+def test_reference_side_binding_matches_reference():
+    """INTEGRATION.md §2's binding (hetsim types -> hetbridge C-ABI), compiled against
+    the reference headers, answers every grid/bridge call of a layout sweep exactly
+    like the reference grid and the oracle bridge (oracle/refcheck/shim)."""
+    exe = os.path.join(BIN, "shim_check")
+    if not os.path.exists(exe):
+        if os.path.isdir("/root/reference/proj"):
+            subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "refcheck"], check=True)
+        else:
+            pytest.skip("shim check not built and /root/reference absent")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert " 0 mismatches" in r.stdout
