@@ -136,7 +136,8 @@ def traffic_model(cfg, n_gpus):
         reads.setdefault((r2g[dr], sr, ss), []).append((so, so + n))
     account("fwd", reads, a)
     reads = {}
-    for (dr, ds, do, n, terms) in hbb.index_backward(plan, sp):
+    # the map the runtime executes by default (terms read from the holder's tp replicas in turn)
+    for (dr, ds, do, n, terms) in hbb.index_backward(plan, sp, balanced=True):
         out["bwd_hbm"][r2g[dr]] += n * go * (2 if cfg.beta else 1)
         for (tr, ts, to) in terms:
             reads.setdefault((r2g[dr], tr, ts), []).append((to, to + n))

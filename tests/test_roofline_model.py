@@ -1,0 +1,72 @@
+"""The roofline's algorithmic bytes (bench.traffic_model, DESIGN §4/§6) against the
+per-GPU figures SURVEY §8(d) derives by hand for the 8-GPU configs, and the
+payload accounting of the BASELINE metric. CPU only."""
+import pytest
+
+import bench
+from paper_2605_27678_b200 import configs
+
+MB = 1e6
+PK = {"hbm_gbs": 6539.2, "nvl_gbs": 770.0}
+
+
+def tm8(name):
+    return bench.traffic_model(configs.get(name), 8)
+
+
+def test_c2_fan_in_8_gpus():
+    t = tm8("c2")
+    # fwd: out 151.0 MB + own read 37.75 + served to 3 peers -> 302.0 MB HBM, 113.2 MB NVLink in
+    assert all(x == pytest.approx(302.0 * MB, rel=1e-3) for x in t["fwd_hbm"])
+    assert all(x == pytest.approx(113.2 * MB, rel=1e-3) for x in t["fwd_nvl"])
+    # bwd: 37.75 MB bf16 read + fp32 accumulator read-modify-write
+    assert all(x == pytest.approx(188.7 * MB, rel=1e-3) for x in t["bwd_hbm"])
+    assert not any(t["bwd_nvl"])
+
+
+def test_c3_fan_out_8_gpus():
+    t = tm8("c3")
+    assert all(x == pytest.approx(94.4 * MB, rel=1e-3) for x in t["fwd_hbm"])
+    assert not any(t["fwd_nvl"])
+    assert all(x == pytest.approx(141.6 * MB, rel=1e-3) for x in t["bwd_nvl"])
+    assert all(x == pytest.approx(943.7 * MB, rel=1e-3) for x in t["bwd_hbm"])
+
+
+def test_c4_cp_splice_8_gpus():
+    t = tm8("c4")
+    # each GPU writes its 8192-position slice (67.1 MB) and reads what it copies locally
+    assert all(x == pytest.approx(134.2 * MB, rel=1e-3) for x in t["fwd_hbm"])
+    # vision rows from other GPUs: whole images (4.72 MB each), 3-4 per slice
+    img = 576 * 4096 * 2
+    assert all(x % img == 0 and 3 * img <= x <= 4 * img for x in t["fwd_nvl"])
+    # grads come back from one of the two TP replicas (the owner's own GPU when it holds one)
+    assert 0 < sum(t["bwd_nvl"]) <= sum(t["fwd_nvl"]) / 2
+
+
+def test_c5_noncolocated_8_gpus():
+    t = tm8("c5")
+    # dest leader's TP pair (GPUs 2, 3) each ingest 16 images; the return splits over both replicas
+    assert t["fwd_nvl"][2] == t["fwd_nvl"][3] == pytest.approx(75.5 * MB, rel=1e-3)
+    assert sum(t["fwd_nvl"]) == t["fwd_nvl"][2] + t["fwd_nvl"][3]
+    assert t["bwd_nvl"][0] == t["bwd_nvl"][1] == pytest.approx(37.75 * MB, rel=1e-3)
+    assert t["bwd_hbm"][2] == t["bwd_hbm"][3]  # balanced return: both replicas serve half
+
+
+def test_tstar_8_gpus_binding_resource():
+    f = bench.kernel_bound(tm8("c2"), "fwd", 1.0, PK, 8)
+    b = bench.kernel_bound(tm8("c2"), "bwd", 1.0, PK, 8)
+    assert f["bound"] == "nvlink" and f["tstar_ms"] * 1e3 == pytest.approx(113.25e6 / 770e9 * 1e6, rel=5e-3)
+    assert b["bound"] == "hbm" and b["tstar_ms"] * 1e3 == pytest.approx(188.74e6 / 6539.2e9 * 1e6, rel=5e-3)
+    assert bench.kernel_bound(tm8("c3"), "bwd", 1.0, PK, 8)["bound"] == "nvlink"
+
+
+def test_one_gpu_is_hbm_only():
+    for name in ("c2", "c3", "c4", "c5"):
+        t = bench.traffic_model(configs.get(name), 1)
+        assert t["fwd_nvl"] == [0] and t["bwd_nvl"] == [0]
+
+
+def test_payload_bytes():
+    fwd, bwd = bench.payload_bytes(configs.get("c2"))
+    assert fwd == 8 * 32 * 576 * 4096 * 2  # every LLM rank's 32-sample shard
+    assert bwd == 64 * 576 * 4096 * 2      # every sample's gradient returned once
