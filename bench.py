@@ -272,6 +272,43 @@ def cpu_reference_run(cfg, sample_batch: int, repeats: int = 1):
     return (fwd_b + bwd_b) / best / 1e9, best, desc
 
 
+def direct_cpu_run(cfg, sample_batch: int):
+    """SURVEY §8(d)'s informative "direct CPU" executor (oracle/direct_cpu.py):
+    the same sample's index maps executed on the host over all cores. Returns
+    (payload GB/s, seconds, threads, description); None for splice configs."""
+    import numpy as np
+
+    from oracle import direct_cpu
+    from paper_2605_27678_b200 import bridge as hbb
+    from paper_2605_27678_b200.grid import BoundaryEdge
+
+    if cfg.splice or cfg.act != "bf16" or cfg.grad_in != "bf16" or cfg.grad_out != "fp32":
+        return None
+    B, W = sample_batch, cfg.width
+    plan = hbb.plan_bridge(BoundaryEdge(cfg.src, cfg.dst, B, W))
+    rng = np.random.default_rng(11)
+    bufs = {}
+    fwd_b = bwd_b = 0
+    for r in range(plan.world):
+        for slot in (hbb.SLOT_SRC_ACT, hbb.SLOT_DST_ACT, hbb.SLOT_DST_GRAD, hbb.SLOT_SRC_GRAD):
+            n = hbb.buffer_elems(plan, r, slot)
+            if n <= 0:
+                continue
+            if slot == hbb.SLOT_SRC_GRAD:
+                bufs[(r, slot)] = np.zeros(n, dtype=np.float32)
+                bwd_b += n * DT_SIZE[cfg.grad_in]
+            elif slot == hbb.SLOT_DST_ACT:
+                bufs[(r, slot)] = np.zeros(n, dtype=np.uint16)
+                fwd_b += n * DT_SIZE[cfg.act]
+            else:
+                bufs[(r, slot)] = rng.integers(0x3000, 0x4000, n, dtype=np.uint16)  # finite bf16 bits
+    sec, threads = direct_cpu.run(hbb.index_forward(plan), hbb.index_backward(plan, balanced=True), bufs,
+                                  beta=cfg.beta, repeats=2)
+    desc = (f"{cfg.name} layouts with B={B} samples x {cfg.tokens}x{cfg.hidden}: index maps executed on the "
+            f"host (numpy slices, thread pool), best of 2")
+    return (fwd_b + bwd_b) / sec / 1e9, sec, threads, desc
+
+
 def cpu_sample_batch(cfg):
     # smallest batch the layouts admit (divisible by both dp): bounded CPU work
     return max(cfg.src.dp, cfg.dst.dp)
@@ -554,6 +591,10 @@ def main():
             gbs, sec, desc = cpu_reference_run(cfg, B)
             cpu = {"value": round(gbs, 4), "unit": "GB/s", "cores": 1, "kind": "port", "sample": desc,
                    "cpu": _cpu_model(), "nproc": os.cpu_count()}
+            d = direct_cpu_run(cfg, B)
+            if d is not None:  # informative: the same maps on every host core
+                cpu["direct"] = {"value": round(d[0], 3), "unit": "GB/s", "cores": d[2], "kind": "port",
+                                 "sample": d[3]}
         except Exception as exc:  # the oracle is a reported baseline, never the product
             cpu = {"value": None, "unit": "GB/s", "cores": 1, "kind": "port", "sample": f"unavailable: {exc}"}
 
