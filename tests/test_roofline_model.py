@@ -70,3 +70,27 @@ def test_payload_bytes():
     fwd, bwd = bench.payload_bytes(configs.get("c2"))
     assert fwd == 8 * 32 * 576 * 4096 * 2  # every LLM rank's 32-sample shard
     assert bwd == 64 * 576 * 4096 * 2      # every sample's gradient returned once
+
+
+def test_reference_arm_line_contract():
+    """`bench.py --impl reference` (the reference CPU path on host cores) prints one
+    JSON line with the contract's keys; runs here without a GPU."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    if not os.path.exists(os.path.join(bench.ROOT, "oracle", "_ref", "libhb_oracle.so")):
+        pytest.skip("oracle not built")
+    r = subprocess.run([sys.executable, os.path.join(bench.ROOT, "bench.py"), "--impl", "reference",
+                        "--steps", "1", "--warmup", "1"], capture_output=True, text=True, timeout=300,
+                       env={**os.environ, "RANK": "0"})
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
+    for k in ("impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e"):
+        assert k in line, k
+    assert line["impl"] == "reference" and line["unit"] == "GB/s" and line["value"] > 0
+    assert line["e2e"] == {"value": line["value"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+    cb = line["cpu_baseline"]
+    assert cb["kind"] == "port" and cb["cores"] >= 1 and cb["value"] == line["value"] and cb["sample"]
