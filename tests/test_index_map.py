@@ -222,3 +222,33 @@ def test_balanced_backward_spreads_serving_ranks(name):
 def plan_coord_tp(layout, r):
     from paper_2605_27678_b200 import grid as hbg
     return hbg.coord_of_rank(layout, r).tp_idx
+
+
+def random_codes(rng, n_vis_rows, Q, S):
+    """A placeholder table with every vision row of the shard at a random position
+    (images split across sequences and CP slices, tokens out of order) and text
+    rows numbered in position order elsewhere."""
+    pos = rng.choice(Q * S, size=n_vis_rows, replace=False)
+    codes = np.full(Q * S, 0, dtype=np.int64)
+    vis = np.zeros(Q * S, dtype=bool)
+    vis[pos] = True
+    codes[pos] = rng.permutation(n_vis_rows)
+    text_idx = np.cumsum(~vis) - 1
+    codes[~vis] = -1 - text_idx[~vis]
+    return codes.astype(np.int32)
+
+
+@pytest.mark.parametrize("seed", range(6))
+@pytest.mark.parametrize("text_mode", [0, 1])
+def test_random_placeholder_tables(seed, text_mode):
+    """Scattered vision tokens: runs break at every discontinuity, slices start and
+    end mid-image; placement stays bit-exact and the gradient return exact."""
+    rng = np.random.default_rng(100 + seed)
+    s = [O.Layout("vit", dp=4), O.Layout("vit", tp=2, dp=2), O.Layout("vit", dp=8)][seed % 3]
+    d = [O.Layout("llm", tp=2, cp=2), O.Layout("llm", cp=4), O.Layout("llm", tp=2, cp=2, dp=2)][seed % 3]
+    B, S_v, d_h = 8, 3, 2
+    Q = 2
+    S = 8 * d.cp
+    n_vis = (B // d.dp) * S_v
+    codes = random_codes(rng, n_vis, Q, S)
+    splice_case(s, d, B, S_v, d_h, Q, S, codes, text_mode, seed=seed)
