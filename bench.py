@@ -30,6 +30,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 L2_BYTES = 126 * 1024 * 1024
+METRIC = "boundary reshard GB/s per GPU (fwd+bwd) vs NVLink/HBM roofline at 1/2/4/8 GPUs"
 DT_SIZE = {"bf16": 2, "fp16": 2, "fp32": 4, "fp64": 8}
 
 
@@ -61,6 +62,7 @@ def parse():
                     help="configs also measured (short) in the same run, so every N of the driver's scaling "
                          "run records the fan-in / fan-out / CP-splice / non-colocated step ('' = none)")
     ap.add_argument("--matrix-steps", type=int, default=200)
+    ap.add_argument("--ref-procs", type=int, default=0, help="reference arm: worker processes (0 = auto)")
     return ap.parse_args()
 
 
@@ -240,6 +242,128 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(inwin)}
 
 
+# ----------------------------------------------------------------------------- synthetic inputs + parity
+
+SLOT_KEYS = {0: 1, 2: 2, 4: 3}  # SRC_ACT, DST_GRAD, TEXT
+
+
+def input_key(buffer_set: int, slot: int, rank: int) -> int:
+    return ((buffer_set * 8 + SLOT_KEYS[slot]) * 64 + rank + 1) * 7919
+
+
+def fill_values(n: int, key: int, dtype, device):
+    """Counter-based synthetic values: element i of a buffer is a
+    fixed integer hash of (key, i) mapped to a finite bf16 in +-[2^-9, 2^7),
+    identical on any device and any rank, so every rank can regenerate a peer's
+    inputs for the parity check without communication. fp32 buffers get the
+    same values (exact widening)."""
+    import torch
+
+    i = torch.arange(n, device=device, dtype=torch.int64)
+    x = (i * 2654435761 + key) & 0xFFFFFFFF
+    x = ((x ^ (x >> 15)) * 0x2C1B3C6D) & 0xFFFFFFFF
+    x = ((x ^ (x >> 12)) * 0x297A2D39) & 0xFFFFFFFF
+    x = x ^ (x >> 15)
+    bits = (((x >> 31) & 1) << 15) | ((118 + ((x >> 20) & 15)) << 7) | (x & 127)
+    bits = torch.where(bits >= 32768, bits - 65536, bits)  # the int16 with those bits
+    v = bits.to(torch.int16).view(torch.bfloat16)
+    return v if dtype == torch.bfloat16 else v.to(dtype)
+
+
+def fill_inputs(rt, local, slots, dev):
+    """Inputs of every buffer set: hashed activations, gradients and text rows;
+    source-gradient accumulators start at zero."""
+    from paper_2605_27678_b200 import bridge as hbb
+
+    for s in range(slots):
+        for r in local:
+            for slot in (hbb.SLOT_SRC_ACT, hbb.SLOT_DST_GRAD, hbb.SLOT_TEXT, hbb.SLOT_SRC_GRAD):
+                b = rt.buffer(r, slot, s)
+                if b is None:
+                    continue
+                if slot == hbb.SLOT_SRC_GRAD:
+                    b.zero_()
+                else:
+                    b.copy_(fill_values(b.numel(), input_key(s, slot, r), b.dtype, dev))
+
+
+def check_parity(rt, cfg, plan, sp, r2g, rank, N, dev, stream, barrier, run_step, buffer_set):
+    """Parity on the buffers the timed loop used (parity in the
+    same run). Snapshots this rank's source-gradient accumulators of
+    `buffer_set` (holding every timed step's beta=1 sums), runs one more step on
+    that set through the same captured graph (`run_step`), and compares, on every
+    rank, its resident destination shards (bit-exact) and accumulators (fp32,
+    |a-b|/max(1,|b|) <= 1e-6, bit-exactness reported) with the torch restatement
+    of the plan's index maps (paper_2605_27678_b200.parity) over inputs
+    regenerated from their hash keys. Full width; every config; every N."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_27678_b200 import bridge as hbb
+    from paper_2605_27678_b200 import parity as P
+
+    tdt = {"bf16": torch.bfloat16, "fp16": torch.float16, "fp32": torch.float32}
+    dt_of = {hbb.SLOT_SRC_ACT: tdt[cfg.act], hbb.SLOT_TEXT: tdt[cfg.act], hbb.SLOT_DST_GRAD: tdt[cfg.grad_in]}
+    local = [r for r in range(plan.world) if r2g[r] == rank]
+    prev = {}
+    for r in local:
+        b = rt.buffer(r, hbb.SLOT_SRC_GRAD, buffer_set)
+        if b is not None:
+            prev[r] = b.float().clone()
+    barrier()
+    run_step(buffer_set)
+    stream.synchronize()
+    barrier()
+    cache = {}
+
+    def regen(r, slot):
+        if (r, slot) not in cache:
+            n = hbb.buffer_elems(plan, r, slot, sp)
+            cache[(r, slot)] = fill_values(n, input_key(buffer_set, slot, r), dt_of[slot], dev)
+        return cache[(r, slot)]
+
+    fwd_map = hbb.index_forward(plan, sp)
+    bwd_map = hbb.index_backward(plan, sp, balanced=True)
+    fwd_ok, covered_ok, bwd_bitexact, worst = True, True, True, 0.0
+    checked_fwd, checked_bwd = [], []
+    for r in local:
+        out = rt.buffer(r, hbb.SLOT_DST_ACT, buffer_set)
+        if out is not None:
+            exp, cov = P.expected_forward(fwd_map, r, out.numel(), regen)
+            covered_ok &= cov == out.numel()
+            ib = torch.int16 if out.element_size() == 2 else torch.int32
+            fwd_ok &= exp is not None and bool(torch.equal(out.view(ib), exp.to(out.dtype).view(ib)))
+            checked_fwd.append(r)
+        if r in prev:
+            got = rt.buffer(r, hbb.SLOT_SRC_GRAD, buffer_set)
+            exp = P.expected_backward(bwd_map, r, prev[r], cfg.beta, regen)
+            rep = P.parity_compare({f"src_grad[r{r}]": got.float()}, {f"src_grad[r{r}]": exp}, tolerance=1e-6)
+            worst = max(worst, rep.worst())
+            bwd_bitexact &= bool(torch.equal(got.float(), exp))
+            checked_bwd.append(r)
+    cache.clear()
+    flags = torch.tensor([0.0 if fwd_ok else 1.0, 0.0 if covered_ok else 1.0, 0.0 if bwd_bitexact else 1.0, worst],
+                         dtype=torch.float64, device=dev)
+    if N > 1:
+        dist.all_reduce(flags, op=dist.ReduceOp.MAX)
+        gathered = [None] * N
+        dist.all_gather_object(gathered, (checked_fwd, checked_bwd))
+    else:
+        gathered = [(checked_fwd, checked_bwd)]
+    f = flags.tolist()
+    res = {"pass": f[0] == 0 and f[1] == 0 and f[3] <= 1e-6, "fwd_bitexact": f[0] == 0,
+           "fwd_fully_covered": f[1] == 0, "bwd_bitexact": f[2] == 0, "bwd_max_rel": f[3], "bwd_tolerance": 1e-6,
+           "beta": cfg.beta, "buffer_set": buffer_set,
+           "checked_ranks": {"fwd": sorted(x for g in gathered for x in g[0]),
+                             "bwd": sorted(x for g in gathered for x in g[1])},
+           "ranks_checked_on": "each GPU checks its resident ranks; flags max-reduced over all GPUs",
+           "method": "one more fwd+bwd step on a timed buffer set (same CUDA graph, beta=1 onto the timed "
+                     "accumulators) vs the torch restatement of hb_index_forward/hb_index_backward_balanced over "
+                     "hash-regenerated inputs, full width"}
+    barrier()
+    return res
+
+
 # ----------------------------------------------------------------------------- CPU leg
 
 
@@ -314,43 +438,143 @@ def cpu_sample_batch(cfg):
     return max(cfg.src.dp, cfg.dst.dp)
 
 
+def workload_config(cfg, N, slots, scale=1):
+    """The `config` block both arms print (identical for the same command): the
+    workload (layouts, shape, dtypes, beta) and the L2 rule of the timed loop."""
+    from paper_2605_27678_b200 import configs
+
+    world = max(cfg.src.rank_end(), cfg.dst.rank_end())
+    tm_step = None
+    try:
+        tm = traffic_model(cfg, N)
+        tm_step = max(f + b for f, b in zip(tm["fwd_hbm"], tm["bwd_hbm"]))
+    except Exception:
+        pass
+    return {"workload": cfg.description + (f" (hidden /{scale})" if scale > 1 else ""), "name": cfg.name,
+            "global_batch": cfg.batch, "tokens_per_sample": cfg.tokens, "hidden": cfg.hidden,
+            "logical_ranks": world, "rank_to_gpu": configs.rank_to_gpu(world, N),
+            "act": cfg.act, "grad_in": cfg.grad_in, "grad_out": cfg.grad_out, "beta": cfg.beta,
+            "step": "one boundary forward (+ CP splice) and one backward gradient return with fp32 "
+                    "sum-accumulate over the whole global batch",
+            "l2": (f"inputs rotate over {slots} buffer sets; per-GPU bytes per step "
+                   f"{(tm_step or 0) / 1e6:.1f} MB x {slots} sets > 126 MB L2")}
+
+
+def default_slots(cfg, N, args):
+    tm = traffic_model(cfg, N)
+    per_gpu_step = max(f + b for f, b in zip(tm["fwd_hbm"], tm["bwd_hbm"]))
+    # >= 3x L2 of inputs across the rotation, and >= 4 sets so one cycle graph covers 4+ steps
+    slots = args.slots or max(4, min(8, math.ceil(3 * L2_BYTES / max(per_gpu_step, 1))))
+    if not args.no_e2e:
+        slots = max(slots, 2)  # the pipelined e2e leg alternates two buffer sets
+    return slots
+
+
+# The reference arm runs the full workload (cfg.batch samples, full width) once
+# per step through the oracle over the reference's own simnet/grid. simnet runs
+# one rank at a time (R:core/include/hetsim/simnet.hpp:17-27), so one step uses
+# one core; independent steps run concurrently in worker processes, as many as
+# the host's cores and memory allow, and the line reports that core count.
+_REF = {}
+
+
+def _ref_worker_init(name):
+    import numpy as np
+
+    from oracle import oracle as O
+    from paper_2605_27678_b200 import configs
+
+    cfg = configs.get(name)
+    src = O.Layout(cfg.src.name, cfg.src.tp, cfg.src.cp, cfg.src.pp, cfg.src.dp, cfg.src.rank_offset)
+    dst = O.Layout(cfg.dst.name, cfg.dst.tp, cfg.dst.cp, cfg.dst.pp, cfg.dst.dp, cfg.dst.rank_offset)
+    B, W = cfg.batch, cfg.width
+    rng = np.random.default_rng(7)
+    SI, DI = O.intervals(B, src.dp), O.intervals(B, dst.dp)
+    # replicas of one shard share one array (the contract: tp replicas hold identical data)
+    per_s = {d: rng.standard_normal((SI[d][1], W)) for d in range(src.dp)}
+    per_d = {d: rng.standard_normal((DI[d][1], W)) for d in range(dst.dp)}
+    _REF.update(src=src, dst=dst, B=B, W=W,
+                shards={r: per_s[src.coord(r)[3]] for r in src.stage_ranks(src.pp - 1)},
+                grads={r: per_d[dst.coord(r)[3]] for r in dst.stage_ranks(0)})
+
+
+def _ref_step(_i):
+    from oracle import oracle as O
+
+    R = _REF
+    _, _, tf = O.bridge_forward(R["src"], R["dst"], R["B"], R["W"], R["shards"])
+    _, _, tb = O.bridge_backward(R["src"], R["dst"], R["B"], R["W"], R["grads"])
+    return tf + tb
+
+
+def _mem_available():
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemAvailable:"):
+                    return int(line.split()[1]) * 1024
+    except Exception:
+        pass
+    return 16 << 30
+
+
+def ref_step_bytes(cfg):
+    """Peak host bytes of one oracle step (doubles): inputs, forward outputs,
+    returned gradients, and simnet's in-flight message copies (~1x outputs)."""
+    from paper_2605_27678_b200 import bridge as hbb
+
+    plan = hbb.plan_bridge(cfg.edge())
+    fwd = sum(hbb.buffer_elems(plan, r, hbb.SLOT_DST_ACT) for r in range(plan.world))
+    bwd = sum(hbb.buffer_elems(plan, r, hbb.SLOT_SRC_GRAD) for r in range(plan.world))
+    return 8 * (2 * cfg.batch * cfg.width + 2 * fwd + 2 * bwd)
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    import multiprocessing as mp
+
     from paper_2605_27678_b200 import configs
 
     cfg = configs.get(args.config)
-    B = cpu_sample_batch(cfg)
-    times = []
-    desc = ""
-    for _ in range(args.warmup if args.warmup < 2 else 1):
-        cpu_reference_run(cfg, B)
-    for _ in range(max(1, min(args.steps, 3))):
-        gbs, sec, desc = cpu_reference_run(cfg, B)
-        times.append(sec)
-    sec = min(times)
-    fwd_b, bwd_b = 0, 0
-    from oracle import oracle as O
-    SI = O.intervals(B, cfg.src.dp)
-    DI = O.intervals(B, cfg.dst.dp)
-    fwd_b = len(O.Layout("d", cfg.dst.tp, cfg.dst.cp, 1, cfg.dst.dp).stage_ranks(0)) * DI[0][1] * cfg.width * DT_SIZE[cfg.act]
-    bwd_b = len(O.Layout("s", cfg.src.tp, cfg.src.cp, 1, cfg.src.dp).stage_ranks(0)) * SI[0][1] * cfg.width * DT_SIZE[cfg.grad_in]
-    value = (fwd_b + bwd_b) / sec / 1e9
-    tokens = B * cfg.tokens / sec
+    N = args.gpus
+    K, Wm = max(1, args.steps), max(0, args.warmup)
+    cores = os.cpu_count() or 1
+    procs = max(1, min(cores, int(_mem_available() * 0.7 // ref_step_bytes(cfg)), K))
+    if args.ref_procs:
+        procs = args.ref_procs
+    ctx = mp.get_context("fork")
+    t_init = time.time()
+    with ctx.Pool(procs, initializer=_ref_worker_init, initargs=(cfg.name,)) as pool:
+        pool.map(_ref_step, range(max(Wm, procs)), chunksize=1)  # warm-up (every worker has its inputs)
+        t0 = time.time()
+        step_s = pool.map(_ref_step, range(K), chunksize=1)
+        wall = time.time() - t0
+    fwd_b, bwd_b = payload_bytes(cfg)
+    payload = fwd_b + bwd_b
+    value = payload * K / wall / 1e9
+    one = payload / statistics.median(step_s) / 1e9
+    f64 = ref_step_bytes(cfg) // 2  # doubles the oracle writes and reads per step (inputs + outputs)
+    desc = (f"full workload per step ({cfg.batch} samples x {cfg.tokens}x{cfg.hidden}): oracle bridge_forward + "
+            f"bridge_backward over the reference simnet/grid in doubles; {K} steps over {procs} worker processes "
+            f"(simnet runs one rank at a time: one core per step)")
     line = {
-        "impl": "reference", "metric": "boundary reshard GB/s per GPU (fwd+bwd) vs NVLink/HBM roofline at 1/2/4/8 GPUs",
-        "value": round(value, 4), "unit": "GB/s", "n_gpus": args.gpus, "steps": len(times),
-        "warmup": args.warmup, "ms_per_step": round(sec * 1e3, 3), "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg.description, "sample_batch": B, "width": cfg.width},
-        "tokens_per_s": round(tokens, 1),
-        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": 1, "kind": "port",
-                         "sample": desc},
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s", "n_gpus": N, "steps": K,
+        "warmup": Wm, "ms_per_step": round(wall / K * 1e3, 3), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(cfg, N, default_slots(cfg, N, args)),
+        "tokens_per_s": round(cfg.batch * cfg.tokens * K / wall, 1),
+        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": procs, "kind": "port", "sample": desc,
+                         "cpu": _cpu_model(), "nproc": cores},
         "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "note": "reference bridge body is a stub (bridge.cpp); oracle restatement runs over the "
-                "reference's own simnet/grid compiled from /root/reference sources; simnet admits one "
-                "runnable rank at a time, so 1 effective core",
+        "per_core_gbs": round(one, 4),
+        "payload": {"unit_bytes": "bf16 activations / bf16 gradients as on the device (same as the GPU arm's value)",
+                    "bytes_per_step": payload, "f64_bytes_moved_per_step": f64,
+                    "gbs_at_f64_bytes": round(f64 * K / wall / 1e9, 4)},
+        "setup_s": round(t0 - t_init, 1),
+        "note": "reference bridge body is a stub (bridge.cpp); the oracle restatement runs over the reference's own "
+                "simnet/grid compiled from /root/reference sources (oracle/_ref)",
     }
     print(json.dumps(line), flush=True)
 
@@ -391,11 +615,7 @@ def main():
 
     tm = traffic_model(cfg, N)
     # rank-independent (every process must allocate the same number of buffer sets)
-    per_gpu_step = max(f + b for f, b in zip(tm["fwd_hbm"], tm["bwd_hbm"]))
-    # >= 3x L2 of inputs across the rotation, and >= 4 sets so one cycle graph covers 4+ steps
-    slots = args.slots or max(4, min(8, math.ceil(3 * L2_BYTES / max(per_gpu_step, 1))))
-    if not args.no_e2e:
-        slots = max(slots, 2)  # the pipelined e2e leg alternates two buffer sets
+    slots = default_slots(cfg, N, args)
 
     rt = hbb.BridgeRuntime(plan, sp, n_gpus=N, my_gpu=rank, rank_to_gpu=r2g, act_dtype=tdt[cfg.act],
                            grad_in_dtype=tdt[cfg.grad_in], grad_out_dtype=tdt[cfg.grad_out],
@@ -403,18 +623,7 @@ def main():
                            fwd_mode=args.fwd_mode, partition=args.partition)
     if N > 1:
         rt.exchange_handles()
-    gen = torch.Generator(device=dev)
-    gen.manual_seed(1234 + rank)
-    for s in range(slots):
-        for r in local:
-            for slot in (hbb.SLOT_SRC_ACT, hbb.SLOT_DST_GRAD, hbb.SLOT_TEXT, hbb.SLOT_SRC_GRAD):
-                b = rt.buffer(r, slot, s)
-                if b is None:
-                    continue
-                if slot == hbb.SLOT_SRC_GRAD:
-                    b.zero_()
-                else:
-                    b.copy_(torch.randn(b.numel(), generator=gen, device=dev, dtype=torch.float32).to(b.dtype))
+    fill_inputs(rt, local, slots, dev)
     torch.cuda.synchronize()
     stream = torch.cuda.Stream(priority=-1)
 
@@ -478,6 +687,18 @@ def main():
     if rt.status():
         raise RuntimeError("device flag wait timed out")
 
+    def run_step(k):  # one more step on buffer set k, the way the timed loop ran it
+        nonlocal mb
+        if use_graph:
+            rt.replay_step(k, stream)
+        else:
+            mb += (k - mb) % slots
+            rt.forward(mb, stream)
+            rt.backward(mb, cfg.beta, stream)
+            mb += 1
+
+    parity = check_parity(rt, cfg, plan, sp, r2g, rank, N, dev, stream, barrier, run_step, (K - 1) % slots)
+
     # per-kernel steady state: each op alone, replayed back to back as a CUDA graph
     # (includes its share of launch and barrier cost; the headline is the step above)
     K2 = max(20, min(K, 200))
@@ -538,7 +759,7 @@ def main():
             traffic = None
     tstar_step = fk["tstar_ms"] + bk["tstar_ms"]
     roofline = {
-        "bound": dom["bound"], "kernel": "copy_segments_kernel" if dom_is_fwd else "reduce_segments_kernel",
+        "bound": dom["bound"], "kernel": copy_kernel_name(args) if dom_is_fwd else reduce_kernel_name(cfg),
         "achieved": dom["achieved_gbs"], "peak": dom["peak_gbs"], "unit": "GB/s", "frac": dom["frac"],
         "traffic": traffic,
         "peak_source": pk["src"] if dom["bound"] == "hbm" else "measured peer copy 770 GB/s (B200_PROFILING.md)",
@@ -585,12 +806,13 @@ def main():
                 matrix[name] = {"error": f"{type(exc).__name__}: {exc}"}
 
     cpu = None
-    if rank == 0 and N == 1 and not args.no_cpu:
+    if rank == 0 and not args.no_cpu:  # rank 0 at every N (host cores of the GPU box)
         try:
             B = cpu_sample_batch(cfg)
             gbs, sec, desc = cpu_reference_run(cfg, B)
             cpu = {"value": round(gbs, 4), "unit": "GB/s", "cores": 1, "kind": "port", "sample": desc,
-                   "cpu": _cpu_model(), "nproc": os.cpu_count()}
+                   "cpu": _cpu_model(), "nproc": os.cpu_count(),
+                   "full_workload_arm": "bench.py --impl reference runs the full workload per step"}
             d = direct_cpu_run(cfg, B)
             if d is not None:  # informative: the same maps on every host core
                 cpu["direct"] = {"value": round(d[0], 3), "unit": "GB/s", "cores": d[2], "kind": "port",
@@ -600,22 +822,22 @@ def main():
 
     if rank == 0:
         line = {
-            "metric": "boundary reshard GB/s per GPU (fwd+bwd) vs NVLink/HBM roofline at 1/2/4/8 GPUs",
+            "metric": METRIC,
             "value": round(value, 2), "unit": "GB/s", "n_gpus": N, "steps": K, "warmup": args.warmup,
             "ms_per_step": round(ms_step, 5), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": cfg.act, "data": "synthetic",
-            "config": {"workload": cfg.description + (f" (hidden /{args.scale})" if args.scale > 1 else ""), "name": cfg.name, "global_batch": cfg.batch,
-                       "tokens_per_sample": cfg.tokens, "hidden": cfg.hidden,
-                       "logical_ranks": plan.world, "rank_to_gpu": r2g,
-                       "grad_in": cfg.grad_in, "grad_out": cfg.grad_out, "beta": cfg.beta,
-                       "launch": (f"one CUDA graph per cycle of {slots} steps (fwd+bwd on each buffer set in "
+            "config": workload_config(cfg, N, slots, args.scale),
+            "value_semantics": "whole job: boundary payload bytes of all N GPUs per second (bench contract); "
+                               "per GPU = per_gpu_gbs",
+            "per_gpu_gbs": round(value / N, 2), "tokens_per_s": round(tokens_s, 1),
+            "method": {"launch": (f"one CUDA graph per cycle of {slots} steps (fwd+bwd on each buffer set in "
                                   f"turn; K % {slots} steps as one graph each)") if cycle else
                                  ("one CUDA graph (fwd+bwd) per step" if use_graph else "per-op C-ABI launches"),
                        "ms_per_step_one_graph_per_step": ms_graph_per_step,
-                       "l2": f"inputs rotate over {slots} buffer set(s); per-GPU bytes per step "
-                             f"{per_gpu_step / 1e6:.1f} MB x {slots} sets > 126 MB L2"},
-            "per_gpu_gbs": round(value / N, 2), "tokens_per_s": round(tokens_s, 1),
+                       "timing": "CUDA events on the launching stream, barrier + synchronize on both sides, "
+                                 "max over ranks"},
             "payload_bytes_per_step": {"fwd": fwd_b, "bwd": bwd_b},
+            "parity": parity,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clocks,
             "nccl_comparison": nccl,
@@ -627,6 +849,15 @@ def main():
         rt.close()
     if N > 1:
         dist.destroy_process_group()
+
+
+def copy_kernel_name(args):
+    return "copy_segments_tma_kernel" if args.partition in (0, 4) else "copy_segments_kernel"
+
+
+def reduce_kernel_name(cfg):
+    tn = {"bf16": "__nv_bfloat16", "fp16": "__half", "fp32": "float"}
+    return f"reduce_segments_kernel<{tn[cfg.grad_in]},{tn[cfg.grad_out]}>"
 
 
 def run_matrix_config(args, name, N, rank, dev, barrier, stream, pk):
@@ -653,18 +884,7 @@ def run_matrix_config(args, name, N, rank, dev, barrier, stream, pk):
     try:
         if N > 1:
             rt.exchange_handles()
-        gen = torch.Generator(device=dev)
-        gen.manual_seed(4321 + rank)
-        for s in range(slots):
-            for r in local:
-                for slot in (hbb.SLOT_SRC_ACT, hbb.SLOT_DST_GRAD, hbb.SLOT_TEXT, hbb.SLOT_SRC_GRAD):
-                    b = rt.buffer(r, slot, s)
-                    if b is None:
-                        continue
-                    if slot == hbb.SLOT_SRC_GRAD:
-                        b.zero_()
-                    else:
-                        b.copy_(torch.randn(b.numel(), generator=gen, device=dev).to(b.dtype))
+        fill_inputs(rt, local, slots, dev)
         for mb in range(3):
             rt.forward(mb, stream)
             rt.backward(mb, cfg.beta, stream)
@@ -706,6 +926,8 @@ def run_matrix_config(args, name, N, rank, dev, barrier, stream, pk):
                 dist.all_reduce(t, op=dist.ReduceOp.MAX)
             barrier()
             ms_step = t.item()
+        parity = check_parity(rt, cfg, plan, sp, r2g, rank, N, dev, stream, barrier,
+                              lambda k: rt.replay_step(k, stream), 0)
         f_ms, b_ms = timed(0, K), timed(2, K)
         if rt.status():
             raise RuntimeError("device flag wait timed out")
@@ -719,7 +941,7 @@ def run_matrix_config(args, name, N, rank, dev, barrier, stream, pk):
                "fwd_ms": fk["ms"], "fwd_tstar_ms": fk["tstar_ms"], "fwd_bound": fk["bound"],
                "bwd_ms": bk["ms"], "bwd_tstar_ms": bk["tstar_ms"], "bwd_bound": bk["bound"],
                "ms_per_step_one_graph_per_step": round(ms_step_pg, 5),
-               "steps": K, "buffer_sets": slots, "rank_to_gpu": r2g}
+               "steps": K, "buffer_sets": slots, "rank_to_gpu": r2g, "parity": parity}
         if N > 1 and cfg.dst.pp > 1 and cfg.src.rank_offset != cfg.dst.rank_offset and not args.no_overlap:
             out["overlap_with_pp_p2p"] = run_pp_overlap(args, cfg, plan, rt, r2g, rank, dev, barrier, stream,
                                                         slots)

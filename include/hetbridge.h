@@ -172,8 +172,12 @@ typedef struct {
    * the forward gathers each text row from the embedding table set with
    * hb_exec_set_text_embedding (the LLM's embedding lookup fused into the
    * splice). An id outside [0, vocab) makes hb_exec_status
-   * return InvalidArgument (device error 2). */
+   * return InvalidArgument (device error 2); that row is left unwritten. */
   int text_embedding;
+  /* cap on every boundary kernel's grid (0 = fill the GPU): leaves SMs to
+   * concurrent work such as pipeline P2P, and lets several execs of one group
+   * share a device (hb_exec_open_peers_local). */
+  int max_ctas;
 } hb_exec_config;
 void hb_exec_config_default(hb_exec_config* c);
 
@@ -186,6 +190,13 @@ int hb_exec_create(const hb_plan* p, const hb_splice* s, int n_gpus, int my_gpu,
 void hb_exec_destroy(hb_exec* x);
 int hb_exec_ipc_handle(hb_exec* x, void* out64);
 int hb_exec_open_peers(hb_exec* x, const void* handles, size_t nbytes); /* n_gpus*64 bytes */
+/* Single-process form of the group setup (one host thread drives every GPU of
+ * the group, as the reference's "one script per rank" collapsed into one
+ * process): execs[g] = this process's exec of GPU g (n = n_gpus; execs[my_gpu]
+ * ignored). Peer regions are used directly; peer access is enabled between
+ * distinct devices; execs of one group may also share a device (set max_ctas
+ * so their grids are co-resident). Every exec must outlive its peers' ops. */
+int hb_exec_open_peers_local(hb_exec* x, hb_exec* const* execs, int n);
 int hb_exec_buffer(hb_exec* x, int rank, int slot, int mb_slot, void** ptr, size_t* bytes);
 int hb_exec_bind(hb_exec* x, int rank, int slot, int mb_slot, void* ptr, size_t bytes);
 /* forward: BridgeRuntime::forward_{source,dest,colocated} for every resident rank */
@@ -223,13 +234,15 @@ int hb_exec_trace(hb_exec* x, int kind, unsigned long long* out, int max_ctas, i
 int hb_projector_gemm(const void* x, long long ldx, const void* w, long long ldw, void* const* row_dst, int fan,
                       int M, int N, int K, void* cuda_stream);
 /* Boundary forward with the projector fused in: x = the pre-projection token
- * rows of every local source rank stacked in ascending rank order [rows x K],
- * w = the projector weight [d_h x K]; each projected row is stored straight
- * into every destination row of the plan (the source shards are never
- * written). Replaces forward_* for that microbatch (records it like
- * hb_exec_forward). One GPU, non-splice edges, bf16 activations. */
-int hb_exec_forward_projected(hb_exec* x, int mb, const void* act, long long ldx, const void* w, long long ldw,
-                              int d_h, int K, void* cuda_stream);
+ * rows of every local source rank stacked in ascending rank order [x_rows x K]
+ * (x_rows must equal those ranks' token rows, else ShapeMismatch), w = the
+ * projector weight [d_h x K]; each projected row is stored straight into
+ * every destination row of the plan, local or on a peer GPU (push over
+ * NVSwitch; the source shards are never written). Replaces forward_* for that
+ * microbatch (records it like hb_exec_forward). Any GPU count, non-splice
+ * edges, bf16 activations. */
+int hb_exec_forward_projected(hb_exec* x, int mb, const void* act, long long x_rows, long long ldx, const void* w,
+                              long long ldw, int d_h, int K, void* cuda_stream);
 
 #ifdef __cplusplus
 }

@@ -31,7 +31,7 @@ EXPORTS = [
     "hb_cp_token_slice", "hb_splice_create", "hb_splice_destroy",
     "hb_index_forward", "hb_index_backward", "hb_index_backward_balanced", "hb_index_buffer_elems",
     "hb_exec_config_default", "hb_exec_create", "hb_exec_destroy", "hb_exec_ipc_handle",
-    "hb_exec_open_peers", "hb_exec_buffer", "hb_exec_bind", "hb_exec_forward", "hb_exec_backward",
+    "hb_exec_open_peers", "hb_exec_open_peers_local", "hb_exec_buffer", "hb_exec_bind", "hb_exec_forward", "hb_exec_backward",
     "hb_exec_seed_forward_record", "hb_exec_status", "hb_exec_stats", "hb_exec_graph_capture", "hb_projector_gemm",
     "hb_exec_forward_projected", "hb_exec_set_text_embedding",
     "hb_exec_graph_launch", "hb_exec_trace",
@@ -80,7 +80,7 @@ class ExecConfig(ctypes.Structure):
                 ("internal_alloc", ctypes.c_int), ("blocks_per_sm", ctypes.c_int),
                 ("threads", ctypes.c_int), ("timeout_s", ctypes.c_double), ("fwd_mode", ctypes.c_int),
                 ("partition", ctypes.c_int), ("strict_provenance", ctypes.c_int),
-                ("text_embedding", ctypes.c_int)]
+                ("text_embedding", ctypes.c_int), ("max_ctas", ctypes.c_int)]
 
 
 _lib = None
@@ -119,6 +119,7 @@ def _declare(L):
         "hb_exec_destroy": (None, [V]),
         "hb_exec_ipc_handle": (I, [V, V]),
         "hb_exec_open_peers": (I, [V, V, Sz]),
+        "hb_exec_open_peers_local": (I, [V, P(V), I]),
         "hb_exec_buffer": (I, [V, I, I, I, P(V), P(Sz)]),
         "hb_exec_bind": (I, [V, I, I, I, V, Sz]),
         "hb_exec_forward": (I, [V, I, V]),
@@ -129,7 +130,7 @@ def _declare(L):
         "hb_exec_status": (I, [V, P(U)]),
         "hb_exec_stats": (I, [V, P(LL), P(LL), P(LL), P(LL), P(LL)]),
         "hb_projector_gemm": (I, [V, LL, V, LL, V, I, I, I, I, V]),
-        "hb_exec_forward_projected": (I, [V, I, V, LL, V, LL, I, I, V]),
+        "hb_exec_forward_projected": (I, [V, I, V, LL, LL, V, LL, I, I, V]),
         "hb_exec_set_text_embedding": (I, [V, V, LL]),
         "hb_exec_trace": (I, [V, I, V, I, P(I), P(I)]),
         "hb_config_parse": (I, [C, P(V)]),

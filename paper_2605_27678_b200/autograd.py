@@ -79,7 +79,10 @@ class _Boundary(torch.autograd.Function):
             elif g.data_ptr() != buf.data_ptr():
                 buf.copy_(g.reshape(buf.shape))
         rt.backward(mb, 0.0, torch.cuda.current_stream())
-        out = [_view(rt, r, SLOT_SRC_GRAD, mb).to(dt).view(shape) for r, (dt, shape) in zip(src_ranks, ctx.src_meta)]
+        # always a fresh tensor: an alias of SRC_GRAD could be kept as a leaf's
+        # .grad by AccumulateGrad and then overwritten when the set is reused
+        out = [_view(rt, r, SLOT_SRC_GRAD, mb).to(dt, copy=True).view(shape)
+               for r, (dt, shape) in zip(src_ranks, ctx.src_meta)]
         return (None, None, *out)
 
 
@@ -187,7 +190,7 @@ class PackedBoundary:
                 for t, g in zip(self._enc_out[mb], grads[mb]):
                     if t.requires_grad:
                         outs.append(t)
-                        gs.append(g.to(t.dtype).view(t.shape))
+                        gs.append(g.to(t.dtype, copy=True).view(t.shape))  # never an alias of SRC_GRAD
             if outs:
                 torch.autograd.backward(outs, gs)
         for row in self._leaves:

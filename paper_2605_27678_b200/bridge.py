@@ -210,7 +210,7 @@ class BridgeRuntime:
                  grad_out_dtype=None, mb_slots: int = 1, internal_alloc: bool = True,
                  blocks_per_sm: int = 0, threads: int = 0, timeout_s: float = 0.0,
                  fwd_mode: int = 0, partition: int = 0, strict_provenance: bool = False,
-                 text_embedding: bool = False):
+                 text_embedding: bool = False, max_ctas: int = 0):
         import torch
 
         self.plan, self.splice = plan, splice
@@ -234,9 +234,11 @@ class BridgeRuntime:
         cfg.partition = partition
         cfg.strict_provenance = 1 if strict_provenance else 0
         cfg.text_embedding = 1 if text_embedding else 0
+        cfg.max_ctas = max_ctas
         self.text_embedding = bool(text_embedding)
         if not torch.cuda.is_available():
             raise HetBridgeError(25, "BridgeRuntime needs a CUDA device (no CPU fallback)")
+        self.device = torch.device("cuda", torch.cuda.current_device())  # the exec's GPU
         m = (ctypes.c_int * len(self.rank_to_gpu))(*self.rank_to_gpu)
         h = ctypes.c_void_p()
         check(lib().hb_exec_create(plan._h, splice._h if splice else None, n_gpus, my_gpu, m,
@@ -252,6 +254,12 @@ class BridgeRuntime:
 
     def open_peers(self, handles: bytes):
         check(lib().hb_exec_open_peers(self._h, handles, len(handles)))
+
+    def open_peers_local(self, runtimes):
+        """Single-process group setup (hb_exec_open_peers_local): ``runtimes[g]``
+        is this process's runtime of GPU g of the group."""
+        arr = (ctypes.c_void_p * len(runtimes))(*[rt._h.value if rt is not None else None for rt in runtimes])
+        check(lib().hb_exec_open_peers_local(self._h, arr, len(runtimes)))
 
     def exchange_handles(self, group=None):
         """All-gather the 64-byte IPC handles over torch.distributed and open peers."""
@@ -301,7 +309,7 @@ class BridgeRuntime:
         check(lib().hb_exec_buffer(self._h, rank, slot, mb_slot, ctypes.byref(p), ctypes.byref(n)))
         if not p.value or n.value == 0:
             return None
-        raw = torch.as_tensor(_CAI(p.value, n.value), device=f"cuda:{torch.cuda.current_device()}")
+        raw = torch.as_tensor(_CAI(p.value, n.value), device=self.device)
         return raw.view(self._dtype_of(slot))
 
     def bind(self, rank: int, slot: int, tensor, mb_slot: int = 0):
@@ -336,15 +344,28 @@ class BridgeRuntime:
     def forward_projected(self, mb: int, x, w, stream=None):
         """Forward with the encoder projector fused in (hb_exec_forward_projected):
         x [rows, K] bf16 = pre-projection token rows of the local source ranks
-        stacked in ascending rank order; w [d_h, K] bf16. Each projected row goes
-        straight to every destination row; SRC_ACT is not written."""
+        stacked in ascending rank order (``rows`` = those ranks' token rows; x
+        may be None when this GPU hosts no source rank); w [d_h, K] bf16. Each
+        projected row goes straight to every destination row; SRC_ACT is not
+        written."""
         import torch
 
-        if x.dtype != torch.bfloat16 or w.dtype != torch.bfloat16 or x.stride(1) != 1 or w.stride(1) != 1:
-            raise HetBridgeError(24, "forward_projected takes row-major bf16 x and w")
-        check(lib().hb_exec_forward_projected(self._h, mb, ctypes.c_void_p(x.data_ptr()), x.stride(0),
-                                              ctypes.c_void_p(w.data_ptr()), w.stride(0), w.shape[0], w.shape[1],
-                                              self._stream(stream)))
+        if w.dtype != torch.bfloat16 or w.dim() != 2 or w.stride(1) != 1:
+            raise HetBridgeError(24, "forward_projected takes a row-major bf16 weight [d_h, K]")
+        d_h, K = w.shape
+        rows = sum(self.buffer_numel(r, SLOT_SRC_ACT) for r in self.local_ranks(SLOT_SRC_ACT)) // d_h
+        if x is None:
+            if rows:
+                raise HetBridgeError(13, f"forward_projected needs x [{rows}, {K}] for the local source ranks")
+            xp, ldx = None, K
+        else:
+            if x.dtype != torch.bfloat16 or x.dim() != 2 or x.stride(1) != 1 or not x.is_cuda:
+                raise HetBridgeError(24, "forward_projected takes a row-major bf16 CUDA x [rows, K]")
+            if tuple(x.shape) != (rows, K):
+                raise HetBridgeError(13, f"x is {tuple(x.shape)}, the local source ranks need ({rows}, {K})")
+            xp, ldx = ctypes.c_void_p(x.data_ptr()), x.stride(0)
+        check(lib().hb_exec_forward_projected(self._h, mb, xp, rows, ldx, ctypes.c_void_p(w.data_ptr()),
+                                              w.stride(0), d_h, K, self._stream(stream)))
 
     def backward(self, mb: int = 0, beta: float = 0.0, stream=None):
         check(lib().hb_exec_backward(self._h, mb, ctypes.c_float(beta), self._stream(stream)))
@@ -398,6 +419,69 @@ class BridgeRuntime:
             self.close()
         except Exception:
             pass
+
+
+class LocalGroup:
+    """One process driving a whole exec group: one :class:`BridgeRuntime` per
+    (virtual) GPU g on ``devices[g]``, peers opened with
+    hb_exec_open_peers_local, each op launched on every GPU's stream from this
+    thread (the kernels of one op run concurrently and meet in the in-kernel
+    barrier). ``devices`` may repeat a device: several execs then share it and
+    ``max_ctas`` (default: an equal share of two CTAs per SM) keeps their grids
+    co-resident, so the cross-GPU protocol runs on a single physical GPU."""
+
+    def __init__(self, plan: BridgePlan, splice: SpliceSpec | None = None, *, devices, rank_to_gpu=None,
+                 max_ctas: int | None = None, **kw):
+        import torch
+
+        self.devices = [torch.device("cuda", d) if isinstance(d, int) else torch.device(d) for d in devices]
+        n = len(self.devices)
+        shared = len({d.index for d in self.devices}) < n
+        if max_ctas is None:
+            per_dev = {}
+            for d in self.devices:
+                per_dev[d.index] = per_dev.get(d.index, 0) + 1
+            sms = torch.cuda.get_device_properties(self.devices[0]).multi_processor_count
+            max_ctas = (2 * sms) // max(per_dev.values()) if shared else 0
+        from .configs import rank_to_gpu as _r2g
+
+        r2g = list(rank_to_gpu) if rank_to_gpu is not None else _r2g(plan.world, n)
+        self.rts, self.streams = [], []
+        for g, d in enumerate(self.devices):
+            with torch.cuda.device(d):
+                self.rts.append(BridgeRuntime(plan, splice, n_gpus=n, my_gpu=g, rank_to_gpu=r2g,
+                                              max_ctas=max_ctas, **kw))
+                self.streams.append(torch.cuda.Stream(device=d))
+        for rt in self.rts:
+            rt.open_peers_local(self.rts)
+        self.plan, self.splice, self.rank_to_gpu, self.max_ctas = plan, splice, r2g, max_ctas
+
+    def runtime_of(self, rank: int) -> "BridgeRuntime":
+        return self.rts[self.rank_to_gpu[rank]]
+
+    def buffer(self, rank: int, slot: int, mb_slot: int = 0):
+        return self.runtime_of(rank).buffer(rank, slot, mb_slot)
+
+    def forward(self, mb: int = 0):
+        for rt, st in zip(self.rts, self.streams):
+            rt.forward(mb, st)
+
+    def backward(self, mb: int = 0, beta: float = 0.0):
+        for rt, st in zip(self.rts, self.streams):
+            rt.backward(mb, beta, st)
+
+    def synchronize(self):
+        for st in self.streams:
+            st.synchronize()
+
+    def status(self) -> int:
+        return max(rt.status() for rt in self.rts)
+
+    def close(self):
+        self.synchronize()
+        for rt in self.rts:
+            rt.close()
+        self.rts = []
 
 
 def _stage_ranks(layout: ModuleLayout, stage: int):

@@ -116,6 +116,16 @@ def get(name: str, scale: int = 1) -> BoundaryConfig:
         return BoundaryConfig("c3x4", "fan-out colocated enc{tp4} -> llm{dp4}, bf16 h5120, 32 img x 576",
                               ModuleLayout("encoder", tp=4), ModuleLayout("llm", dp=4), 32, 576, h(5120),
                               logical_world=4)
+    # Deliver layouts: the source's last stage is not the
+    # whole rank range, so destination ranks without the data get a DeliverStep.
+    if name == "c3p":  # C3' (SURVEY §8 config shorthand): encoder pp4, last stage {r6, r7}
+        return BoundaryConfig("c3p", "fan-out with deliver enc{pp4,dp2} -> llm{dp8}, bf16 h5120, 64 img x 576",
+                              ModuleLayout("encoder", pp=4, dp=2), ModuleLayout("llm", dp=8), 64, 576, h(5120))
+    if name == "appc":  # paper App. C tp2_pp2 colocated doubled: dest stage 0 = {0..3}
+        return BoundaryConfig("appc", "equal-DP with deliver vision{tp4,dp2} -> language{tp2,pp2,dp2}, bf16 h4096, "
+                                      "64 img x 576",
+                              ModuleLayout("vision", tp=4, dp=2), ModuleLayout("language", tp=2, pp=2, dp=2), 64, 576,
+                              h(4096))
     raise KeyError(name)
 
 

@@ -93,7 +93,7 @@ const char* hb_error_name(int status) {
   return hb::error_code_name(static_cast<hb::ErrorCode>(status - 1));
 }
 
-int hb_abi_version(void) { return 6; }
+int hb_abi_version(void) { return 7; }
 
 int hb_coord_of_rank(const hb_layout* l, int rank, int coord4[4]) {
   return guard([&] {
@@ -378,6 +378,7 @@ void hb_exec_config_default(hb_exec_config* c) {
   c->partition = d.partition;
   c->strict_provenance = d.strict_provenance;
   c->text_embedding = d.text_embedding;
+  c->max_ctas = d.max_ctas;
 }
 
 int hb_exec_create(const hb_plan* p, const hb_splice* s, int n_gpus, int my_gpu, const int* rank_to_gpu,
@@ -400,6 +401,7 @@ int hb_exec_create(const hb_plan* p, const hb_splice* s, int n_gpus, int my_gpu,
       c.partition = cfg->partition;
       c.strict_provenance = cfg->strict_provenance;
       c.text_embedding = cfg->text_embedding;
+      c.max_ctas = cfg->max_ctas > 0 ? cfg->max_ctas : 0;
     }
     std::vector<int> map;
     if (rank_to_gpu) map.assign(rank_to_gpu, rank_to_gpu + n_ranks);
@@ -426,6 +428,17 @@ int hb_exec_open_peers(hb_exec* x, const void* handles, size_t nbytes) {
     need(handles, "handles");
     (void)nbytes;
     x->x->open_peers(handles);
+  });
+}
+
+int hb_exec_open_peers_local(hb_exec* x, hb_exec* const* execs, int n) {
+  return guard([&] {
+    need(x, "exec");
+    need(execs, "execs");
+    if (n < 1 || n > hb::dev::kMaxGpus) hb::raise(hb::ErrorCode::InvalidArgument, "bad exec count");
+    std::vector<hb::rt::Exec*> v(n, nullptr);
+    for (int g = 0; g < n; ++g) v[g] = execs[g] ? execs[g]->x.get() : nullptr;
+    x->x->open_peers_local(v.data(), n);
   });
 }
 
@@ -515,12 +528,12 @@ int hb_exec_set_text_embedding(hb_exec* x, const void* table, long long vocab) {
   });
 }
 
-int hb_exec_forward_projected(hb_exec* x, int mb, const void* act, long long ldx, const void* w, long long ldw,
-                              int d_h, int K, void* cuda_stream) {
+int hb_exec_forward_projected(hb_exec* x, int mb, const void* act, long long x_rows, long long ldx, const void* w,
+                              long long ldw, int d_h, int K, void* cuda_stream) {
   return guard([&] {
     need(x, "exec");
     need(w, "w");  // act may be null when this GPU hosts no source rank
-    x->x->forward_projected(mb, act, ldx, w, ldw, d_h, K, cuda_stream);
+    x->x->forward_projected(mb, act, ldx, w, ldw, d_h, K, x_rows, cuda_stream);
   });
 }
 

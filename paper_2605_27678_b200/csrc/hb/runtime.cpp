@@ -20,6 +20,20 @@ void ck(cudaError_t e, const char* what) {
     raise(ErrorCode::CudaError, std::string(what) + ": " + cudaGetErrorString(e));
 }
 constexpr uint64_t kPadBytes = 4096;
+// Makes the exec's device current for the scope (one host thread may drive
+// several GPUs' execs; kernels must go to the device their stream belongs to).
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) == cudaSuccess && prev != dev) cudaSetDevice(dev);
+    else prev = -1;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
 constexpr uint64_t kAlign = 256;
 uint64_t align_up(uint64_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 }  // namespace
@@ -120,6 +134,7 @@ Exec::Exec(const bridge::BridgePlan& plan, const index::SpliceSpec* splice, int 
     ck(cudaMemset(trace_, 0, tb), "cudaMemset(trace)");
   }
   peer_base_.assign(n_gpus_, nullptr);
+  peer_ipc_.assign(n_gpus_, 0);
   peer_base_[my_gpu_] = local_base_;
   tables_.resize(cfg.mb_slots);
   proj_.resize(cfg.mb_slots);
@@ -132,6 +147,7 @@ Exec::Exec(const bridge::BridgePlan& plan, const index::SpliceSpec* splice, int 
 }
 
 Exec::~Exec() {
+  DeviceGuard dg(device_);
   for (auto& kv : graphs_) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(kv.second.first));
   for (auto& t : proj_) cudaFree(t.rows_dev);
   for (auto& t : tables_) {
@@ -146,7 +162,7 @@ Exec::~Exec() {
   }
   cudaFree(bwd_part_.first_seg);
   for (int g = 0; g < n_gpus_; ++g)
-    if (g != my_gpu_ && peer_base_[g]) cudaIpcCloseMemHandle(peer_base_[g]);
+    if (g != my_gpu_ && peer_base_[g] && peer_ipc_[g]) cudaIpcCloseMemHandle(peer_base_[g]);
   cudaFree(local_base_);
   cudaFree(ctr_);
   cudaFree(trace_);
@@ -189,6 +205,7 @@ void Exec::ipc_handle(void* out64) const {
 }
 
 void Exec::open_peers(const void* handles) {
+  DeviceGuard dg(device_);
   for (int g = 0; g < n_gpus_; ++g) {
     if (g == my_gpu_ || !((group_mask_ >> g) & 1u) || peer_base_[g]) continue;
     cudaIpcMemHandle_t h;
@@ -196,11 +213,53 @@ void Exec::open_peers(const void* handles) {
     void* p = nullptr;
     ck(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
     peer_base_[g] = static_cast<unsigned char*>(p);
+    peer_ipc_[g] = 1;
   }
   sync_fwd_ = make_sync_args(kFwdKind, fwd_push_);
   sync_bwd_ = make_sync_args(kBwdKind, false);
   sync_proj_ = make_sync_args(kProjKind, true);
+  mark_dirty();
+}
+
+void Exec::open_peers_local(Exec* const* execs, int n) {
+  DeviceGuard dg(device_);
+  if (n != n_gpus_) raise(ErrorCode::InvalidArgument, "open_peers_local needs one exec per GPU of the group");
+  for (int g = 0; g < n_gpus_; ++g) {
+    if (g == my_gpu_ || !((group_mask_ >> g) & 1u) || peer_base_[g]) continue;
+    const Exec* p = execs[g];
+    if (!p || p == this) raise(ErrorCode::InvalidArgument, "open_peers_local: missing exec of GPU " + std::to_string(g));
+    // the symmetric layout: every exec of the group derived the same offsets from the same plan
+    if (p->my_gpu_ != g || p->n_gpus_ != n_gpus_ || p->rank_to_gpu_ != rank_to_gpu_ || p->offsets_ != offsets_ ||
+        p->mb_stride_ != mb_stride_ || p->cfg_.mb_slots != cfg_.mb_slots || !p->local_base_)
+      raise(ErrorCode::InvalidArgument, "open_peers_local: exec of GPU " + std::to_string(g) +
+                                            " has a different configuration or no device region");
+    if (p->device_ != device_) {
+      int can = 0;
+      ck(cudaDeviceCanAccessPeer(&can, device_, p->device_), "cudaDeviceCanAccessPeer");
+      if (!can) raise(ErrorCode::CudaError, "no peer access from device " + std::to_string(device_) + " to " +
+                                                std::to_string(p->device_));
+      const cudaError_t e = cudaDeviceEnablePeerAccess(p->device_, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+      else ck(e, "cudaDeviceEnablePeerAccess");
+    }
+    peer_base_[g] = p->local_base_;
+  }
+  sync_fwd_ = make_sync_args(kFwdKind, fwd_push_);
+  sync_bwd_ = make_sync_args(kBwdKind, false);
+  sync_proj_ = make_sync_args(kProjKind, true);
+  mark_dirty();
+}
+
+// Every change of a buffer pointer, the peer mapping or the embedding table
+// rebuilds the device tables at the next op, and captured graphs hold the old
+// tables' addresses as kernel arguments: drop them (an in-flight replay
+// finishes first, cudaGraphExecDestroy defers) so a stale replay cannot
+// touch freed tables; graph_launch then asks for a recapture.
+void Exec::mark_dirty() {
   dirty_fwd_ = dirty_bwd_ = true;
+  for (auto& kv : graphs_) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(kv.second.first));
+  if (!graphs_.empty()) graphs_invalidated_ = true;
+  graphs_.clear();
 }
 
 void* Exec::buffer(int rank, int slot, int mb_slot, size_t* bytes) const {
@@ -221,7 +280,7 @@ void Exec::bind(int rank, int slot, int mb_slot, void* ptr, size_t bytes) {
   if (n_gpus_ > 1)
     raise(ErrorCode::InvalidArgument, "external buffers are single-GPU only; use buffer() on multi-GPU");
   bound_[rank * index::kNumSlots + slot][mb_slot] = ptr;
-  dirty_fwd_ = dirty_bwd_ = true;
+  mark_dirty();
 }
 
 const void* Exec::resolve(int rank, int slot, int mb_slot) const {
@@ -393,10 +452,10 @@ void Exec::upload_copies(int mb, uint64_t unit, std::vector<uint64_t>* w0s, std:
 int Exec::copy_grid() const {
   if (copy_mode() == dev::kPartTma) {
     const int occ = dev::tma_blocks_per_sm(dev::tma_chunk_bytes(kTmaChunkKiB));
-    return sm_count_ * (cfg_.blocks_per_sm > 0 ? std::min(cfg_.blocks_per_sm, occ) : occ);
+    return grid_cap(sm_count_ * (cfg_.blocks_per_sm > 0 ? std::min(cfg_.blocks_per_sm, occ) : occ));
   }
   const int occ = dev::copy_blocks_per_sm(cfg_.threads);
-  return sm_count_ * (cfg_.blocks_per_sm > 0 ? std::min(cfg_.blocks_per_sm, occ) : occ);
+  return grid_cap(sm_count_ * (cfg_.blocks_per_sm > 0 ? std::min(cfg_.blocks_per_sm, occ) : occ));
 }
 
 void Exec::prepare_fwd() {
@@ -431,8 +490,8 @@ void Exec::prepare_bwd() {
     // at 1/8 width 12.5 -> 9.0 us with 8K chunks; C2 N=1 best at 32K)
     uint64_t total = 0;
     for (const auto& s : bwd_local_) total += static_cast<uint64_t>(s.n);
-    const uint64_t grid = static_cast<uint64_t>(sm_count_) *
-                          dev::reduce_blocks_per_sm(cfg_.threads, cfg_.grad_in_dtype, cfg_.grad_out_dtype);
+    const uint64_t grid = static_cast<uint64_t>(
+        grid_cap(sm_count_ * dev::reduce_blocks_per_sm(cfg_.threads, cfg_.grad_in_dtype, cfg_.grad_out_dtype)));
     unit = 8192;
     while (unit < 32768 && total / (2 * unit) >= 2 * grid) unit *= 2;
   }
@@ -521,7 +580,7 @@ void Exec::prepare_bwd() {
   bwd_groups_ = static_cast<int>(groups.size());
   int fan = 0;
   for (const auto& g : groups) fan |= g.size() > 1;
-  build_partition(w0s, ns, rem, lb, rb, sm_count_ * bps, mode, unit, &bwd_part_);
+  build_partition(w0s, ns, rem, lb, rb, grid_cap(sm_count_ * bps), mode, unit, &bwd_part_);
   bwd_part_.ring = static_cast<int>(env_u64("HB_RED_RING", 1));  // A/B knob: 0 = LDG for remote chunks too
   bwd_part_.fan = fan;
   dirty_bwd_ = false;
@@ -575,18 +634,33 @@ void Exec::launch_backward(int mb_slot, float beta, void* stream) {
   ++launches_;
 }
 
-void Exec::forward(int mb, void* stream) {
+// A forward writes buffer set mb % mb_slots; a microbatch still awaiting its
+// backward on the same set would have its activations (and, later, its
+// gradients) overwritten, so in-flight microbatches must map to distinct sets
+// (mb_slots >= microbatches in flight).
+void Exec::check_forward_mb(int mb) const {
+  if (mb < 0) raise(ErrorCode::InvalidArgument, "microbatch index must be >= 0");
   if (fwd_done_.count(mb))
     raise(ErrorCode::InvalidArgument, "microbatch " + std::to_string(mb) + " forwarded twice without backward");
+  for (int m : fwd_done_)
+    if (m % cfg_.mb_slots == mb % cfg_.mb_slots)
+      raise(ErrorCode::InvalidArgument, "microbatch " + std::to_string(mb) + " shares buffer set " +
+                                            std::to_string(mb % cfg_.mb_slots) + " with in-flight microbatch " +
+                                            std::to_string(m) + " (raise mb_slots)");
+}
+
+void Exec::forward(int mb, void* stream) {
+  DeviceGuard dg(device_);
+  check_forward_mb(mb);
   prepare_fwd();
   launch_forward(mb % cfg_.mb_slots, stream);
   fwd_done_.insert(mb);
 }
 
 void Exec::forward_projected(int mb, const void* x, int64_t ldx, const void* w, int64_t ldw, int d_h, int K,
-                             void* stream) {
-  if (fwd_done_.count(mb))
-    raise(ErrorCode::InvalidArgument, "microbatch " + std::to_string(mb) + " forwarded twice without backward");
+                             int64_t x_rows, void* stream) {
+  DeviceGuard dg(device_);
+  check_forward_mb(mb);
   if (cfg_.act_dtype != dev::kBF16) raise(ErrorCode::InvalidArgument, "the fused projector writes bf16 activations");
   for (int r = 0; r < map_.world; ++r)
     if (map_.elems[r][index::kText])
@@ -633,8 +707,16 @@ void Exec::forward_projected(int mb, const void* x, int64_t ldx, const void* w, 
     P.rows = static_cast<int>(rows);
   }
   if (P.rows > 0 && !x) raise(ErrorCode::InvalidArgument, "null projector input for the local source rows");
+  // the TMA map spans P.rows x K of x: a shorter or narrower operand would be read out of bounds
+  if (x_rows != P.rows)
+    raise(ErrorCode::ShapeMismatch, "projector input has " + std::to_string(x_rows) + " rows, the local source ranks need " +
+                                        std::to_string(P.rows));
+  if (P.rows > 0 && ldx < K) raise(ErrorCode::ShapeMismatch, "projector input leading dimension < K");
+  if (ldw < K) raise(ErrorCode::ShapeMismatch, "projector weight leading dimension < K");
   const dev::ProjectorArgs a{P.rows, d_h, K, P.rows_dev, P.fan, sync_proj_};
-  const int st = dev::launch_projector(x, ldx, w, ldw, a, sm_count_, stream);
+  // persistent GEMM: one CTA per SM in CTA pairs, so the cap is rounded down to even
+  const int proj_ctas = cfg_.max_ctas > 0 ? std::max(2, std::min(sm_count_, cfg_.max_ctas) & ~1) : sm_count_;
+  const int st = dev::launch_projector(x, ldx, w, ldw, a, proj_ctas, stream);
   if (st) raise(st == 3 ? ErrorCode::InvalidArgument : ErrorCode::CudaError,
                 "projector GEMM launch failed (" + std::to_string(st) + ")");
   ++launches_;
@@ -642,6 +724,7 @@ void Exec::forward_projected(int mb, const void* x, int64_t ldx, const void* w, 
 }
 
 void Exec::backward(int mb, float beta, void* stream) {
+  DeviceGuard dg(device_);
   if (!fwd_done_.count(mb))
     raise(ErrorCode::UnknownMicrobatch, "no forward record for microbatch " + std::to_string(mb));
   prepare_bwd();
@@ -650,6 +733,7 @@ void Exec::backward(int mb, float beta, void* stream) {
 }
 
 void Exec::graph_capture(int mb_slot, int what, float beta, void* stream) {
+  DeviceGuard dg(device_);
   if (mb_slot < 0 || mb_slot >= cfg_.mb_slots) raise(ErrorCode::InvalidArgument, "mb slot out of range");
   if (what < 0 || what > 3)
     raise(ErrorCode::InvalidArgument, "graph 'what' must be 0 (fwd), 1 (fwd+bwd), 2 (bwd), 3 (a step per buffer set)");
@@ -685,24 +769,32 @@ void Exec::graph_capture(int mb_slot, int what, float beta, void* stream) {
 }
 
 void Exec::graph_launch(int mb_slot, int what, void* stream) {
+  DeviceGuard dg(device_);
   auto it = graphs_.find(std::make_pair(what == 3 ? 0 : mb_slot, what));
-  if (it == graphs_.end()) raise(ErrorCode::InvalidArgument, "no graph captured for this (mb slot, what)");
+  if (it == graphs_.end())
+    raise(ErrorCode::InvalidArgument,
+          graphs_invalidated_ ? "graph invalidated by bind / open_peers / set_text_embedding: recapture it"
+                              : "no graph captured for this (mb slot, what)");
   ck(cudaGraphLaunch(static_cast<cudaGraphExec_t>(it->second.first), static_cast<cudaStream_t>(stream)),
      "cudaGraphLaunch");
   launches_ += it->second.second;
 }
 
-void Exec::seed_forward_record(int mb) { fwd_done_.insert(mb); }
+void Exec::seed_forward_record(int mb) {
+  if (mb < 0) raise(ErrorCode::InvalidArgument, "microbatch index must be >= 0");
+  fwd_done_.insert(mb);
+}
 
 void Exec::set_text_embedding(const void* table, int64_t vocab) {
   if (!cfg_.text_embedding) raise(ErrorCode::InvalidArgument, "exec was created without text_embedding");
   if (!table || vocab < 1) raise(ErrorCode::InvalidArgument, "embedding table must be non-null with vocab >= 1");
   embed_table_ = static_cast<const unsigned char*>(table);
   embed_vocab_ = vocab;
-  dirty_fwd_ = true;
+  mark_dirty();
 }
 
 int Exec::read_trace(int kind, unsigned long long* out, int max_ctas, int* grid) const {
+  DeviceGuard dg(device_);
   if (kind < 0 || kind >= kNumKinds) raise(ErrorCode::InvalidArgument, "trace kind out of range");
   const int g = kind == kFwdKind ? fwd_part_.grid : kind == kBwdKind ? bwd_part_.grid : 0;
   if (grid) *grid = g;
@@ -714,6 +806,7 @@ int Exec::read_trace(int kind, unsigned long long* out, int max_ctas, int* grid)
 }
 
 uint32_t Exec::device_error() const {
+  DeviceGuard dg(device_);
   uint32_t v = 0;
   ck(cudaMemcpy(&v, ctr_ + 3 * dev::kCtrLine + 1, sizeof(v), cudaMemcpyDeviceToHost), "read status");
   return v;

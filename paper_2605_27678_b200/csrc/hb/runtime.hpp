@@ -40,6 +40,8 @@ struct ExecConfig {
   int partition = 0;                // 0 auto, 1 contiguous, 2 interleaved, 3 dynamic, 4 TMA bulk (copy)
   int strict_provenance = 0;        // 1: backward reads tp=0 copies only (index_map.hpp balance_replicas)
   int text_embedding = 0;           // splice: TEXT holds int32 token ids, rows gathered from an embedding table
+  int max_ctas = 0;                 // cap on every boundary kernel's grid (0: fill the GPU); leaves SMs to
+                                    // concurrent work (PP P2P, compute) and lets several execs share one GPU
 };
 
 class Exec {
@@ -53,6 +55,11 @@ class Exec {
   // Multi-GPU setup (collective across the exec group's processes).
   void ipc_handle(void* out64) const;
   void open_peers(const void* handles);  // n_gpus * 64 bytes, ordered by GPU index
+  // Single-process form: execs[g] is the exec of GPU g of the same group in
+  // this process (one host thread drives every GPU); peer regions are used
+  // directly (peer access enabled between distinct devices, none needed when
+  // several execs share one device).
+  void open_peers_local(Exec* const* execs, int n);
 
   // Buffers of logical rank `rank` (must be resident here unless peer-mapped read-only use).
   void* buffer(int rank, int slot, int mb_slot, size_t* bytes) const;
@@ -66,8 +73,9 @@ class Exec {
   // stores each output row straight into every destination row the plan maps
   // it to; the source shards are never materialised. One GPU (all destinations
   // resident) for now.
+  // x_rows: rows of x (must equal the local source ranks' token rows).
   void forward_projected(int mb, const void* x, int64_t ldx, const void* w, int64_t ldw, int d_h, int K,
-                         void* stream);
+                         int64_t x_rows, void* stream);
   void backward(int mb, float beta, void* stream);
   void seed_forward_record(int mb);
   // Embedding table [vocab x d_h] (act dtype, on this GPU) the splice gathers
@@ -122,6 +130,8 @@ class Exec {
   uint64_t region_bytes_ = 0;
   unsigned char* local_base_ = nullptr;
   std::vector<unsigned char*> peer_base_;
+  std::vector<char> peer_ipc_;  // peer_base_[g] was opened with cudaIpcOpenMemHandle (closed at exit)
+  int grid_cap(int grid) const { return cfg_.max_ctas > 0 && cfg_.max_ctas < grid ? cfg_.max_ctas : grid; }
   std::vector<std::vector<void*>> bound_;  // [rank*kNumSlots+slot][mb] external binding
 
   // Forward work of this GPU: source runs with every destination that needs
@@ -181,6 +191,9 @@ class Exec {
                        const std::vector<char>& remote, double local_bytes, double remote_bytes, int grid,
                        int mode, uint64_t unit, DevPartition* out);
   bool dirty_fwd_ = true, dirty_bwd_ = true;
+  bool graphs_invalidated_ = false;
+  void mark_dirty();  // tables rebuilt at the next op; captured graphs dropped
+  void check_forward_mb(int mb) const;
   int bwd_groups_ = 0;  // device reduce segments (fan-out groups of bwd_local_)
   uint32_t* ctr_ = nullptr;  // device counters
   unsigned long long* trace_ = nullptr;  // HB_TRACE diagnostics

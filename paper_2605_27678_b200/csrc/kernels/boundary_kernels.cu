@@ -403,6 +403,7 @@ __global__ void __launch_bounds__(32) copy_segments_tma_kernel(const CopySeg* __
   uint32_t pend_seg[kTmaStages];
   uint32_t pend_bytes[kTmaStages];
   uint64_t pend_off[kTmaStages];
+  bool pend_bad[kTmaStages];  // gather chunk with an out-of-range id: its rows are not stored
   uint32_t issued = 0, nremote = 0;
   bool more = true, arrived = false;
   Claimer cl;
@@ -453,6 +454,7 @@ __global__ void __launch_bounds__(32) copy_segments_tma_kernel(const CopySeg* __
         continue;
       }
       const int st = issued % kTmaStages;
+      bool bad = false;
       mbar_expect(&full[st], bytes);
       if (!sg.ids) {
         bulk_g2s(stage_mem + st * kTmaStageBytes, sg.src + a, bytes, &full[st]);
@@ -460,11 +462,13 @@ __global__ void __launch_bounds__(32) copy_segments_tma_kernel(const CopySeg* __
         for (uint64_t off = a; off < e;) {
           const uint64_t end = min(e, (off / sg.row_bytes + 1) * sg.row_bytes);
           const unsigned char* p = gather_src(sg, off, sync.err);
+          bad |= p == nullptr;
           bulk_g2s(stage_mem + st * kTmaStageBytes + (off - a), p ? p : sg.src + off % sg.row_bytes,
                    static_cast<uint32_t>(end - off), &full[st]);
           off = end;
         }
       }
+      pend_bad[st] = bad;
       pend_seg[st] = t.x;
       pend_off[st] = a;
       pend_bytes[st] = bytes;
@@ -482,7 +486,20 @@ __global__ void __launch_bounds__(32) copy_segments_tma_kernel(const CopySeg* __
     // one bulk group per chunk: a store to every destination of the run
     const CopySeg& sg = segs[pend_seg[st]];
     const int nd = sg.ndst;
-    for (int d = 0; d < nd; ++d) bulk_store(sg.dst[d] + pend_off[st], stage_mem + st * kTmaStageBytes, pend_bytes[st]);
+    if (!pend_bad[st]) {
+      for (int d = 0; d < nd; ++d)
+        bulk_store(sg.dst[d] + pend_off[st], stage_mem + st * kTmaStageBytes, pend_bytes[st]);
+    } else {  // error path: store the good row pieces only (bad rows stay untouched, as in copy_range)
+      const uint64_t a = pend_off[st], e = a + pend_bytes[st];
+      for (uint64_t off = a; off < e;) {
+        const uint64_t end = min(e, (off / sg.row_bytes + 1) * sg.row_bytes);
+        const int64_t id = sg.ids[off / sg.row_bytes];
+        if (id >= 0 && id < sg.vocab)
+          for (int d = 0; d < nd; ++d)
+            bulk_store(sg.dst[d] + off, stage_mem + st * kTmaStageBytes + (off - a), static_cast<uint32_t>(end - off));
+        off = end;
+      }
+    }
     bulk_commit();
     if (k >= 1 && more) {
       bulk_wait_read<1>();  // store k-1 has finished reading its stage

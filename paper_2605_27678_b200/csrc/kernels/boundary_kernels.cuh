@@ -27,7 +27,7 @@ constexpr int kMaxFan = 8;
 // Gather runs (text-embedding lookup fused into the splice): when `ids` is set,
 // the run is nbytes/row_bytes rows and row i comes from src + ids[i]*row_bytes
 // (src = the embedding table, `vocab` rows); an id outside [0, vocab) sets the
-// error word to kErrBadId (that row's contents are then unspecified).
+// error word to kErrBadId and that row of the destination is left unwritten.
 struct CopySeg {
   const unsigned char* src;
   unsigned char* dst[kMaxFan];

@@ -21,29 +21,17 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.dirname(HERE))
 sys.path.insert(0, HERE)
 
-from oracle import oracle as O  # noqa: E402
 from paper_2605_27678_b200 import bridge as hbb  # noqa: E402
 from paper_2605_27678_b200 import configs  # noqa: E402
-
-
-def o_layout(l):
-    return O.Layout(l.name, l.tp, l.cp, l.pp, l.dp, l.rank_offset)
-
+from parity_core import ProcessDriver, group_parity, make_splice, o_layout  # noqa: E402
 
 STRICT = os.environ.get("HB_STRICT", "0") == "1"
-
-
-def bf16_round(a):
-    return torch.from_numpy(a.astype(np.float32)).to(torch.bfloat16).double().numpy()
 
 
 def run(name, rank, N, dev, steps=3):
     cfg = configs.get(name, scale=64)
     plan = hbb.plan_bridge(cfg.edge())
-    sp = None
-    if cfg.splice:
-        s = cfg.splice
-        sp = hbb.SpliceSpec(s["Q"], s["S"], cfg.hidden, cfg.tokens, s["codes"], s["text_mode"])
+    sp = make_splice(cfg)
     r2g = configs.rank_to_gpu(plan.world, N)
     local = [r for r in range(plan.world) if r2g[r] == rank]
     rt = hbb.BridgeRuntime(plan, sp, n_gpus=N, my_gpu=rank, rank_to_gpu=r2g, act_dtype=torch.bfloat16,
@@ -51,81 +39,7 @@ def run(name, rank, N, dev, steps=3):
                            fwd_mode=int(os.environ.get("HB_FWD_MODE", "0")),
                            partition=int(os.environ.get("HB_PARTITION", "0")), strict_provenance=STRICT)
     rt.exchange_handles()
-    src, dst = o_layout(cfg.src), o_layout(cfg.dst)
-    B, W = cfg.batch, cfg.width
-    SI, DI = O.intervals(B, src.dp), O.intervals(B, dst.dp)
-    rng = np.random.default_rng(17)
-    X = bf16_round(rng.standard_normal((B, W)))
-    shards = {}
-    for r in src.stage_ranks(src.pp - 1):
-        t, c, p, d = src.coord(r)
-        shards[r] = bf16_round(X[SI[d][0]:SI[d][0] + SI[d][1]] + (8.0 * t if t else 0.0))
-        if r in local:
-            rt.buffer(r, hbb.SLOT_SRC_ACT).copy_(torch.from_numpy(shards[r].reshape(-1)).to(dev).to(torch.bfloat16))
-    L = cfg.splice["S"] // dst.cp if sp else 0
-    text = None
-    if sp:
-        codes = cfg.splice["codes"]
-        text = bf16_round(rng.standard_normal((int((codes < 0).sum()), cfg.hidden)))
-        for r in local:
-            b = rt.buffer(r, hbb.SLOT_TEXT)
-            if b is None:
-                continue
-            c = dst.coord(r)[1]
-            sl = codes.reshape(-1, cfg.splice["S"])[:, c * L:(c + 1) * L].reshape(-1)
-            b.copy_(torch.from_numpy(text[[-1 - int(x) for x in sl if x < 0]].reshape(-1)).to(dev).to(b.dtype))
-    ref, _, _ = O.bridge_forward(src, dst, B, W, shards)
-    ok = True
-    worst = 0.0
-    for step in range(steps):
-        # fresh gradients every step; source gradients accumulate (beta=1)
-        G = {}
-        vg = {}
-        for r in dst.stage_ranks(0):
-            t, c, p, d = dst.coord(r)
-            n = (cfg.splice["Q"] * L * cfg.hidden) if sp else DI[d][1] * W
-            # strict: every rank its own gradient (pins the tp=0 data path);
-            # default: contract gradients, tp replicas of a (cp, dp) cell equal
-            seed = 100 * step + (r if STRICT else 10 * c + d)
-            g = bf16_round(np.random.default_rng(seed).standard_normal(n))
-            G[r] = g
-            gg = g
-            if sp:
-                gg = O.splice_backward(cfg.splice["codes"], cfg.splice["Q"], cfg.splice["S"], cfg.hidden, c * L, L,
-                                       g.reshape(-1, cfg.hidden), DI[d][1] * cfg.tokens)
-            vg[r] = gg.reshape(-1, W)
-            if r in local:
-                rt.buffer(r, hbb.SLOT_DST_GRAD).copy_(torch.from_numpy(g).to(dev).to(torch.bfloat16))
-        if step == 0:
-            for r in local:
-                b = rt.buffer(r, hbb.SLOT_SRC_GRAD)
-                if b is not None:
-                    b.zero_()
-            acc = {r: np.zeros(SI[src.coord(r)[3]][1] * W) for r in src.stage_ranks(src.pp - 1)}
-        torch.cuda.synchronize()
-        dist.barrier()
-        rt.forward(step)
-        rt.backward(step, 1.0)
-        torch.cuda.synchronize()
-        if rt.status():
-            raise RuntimeError("flag wait timed out")
-        for r in local:
-            if r in ref:
-                exp = ref[r]
-                if sp:
-                    c = dst.coord(r)[1]
-                    exp = O.splice_forward(cfg.splice["codes"], cfg.splice["Q"], cfg.splice["S"], cfg.hidden, c * L,
-                                           L, exp.reshape(-1, cfg.hidden), text)
-                got = rt.buffer(r, hbb.SLOT_DST_ACT).double().cpu().numpy()
-                ok &= bool(np.array_equal(got, exp.reshape(-1)))
-        refb, _, _ = O.bridge_backward(src, dst, B, W, vg)
-        for r in refb:
-            acc[r] = acc[r] + refb[r].reshape(-1)
-            if r in local:
-                got = rt.buffer(r, hbb.SLOT_SRC_GRAD).double().cpu().numpy()
-                rel = float(np.max(np.abs(got - acc[r]) / np.maximum(1.0, np.abs(acc[r]))))
-                worst = max(worst, rel)
-                ok &= rel <= 1e-6
+    ok, worst = group_parity(cfg, ProcessDriver(rt, local), steps=steps, strict=STRICT)
     flag = torch.tensor([0 if ok else 1], device=dev)
     dist.all_reduce(flag)
     w = torch.tensor([worst], dtype=torch.float64, device=dev)

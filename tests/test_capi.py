@@ -33,7 +33,7 @@ def test_status_convention_matches_reference_error_codes():
         assert L.hb_error_name(i + 1).decode() == n
     assert L.hb_error_name(0).decode() == "OK"
     assert L.hb_error_name(25).decode() == "CudaError"
-    assert L.hb_abi_version() == 6
+    assert L.hb_abi_version() == 7
 
 
 def test_error_message_and_no_exception_across_abi():

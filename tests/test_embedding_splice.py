@@ -76,3 +76,36 @@ def test_embedding_requires_table_and_splice():
     rt.close()
     with pytest.raises(hbb.HetBridgeError):
         hbb.BridgeRuntime(hbb.plan_bridge(configs.get("c2", scale=64).edge()), text_embedding=True)
+
+
+@pytest.mark.parametrize("partition", [0, 1, 3])
+def test_embedding_bad_row_left_unwritten(partition):
+    """A bad id's row is left untouched by both copy engines (TMA: the chunk's
+    good row pieces are stored one by one; LDG: the row is skipped)."""
+    cfg = configs.get("c4", scale=64)
+    plan = hbb.plan_bridge(cfg.edge())
+    rt = hbb.BridgeRuntime(plan, _spec(cfg), text_embedding=True, partition=partition)
+    table = torch.ones(10, cfg.hidden, device="cuda", dtype=torch.bfloat16)
+    rt.set_text_embedding(table)
+    for r in rt.local_ranks(hbb.SLOT_SRC_ACT):
+        rt.buffer(r, hbb.SLOT_SRC_ACT).fill_(2.0)
+    for r in rt.local_ranks(hbb.SLOT_TEXT):
+        rt.buffer(r, hbb.SLOT_TEXT).fill_(3)
+    r0 = rt.local_ranks(hbb.SLOT_TEXT)[0]
+    rt.buffer(r0, hbb.SLOT_TEXT)[5] = -4  # out of range
+    for r in rt.local_ranks(hbb.SLOT_DST_ACT):
+        rt.buffer(r, hbb.SLOT_DST_ACT).fill_(7.0)
+    rt.forward(0)
+    torch.cuda.synchronize()
+    with pytest.raises(hbb.HetBridgeError):
+        rt.status()
+    untouched = 0
+    for r in rt.local_ranks(hbb.SLOT_DST_ACT):
+        rows = rt.buffer(r, hbb.SLOT_DST_ACT).view(-1, cfg.hidden).float()
+        sentinel = (rows == 7.0).all(dim=1)
+        assert bool(((rows == 1.0) | (rows == 2.0)).all(dim=1)[~sentinel].all()), f"rank {r}: garbage row"
+        untouched += int(sentinel.sum())
+        if r != r0:
+            assert int(sentinel.sum()) == 0, f"rank {r}"
+    assert untouched == 1
+    rt.close()

@@ -1,0 +1,87 @@
+"""Multi-exec parity in ONE process (hb_exec_open_peers_local): one exec per
+(virtual) GPU of the group, every op launched on every GPU's stream from this
+thread, the execs meeting in the same in-kernel barrier (arrival epochs,
+"started" posts, lazy peer waits) and pulling rows from each other's regions
+through the same remote queues, TMA rings and fan-out paths as a torchrun
+group over NVSwitch.
+
+On a one-GPU box the group's execs share cuda:0 (max_ctas keeps their grids
+co-resident), so the driver's single-GPU `-m gpu` run exercises the whole
+cross-GPU protocol; with >= N devices the same test runs on N real GPUs with
+peer access over NVLink. Parity is against the oracle (tests/parity_core.py).
+"""
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from parity_core import LocalGroupDriver, group_parity, make_splice  # noqa: E402
+
+from paper_2605_27678_b200 import bridge as hbb  # noqa: E402
+from paper_2605_27678_b200 import configs  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+CONFIGS = ["c1", "c2", "c3", "c4", "c5", "c3p", "appc", "c2x4", "c3x4", "c4w4"]
+
+
+def _group(name, n, devices, **kw):
+    cfg = configs.get(name, scale=64)
+    plan = hbb.plan_bridge(cfg.edge())
+    if plan.world < n:
+        pytest.skip(f"{name} has {plan.world} logical ranks")
+    sp = make_splice(cfg)
+    g = hbb.LocalGroup(plan, sp, devices=devices, act_dtype=torch.bfloat16 if cfg.act == "bf16" else torch.float32,
+                       grad_in_dtype=torch.bfloat16 if cfg.grad_in == "bf16" else torch.float32,
+                       grad_out_dtype=torch.float32, timeout_s=20.0, **kw)
+    return cfg, g
+
+
+@pytest.mark.parametrize("n", [2, 4])
+@pytest.mark.parametrize("name", CONFIGS)
+def test_virtual_gpus_on_one_device(name, n):
+    """n execs sharing cuda:0: the whole protocol on one physical GPU."""
+    cfg, g = _group(name, n, [0] * n)
+    try:
+        ok, worst = group_parity(cfg, LocalGroupDriver(g), steps=2)
+        assert g.status() == 0
+        assert ok, f"{name} n={n}: parity failed (bwd worst {worst:.3g})"
+    finally:
+        g.close()
+
+
+@pytest.mark.parametrize("mode", [dict(fwd_mode=2), dict(partition=1), dict(strict_provenance=True)])
+@pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5"])
+def test_virtual_gpus_modes(name, mode):
+    """push forward, contiguous partition and strict provenance across execs."""
+    cfg, g = _group(name, 2, [0, 0], **mode)
+    try:
+        ok, worst = group_parity(cfg, LocalGroupDriver(g), steps=2, strict=bool(mode.get("strict_provenance")))
+        assert g.status() == 0
+        assert ok, f"{name} {mode}: parity failed (bwd worst {worst:.3g})"
+    finally:
+        g.close()
+
+
+@pytest.mark.parametrize("n", [2, 4, 8])
+@pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5", "c3p"])
+def test_real_gpus_one_process(name, n):
+    """one process, n real GPUs, peer access over NVLink (skips below n GPUs)."""
+    if torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    cfg, g = _group(name, n, list(range(n)))
+    try:
+        ok, worst = group_parity(cfg, LocalGroupDriver(g), steps=2)
+        assert ok, f"{name} n={n}: parity failed (bwd worst {worst:.3g})"
+    finally:
+        g.close()
+
+
+def test_open_peers_local_rejects_mismatched_group():
+    cfg = configs.get("c2", scale=64)
+    plan = hbb.plan_bridge(cfg.edge())
+    a = hbb.BridgeRuntime(plan, n_gpus=2, my_gpu=0, rank_to_gpu=configs.rank_to_gpu(8, 2))
+    b = hbb.BridgeRuntime(plan, n_gpus=2, my_gpu=1, rank_to_gpu=configs.rank_to_gpu(8, 2), mb_slots=2)
+    with pytest.raises(hbb.HetBridgeError):
+        a.open_peers_local([a, b])  # different buffer-set count: not the same symmetric layout
+    a.close()
+    b.close()
