@@ -795,7 +795,7 @@ def main():
                              "tstar_ms": round(tstar_step, 4), "frac_of_tstar": round(tstar_step / ms_step, 4),
                              "fwd_ms": fk["ms"], "fwd_tstar_ms": fk["tstar_ms"], "fwd_bound": fk["bound"],
                              "bwd_ms": bk["ms"], "bwd_tstar_ms": bk["tstar_ms"], "bwd_bound": bk["bound"],
-                             "overlap_with_pp_p2p": overlap}}
+                             "overlap_with_pp_p2p": overlap, "parity": parity}}
         rt.close()
         rt = None
         torch.cuda.synchronize()

@@ -198,7 +198,23 @@ int hb_exec_open_peers(hb_exec* x, const void* handles, size_t nbytes); /* n_gpu
  * so their grids are co-resident). Every exec must outlive its peers' ops. */
 int hb_exec_open_peers_local(hb_exec* x, hb_exec* const* execs, int n);
 int hb_exec_buffer(hb_exec* x, int rank, int slot, int mb_slot, void** ptr, size_t* bytes);
+/* Caller-owned device buffer for a resident rank's slot (replaces the
+ * reference's ShardedTensor payload, bridge.hpp:47-57: the caller keeps
+ * ownership, the library reads/writes it in place). ptr = NULL reverts to the
+ * library's region. Rebinding rebuilds the device tables at the next op and
+ * drops captured graphs (recapture them). Any GPU count: in a multi-process
+ * group every process then calls hb_exec_export_bindings, all-gathers the
+ * blobs and hb_exec_import_bindings each peer's blob before its next op. */
 int hb_exec_bind(hb_exec* x, int rank, int slot, int mb_slot, void* ptr, size_t bytes);
+/* As hb_exec_bind with a row stride in elements (DeviceShard.row_stride):
+ * row i of the shard starts at element i*row_stride; rows are samples
+ * (feature_width elements) or, for splice token slices / text rows, tokens
+ * (d_h). 0 or the row width = packed. */
+int hb_exec_bind_strided(hb_exec* x, int rank, int slot, int mb_slot, void* ptr, size_t bytes, long long row_stride);
+/* Multi-process binding exchange: *len = blob size (buf may be NULL to query);
+ * import a peer GPU's blob (CUDA IPC handles of the bound allocations). */
+int hb_exec_export_bindings(hb_exec* x, void* buf, size_t cap, size_t* len);
+int hb_exec_import_bindings(hb_exec* x, int gpu, const void* blob, size_t len);
 /* forward: BridgeRuntime::forward_{source,dest,colocated} for every resident rank */
 int hb_exec_forward(hb_exec* x, int mb, void* cuda_stream);
 /* backward: BridgeRuntime::backward_* ; src_grad = beta*src_grad + returned gradient */

@@ -31,7 +31,8 @@ EXPORTS = [
     "hb_cp_token_slice", "hb_splice_create", "hb_splice_destroy",
     "hb_index_forward", "hb_index_backward", "hb_index_backward_balanced", "hb_index_buffer_elems",
     "hb_exec_config_default", "hb_exec_create", "hb_exec_destroy", "hb_exec_ipc_handle",
-    "hb_exec_open_peers", "hb_exec_open_peers_local", "hb_exec_buffer", "hb_exec_bind", "hb_exec_forward", "hb_exec_backward",
+    "hb_exec_open_peers", "hb_exec_open_peers_local", "hb_exec_buffer", "hb_exec_bind", "hb_exec_bind_strided",
+    "hb_exec_export_bindings", "hb_exec_import_bindings", "hb_exec_forward", "hb_exec_backward",
     "hb_exec_seed_forward_record", "hb_exec_status", "hb_exec_stats", "hb_exec_graph_capture", "hb_projector_gemm",
     "hb_exec_forward_projected", "hb_exec_set_text_embedding",
     "hb_exec_graph_launch", "hb_exec_trace",
@@ -122,6 +123,9 @@ def _declare(L):
         "hb_exec_open_peers_local": (I, [V, P(V), I]),
         "hb_exec_buffer": (I, [V, I, I, I, P(V), P(Sz)]),
         "hb_exec_bind": (I, [V, I, I, I, V, Sz]),
+        "hb_exec_bind_strided": (I, [V, I, I, I, V, Sz, LL]),
+        "hb_exec_export_bindings": (I, [V, V, Sz, P(Sz)]),
+        "hb_exec_import_bindings": (I, [V, I, V, Sz]),
         "hb_exec_forward": (I, [V, I, V]),
         "hb_exec_backward": (I, [V, I, ctypes.c_float, V]),
         "hb_exec_seed_forward_record": (I, [V, I]),

@@ -42,26 +42,47 @@ def _shape(rt: BridgeRuntime, rank: int, slot: int) -> tuple[int, int]:
 
 
 def _view(rt: BridgeRuntime, rank: int, slot: int, mb: int):
-    return rt.buffer(rank, slot, mb % rt.mb_slots).view(_shape(rt, rank, slot))
+    return rt.buffer(rank, slot, mb % rt.mb_slots).reshape(_shape(rt, rank, slot))
+
+
+def _attach(rt: BridgeRuntime, rank: int, slot: int, mb: int, t, zero_copy: bool):
+    """Make ``t`` the (rank, slot) buffer of microbatch mb's set: bound in place
+    (zero_copy; a no-op when already bound) or copied into the runtime's own
+    buffer (the runtime keeps its previous binding otherwise)."""
+    buf_shape = _shape(rt, rank, slot)
+    if t.numel() != buf_shape[0] * buf_shape[1]:
+        raise HetBridgeError(13, f"rank {rank} slot {slot}: {t.numel()} elements, plan needs "
+                                 f"{buf_shape[0] * buf_shape[1]}")
+    if zero_copy:
+        t2 = t.detach()
+        if t2.dtype != rt._dtype_of(slot):
+            raise HetBridgeError(13, f"rank {rank} slot {slot}: dtype {t2.dtype}, runtime carries "
+                                     f"{rt._dtype_of(slot)} (zero_copy needs the runtime's dtype)")
+        if not (t2.dim() == 2 and t2.shape == buf_shape and t2.stride(1) == 1) and not t2.is_contiguous():
+            t2 = t2.contiguous()
+        if t2.dim() != 2:
+            t2 = t2.reshape(buf_shape)
+        rt.bind(rank, slot, t2, mb % rt.mb_slots)
+        return
+    buf = _view(rt, rank, slot, mb)
+    if t.data_ptr() != buf.data_ptr():  # the producer may already have written into the buffer
+        buf.copy_(t.reshape(buf.shape))
 
 
 class _Boundary(torch.autograd.Function):
     """One boundary op pair: forward reshard (+splice) / gradient return."""
 
     @staticmethod
-    def forward(ctx, rt: BridgeRuntime, mb: int, *src):
+    def forward(ctx, rt: BridgeRuntime, mb: int, zero_copy: bool, *src):
         src_ranks, dst_ranks = rt.local_ranks(SLOT_SRC_ACT), rt.local_ranks(SLOT_DST_ACT)
         if len(src) != len(src_ranks):
             raise HetBridgeError(24, f"expected {len(src_ranks)} source shards (ranks {src_ranks}), got {len(src)}")
         stream = torch.cuda.current_stream()
         for r, t in zip(src_ranks, src):
-            buf = _view(rt, r, SLOT_SRC_ACT, mb)
-            if t.numel() != buf.numel():
-                raise HetBridgeError(13, f"source shard of rank {r}: {t.numel()} elements, plan needs {buf.numel()}")
-            if t.data_ptr() != buf.data_ptr():  # the encoder may already have written into the buffer
-                buf.copy_(t.reshape(buf.shape))
+            _attach(rt, r, SLOT_SRC_ACT, mb, t, zero_copy)
+        rt.sync_bindings()  # collective at N > 1 when a binding changed on any GPU
         rt.forward(mb, stream)
-        ctx.rt, ctx.mb = rt, mb
+        ctx.rt, ctx.mb, ctx.zero_copy = rt, mb, zero_copy
         ctx.src_meta = [(t.dtype, t.shape) for t in src]
         outs = tuple(_view(rt, r, SLOT_DST_ACT, mb) for r in dst_ranks)
         # outputs alias the runtime's buffers of this microbatch's set: they
@@ -70,31 +91,53 @@ class _Boundary(torch.autograd.Function):
 
     @staticmethod
     def backward(ctx, *grads):
-        rt, mb = ctx.rt, ctx.mb
+        rt, mb, zc = ctx.rt, ctx.mb, ctx.zero_copy
         dst_ranks, src_ranks = rt.local_ranks(SLOT_DST_ACT), rt.local_ranks(SLOT_SRC_ACT)
         for r, g in zip(dst_ranks, grads):
-            buf = _view(rt, r, SLOT_DST_GRAD, mb)
             if g is None:
-                buf.zero_()
-            elif g.data_ptr() != buf.data_ptr():
-                buf.copy_(g.reshape(buf.shape))
+                g = torch.zeros(_shape(rt, r, SLOT_DST_GRAD), dtype=rt._dtype_of(SLOT_DST_GRAD),
+                                device=rt.device)
+            _attach(rt, r, SLOT_DST_GRAD, mb, g.to(rt._dtype_of(SLOT_DST_GRAD)) if zc else g, zc)
+        # zero_copy: the kernel writes each returned gradient straight into a
+        # fresh tensor (bound as the SRC_GRAD buffer, beta=0) when the runtime
+        # already carries the source dtype; otherwise fp32 buffer + cast copy
+        direct = zc and all(dt == rt._dtype_of(SLOT_SRC_GRAD) for dt, _ in ctx.src_meta)
+        fresh = []
+        if direct:
+            for r in src_ranks:
+                o = torch.empty(_shape(rt, r, SLOT_SRC_GRAD), dtype=rt._dtype_of(SLOT_SRC_GRAD), device=rt.device)
+                rt.bind(r, SLOT_SRC_GRAD, o, mb % rt.mb_slots)
+                fresh.append(o)
+        rt.sync_bindings()
         rt.backward(mb, 0.0, torch.cuda.current_stream())
-        # always a fresh tensor: an alias of SRC_GRAD could be kept as a leaf's
-        # .grad by AccumulateGrad and then overwritten when the set is reused
-        out = [_view(rt, r, SLOT_SRC_GRAD, mb).to(dt, copy=True).view(shape)
-               for r, (dt, shape) in zip(src_ranks, ctx.src_meta)]
-        return (None, None, *out)
+        if direct:
+            out = [o.view(shape) for o, (dt, shape) in zip(fresh, ctx.src_meta)]
+        else:
+            # always a fresh tensor: an alias of SRC_GRAD could be kept as a leaf's
+            # .grad by AccumulateGrad and then overwritten when the set is reused
+            out = [_view(rt, r, SLOT_SRC_GRAD, mb).to(dt, copy=True).view(shape)
+                   for r, (dt, shape) in zip(src_ranks, ctx.src_meta)]
+        return (None, None, None, *out)
 
 
-def boundary(rt: BridgeRuntime, mb: int, *src_shards):
+def boundary(rt: BridgeRuntime, mb: int, *src_shards, zero_copy: bool = True):
     """Differentiable boundary op for microbatch ``mb``.
 
     ``src_shards``: this process's source-rank shards in ascending rank order
     (``rt.local_ranks(SLOT_SRC_ACT)``). Returns the destination shards of the
     local destination ranks (ascending), as views of the runtime's buffers.
     Backward returns the gradient to each source shard (the reference's
-    ``backward_*`` role calls), fp32-accumulated and cast to the shard dtype."""
-    return _Boundary.apply(rt, mb, *src_shards)
+    ``backward_*`` role calls), fp32-accumulated and cast to the shard dtype.
+
+    zero_copy (default): the caller's shards and the incoming gradients are
+    bound as the runtime's buffers (hb_exec_bind; across GPUs the peers map
+    them through CUDA IPC, one binding exchange when a pointer changed) and the
+    returned gradients are written by the kernel into fresh tensors, so no
+    staging copy touches HBM. A changed pointer rebuilds the device tables at
+    the next op (host cost), so a steady-state caller keeps its tensors or
+    writes into ``rt.buffer`` views; zero_copy=False copies into the runtime's
+    buffers instead."""
+    return _Boundary.apply(rt, mb, zero_copy, *src_shards)
 
 
 class PackedBoundary:

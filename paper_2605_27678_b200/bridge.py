@@ -245,6 +245,8 @@ class BridgeRuntime:
                                    len(self.rank_to_gpu), ctypes.byref(cfg), ctypes.byref(h)))
         self._h = h
         self._keep = {}
+        self._bind_dirty = False
+        self._local_group = None  # set by LocalGroup (bindings shared in-process)
 
     # -- multi-GPU
     def ipc_handle(self) -> bytes:
@@ -305,6 +307,8 @@ class BridgeRuntime:
         """Device tensor view (1-D, element dtype of the slot) of a resident rank's buffer."""
         import torch
 
+        if (rank, slot, mb_slot) in self._keep:  # a caller-bound tensor (possibly row-strided)
+            return self._keep[(rank, slot, mb_slot)]
         p, n = ctypes.c_void_p(), ctypes.c_size_t()
         check(lib().hb_exec_buffer(self._h, rank, slot, mb_slot, ctypes.byref(p), ctypes.byref(n)))
         if not p.value or n.value == 0:
@@ -312,14 +316,70 @@ class BridgeRuntime:
         raw = torch.as_tensor(_CAI(p.value, n.value), device=self.device)
         return raw.view(self._dtype_of(slot))
 
-    def bind(self, rank: int, slot: int, tensor, mb_slot: int = 0):
-        if not tensor.is_cuda or not tensor.is_contiguous():
-            raise HetBridgeError(24, "bind needs a contiguous CUDA tensor")
+    def bind(self, rank: int, slot: int, tensor, mb_slot: int = 0, row_stride: int | None = None):
+        """Use a caller-owned CUDA tensor as a resident rank's buffer (no copy).
+
+        ``tensor``: 1-D contiguous, or 2-D [rows, row width] with a unit inner
+        stride (its row stride is taken from ``tensor.stride(0)`` unless
+        ``row_stride`` is given). ``None`` reverts to the runtime's region. In a
+        multi-GPU group call :meth:`exchange_bindings` on every process
+        afterwards (collective)."""
+        if tensor is None:
+            check(lib().hb_exec_bind(self._h, rank, slot, mb_slot, None, 0))
+            self._bind_dirty |= self._keep.pop((rank, slot, mb_slot), None) is not None
+            return
+        if not tensor.is_cuda:
+            raise HetBridgeError(24, "bind needs a CUDA tensor")
         if tensor.dtype != self._dtype_of(slot):
             raise HetBridgeError(13, f"slot {slot} expects {self._dtype_of(slot)}, got {tensor.dtype}")
-        check(lib().hb_exec_bind(self._h, rank, slot, mb_slot, ctypes.c_void_p(tensor.data_ptr()),
-                                 tensor.numel() * tensor.element_size()))
+        if tensor.dim() == 2 and tensor.stride(1) == 1:
+            stride = tensor.stride(0) if row_stride is None else row_stride
+            nbytes = ((tensor.shape[0] - 1) * tensor.stride(0) + tensor.shape[1]) * tensor.element_size()
+        elif tensor.is_contiguous():
+            stride = row_stride or 0
+            nbytes = tensor.numel() * tensor.element_size()
+        else:
+            raise HetBridgeError(24, "bind needs a contiguous tensor or rows with a unit inner stride")
+        old = self._keep.get((rank, slot, mb_slot))
+        if old is not None and old.data_ptr() == tensor.data_ptr() and old.stride() == tensor.stride() and \
+                old.shape == tensor.shape:
+            self._keep[(rank, slot, mb_slot)] = tensor
+            return  # already bound here: tables and graphs stay valid
+        check(lib().hb_exec_bind_strided(self._h, rank, slot, mb_slot, ctypes.c_void_p(tensor.data_ptr()),
+                                         nbytes, stride))
         self._keep[(rank, slot, mb_slot)] = tensor
+        self._bind_dirty = True
+
+    def sync_bindings(self, group=None):
+        """Collective at N > 1: exchange bindings if any process rebound a
+        buffer since the last exchange (one tiny all-reduce otherwise)."""
+        if self.n_gpus == 1 or self._local_group is not None:
+            self._bind_dirty = False
+            return
+        import torch
+        import torch.distributed as dist
+
+        dev = self.device if dist.get_backend(group) == "nccl" else "cpu"
+        flag = torch.tensor([1 if self._bind_dirty else 0], device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=group)
+        if flag.item():
+            self.exchange_bindings(group)
+
+    def exchange_bindings(self, group=None):
+        """Collective: all-gather every process's binding blob (CUDA IPC handles
+        of its caller-bound buffers) and import the peers' ones."""
+        import torch.distributed as dist
+
+        n = ctypes.c_size_t()
+        check(lib().hb_exec_export_bindings(self._h, None, 0, ctypes.byref(n)))
+        buf = ctypes.create_string_buffer(n.value)
+        check(lib().hb_exec_export_bindings(self._h, buf, n.value, ctypes.byref(n)))
+        blobs = [None] * dist.get_world_size(group)
+        dist.all_gather_object(blobs, (self.my_gpu, buf.raw[: n.value]), group=group)
+        for g, blob in blobs:
+            if g != self.my_gpu:
+                check(lib().hb_exec_import_bindings(self._h, g, blob, len(blob)))
+        self._bind_dirty = False
 
     def buffer_numel(self, rank: int, slot: int) -> int:
         """Elements of a logical rank's buffer (0: the rank has none in this slot)."""
@@ -454,6 +514,7 @@ class LocalGroup:
                 self.streams.append(torch.cuda.Stream(device=d))
         for rt in self.rts:
             rt.open_peers_local(self.rts)
+            rt._local_group = self
         self.plan, self.splice, self.rank_to_gpu, self.max_ctas = plan, splice, r2g, max_ctas
 
     def runtime_of(self, rank: int) -> "BridgeRuntime":
@@ -461,6 +522,13 @@ class LocalGroup:
 
     def buffer(self, rank: int, slot: int, mb_slot: int = 0):
         return self.runtime_of(rank).buffer(rank, slot, mb_slot)
+
+    def bind(self, rank: int, slot: int, tensor, mb_slot: int = 0, row_stride: int | None = None):
+        """Caller-owned buffer for ``rank`` (on its GPU); every exec re-reads its
+        peers' bindings (hb_exec_open_peers_local)."""
+        self.runtime_of(rank).bind(rank, slot, tensor, mb_slot, row_stride)
+        for rt in self.rts:
+            rt.open_peers_local(self.rts)
 
     def forward(self, mb: int = 0):
         for rt, st in zip(self.rts, self.streams):

@@ -457,6 +457,30 @@ int hb_exec_bind(hb_exec* x, int rank, int slot, int mb_slot, void* ptr, size_t 
   });
 }
 
+int hb_exec_bind_strided(hb_exec* x, int rank, int slot, int mb_slot, void* ptr, size_t bytes, long long row_stride) {
+  return guard([&] {
+    need(x, "exec");
+    x->x->bind(rank, slot, mb_slot, ptr, bytes, row_stride);
+  });
+}
+
+int hb_exec_export_bindings(hb_exec* x, void* buf, size_t cap, size_t* len) {
+  return guard([&] {
+    need(x, "exec");
+    need(len, "len");
+    *len = x->x->export_bindings(buf, cap);
+    if (buf && cap < *len) hb::raise(hb::ErrorCode::InvalidArgument, "binding buffer too small");
+  });
+}
+
+int hb_exec_import_bindings(hb_exec* x, int gpu, const void* blob, size_t len) {
+  return guard([&] {
+    need(x, "exec");
+    need(blob, "blob");
+    x->x->import_bindings(gpu, blob, len);
+  });
+}
+
 int hb_exec_forward(hb_exec* x, int mb, void* stream) {
   return guard([&] {
     need(x, "exec");

@@ -78,7 +78,9 @@ Exec::Exec(const bridge::BridgePlan& plan, const index::SpliceSpec* splice, int 
     mb_stride_[g] = off;
     region_bytes_ = std::max(region_bytes_, kPadBytes + off * cfg.mb_slots);
   }
-  bound_.assign(map_.world * index::kNumSlots, std::vector<void*>(cfg.mb_slots, nullptr));
+  bound_.assign(map_.world * index::kNumSlots, std::vector<Binding>(cfg.mb_slots));
+  peer_bound_.assign(map_.world * index::kNumSlots, std::vector<Binding>(cfg.mb_slots));
+  peer_exec_.assign(n_gpus_, nullptr);
 
   // Forward mode. Pull (consumers read the owners' HBM) needs one barrier;
   // push (owners write the consumers' HBM) needs a second "writes done"
@@ -87,37 +89,7 @@ Exec::Exec(const bridge::BridgePlan& plan, const index::SpliceSpec* splice, int 
   // and bidirectional (c2w4 68 vs 72 us, c4w4 68 vs 81 us, c2 150 vs 168 us),
   // so auto means pull; push stays selectable.
   fwd_push_ = cfg_.fwd_mode == 2 && n_gpus_ > 1;
-  // Fan-out grouping: every destination of one source run that this GPU
-  // executes shares a single read of the run (decided per GPU; the symmetric
-  // layout means no process needs another's grouping).
-  std::map<std::tuple<int, int, int64_t, int64_t>, std::vector<size_t>> groups;
-  std::vector<std::tuple<int, int, int64_t, int64_t>> order;
-  for (size_t i = 0; i < map_.fwd.size(); ++i) {
-    const auto& s = map_.fwd[i];
-    if (gpu_of(fwd_push_ ? s.src.rank : s.dst.rank) != my_gpu_) continue;
-    const auto key = std::make_tuple(s.src.rank, s.src.slot, s.src.off, s.n);
-    auto& g = groups[key];
-    if (g.empty()) order.push_back(key);
-    g.push_back(i);
-  }
-  for (const auto& key : order) {
-    const auto& idx = groups[key];
-    for (size_t k = 0; k < idx.size(); k += dev::kMaxFan) {
-      FanSeg f;
-      const auto& first = map_.fwd[idx[k]];
-      f.src = first.src;
-      f.n = first.n;
-      f.remote = !fwd_push_ && gpu_of(first.src.rank) != my_gpu_;
-      for (size_t j = k; j < std::min(idx.size(), k + dev::kMaxFan); ++j) {
-        const auto& d = map_.fwd[idx[j]].dst;
-        f.dsts.push_back(d);
-        if (fwd_push_ && gpu_of(d.rank) != my_gpu_) f.remote = true;
-      }
-      fwd_local_.push_back(std::move(f));
-    }
-  }
-  for (const auto& s : map_.bwd)
-    if (gpu_of(s.dst.rank) == my_gpu_) bwd_local_.push_back(s);
+  build_work();
 
   ck(cudaGetDevice(&device_), "cudaGetDevice");
   sm_count_ = dev::device_sm_count();
@@ -163,9 +135,119 @@ Exec::~Exec() {
   cudaFree(bwd_part_.first_seg);
   for (int g = 0; g < n_gpus_; ++g)
     if (g != my_gpu_ && peer_base_[g] && peer_ipc_[g]) cudaIpcCloseMemHandle(peer_base_[g]);
+  for (auto& kv : ipc_open_) cudaIpcCloseMemHandle(kv.second);
   cudaFree(local_base_);
   cudaFree(ctr_);
   cudaFree(trace_);
+}
+
+// Elements per row of a slot's buffer: a sample (W) for activations and
+// gradients, a token (d_h) for splice token slices and text rows. A bound
+// buffer with a row stride places row i at element i*stride.
+int64_t Exec::row_width(int slot) const {
+  if (splice_d_h_ && (slot == index::kDstAct || slot == index::kDstGrad || slot == index::kText)) return splice_d_h_;
+  return plan_.edge.feature_width;
+}
+
+const Exec::Binding* Exec::binding_of(int rank, int slot, int mb) const {
+  const auto& b = bound_[rank * index::kNumSlots + slot][mb];
+  if (b.ptr) return &b;
+  const auto& p = peer_bound_[rank * index::kNumSlots + slot][mb];
+  return p.ptr ? &p : nullptr;
+}
+
+// Rows of (rank, slot) are not packed in some buffer set: runs over it are
+// split at row boundaries so every piece is contiguous in memory.
+bool Exec::strided(int rank, int slot) const {
+  for (int mb = 0; mb < cfg_.mb_slots; ++mb) {
+    const Binding* b = binding_of(rank, slot, mb);
+    if (b && b->stride) return true;
+  }
+  return false;
+}
+
+unsigned char* Exec::addr(int rank, int slot, int mb, int64_t off, int es) const {
+  const Binding* b = binding_of(rank, slot, mb);
+  if (b) {
+    if (b->stride) {
+      const int64_t w = row_width(slot);
+      off = off / w * b->stride + off % w;
+    }
+    return static_cast<unsigned char*>(b->ptr) + off * es;
+  }
+  const int g = gpu_of(rank);
+  if (!peer_base_[g])
+    raise(ErrorCode::InvalidArgument, "buffer of rank " + std::to_string(rank) +
+                                          " unavailable (peer not opened or not bound)");
+  return peer_base_[g] + offset_of(g, rank, slot, mb) + off * es;
+}
+
+// This GPU's forward and backward work from the index map: runs split at the
+// row boundaries of strided bound buffers, forward runs grouped by source run
+// (fan-out: one read, up to kMaxFan destinations).
+void Exec::build_work() {
+  auto next_cut = [&](const index::Ref& r, int64_t pos) -> int64_t {  // elements left in r's current row
+    if (!strided(r.rank, r.slot)) return INT64_MAX;
+    const int64_t w = row_width(r.slot);
+    return w - (r.off + pos) % w;
+  };
+  std::vector<index::CopySeg> fwd;
+  for (const auto& s : map_.fwd) {
+    if (gpu_of(fwd_push_ ? s.src.rank : s.dst.rank) != my_gpu_) continue;
+    for (int64_t pos = 0; pos < s.n;) {
+      const int64_t len = std::min({s.n - pos, next_cut(s.src, pos), next_cut(s.dst, pos)});
+      index::CopySeg c = s;
+      c.src.off += pos;
+      c.dst.off += pos;
+      c.n = len;
+      fwd.push_back(c);
+      pos += len;
+    }
+  }
+  // Fan-out grouping: every destination of one source run that this GPU
+  // executes shares a single read of the run (decided per GPU; the symmetric
+  // layout means no process needs another's grouping).
+  fwd_local_.clear();
+  std::map<std::tuple<int, int, int64_t, int64_t>, std::vector<size_t>> groups;
+  std::vector<std::tuple<int, int, int64_t, int64_t>> order;
+  for (size_t i = 0; i < fwd.size(); ++i) {
+    const auto& s = fwd[i];
+    const auto key = std::make_tuple(s.src.rank, s.src.slot, s.src.off, s.n);
+    auto& g = groups[key];
+    if (g.empty()) order.push_back(key);
+    g.push_back(i);
+  }
+  for (const auto& key : order) {
+    const auto& idx = groups[key];
+    for (size_t k = 0; k < idx.size(); k += dev::kMaxFan) {
+      FanSeg f;
+      const auto& first = fwd[idx[k]];
+      f.src = first.src;
+      f.n = first.n;
+      f.remote = !fwd_push_ && gpu_of(first.src.rank) != my_gpu_;
+      for (size_t j = k; j < std::min(idx.size(), k + dev::kMaxFan); ++j) {
+        const auto& d = fwd[idx[j]].dst;
+        f.dsts.push_back(d);
+        if (fwd_push_ && gpu_of(d.rank) != my_gpu_) f.remote = true;
+      }
+      fwd_local_.push_back(std::move(f));
+    }
+  }
+  bwd_local_.clear();
+  for (const auto& s : map_.bwd) {
+    if (gpu_of(s.dst.rank) != my_gpu_) continue;
+    for (int64_t pos = 0; pos < s.n;) {
+      int64_t len = std::min(s.n - pos, next_cut(s.dst, pos));
+      for (const auto& t : s.terms) len = std::min(len, next_cut(t, pos));
+      index::ReduceSeg r = s;
+      r.dst.off += pos;
+      for (auto& t : r.terms) t.off += pos;
+      r.n = len;
+      bwd_local_.push_back(std::move(r));
+      pos += len;
+    }
+  }
+  work_dirty_ = false;
 }
 
 int Exec::slot_dtype(int slot) const {
@@ -244,6 +326,16 @@ void Exec::open_peers_local(Exec* const* execs, int n) {
     }
     peer_base_[g] = p->local_base_;
   }
+  // the peers' caller-bound buffers (same address space): re-read on every call
+  for (int g = 0; g < n_gpus_; ++g) {
+    if (g == my_gpu_ || !execs[g]) continue;
+    peer_exec_[g] = execs[g];
+    for (int r = 0; r < map_.world; ++r)
+      if (gpu_of(r) == g)
+        for (int sl = 0; sl < index::kNumSlots; ++sl)
+          peer_bound_[r * index::kNumSlots + sl] = execs[g]->bound_[r * index::kNumSlots + sl];
+  }
+  work_dirty_ = true;
   sync_fwd_ = make_sync_args(kFwdKind, fwd_push_);
   sync_bwd_ = make_sync_args(kBwdKind, false);
   sync_proj_ = make_sync_args(kProjKind, true);
@@ -266,30 +358,127 @@ void* Exec::buffer(int rank, int slot, int mb_slot, size_t* bytes) const {
   const size_t n = buffer_bytes(rank, slot);
   if (bytes) *bytes = n;
   if (mb_slot < 0 || mb_slot >= cfg_.mb_slots) raise(ErrorCode::InvalidArgument, "mb slot out of range");
-  if (void* b = bound_[rank * index::kNumSlots + slot][mb_slot]) return b;
+  if (void* b = bound_[rank * index::kNumSlots + slot][mb_slot].ptr) return b;
   if (gpu_of(rank) != my_gpu_) raise(ErrorCode::InvalidArgument, "rank is not resident on this GPU");
   if (!local_base_ || n == 0) return nullptr;
   return local_base_ + offset_of(my_gpu_, rank, slot, mb_slot);
 }
 
-void Exec::bind(int rank, int slot, int mb_slot, void* ptr, size_t bytes) {
+void Exec::bind(int rank, int slot, int mb_slot, void* ptr, size_t bytes, int64_t row_stride) {
   const size_t n = buffer_bytes(rank, slot);
   if (mb_slot < 0 || mb_slot >= cfg_.mb_slots) raise(ErrorCode::InvalidArgument, "mb slot out of range");
-  if (bytes < n) raise(ErrorCode::ShapeMismatch, "bound buffer smaller than the planned shard");
   if (gpu_of(rank) != my_gpu_) raise(ErrorCode::InvalidArgument, "can only bind resident ranks");
-  if (n_gpus_ > 1)
-    raise(ErrorCode::InvalidArgument, "external buffers are single-GPU only; use buffer() on multi-GPU");
-  bound_[rank * index::kNumSlots + slot][mb_slot] = ptr;
+  if (row_stride < 0) raise(ErrorCode::InvalidArgument, "row stride must be >= 0");
+  const int64_t w = row_width(slot);
+  if (row_stride == w) row_stride = 0;  // packed
+  if (row_stride && row_stride < w) raise(ErrorCode::ShapeMismatch, "row stride smaller than the row width");
+  if (row_stride && slot == index::kText && cfg_.text_embedding)
+    raise(ErrorCode::InvalidArgument, "token-id buffers are packed (no row stride)");
+  const int es = dev::dtype_size(slot_dtype(slot));
+  const int64_t elems = map_.elems[rank][slot];
+  const size_t need = row_stride && elems ? static_cast<size_t>(((elems / w - 1) * row_stride + w) * es) : n;
+  if (ptr && bytes < need) raise(ErrorCode::ShapeMismatch, "bound buffer smaller than the planned shard");
+  Binding& b = bound_[rank * index::kNumSlots + slot][mb_slot];
+  if (b.ptr == ptr && b.stride == row_stride) return;  // unchanged: keep tables and graphs
+  const bool was_strided = strided(rank, slot);
+  b = {ptr, ptr ? row_stride : 0};
+  if (strided(rank, slot) != was_strided) work_dirty_ = true;
+  ++bind_version_;
   mark_dirty();
 }
 
-const void* Exec::resolve(int rank, int slot, int mb_slot) const {
-  if (void* b = bound_[rank * index::kNumSlots + slot][mb_slot]) return b;
-  const int g = gpu_of(rank);
-  if (!peer_base_[g])
-    raise(ErrorCode::InvalidArgument, "buffer of rank " + std::to_string(rank) +
-                                          " unavailable (peer not opened or not bound)");
-  return peer_base_[g] + offset_of(g, rank, slot, mb_slot);
+namespace {
+// cuMemGetAddressRange through the runtime's driver entry point (no -lcuda).
+void* allocation_base(void* p, size_t* size) {
+  using Fn = int (*)(unsigned long long*, size_t*, unsigned long long);
+  static Fn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<Fn>(f);
+  }();
+  if (!fn) raise(ErrorCode::CudaError, "cuMemGetAddressRange unavailable");
+  unsigned long long base = 0;
+  if (fn(&base, size, reinterpret_cast<unsigned long long>(p)) != 0)
+    raise(ErrorCode::CudaError, "cuMemGetAddressRange failed (not a device allocation?)");
+  return reinterpret_cast<void*>(base);
+}
+
+struct BindRecord {  // one exported binding (fixed 96-byte record)
+  int32_t rank, slot, mb_slot, pad;
+  int64_t offset;  // bytes from the allocation base
+  int64_t stride;  // elements (0: packed)
+  unsigned char handle[64];
+};
+static_assert(sizeof(BindRecord) == 96, "record layout");
+}  // namespace
+
+size_t Exec::export_bindings(void* out, size_t cap) const {
+  DeviceGuard dg(device_);
+  std::vector<BindRecord> recs;
+  for (int r = 0; r < map_.world; ++r) {
+    if (gpu_of(r) != my_gpu_) continue;
+    for (int s = 0; s < index::kNumSlots; ++s)
+      for (int mb = 0; mb < cfg_.mb_slots; ++mb) {
+        const Binding& b = bound_[r * index::kNumSlots + s][mb];
+        if (!b.ptr) continue;
+        BindRecord rec{};
+        rec.rank = r;
+        rec.slot = s;
+        rec.mb_slot = mb;
+        size_t sz = 0;
+        void* base = allocation_base(b.ptr, &sz);
+        rec.offset = static_cast<unsigned char*>(b.ptr) - static_cast<unsigned char*>(base);
+        rec.stride = b.stride;
+        cudaIpcMemHandle_t h;
+        ck(cudaIpcGetMemHandle(&h, base), "cudaIpcGetMemHandle(bound buffer)");
+        std::memcpy(rec.handle, &h, 64);
+        recs.push_back(rec);
+      }
+  }
+  const size_t need = 8 + recs.size() * sizeof(BindRecord);
+  if (out && cap >= need) {
+    const uint64_t n = recs.size();
+    std::memcpy(out, &n, 8);
+    if (!recs.empty()) std::memcpy(static_cast<unsigned char*>(out) + 8, recs.data(), recs.size() * sizeof(BindRecord));
+  }
+  return need;
+}
+
+void Exec::import_bindings(int gpu, const void* blob, size_t len) {
+  DeviceGuard dg(device_);
+  if (gpu < 0 || gpu >= n_gpus_) raise(ErrorCode::InvalidArgument, "bad GPU index");
+  if (gpu == my_gpu_) return;
+  if (len < 8) raise(ErrorCode::InvalidArgument, "binding blob too short");
+  uint64_t n = 0;
+  std::memcpy(&n, blob, 8);
+  if (len < 8 + n * sizeof(BindRecord)) raise(ErrorCode::InvalidArgument, "binding blob truncated");
+  // bindings of `gpu`'s ranks not in the blob revert to the peer region
+  for (int r = 0; r < map_.world; ++r)
+    if (gpu_of(r) == gpu)
+      for (int s = 0; s < index::kNumSlots; ++s)
+        for (auto& b : peer_bound_[r * index::kNumSlots + s]) b = {};
+  for (uint64_t i = 0; i < n; ++i) {
+    BindRecord rec;
+    std::memcpy(&rec, static_cast<const unsigned char*>(blob) + 8 + i * sizeof(BindRecord), sizeof(rec));
+    if (rec.rank < 0 || rec.rank >= map_.world || gpu_of(rec.rank) != gpu || rec.slot < 0 ||
+        rec.slot >= index::kNumSlots || rec.mb_slot < 0 || rec.mb_slot >= cfg_.mb_slots)
+      raise(ErrorCode::InvalidArgument, "binding record does not match this group's layout");
+    const std::string key(reinterpret_cast<const char*>(rec.handle), 64);
+    auto it = ipc_open_.find(key);
+    if (it == ipc_open_.end()) {
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, rec.handle, 64);
+      void* p = nullptr;
+      ck(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle(bound buffer)");
+      it = ipc_open_.emplace(key, static_cast<unsigned char*>(p)).first;
+    }
+    peer_bound_[rec.rank * index::kNumSlots + rec.slot][rec.mb_slot] = {it->second + rec.offset, rec.stride};
+  }
+  work_dirty_ = true;
+  mark_dirty();
 }
 
 namespace {
@@ -418,16 +607,15 @@ void Exec::upload_copies(int mb, uint64_t unit, std::vector<uint64_t>* w0s, std:
     if (gather) {  // rows table[ids[k]] for the run's text rows k
       if (!embed_table_) raise(ErrorCode::InvalidArgument, "text_embedding: call set_text_embedding first");
       c.src = embed_table_;
-      c.ids = static_cast<const int32_t*>(resolve(f.src.rank, f.src.slot, mb)) + f.src.off / splice_d_h_;
+      c.ids = reinterpret_cast<const int32_t*>(addr(f.src.rank, f.src.slot, mb, f.src.off / splice_d_h_, 4));
       c.row_bytes = static_cast<uint32_t>(splice_d_h_ * es);
       c.vocab = embed_vocab_;
     } else {
-      c.src = static_cast<const unsigned char*>(resolve(f.src.rank, f.src.slot, mb)) + f.src.off * es;
+      c.src = addr(f.src.rank, f.src.slot, mb, f.src.off, es);
     }
     c.ndst = static_cast<int32_t>(f.dsts.size());
     for (size_t d = 0; d < f.dsts.size(); ++d)
-      c.dst[d] = static_cast<unsigned char*>(const_cast<void*>(resolve(f.dsts[d].rank, f.dsts[d].slot, mb))) +
-                 f.dsts[d].off * es;
+      c.dst[d] = addr(f.dsts[d].rank, f.dsts[d].slot, mb, f.dsts[d].off, es);
     c.nbytes = nbytes;
     c.w0 = w;
     // the peers whose arrival this run waits for: a remote source (pull), remote destinations (push)
@@ -460,6 +648,7 @@ int Exec::copy_grid() const {
 
 void Exec::prepare_fwd() {
   if (!dirty_fwd_) return;
+  if (work_dirty_) build_work();
   const int mode = copy_mode();
   const uint64_t unit = pad_unit(mode, true);
   std::vector<uint64_t> w0s, ns;
@@ -482,6 +671,7 @@ void Exec::prepare_fwd() {
 
 void Exec::prepare_bwd() {
   if (!dirty_bwd_) return;
+  if (work_dirty_) build_work();
   const int mode = reduce_mode();
   uint64_t unit = pad_unit(mode, false);
   if (mode == dev::kPartDynamic && unit == 0) {
@@ -533,8 +723,7 @@ void Exec::prepare_bwd() {
       const auto& s = bwd_local_[grp[0]];
       auto acc_ptr = [&](size_t k) {
         const auto& g = bwd_local_[k];
-        return static_cast<unsigned char*>(const_cast<void*>(resolve(g.dst.rank, g.dst.slot, mb))) +
-               g.dst.off * es_out;
+        return addr(g.dst.rank, g.dst.slot, mb, g.dst.off, es_out);
       };
       dev::ReduceSeg d{};
       d.dst = acc_ptr(grp[0]);
@@ -543,7 +732,7 @@ void Exec::prepare_bwd() {
       d.nterms = static_cast<int32_t>(s.terms.size());
       d.term0 = static_cast<int32_t>(terms.size());
       for (const auto& t : s.terms) {
-        terms.push_back(static_cast<const unsigned char*>(resolve(t.rank, t.slot, mb)) + t.off * es_in);
+        terms.push_back(addr(t.rank, t.slot, mb, t.off, es_in));
         if (gpu_of(t.rank) != my_gpu_) d.peers |= 1u << gpu_of(t.rank);
       }
       d.ndst = static_cast<int32_t>(grp.size());
@@ -689,9 +878,9 @@ void Exec::forward_projected(int mb, const void* x, int64_t ldx, const void* w, 
       if (sg.src.slot != index::kSrcAct || gpu_of(sg.src.rank) != my_gpu_) continue;
       if (sg.src.off % d_h || sg.dst.off % d_h || sg.n % d_h)
         raise(ErrorCode::ShapeMismatch, "forward runs are not whole d_h rows");
-      auto* base = static_cast<unsigned char*>(const_cast<void*>(resolve(sg.dst.rank, sg.dst.slot, slot)));
       for (int64_t i = 0; i < sg.n / d_h; ++i)
-        dst[row_base.at(sg.src.rank) + sg.src.off / d_h + i].push_back(base + (sg.dst.off + i * d_h) * es);
+        dst[row_base.at(sg.src.rank) + sg.src.off / d_h + i].push_back(
+            addr(sg.dst.rank, sg.dst.slot, slot, sg.dst.off + i * d_h, es));
     }
     int fan = 1;
     for (const auto& v : dst) fan = std::max<int>(fan, static_cast<int>(v.size()));

@@ -19,6 +19,7 @@
 #include <map>
 #include <memory>
 #include <set>
+#include <string>
 #include <vector>
 
 #include "hb/bridge.hpp"
@@ -63,7 +64,17 @@ class Exec {
 
   // Buffers of logical rank `rank` (must be resident here unless peer-mapped read-only use).
   void* buffer(int rank, int slot, int mb_slot, size_t* bytes) const;
-  void bind(int rank, int slot, int mb_slot, void* ptr, size_t bytes);
+  // Caller-owned buffer of a resident rank (ptr null: back to the library's
+  // region). row_stride: elements between consecutive rows (0 or the row
+  // width: packed); rows are samples (W) or, for splice slots, tokens (d_h).
+  void bind(int rank, int slot, int mb_slot, void* ptr, size_t bytes, int64_t row_stride = 0);
+  // Multi-process groups: this GPU's bindings as a blob (CUDA IPC handle of
+  // each bound buffer's allocation + offset + stride; returns the size) and
+  // the import of a peer GPU's blob (collective: every process exports,
+  // all-gathers, imports every peer's blob before its next op).
+  size_t export_bindings(void* out, size_t cap) const;
+  void import_bindings(int gpu, const void* blob, size_t len);
+  uint64_t bind_version() const { return bind_version_; }
   size_t buffer_bytes(int rank, int slot) const;
 
   void forward(int mb, void* stream);
@@ -110,7 +121,6 @@ class Exec {
   const unsigned char* embed_table_ = nullptr;
   int64_t embed_vocab_ = 0;
   uint64_t offset_of(int gpu, int rank, int slot, int mb_slot) const;
-  const void* resolve(int rank, int slot, int mb_slot) const;
   void prepare_fwd();  // resolve pointers, upload descriptors (after bind/open)
   void prepare_bwd();
   static constexpr int kFwdKind = 0, kBwdKind = 1, kProjKind = 2, kNumKinds = 3;
@@ -132,7 +142,21 @@ class Exec {
   std::vector<unsigned char*> peer_base_;
   std::vector<char> peer_ipc_;  // peer_base_[g] was opened with cudaIpcOpenMemHandle (closed at exit)
   int grid_cap(int grid) const { return cfg_.max_ctas > 0 && cfg_.max_ctas < grid ? cfg_.max_ctas : grid; }
-  std::vector<std::vector<void*>> bound_;  // [rank*kNumSlots+slot][mb] external binding
+  struct Binding {
+    void* ptr = nullptr;
+    int64_t stride = 0;  // elements between rows (0: packed)
+  };
+  std::vector<std::vector<Binding>> bound_;       // [rank*kNumSlots+slot][mb]: caller buffers of resident ranks
+  std::vector<std::vector<Binding>> peer_bound_;  // same for peers' ranks (imported, or read from a local peer exec)
+  std::vector<Exec*> peer_exec_;                  // single-process groups
+  std::map<std::string, unsigned char*> ipc_open_;  // opened binding handles (by handle bytes)
+  uint64_t bind_version_ = 0;
+  bool work_dirty_ = true;
+  void build_work();
+  int64_t row_width(int slot) const;
+  const Binding* binding_of(int rank, int slot, int mb) const;
+  bool strided(int rank, int slot) const;
+  unsigned char* addr(int rank, int slot, int mb, int64_t off, int es) const;
 
   // Forward work of this GPU: source runs with every destination that needs
   // them (pull: destinations resident here; push: sources resident here), so a

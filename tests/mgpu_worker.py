@@ -23,7 +23,7 @@ sys.path.insert(0, HERE)
 
 from paper_2605_27678_b200 import bridge as hbb  # noqa: E402
 from paper_2605_27678_b200 import configs  # noqa: E402
-from parity_core import ProcessDriver, group_parity, make_splice, o_layout  # noqa: E402
+from parity_core import ProcessDriver, bind_caller_buffers, group_parity, make_splice, o_layout  # noqa: E402
 
 STRICT = os.environ.get("HB_STRICT", "0") == "1"
 
@@ -39,6 +39,13 @@ def run(name, rank, N, dev, steps=3):
                            fwd_mode=int(os.environ.get("HB_FWD_MODE", "0")),
                            partition=int(os.environ.get("HB_PARTITION", "0")), strict_provenance=STRICT)
     rt.exchange_handles()
+    pad = int(os.environ.get("HB_BIND_PAD", "-1"))
+    if pad >= 0:  # caller-owned (row-strided when pad > 0) buffers, mapped by peers through CUDA IPC
+        tdt = {"bf16": torch.bfloat16, "fp32": torch.float32}
+        dt = {hbb.SLOT_SRC_ACT: tdt[cfg.act], hbb.SLOT_DST_ACT: tdt[cfg.act], hbb.SLOT_TEXT: tdt[cfg.act],
+              hbb.SLOT_DST_GRAD: tdt[cfg.grad_in], hbb.SLOT_SRC_GRAD: torch.float32}
+        bind_caller_buffers(rt.bind, rt.buffer_numel, cfg, local, lambda r: dev, lambda sl: dt[sl], pad)
+        rt.exchange_bindings()
     ok, worst = group_parity(cfg, ProcessDriver(rt, local), steps=steps, strict=STRICT)
     flag = torch.tensor([0 if ok else 1], device=dev)
     dist.all_reduce(flag)
@@ -103,6 +110,58 @@ def run_projected(name, rank, N, dev):
     return flag.item() == 0, 0.0, r2g
 
 
+def run_autograd(name, rank, N, dev):
+    """boundary() autograd op across processes with zero-copy binding: the
+    caller's shards are bound (exchanged through CUDA IPC), no staging copy;
+    forward bit-exact and source gradients against the oracle."""
+    from oracle import oracle as O
+    from paper_2605_27678_b200.autograd import boundary
+
+    cfg = configs.get(name, scale=256)
+    plan = hbb.plan_bridge(cfg.edge())
+    r2g = configs.rank_to_gpu(plan.world, N)
+    rt = hbb.BridgeRuntime(plan, n_gpus=N, my_gpu=rank, rank_to_gpu=r2g, act_dtype=torch.float32,
+                           grad_in_dtype=torch.float32, grad_out_dtype=torch.float32, timeout_s=30.0, mb_slots=2)
+    rt.exchange_handles()
+    src, dst = o_layout(cfg.src), o_layout(cfg.dst)
+    B, W = cfg.batch, cfg.width
+    SI, DI = O.intervals(B, src.dp), O.intervals(B, dst.dp)
+    ok = True
+    for mb in range(2):
+        rng = np.random.default_rng(100 + mb)
+        X = rng.standard_normal((B, W))
+        G = rng.standard_normal((B, W))
+        src_ranks = rt.local_ranks(hbb.SLOT_SRC_ACT)
+        xs = [torch.tensor(X[SI[src.coord(r)[3]][0]:SI[src.coord(r)[3]][0] + SI[src.coord(r)[3]][1]], device=dev,
+                           dtype=torch.float32, requires_grad=True) for r in src_ranks]
+        outs = boundary(rt, mb, *xs)
+        outs = outs if isinstance(outs, tuple) else (outs,)
+        for r, x in zip(src_ranks, xs):  # no staging copy: the runtime reads the caller's tensor
+            ok &= rt.buffer(r, hbb.SLOT_SRC_ACT, mb % 2).data_ptr() == x.data_ptr()
+        shards = {r: X[SI[src.coord(r)[3]][0]:SI[src.coord(r)[3]][0] + SI[src.coord(r)[3]][1]]
+                  for r in src.stage_ranks(src.pp - 1)}
+        ref, _, _ = O.bridge_forward(src, dst, B, W, shards)
+        loss = 0
+        gd = {}
+        for r in dst.stage_ranks(0):
+            d = dst.coord(r)[3]
+            gd[r] = G[DI[d][0]:DI[d][0] + DI[d][1]]
+        for r, o in zip(rt.local_ranks(hbb.SLOT_DST_ACT), outs):
+            ok &= bool(np.array_equal(o.detach().cpu().numpy(), ref[r].astype(np.float32)))
+            loss = loss + (o * torch.tensor(gd[r], device=dev, dtype=torch.float32)).sum()
+        torch.cuda.synchronize()
+        dist.barrier()
+        loss.backward()  # c2 / c3: every GPU hosts destination ranks, so every GPU runs the backward op
+        refb, _, _ = O.bridge_backward(src, dst, B, W, gd)
+        torch.cuda.synchronize()
+        for r, x in zip(src_ranks, xs):
+            ok &= bool(np.allclose(x.grad.cpu().numpy(), refb[r], rtol=1e-6, atol=1e-6))
+    flag = torch.tensor([0 if ok else 1], device=dev)
+    dist.all_reduce(flag)
+    rt.close()
+    return flag.item() == 0, 0.0, r2g
+
+
 def main():
     rank = int(os.environ["RANK"])
     N = int(os.environ["WORLD_SIZE"])
@@ -113,8 +172,9 @@ def main():
     names = sys.argv[1:] or ["c2", "c3", "c4", "c5", "c1"]
     all_ok = True
     proj = os.environ.get("HB_PROJ", "0") == "1"
+    ag = os.environ.get("HB_AUTOGRAD", "0") == "1"
     for name in names:
-        ok, worst, r2g = (run_projected if proj else run)(name, rank, N, dev)
+        ok, worst, r2g = (run_projected if proj else run_autograd if ag else run)(name, rank, N, dev)
         all_ok &= ok
         if rank == 0:
             print(json.dumps({"config": name, "n_gpus": N, "parity": ok, "bwd_max_rel": worst,

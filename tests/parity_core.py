@@ -54,7 +54,7 @@ def group_parity(cfg, drv, steps: int = 3, strict: bool = False):
         shards[r] = bf16_round(X[SI[d][0]:SI[d][0] + SI[d][1]] + (8.0 * t if t else 0.0))
         if r in drv.local:
             b = drv.buf(r, hbb.SLOT_SRC_ACT)
-            b.copy_(torch.from_numpy(shards[r].reshape(-1)).to(b.device).to(torch.bfloat16))
+            b.copy_(torch.from_numpy(shards[r]).to(b.device).to(torch.bfloat16).reshape(b.shape))
     L = sp["S"] // dst.cp if sp else 0
     text = None
     if sp:
@@ -66,7 +66,7 @@ def group_parity(cfg, drv, steps: int = 3, strict: bool = False):
                 continue
             c = dst.coord(r)[1]
             sl = codes.reshape(-1, sp["S"])[:, c * L:(c + 1) * L].reshape(-1)
-            b.copy_(torch.from_numpy(text[[-1 - int(x) for x in sl if x < 0]].reshape(-1)).to(b.device).to(b.dtype))
+            b.copy_(torch.from_numpy(text[[-1 - int(x) for x in sl if x < 0]]).to(b.device).to(b.dtype).reshape(b.shape))
     ref, _, _ = O.bridge_forward(src, dst, B, W, shards)
     ok = True
     worst = 0.0
@@ -88,7 +88,7 @@ def group_parity(cfg, drv, steps: int = 3, strict: bool = False):
             vg[r] = gg.reshape(-1, W)
             if r in drv.local:
                 b = drv.buf(r, hbb.SLOT_DST_GRAD)
-                b.copy_(torch.from_numpy(g).to(b.device).to(torch.bfloat16))
+                b.copy_(torch.from_numpy(g).to(b.device).to(torch.bfloat16).reshape(b.shape))
         if step == 0:
             for r in drv.local:
                 b = drv.buf(r, hbb.SLOT_SRC_GRAD)
@@ -108,13 +108,13 @@ def group_parity(cfg, drv, steps: int = 3, strict: bool = False):
                     c = dst.coord(r)[1]
                     exp = O.splice_forward(sp["codes"], sp["Q"], sp["S"], cfg.hidden, c * L, L,
                                            exp.reshape(-1, cfg.hidden), text)
-                got = drv.buf(r, hbb.SLOT_DST_ACT).double().cpu().numpy()
+                got = drv.buf(r, hbb.SLOT_DST_ACT).double().cpu().numpy().reshape(-1)
                 ok &= bool(np.array_equal(got, exp.reshape(-1)))
         refb, _, _ = O.bridge_backward(src, dst, B, W, vg)
         for r in refb:
             acc[r] = acc[r] + refb[r].reshape(-1)
             if r in drv.local:
-                got = drv.buf(r, hbb.SLOT_SRC_GRAD).double().cpu().numpy()
+                got = drv.buf(r, hbb.SLOT_SRC_GRAD).double().cpu().numpy().reshape(-1)
                 rel = float(np.max(np.abs(got - acc[r]) / np.maximum(1.0, np.abs(acc[r]))))
                 worst = max(worst, rel)
                 ok &= rel <= 1e-6
@@ -168,6 +168,30 @@ class ProcessDriver:
 
     def status(self):
         return self.rt.status()
+
+
+def row_width(cfg, slot):
+    if cfg.splice and slot in (hbb.SLOT_DST_ACT, hbb.SLOT_DST_GRAD, hbb.SLOT_TEXT):
+        return cfg.hidden
+    return cfg.width
+
+
+def bind_caller_buffers(bind, numel_of, cfg, ranks, device_of, dtype_of, pad=0):
+    """Caller-owned buffers for every (rank, slot) in ``ranks``: [rows, W + pad]
+    allocations bound through their [:, :W] view (row stride W + pad; pad=0:
+    packed). Returns {(rank, slot): view}."""
+    out = {}
+    for r in ranks:
+        for slot in (hbb.SLOT_SRC_ACT, hbb.SLOT_DST_ACT, hbb.SLOT_DST_GRAD, hbb.SLOT_SRC_GRAD, hbb.SLOT_TEXT):
+            n = numel_of(r, slot)
+            if not n:
+                continue
+            w = row_width(cfg, slot)
+            full = torch.full((n // w, w + pad), float("nan"), dtype=dtype_of(slot), device=device_of(r))
+            v = full[:, :w]
+            bind(r, slot, v)
+            out[(r, slot)] = v
+    return out
 
 
 def config(name, scale=64):

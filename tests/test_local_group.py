@@ -85,3 +85,35 @@ def test_open_peers_local_rejects_mismatched_group():
         a.open_peers_local([a, b])  # different buffer-set count: not the same symmetric layout
     a.close()
     b.close()
+
+
+def _dtypes(cfg):
+    tdt = {"bf16": torch.bfloat16, "fp32": torch.float32}
+    return {hbb.SLOT_SRC_ACT: tdt[cfg.act], hbb.SLOT_DST_ACT: tdt[cfg.act], hbb.SLOT_TEXT: tdt[cfg.act],
+            hbb.SLOT_DST_GRAD: tdt[cfg.grad_in], hbb.SLOT_SRC_GRAD: torch.float32}
+
+
+@pytest.mark.parametrize("pad", [0, 40])
+@pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5", "c3p"])
+def test_caller_bound_buffers_across_execs(name, pad):
+    """a7 DeviceShard: every rank's slots are caller-owned tensors (row-strided
+    when pad > 0), bound on their exec and read/written in place by peers."""
+    from parity_core import bind_caller_buffers
+
+    cfg, g = _group(name, 2, [0, 0])
+    try:
+        dt = _dtypes(cfg)
+        bufs = bind_caller_buffers(g.bind, lambda r, s: hbb.buffer_elems(g.plan, r, s, g.splice), cfg,
+                                   range(g.plan.world), lambda r: torch.device("cuda", 0), lambda s: dt[s], pad)
+        assert bufs
+        drv = LocalGroupDriver(g)
+        ok, worst = group_parity(cfg, drv, steps=2)
+        assert ok, f"{name} pad={pad}: parity failed (bwd worst {worst:.3g})"
+        for (r, slot), v in bufs.items():  # the runtime wrote the caller's tensors, and nothing else
+            base = v.as_strided((v.shape[0], v.shape[1] + pad), (v.stride(0), 1))
+            if pad:
+                assert bool(torch.isnan(base[:, v.shape[1]:].float()).all()), f"rank {r} slot {slot}: padding written"
+            if slot in (hbb.SLOT_DST_ACT, hbb.SLOT_SRC_GRAD):
+                assert not bool(torch.isnan(v.float()).any()), f"rank {r} slot {slot}: row not written"
+    finally:
+        g.close()

@@ -22,3 +22,26 @@ def test_multigpu_parity(n):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
     print(r.stdout[-4000:], r.stderr[-4000:])
     assert r.returncode == 0
+
+
+@pytest.mark.parametrize("n", [2, 4])
+@pytest.mark.parametrize("mode", ["bind_packed", "bind_strided", "autograd"])
+def test_multigpu_caller_buffers(n, mode):
+    """Caller-owned shards at N > 1 (hb_exec_bind + binding exchange over CUDA
+    IPC, row strides) and the zero-copy autograd op, against the oracle."""
+    if torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    env = dict(os.environ)
+    names = ["c2", "c3", "c4", "c5"]
+    if mode == "bind_packed":
+        env["HB_BIND_PAD"] = "0"
+    elif mode == "bind_strided":
+        env["HB_BIND_PAD"] = "40"
+    else:
+        env["HB_AUTOGRAD"] = "1"
+        names = ["c2", "c3"]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29700 + n), os.path.join(HERE, "mgpu_worker.py")] + names
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env)
+    print(r.stdout[-4000:], r.stderr[-4000:])
+    assert r.returncode == 0

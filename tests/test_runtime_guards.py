@@ -77,19 +77,23 @@ def test_forward_projected_checks_operand_rows():
     rt.close()
 
 
-def test_autograd_gradient_is_not_an_alias():
+@pytest.mark.parametrize("zero_copy", [False, True])
+def test_autograd_gradient_is_not_an_alias(zero_copy):
     from paper_2605_27678_b200.autograd import boundary
 
     cfg, rt = _rt(mb_slots=1, grad_out_dtype=torch.bfloat16)
     srcs = rt.local_ranks(hbb.SLOT_SRC_ACT)
     xs = [torch.randn(rt.buffer_numel(r, hbb.SLOT_SRC_ACT) // cfg.width, cfg.width, device="cuda")
           .to(torch.bfloat16).requires_grad_(True) for r in srcs]
-    outs = boundary(rt, 0, *xs)
+    outs = boundary(rt, 0, *xs, zero_copy=zero_copy)
+    if zero_copy:  # the caller's shards are the runtime's source buffers: no staging copy
+        assert all(rt.buffer(r, hbb.SLOT_SRC_ACT).data_ptr() == x.data_ptr() for r, x in zip(srcs, xs))
     sum(o.float().sum() for o in outs).backward()
     g0 = [x.grad.clone() for x in xs]
-    ptrs = {rt.buffer(r, hbb.SLOT_SRC_GRAD).data_ptr() for r in srcs}
-    assert not any(x.grad.data_ptr() in ptrs for x in xs)
-    outs = boundary(rt, 1, *xs)  # reuses buffer set 0
+    if not zero_copy:
+        ptrs = {rt.buffer(r, hbb.SLOT_SRC_GRAD).data_ptr() for r in srcs}
+        assert not any(x.grad.data_ptr() in ptrs for x in xs)
+    outs = boundary(rt, 1, *xs, zero_copy=zero_copy)  # reuses buffer set 0
     (2 * sum(o.float().sum() for o in outs)).backward()
     for x, g in zip(xs, g0):
         assert torch.equal(x.grad.float(), 3 * g.float())  # g0 + 2*g0, not an overwritten alias
