@@ -260,6 +260,90 @@ int hb_projector_gemm(const void* x, long long ldx, const void* w, long long ldw
 int hb_exec_forward_projected(hb_exec* x, int mb, const void* act, long long x_rows, long long ldx, const void* w,
                               long long ldw, int d_h, int K, void* cuda_stream);
 
+/* ---- graph-aware pipeline dispatch (SPEC.md:358-437
+ *      `sched`: build_stage_graph, generate_1f1b_dispatch, validate_dispatch;
+ *      the reference's sched.cpp is an empty stub) --------------------------- */
+typedef struct hb_stage_graph hb_stage_graph;
+/* cell ops */
+#define HB_OP_COMPUTE 0
+#define HB_OP_SEND_FWD 1
+#define HB_OP_RECV_FWD 2
+#define HB_OP_SEND_BWD 3
+#define HB_OP_RECV_BWD 4
+/* edge kinds */
+#define HB_EDGE_P2P 0
+#define HB_EDGE_NC 1
+typedef struct {
+  int row;  /* schedule call */
+  int node; /* stage-graph node (module, pp) */
+  int op;   /* HB_OP_* */
+  int edge; /* stage-graph edge of a communication op (-1 for compute) */
+  int kind; /* HB_EDGE_* */
+  int mb;
+  int bwd;  /* compute: 1 = backward */
+} hb_cell;
+/* modules[n_modules] with their rank ranges; module edges edge_src[i] ->
+ * edge_dst[i] (indices into modules). Nodes are (module, pp) in module order;
+ * edges: module chains (P2P) then one NC edge per module edge, from the source
+ * module's last stage to the destination's first. Errors: CyclicGraph (17),
+ * DanglingEdge (18), InfeasibleSchedule (19: not exactly one sink). */
+int hb_stage_graph_create(const hb_layout* modules, int n_modules, const int* edge_src, const int* edge_dst,
+                          int n_edges, hb_stage_graph** out);
+void hb_stage_graph_destroy(hb_stage_graph* g);
+/* out[3*i..] = {module, pp, distance to the sink}; out[4*i..] = {src node,
+ * dst node, kind, module-edge index (-1 for P2P)} */
+int hb_stage_graph_nodes(const hb_stage_graph* g, int* out, int cap, int* n);
+int hb_stage_graph_edges(const hb_stage_graph* g, int* out, int cap, int* n);
+/* 1F1B dispatch table (warmup = longest distance to the sink); *n cells,
+ * *rows schedule calls; cells may be NULL to query the count. */
+int hb_dispatch_generate(const hb_stage_graph* g, int nmb, hb_cell* cells, size_t cap, size_t* n, int* rows);
+/* join readiness, edge identity, no double consumption; never fails on a bad
+ * table: *n_violations and one line per violation in report */
+int hb_dispatch_validate(const hb_stage_graph* g, const hb_cell* cells, size_t n, int nmb, char* report, size_t cap,
+                         size_t* len, int* n_violations);
+int hb_dispatch_render(const hb_stage_graph* g, int nmb, char* buf, size_t cap, size_t* len);
+
+/* ---- host-owned per-module runtime (per-module rank groups,
+ *      communicators and streams; §8(f) row 2: executes the graph-aware
+ *      dispatch table). One per process (one GPU), collective at create.
+ *      Modules have disjoint rank ranges (the non-colocated topology). The
+ *      runtime owns: the TP/CP/PP/DP groups of this rank (grid.cpp:41-53,
+ *      87-106), an NCCL world communicator and each module's PP communicator
+ *      (ncclCommSplit), one boundary exec per module edge (IPC handles
+ *      exchanged over NCCL), a boundary stream at the highest priority, a PP
+ *      stream and a compute stream. hb_runtime_step enqueues this rank's
+ *      column of the 1F1B table: P2P cells as grouped ncclSend/ncclRecv on the
+ *      PP stream, NC cells as the edge exec's forward/backward on the
+ *      boundary stream, compute cells through `fn` on the compute stream,
+ *      ordered by CUDA events. ---------------------------------------------- */
+typedef struct hb_runtime hb_runtime;
+typedef struct {
+  int nmb;            /* microbatches per step */
+  int max_ctas;       /* CTA cap of the boundary kernels (0 = fill the GPU) */
+  long long pp_bytes; /* one microbatch's stage activation/gradient per rank (P2P) */
+  int act_dtype, grad_in_dtype, grad_out_dtype;
+  double timeout_s;
+  int skip;           /* bit 0: NC cells, bit 1: P2P cells, bit 2: compute (overlap studies) */
+} hb_runtime_config;
+/* compute callback: stage-graph node, microbatch, 1 = backward, cudaStream_t */
+typedef void (*hb_compute_fn)(void* user, int node, int mb, int bwd, void* stream);
+int hb_nccl_unique_id(void* out128); /* rank 0 creates it; the caller broadcasts it */
+void hb_runtime_config_default(hb_runtime_config* c);
+int hb_runtime_create(const hb_layout* modules, int n_modules, const int* edge_src, const int* edge_dst, int n_edges,
+                      int global_batch, int feature_width, int world, int my_rank, const void* nccl_id128,
+                      const hb_runtime_config* cfg, hb_runtime** out);
+void hb_runtime_destroy(hb_runtime* r);
+/* this rank's stage-graph node (-1: none), module, node count, table rows */
+int hb_runtime_info(const hb_runtime* r, int* node, int* module, int* n_nodes, int* rows);
+int hb_runtime_group(const hb_runtime* r, int kind, int* out, int cap, int* n); /* 0 TP 1 CP 2 PP 3 DP */
+/* the edge's exec (owned by the runtime: do not destroy): its buffers via hb_exec_buffer / hb_exec_bind */
+int hb_runtime_edge_exec(hb_runtime* r, int module_edge, hb_exec** out);
+/* which: 0 act_in (RecvFwd), 1 act_out (SendFwd), 2 grad_in (RecvBwd), 3 grad_out (SendBwd) */
+int hb_runtime_stage_buffer(hb_runtime* r, int which, int mb, void** ptr, size_t* bytes);
+int hb_runtime_stream(hb_runtime* r, int which, void** stream); /* 0 boundary, 1 PP, 2 compute */
+int hb_runtime_step(hb_runtime* r, hb_compute_fn fn, void* user);
+int hb_runtime_last_step_ms(hb_runtime* r, float* ms); /* synchronises; Timeout if a flag wait expired */
+
 #ifdef __cplusplus
 }
 #endif

@@ -36,6 +36,11 @@ EXPORTS = [
     "hb_exec_seed_forward_record", "hb_exec_status", "hb_exec_stats", "hb_exec_graph_capture", "hb_projector_gemm",
     "hb_exec_forward_projected", "hb_exec_set_text_embedding",
     "hb_exec_graph_launch", "hb_exec_trace",
+    "hb_stage_graph_create", "hb_stage_graph_destroy", "hb_stage_graph_nodes", "hb_stage_graph_edges",
+    "hb_dispatch_generate", "hb_dispatch_validate", "hb_dispatch_render",
+    "hb_nccl_unique_id", "hb_runtime_config_default", "hb_runtime_create", "hb_runtime_destroy", "hb_runtime_info",
+    "hb_runtime_group", "hb_runtime_edge_exec", "hb_runtime_stage_buffer", "hb_runtime_stream", "hb_runtime_step",
+    "hb_runtime_last_step_ms",
     "hb_config_parse", "hb_config_destroy", "hb_config_num_modules", "hb_config_module", "hb_config_run",
     "hb_config_edge", "hb_config_render",
 ]
@@ -73,6 +78,11 @@ class Ref(ctypes.Structure):
 class ReduceSeg(ctypes.Structure):
     _fields_ = [("dst_rank", ctypes.c_int), ("dst_slot", ctypes.c_int), ("dst_off", ctypes.c_longlong),
                 ("n", ctypes.c_longlong), ("nterms", ctypes.c_int), ("term0", ctypes.c_int)]
+
+
+class Cell(ctypes.Structure):
+    _fields_ = [("row", ctypes.c_int), ("node", ctypes.c_int), ("op", ctypes.c_int), ("edge", ctypes.c_int),
+                ("kind", ctypes.c_int), ("mb", ctypes.c_int), ("bwd", ctypes.c_int)]
 
 
 class ExecConfig(ctypes.Structure):
@@ -137,6 +147,13 @@ def _declare(L):
         "hb_exec_forward_projected": (I, [V, I, V, LL, LL, V, LL, I, I, V]),
         "hb_exec_set_text_embedding": (I, [V, V, LL]),
         "hb_exec_trace": (I, [V, I, V, I, P(I), P(I)]),
+        "hb_stage_graph_create": (I, [P(Layout), I, P(I), P(I), I, P(V)]),
+        "hb_stage_graph_destroy": (None, [V]),
+        "hb_stage_graph_nodes": (I, [V, P(I), I, P(I)]),
+        "hb_stage_graph_edges": (I, [V, P(I), I, P(I)]),
+        "hb_dispatch_generate": (I, [V, I, P(Cell), Sz, P(Sz), P(I)]),
+        "hb_dispatch_validate": (I, [V, P(Cell), Sz, I, C, Sz, P(Sz), P(I)]),
+        "hb_dispatch_render": (I, [V, I, C, Sz, P(Sz)]),
         "hb_config_parse": (I, [C, P(V)]),
         "hb_config_destroy": (None, [V]),
         "hb_config_num_modules": (I, [V, P(I)]),

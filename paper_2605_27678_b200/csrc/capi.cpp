@@ -15,6 +15,8 @@
 #include "hb/config.hpp"
 #include "hb/index_map.hpp"
 #include "hb/runtime.hpp"
+#include "hb/runtime_host.hpp"
+#include "hb/sched.hpp"
 #include "kernels/projector_gemm.cuh"
 
 struct hb_plan {
@@ -24,10 +26,19 @@ struct hb_splice {
   hb::index::SpliceSpec spec;
 };
 struct hb_exec {
-  std::unique_ptr<hb::rt::Exec> x;
+  std::unique_ptr<hb::rt::Exec> own;
+  hb::rt::Exec* x = nullptr;
+  bool borrowed = false;  // an edge Exec of an hb_runtime (owned by it)
+};
+struct hb_runtime {
+  std::unique_ptr<hb::rt::HostRuntime> r;
+  std::vector<std::unique_ptr<hb_exec>> edge_execs;
 };
 struct hb_config {
   hb::config::ExperimentConfig c;
+};
+struct hb_stage_graph {
+  hb::sched::StageGraph g;
 };
 
 namespace {
@@ -407,12 +418,15 @@ int hb_exec_create(const hb_plan* p, const hb_splice* s, int n_gpus, int my_gpu,
     if (rank_to_gpu) map.assign(rank_to_gpu, rank_to_gpu + n_ranks);
     else map.assign(n_ranks, 0);
     auto x = std::make_unique<hb_exec>();
-    x->x = std::make_unique<hb::rt::Exec>(p->plan, spec(s), n_gpus, my_gpu, std::move(map), c);
+    x->own = std::make_unique<hb::rt::Exec>(p->plan, spec(s), n_gpus, my_gpu, std::move(map), c);
+    x->x = x->own.get();
     *out = x.release();
   });
 }
 
-void hb_exec_destroy(hb_exec* x) { delete x; }
+void hb_exec_destroy(hb_exec* x) {
+  if (x && !x->borrowed) delete x;
+}
 
 int hb_exec_ipc_handle(hb_exec* x, void* out64) {
   return guard([&] {
@@ -437,7 +451,7 @@ int hb_exec_open_peers_local(hb_exec* x, hb_exec* const* execs, int n) {
     need(execs, "execs");
     if (n < 1 || n > hb::dev::kMaxGpus) hb::raise(hb::ErrorCode::InvalidArgument, "bad exec count");
     std::vector<hb::rt::Exec*> v(n, nullptr);
-    for (int g = 0; g < n; ++g) v[g] = execs[g] ? execs[g]->x.get() : nullptr;
+    for (int g = 0; g < n; ++g) v[g] = execs[g] ? execs[g]->x : nullptr;
     x->x->open_peers_local(v.data(), n);
   });
 }
@@ -596,6 +610,222 @@ int hb_projector_gemm(const void* x, long long ldx, const void* w, long long ldw
     const int st = hb::dev::launch_projector(x, ldx, w, ldw, a, hb::dev::device_sm_count(), cuda_stream);
     if (st == 3) hb::raise(hb::ErrorCode::InvalidArgument, "projector operands must be 16-B aligned");
     if (st) hb::raise(hb::ErrorCode::CudaError, "projector GEMM launch failed (" + std::to_string(st) + ")");
+  });
+}
+
+/* ---- graph-aware dispatch (SPEC.md:358-437 sched) ---------------------------- */
+
+int hb_stage_graph_create(const hb_layout* modules, int n_modules, const int* edge_src, const int* edge_dst,
+                          int n_edges, hb_stage_graph** out) {
+  return guard([&] {
+    need(modules, "modules");
+    need(out, "out");
+    *out = nullptr;
+    std::vector<hb::grid::ModuleLayout> ms;
+    for (int i = 0; i < n_modules; ++i) ms.push_back(layout(&modules[i]));
+    std::vector<std::pair<int, int>> es;
+    for (int i = 0; i < n_edges; ++i) es.emplace_back(edge_src[i], edge_dst[i]);
+    auto g = std::make_unique<hb_stage_graph>();
+    g->g = hb::sched::build_stage_graph(ms, es);
+    *out = g.release();
+  });
+}
+
+void hb_stage_graph_destroy(hb_stage_graph* g) { delete g; }
+
+int hb_stage_graph_nodes(const hb_stage_graph* g, int* out, int cap, int* n) {
+  return guard([&] {
+    need(g, "graph");
+    need(n, "n");
+    *n = static_cast<int>(g->g.nodes.size());
+    for (int i = 0; out && i < *n && i < cap; ++i) {
+      out[3 * i] = g->g.nodes[i].module;
+      out[3 * i + 1] = g->g.nodes[i].pp;
+      out[3 * i + 2] = g->g.nodes[i].distance;
+    }
+  });
+}
+
+int hb_stage_graph_edges(const hb_stage_graph* g, int* out, int cap, int* n) {
+  return guard([&] {
+    need(g, "graph");
+    need(n, "n");
+    *n = static_cast<int>(g->g.edges.size());
+    for (int i = 0; out && i < *n && i < cap; ++i) {
+      const auto& e = g->g.edges[i];
+      out[4 * i] = e.src;
+      out[4 * i + 1] = e.dst;
+      out[4 * i + 2] = static_cast<int>(e.kind);
+      out[4 * i + 3] = e.boundary;
+    }
+  });
+}
+
+namespace {
+hb_cell to_c(const hb::sched::Cell& c) {
+  return {c.row, c.node, static_cast<int>(c.op), c.edge, static_cast<int>(c.kind), c.mb, c.bwd ? 1 : 0};
+}
+hb::sched::Cell from_c(const hb_cell& c) {
+  return {c.row, c.node, static_cast<hb::sched::Op>(c.op), c.edge, static_cast<hb::sched::EdgeKind>(c.kind), c.mb,
+          c.bwd != 0};
+}
+void put_text(const std::string& s, char* buf, size_t cap, size_t* len) {
+  need(len, "len");
+  *len = s.size();
+  if (buf && cap) {
+    const size_t n = std::min(cap - 1, s.size());
+    std::memcpy(buf, s.data(), n);
+    buf[n] = 0;
+  }
+}
+}  // namespace
+
+int hb_dispatch_generate(const hb_stage_graph* g, int nmb, hb_cell* cells, size_t cap, size_t* n, int* rows) {
+  return guard([&] {
+    need(g, "graph");
+    need(n, "n");
+    const auto t = hb::sched::generate_1f1b_dispatch(g->g, nmb);
+    *n = t.cells.size();
+    if (rows) *rows = t.rows;
+    for (size_t i = 0; cells && i < t.cells.size() && i < cap; ++i) cells[i] = to_c(t.cells[i]);
+  });
+}
+
+int hb_dispatch_validate(const hb_stage_graph* g, const hb_cell* cells, size_t n, int nmb, char* report, size_t cap,
+                         size_t* len, int* n_violations) {
+  return guard([&] {
+    need(g, "graph");
+    need(n_violations, "n_violations");
+    std::vector<hb::sched::Cell> v;
+    for (size_t i = 0; i < n; ++i) v.push_back(from_c(cells[i]));
+    const auto out = hb::sched::validate_dispatch(g->g, v, nmb);
+    *n_violations = static_cast<int>(out.size());
+    std::string text;
+    for (const auto& s : out) text += s + "\n";
+    put_text(text, report, cap, len);
+  });
+}
+
+int hb_dispatch_render(const hb_stage_graph* g, int nmb, char* buf, size_t cap, size_t* len) {
+  return guard([&] {
+    need(g, "graph");
+    put_text(hb::sched::render(g->g, hb::sched::generate_1f1b_dispatch(g->g, nmb)), buf, cap, len);
+  });
+}
+
+/* ---- host-owned per-module runtime (a24 + the f2 dispatch executor) --------- */
+
+int hb_nccl_unique_id(void* out128) {
+  return guard([&] {
+    need(out128, "out");
+    hb::rt::nccl_unique_id(out128);
+  });
+}
+
+void hb_runtime_config_default(hb_runtime_config* c) {
+  if (!c) return;
+  hb::rt::HostConfig d;
+  c->nmb = d.nmb;
+  c->max_ctas = d.max_ctas;
+  c->pp_bytes = d.pp_bytes;
+  c->act_dtype = d.act_dtype;
+  c->grad_in_dtype = d.grad_in_dtype;
+  c->grad_out_dtype = d.grad_out_dtype;
+  c->timeout_s = d.timeout_s;
+  c->skip = d.skip;
+}
+
+int hb_runtime_create(const hb_layout* modules, int n_modules, const int* edge_src, const int* edge_dst, int n_edges,
+                      int global_batch, int feature_width, int world, int my_rank, const void* nccl_id128,
+                      const hb_runtime_config* cfg, hb_runtime** out) {
+  return guard([&] {
+    need(modules, "modules");
+    need(out, "out");
+    *out = nullptr;
+    std::vector<hb::grid::ModuleLayout> ms;
+    for (int i = 0; i < n_modules; ++i) ms.push_back(layout(&modules[i]));
+    std::vector<std::pair<int, int>> es;
+    for (int i = 0; i < n_edges; ++i) es.emplace_back(edge_src[i], edge_dst[i]);
+    hb::rt::HostConfig c;
+    if (cfg) {
+      c.nmb = cfg->nmb;
+      c.max_ctas = cfg->max_ctas;
+      c.pp_bytes = cfg->pp_bytes;
+      c.act_dtype = cfg->act_dtype;
+      c.grad_in_dtype = cfg->grad_in_dtype;
+      c.grad_out_dtype = cfg->grad_out_dtype;
+      c.timeout_s = cfg->timeout_s > 0 ? cfg->timeout_s : c.timeout_s;
+      c.skip = cfg->skip;
+    }
+    auto r = std::make_unique<hb_runtime>();
+    r->r = std::make_unique<hb::rt::HostRuntime>(ms, es, global_batch, feature_width, world, my_rank, nccl_id128, c);
+    for (int k = 0; k < n_edges; ++k) {
+      auto x = std::make_unique<hb_exec>();
+      x->x = r->r->edge_exec(k);
+      x->borrowed = true;
+      r->edge_execs.push_back(std::move(x));
+    }
+    *out = r.release();
+  });
+}
+
+void hb_runtime_destroy(hb_runtime* r) { delete r; }
+
+int hb_runtime_info(const hb_runtime* r, int* node, int* module, int* n_nodes, int* rows) {
+  return guard([&] {
+    need(r, "runtime");
+    if (node) *node = r->r->my_node();
+    if (module) *module = r->r->my_module();
+    if (n_nodes) *n_nodes = static_cast<int>(r->r->graph().nodes.size());
+    if (rows) *rows = r->r->table().rows;
+  });
+}
+
+int hb_runtime_group(const hb_runtime* r, int kind, int* out, int cap, int* n) {
+  return guard([&] {
+    need(r, "runtime");
+    fill(r->r->group(kind), out, cap, n);
+  });
+}
+
+int hb_runtime_edge_exec(hb_runtime* r, int module_edge, hb_exec** out) {
+  return guard([&] {
+    need(r, "runtime");
+    need(out, "out");
+    if (module_edge < 0 || module_edge >= static_cast<int>(r->edge_execs.size()))
+      hb::raise(hb::ErrorCode::InvalidArgument, "module edge out of range");
+    *out = r->edge_execs[module_edge].get();
+  });
+}
+
+int hb_runtime_stage_buffer(hb_runtime* r, int which, int mb, void** ptr, size_t* bytes) {
+  return guard([&] {
+    need(r, "runtime");
+    need(ptr, "ptr");
+    *ptr = r->r->stage_buffer(which, mb, bytes);
+  });
+}
+
+int hb_runtime_stream(hb_runtime* r, int which, void** stream) {
+  return guard([&] {
+    need(r, "runtime");
+    need(stream, "stream");
+    *stream = r->r->stream(which);
+  });
+}
+
+int hb_runtime_step(hb_runtime* r, hb_compute_fn fn, void* user) {
+  return guard([&] {
+    need(r, "runtime");
+    r->r->step(reinterpret_cast<hb::rt::ComputeFn>(fn), user);
+  });
+}
+
+int hb_runtime_last_step_ms(hb_runtime* r, float* ms) {
+  return guard([&] {
+    need(r, "runtime");
+    need(ms, "ms");
+    *ms = r->r->last_step_ms();
   });
 }
 

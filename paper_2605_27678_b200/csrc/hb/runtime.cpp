@@ -561,6 +561,16 @@ void Exec::build_partition(const std::vector<uint64_t>& w0, const std::vector<ui
         ck(cudaMemcpy(*dst, table.data(), table.size() * sizeof(uint2), cudaMemcpyHostToDevice), "upload");
       }
     }
+    // Grid sized to the op: no more CTAs than chunks (a CTA without a chunk
+    // only adds arrival and claim traffic); a GPU with no work for this kind
+    // keeps one CTA, which posts "started" and waits for its peers.
+    {
+      const uint32_t chunks = out->total_chunks + out->rtotal_chunks;
+      int g = static_cast<int>(std::min<uint64_t>(static_cast<uint64_t>(grid), std::max<uint32_t>(chunks, 1)));
+      if (out->total_chunks && out->rtotal_chunks) g = std::max(g, std::min(grid, 2));
+      grid = g;
+      out->grid = g;
+    }
     // CTAs that start on the remote queue ~ the remote share of the time
     // (NVLink ~770 GB/s vs HBM copy ~6.5 TB/s counted read+write).
     if (out->rtotal_chunks == 0) {
@@ -572,7 +582,7 @@ void Exec::build_partition(const std::vector<uint64_t>& w0, const std::vector<ui
       // HB_REMOTE_PCT overrides the remote share of the grid (tuning knob)
       static const double frac = static_cast<double>(env_u64("HB_REMOTE_PCT", 0)) / 100.0;
       const double f = frac > 0 ? frac : tr / (tr + tl);
-      out->remote_ctas = std::clamp(static_cast<int>(grid * f + 0.5), 1, grid - 1);
+      out->remote_ctas = grid < 2 ? 0 : std::clamp(static_cast<int>(grid * f + 0.5), 1, grid - 1);
     }
     static const int prefetch = static_cast<int>(env_u64("HB_CLAIM_PREFETCH", 1));  // A/B knob
     out->prefetch_other = prefetch;

@@ -45,3 +45,17 @@ def test_multigpu_caller_buffers(n, mode):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env)
     print(r.stdout[-4000:], r.stderr[-4000:])
     assert r.returncode == 0
+
+
+@pytest.mark.parametrize("n,topologies", [(4, ["c5w4", "join4"]), (6, ["fig4a"]), (8, ["fig4a", "c5"])])
+def test_host_runtime_dispatch(n, topologies):
+    """a24 + f2: the host-owned runtime (NCCL world + PP communicators split per
+    module, boundary execs, three streams) executes the graph-aware 1F1B table;
+    NC shards and P2P stage buffers are checked on every rank."""
+    if torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29800 + n), os.path.join(HERE, "runtime_worker.py")]
+    r = subprocess.run(cmd + topologies, capture_output=True, text=True, timeout=900)
+    print(r.stdout[-4000:], r.stderr[-4000:])
+    assert r.returncode == 0
