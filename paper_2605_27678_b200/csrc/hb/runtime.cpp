@@ -315,6 +315,7 @@ void Exec::open_peers_local(Exec* const* execs, int n) {
         p->mb_stride_ != mb_stride_ || p->cfg_.mb_slots != cfg_.mb_slots || !p->local_base_)
       raise(ErrorCode::InvalidArgument, "open_peers_local: exec of GPU " + std::to_string(g) +
                                             " has a different configuration or no device region");
+    if (p->device_ == device_) shared_device_ = true;
     if (p->device_ != device_) {
       int can = 0;
       ck(cudaDeviceCanAccessPeer(&can, device_, p->device_), "cudaDeviceCanAccessPeer");
@@ -814,6 +815,7 @@ dev::SyncArgs Exec::make_sync_args(int kind, bool push) const {
   }
   s.timeout_cycles = static_cast<uint64_t>(cfg_.timeout_s * clock_khz_ * 1e3);
   if (trace_) s.trace = trace_ + static_cast<size_t>(kind) * dev::kTraceMaxCtas * dev::kTraceWords;
+  s.pdl = shared_device_ ? 0 : 1;
   return s;
 }
 

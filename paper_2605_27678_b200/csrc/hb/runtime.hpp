@@ -216,6 +216,7 @@ class Exec {
                        int mode, uint64_t unit, DevPartition* out);
   bool dirty_fwd_ = true, dirty_bwd_ = true;
   bool graphs_invalidated_ = false;
+  bool shared_device_ = false;  // a peer exec of the group runs on this device (no PDL)
   void mark_dirty();  // tables rebuilt at the next op; captured graphs dropped
   void check_forward_mb(int mb) const;
   int bwd_groups_ = 0;  // device reduce segments (fan-out groups of bwd_local_)

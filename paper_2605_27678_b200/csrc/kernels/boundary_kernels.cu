@@ -24,6 +24,7 @@
 // Roofline (pure data movement; tensor cores not applicable): time >=
 // max(HBM bytes / HBM BW, NVLink ingress / NVLink BW); see DESIGN.md.
 #include <cstdlib>
+#include <tuple>
 
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -150,6 +151,7 @@ __device__ __forceinline__ void run_shares(const S* __restrict__ segs, int nseg,
   __shared__ uint32_t cur;  // chunk being processed (kNoChunk: none)
   __shared__ int cur_remote;
   unsigned long long arr = 0;
+  griddep_wait();
   if (blockIdx.x == 0 && threadIdx.x < 32) {
     post_peers_warp(sync, 0);
     __syncwarp();
@@ -207,6 +209,7 @@ __device__ __forceinline__ void run_shares(const S* __restrict__ segs, int nseg,
       __syncthreads();
       if (cur == kNoChunk) break;
     }
+    griddep_launch_dependents();  // this CTA's work is done: the next op may take its slot
     if (threadIdx.x == 0) {
       trace_at(sync, kTrDone);
       launch_end_lane(sync, cs);
@@ -240,6 +243,7 @@ __device__ __forceinline__ void run_shares(const S* __restrict__ segs, int nseg,
       }
     }
     __syncthreads();
+    griddep_launch_dependents();
     if (threadIdx.x == 0) launch_end_lane(sync, cs);
   }
 }
@@ -390,6 +394,7 @@ __global__ void __launch_bounds__(32) copy_segments_tma_kernel(const CopySeg* __
   extern __shared__ __align__(128) unsigned char stage_mem[];
   __shared__ __align__(8) uint64_t full[kTmaStages];
   __shared__ CtaSync cs;
+  griddep_wait();
   if (blockIdx.x == 0) {
     post_peers_warp(sync, 0);
     __syncwarp();
@@ -511,6 +516,7 @@ __global__ void __launch_bounds__(32) copy_segments_tma_kernel(const CopySeg* __
   // stores visible to the stream's next kernel, as a TMA-store epilogue does).
   if (sync.end_sync) bulk_wait_all();
   else bulk_wait_read<0>();
+  griddep_launch_dependents();  // this CTA's work is issued and its stages read: the next op may take its slot
   arrive();
   trace_at(sync, kTrDone);
   launch_end_lane(sync, cs);
@@ -990,14 +996,18 @@ int copy_blocks_per_sm(int threads) {
 
 template <int ST, uint32_t SB>
 static int tma_occupancy() {
-  static int n = -1;
-  if (n < 0) {
+  static PerDeviceOnce once;
+  static int n = 1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  once(dev, [] {
     const int smem = ST * SB;
     cudaFuncSetAttribute(copy_segments_tma_kernel<ST, SB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(copy_segments_tma_kernel<ST, SB>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, copy_segments_tma_kernel<ST, SB>, 32, smem);
-    if (n < 1) n = 1;
-  }
+    int k = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&k, copy_segments_tma_kernel<ST, SB>, 32, smem);
+    n = k < 1 ? 1 : k;  // identical devices: one value serves them all
+  });
   return n;
 }
 
@@ -1009,34 +1019,59 @@ int tma_blocks_per_sm(uint64_t chunk) {
 
 uint64_t tma_chunk_bytes(int kib) { return (kib == 16 || kib == 8) ? kib * 1024ull : 32 * 1024ull; }
 
+// Every boundary kernel goes out with programmatic stream serialisation (PDL,
+// launch_protocol.cuh); HB_PDL=0 launches them plainly (A/B knob).
+template <class... KArgs, class... Args>
+static void launch_pdl(void (*k)(KArgs...), int grid, int block, size_t smem, cudaStream_t st, Args... args) {
+  static const bool env_pdl = [] {
+    const char* v = std::getenv("HB_PDL");
+    return !(v && v[0] == '0');
+  }();
+  // SyncArgs (the last argument) says whether this exec may overlap launches
+  const bool pdl = env_pdl && std::get<sizeof...(Args) - 1>(std::make_tuple(args...)).pdl;
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3(grid);
+  lc.blockDim = dim3(block);
+  lc.dynamicSmemBytes = smem;
+  lc.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = at;
+  lc.numAttrs = pdl ? 1 : 0;
+  cudaLaunchKernelEx(&lc, k, args...);
+}
+
 void launch_copy(const CopySeg* segs, int nseg, Partition part, const SyncArgs& sync, LaunchCfg cfg,
                  void* stream) {
   auto st = static_cast<cudaStream_t>(stream);
   if (part.mode == kPartTma) {
     tma_blocks_per_sm(part.chunk);
     if (part.chunk == 16 * 1024)
-      copy_segments_tma_kernel<6, 16 * 1024><<<cfg.grid, 32, 6 * 16 * 1024, st>>>(segs, nseg, part, sync);
+      launch_pdl(copy_segments_tma_kernel<6, 16 * 1024>, cfg.grid, 32, 6 * 16 * 1024, st, segs, nseg, part, sync);
     else if (part.chunk == 8 * 1024)
-      copy_segments_tma_kernel<8, 8 * 1024><<<cfg.grid, 32, 8 * 8 * 1024, st>>>(segs, nseg, part, sync);
+      launch_pdl(copy_segments_tma_kernel<8, 8 * 1024>, cfg.grid, 32, 8 * 8 * 1024, st, segs, nseg, part, sync);
     else
-      copy_segments_tma_kernel<3, 32 * 1024><<<cfg.grid, 32, 3 * 32 * 1024, st>>>(segs, nseg, part, sync);
+      launch_pdl(copy_segments_tma_kernel<3, 32 * 1024>, cfg.grid, 32, 3 * 32 * 1024, st, segs, nseg, part, sync);
   } else if (part.mode == kPartInterleaved) {
-    copy_segments_kernel<kPartInterleaved><<<cfg.grid, cfg.block, 0, st>>>(segs, nseg, part, sync);
+    launch_pdl(copy_segments_kernel<kPartInterleaved>, cfg.grid, cfg.block, 0, st, segs, nseg, part, sync);
   } else if (part.mode == kPartDynamic) {
-    copy_segments_kernel<kPartDynamic><<<cfg.grid, cfg.block, 0, st>>>(segs, nseg, part, sync);
+    launch_pdl(copy_segments_kernel<kPartDynamic>, cfg.grid, cfg.block, 0, st, segs, nseg, part, sync);
   } else {
-    copy_segments_kernel<kPartContiguous><<<cfg.grid, cfg.block, 0, st>>>(segs, nseg, part, sync);
+    launch_pdl(copy_segments_kernel<kPartContiguous>, cfg.grid, cfg.block, 0, st, segs, nseg, part, sync);
   }
 }
 
 template <class TIn, class TOut, bool FAN>
 static int red_ring_smem() {
-  static const int smem = [] {
+  static PerDeviceOnce once;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  once(dev, [] {
     cudaFuncSetAttribute(reduce_segments_kernel<TIn, TOut, kPartDynamic, FAN>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, kRedRingBytes);
-    return static_cast<int>(kRedRingBytes);
-  }();
-  return smem;
+  });
+  return static_cast<int>(kRedRingBytes);
 }
 
 // HB_RED_CARVEOUT (A/B knob, percent of the unified L1/smem given to shared
@@ -1045,7 +1080,10 @@ static int red_ring_smem() {
 // backward launch.
 template <class TIn, class TOut, bool FAN>
 static void red_carveout() {
-  static const bool done = [] {
+  static PerDeviceOnce once;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  once(dev, [] {
     const char* v = std::getenv("HB_RED_CARVEOUT");
     const int pct = v && *v ? std::atoi(v) : 0;
     if (pct > 0) {
@@ -1056,9 +1094,7 @@ static void red_carveout() {
       cudaFuncSetAttribute(reduce_segments_kernel<TIn, TOut, kPartInterleaved, FAN>,
                            cudaFuncAttributePreferredSharedMemoryCarveout, pct);
     }
-    return true;
-  }();
-  (void)done;
+  });
 }
 
 template <class TIn, class TOut, bool FAN>
@@ -1066,16 +1102,16 @@ static void launch_reduce_f(const ReduceSeg* segs, int nseg, const void* const* 
                             float beta, const SyncArgs& sync, int grid, int block, cudaStream_t st) {
   red_carveout<TIn, TOut, FAN>();
   if (part.mode == kPartInterleaved)
-    reduce_segments_kernel<TIn, TOut, kPartInterleaved, FAN><<<grid, block, 0, st>>>(segs, nseg, terms, part, beta,
-                                                                                    sync);
+    launch_pdl(reduce_segments_kernel<TIn, TOut, kPartInterleaved, FAN>, grid, block, 0, st, segs, nseg, terms, part,
+               beta, sync);
   else if (part.mode == kPartDynamic)
     // the ring's shared memory only when there are remote chunks to stage
-    reduce_segments_kernel<TIn, TOut, kPartDynamic, FAN>
-        <<<grid, block, part.ring && part.rtotal_chunks ? red_ring_smem<TIn, TOut, FAN>() : 0, st>>>(
-            segs, nseg, terms, part, beta, sync);
+    launch_pdl(reduce_segments_kernel<TIn, TOut, kPartDynamic, FAN>, grid, block,
+               part.ring && part.rtotal_chunks ? red_ring_smem<TIn, TOut, FAN>() : 0, st, segs, nseg, terms, part,
+               beta, sync);
   else
-    reduce_segments_kernel<TIn, TOut, kPartContiguous, FAN><<<grid, block, 0, st>>>(segs, nseg, terms, part, beta,
-                                                                                   sync);
+    launch_pdl(reduce_segments_kernel<TIn, TOut, kPartContiguous, FAN>, grid, block, 0, st, segs, nseg, terms, part,
+               beta, sync);
 }
 
 template <class TIn, class TOut>

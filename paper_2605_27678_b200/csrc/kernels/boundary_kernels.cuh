@@ -1,6 +1,7 @@
 // hetbridge — device-side descriptors shared by the runtime and the kernels.
 #pragma once
 
+#include <atomic>
 #include <cstdint>
 
 #include <vector_types.h>
@@ -126,6 +127,10 @@ struct SyncArgs {
   // resolved, peers confirmed, first chunk landed, work done, exit — and the
   // CTA's chunk counts (total, remote).
   unsigned long long* trace;
+  // host-side: launch with programmatic dependent launch (off when execs of
+  // one group share a device: early-scheduled CTAs of one exec could hold the
+  // slots a co-resident peer exec needs to start)
+  int pdl;
 };
 constexpr int kTraceWords = 8;
 constexpr int kTraceMaxCtas = 4096;
@@ -134,6 +139,20 @@ constexpr int kCtrBytes = 4 * 128;  // arrive | queues | fin | err lines
 struct LaunchCfg {
   int grid;
   int block;
+};
+
+// Kernel attributes (dynamic shared memory size, carveout, clusters) are per
+// device: one process may drive several GPUs (hb_exec_open_peers_local), so
+// set them once per device, not once per process.
+struct PerDeviceOnce {
+  std::atomic<uint64_t> done{0};
+  template <class F>
+  void operator()(int device, F&& f) {
+    const uint64_t bit = 1ull << (device & 63);
+    if (done.load(std::memory_order_acquire) & bit) return;
+    f();  // idempotent: two racing threads both setting an attribute is harmless
+    done.fetch_or(bit, std::memory_order_acq_rel);
+  }
 };
 
 // Host-side launchers (defined in boundary_kernels.cu).

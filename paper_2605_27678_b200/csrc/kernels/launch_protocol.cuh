@@ -28,6 +28,21 @@ __device__ __forceinline__ void post_peers_warp(const SyncArgs& s, int word) {
   }
 }
 
+// Programmatic dependent launch (PDL). Boundary kernels are launched with
+// programmatic stream serialisation: the next kernel of the stream may be
+// scheduled as soon as every CTA of this one has called launch_dependents (we
+// call it on entry, so each SM slot this grid frees takes a CTA of the next
+// op at once), and griddepcontrol.wait blocks until this stream's previous
+// grid has completed and its memory is visible. Every boundary kernel waits
+// before its first global access (the "started" post, counters, buffers), so
+// the launch protocol's meaning is unchanged: only launch latency and CTA
+// scheduling overlap the previous kernel's tail. Without a programmatic
+// dependency (first kernel, a producer launched without PDL) wait returns at once.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ unsigned long long global_ns() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));

@@ -366,15 +366,16 @@ int launch_projector(const void* x, int64_t ldx, const void* w, int64_t ldw, con
   // M == 0: this GPU projects no rows but still takes part in the launch protocol
   if (args.M > 0 && (!make_map(&mx, x, args.M, args.K, ldx, kBM) || !make_map(&mw, w, args.N, args.K, ldw, kBN / cm)))
     return 4;
-  static bool attr = [] {
+  static PerDeviceOnce once;  // function attributes are per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  once(dev, [] {
     cudaFuncSetAttribute(projector_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(kSmemBytes));
     cudaFuncSetAttribute(projector_gemm_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(kSmemBytes));
     cudaFuncSetAttribute(projector_gemm_kernel<2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
-    return true;
-  }();
-  (void)attr;
+  });
   const int items = ((args.M + kBM - 1) / kBM + cm - 1) / cm * (args.N / kBN);
   int grid = items * cm < sm_count ? items * cm : sm_count - sm_count % cm;
   if (grid < cm) grid = cm;
