@@ -62,6 +62,8 @@ def parse():
                     help="configs also measured (short) in the same run, so every N of the driver's scaling "
                          "run records the fan-in / fan-out / CP-splice / non-colocated step ('' = none)")
     ap.add_argument("--matrix-steps", type=int, default=200)
+    ap.add_argument("--no-runtime", action="store_true",
+                    help="skip the host-runtime leg (a24 + f2: 1F1B dispatch table with NC || PP P2P, N = 4, 6, 8)")
     ap.add_argument("--ref-procs", type=int, default=0, help="reference arm: worker processes (0 = auto)")
     return ap.parse_args()
 
@@ -582,6 +584,15 @@ def run_reference(args):
 # ----------------------------------------------------------------------------- GPU leg
 
 
+_T0 = time.time()
+
+
+def phase(msg):
+    """HB_BENCH_LOG=1: phase timestamps on stderr (every rank), to locate stalls."""
+    if os.environ.get("HB_BENCH_LOG") == "1":
+        print(f"[bench r{os.environ.get('RANK', '0')} +{time.time() - _T0:7.1f}s] {msg}", file=sys.stderr, flush=True)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -617,14 +628,17 @@ def main():
     # rank-independent (every process must allocate the same number of buffer sets)
     slots = default_slots(cfg, N, args)
 
+    phase("runtime create")
     rt = hbb.BridgeRuntime(plan, sp, n_gpus=N, my_gpu=rank, rank_to_gpu=r2g, act_dtype=tdt[cfg.act],
                            grad_in_dtype=tdt[cfg.grad_in], grad_out_dtype=tdt[cfg.grad_out],
                            mb_slots=slots, blocks_per_sm=args.blocks_per_sm, threads=args.threads,
                            fwd_mode=args.fwd_mode, partition=args.partition)
     if N > 1:
         rt.exchange_handles()
+    phase("fill inputs")
     fill_inputs(rt, local, slots, dev)
     torch.cuda.synchronize()
+    phase("warm-up")
     stream = torch.cuda.Stream(priority=-1)
 
     def barrier():
@@ -655,6 +669,7 @@ def main():
         for k in range(slots):
             rt.replay_step(k, stream)
         barrier()
+    phase("timed loop")
     launches0 = rt.stats()["launches"]
     barrier()
     sampler.mark(True)
@@ -697,6 +712,7 @@ def main():
             rt.backward(mb, cfg.beta, stream)
             mb += 1
 
+    phase("parity")
     parity = check_parity(rt, cfg, plan, sp, r2g, rank, N, dev, stream, barrier, run_step, (K - 1) % slots)
 
     # per-kernel steady state: each op alone, replayed back to back as a CUDA graph
@@ -721,6 +737,7 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     iso_fwd_ms, iso_bwd_ms = t.tolist()
     barrier()
+    phase("isolated ops + one graph per step")
     ms_graph_per_step = None
     if cycle:  # the same steps with one graph launch per step (host launch cost per step)
         for k in range(slots):
@@ -800,10 +817,27 @@ def main():
         rt = None
         torch.cuda.synchronize()
         for name in names:
+            phase(f"matrix {name}")
             try:
                 matrix[name] = run_matrix_config(args, name, N, rank, dev, barrier, stream, pk)
             except Exception as exc:  # a diagnostic leg never voids the headline line
                 matrix[name] = {"error": f"{type(exc).__name__}: {exc}"}
+
+    host_rt = None
+    if N > 1 and host_runtime_topologies(N) and not args.no_runtime:
+        if rt is not None:
+            rt.close()
+            rt = None
+        torch.cuda.synchronize()
+        host_rt = []
+        for name in host_runtime_topologies(N):
+            phase(f"host runtime {name}")
+            try:
+                res = run_host_runtime(name, rank, N, dev)
+            except Exception as exc:  # a diagnostic leg never voids the headline line
+                res = {"topology": name, "error": f"{type(exc).__name__}: {exc}"}
+            if res is not None:
+                host_rt.append(res)
 
     cpu = None
     if rank == 0 and not args.no_cpu:  # rank 0 at every N (host cores of the GPU box)
@@ -843,12 +877,137 @@ def main():
             "nccl_comparison": nccl,
             "overlap_with_pp_p2p": overlap,
             "config_matrix": matrix,
+            "host_runtime": host_rt,
         }
         print(json.dumps(line), flush=True)
     if rt is not None:
         rt.close()
     if N > 1:
         dist.destroy_process_group()
+
+
+# ----------------------------------------------------------------------------- host runtime (a24 + f2)
+
+def host_runtime_topologies(N):
+    """Topologies the host-owned runtime leg runs at N GPUs (one rank per GPU)."""
+    return {4: ["c5w4", "join4"], 6: ["fig4a"], 8: ["c5", "fig4a"]}.get(N, [])
+
+
+def rt_topology(name):
+    """(modules, edges, global batch, feature width, pp bytes)"""
+    from paper_2605_27678_b200 import sched as S
+    from paper_2605_27678_b200.grid import ModuleLayout
+
+    if name == "c5w4":  # C5 at 4 GPUs: vit{dp1}@0 -> llm{pp3}@1-3
+        return [ModuleLayout("vit", rank_offset=0), ModuleLayout("llm", pp=3, rank_offset=1)], [(0, 1)], 8, 576 * 512, 1 << 22
+    if name == "join4":  # Fig. 4(a) shape at 4 GPUs: E1 pp2, E2 pp1 -> LLM pp1 (a join of two NC edges)
+        return ([ModuleLayout("E1", pp=2, rank_offset=0), ModuleLayout("E2", rank_offset=2),
+                 ModuleLayout("LLM", rank_offset=3)], [(0, 2), (1, 2)], 8, 576 * 256, 1 << 20)
+    if name == "fig4a":  # PAPER Fig. 4(a): E1 pp2, E2 pp1, LLM pp3 (6 GPUs)
+        mods, edges = S.fig4a_modules()
+        return mods, edges, 8, 576 * 256, 1 << 20
+    if name == "c5":  # BASELINE C5: vit{dp2}@0-1 -> llm{tp2,pp3}@2-7 (8 GPUs), bf16 h4096, 16 img x 576
+        return ([ModuleLayout("vit", dp=2, rank_offset=0), ModuleLayout("llm", tp=2, pp=3, rank_offset=2)],
+                [(0, 1)], 16, 576 * 4096, 16 * 576 * 4096 * 2)
+    raise KeyError(name)
+
+
+def hkey(*a):
+    k = 0
+    for x in a:
+        k = k * 131 + x + 1
+    return k * 7919
+
+
+def run_host_runtime(name, rank, world, dev, steps=5):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_27678_b200 import bridge as hbb
+    from paper_2605_27678_b200 import parity as P
+    from paper_2605_27678_b200 import runtime as R
+
+    mods, edges, B, W, ppb = rt_topology(name)
+    if max(m.rank_end() for m in mods) > world:
+        return None
+    rt = R.HostRuntime(mods, edges, B, W, nmb=4, pp_bytes=ppb, skip=R.SKIP_COMPUTE)
+    ok = True
+    views = [rt.edge_runtime(k) for k in range(len(edges))]
+    # fill boundary shards (every buffer set = microbatch slot) and stage buffers
+    for k, v in enumerate(views):
+        for mb in range(rt.nmb):
+            for slot in (hbb.SLOT_SRC_ACT, hbb.SLOT_DST_GRAD):
+                if v.buffer_numel(rank, slot) and v.rank_to_gpu[rank] == rank:
+                    try:
+                        b = v.buffer(rank, slot, mb)
+                    except hbb.HetBridgeError:
+                        b = None
+                    if b is not None:
+                        b.copy_(fill_values(b.numel(), hkey(k, slot, mb, rank), b.dtype, dev))
+    for mb in range(rt.nmb):
+        for which in (R.ACT_OUT, R.GRAD_OUT):
+            t = rt.stage_buffer(which, mb)
+            if t is not None:
+                t.view(torch.int16).copy_(fill_values(t.numel() // 2, hkey(9, which, mb, rank), torch.bfloat16,
+                                                            dev).view(torch.int16))
+    torch.cuda.synchronize()
+    dist.barrier()
+    rt.step()
+    ms_first = rt.last_step_ms()
+    torch.cuda.synchronize()
+    dist.barrier()
+    # NC checks
+    for k, v in enumerate(views):
+        fwd_map, bwd_map = hbb.index_forward(v.plan), hbb.index_backward(v.plan, balanced=True)
+        for mb in range(rt.nmb):
+            def regen(r, slot, _k=k, _mb=mb, _v=v):
+                n = _v.buffer_numel(r, slot)
+                dt = _v.act_dtype if slot == hbb.SLOT_SRC_ACT else _v.grad_in_dtype
+                return fill_values(n, hkey(_k, slot, _mb, r), dt, dev)
+            if v.buffer_numel(rank, hbb.SLOT_DST_ACT):
+                out = v.buffer(rank, hbb.SLOT_DST_ACT, mb)
+                exp, cov = P.expected_forward(fwd_map, rank, out.numel(), regen)
+                ok &= cov == out.numel() and bool(torch.equal(out.view(torch.int16), exp.view(torch.int16)))
+            if v.buffer_numel(rank, hbb.SLOT_SRC_GRAD):
+                got = v.buffer(rank, hbb.SLOT_SRC_GRAD, mb)
+                exp = P.expected_backward(bwd_map, rank, torch.zeros_like(got), 0.0, regen)
+                ok &= bool(torch.equal(got, exp))
+    # P2P checks: neighbours in my module's PP group
+    pp = rt.group(2)
+    if rt.module >= 0 and len(pp) > 1:
+        i = pp.index(rank)
+        for mb in range(rt.nmb):
+            if i > 0:
+                exp = fill_values(ppb // 2, hkey(9, R.ACT_OUT, mb, pp[i - 1]), torch.bfloat16, dev)
+                ok &= bool(torch.equal(rt.stage_buffer(R.ACT_IN, mb).view(torch.int16), exp.view(torch.int16)))
+            if i + 1 < len(pp):
+                exp = fill_values(ppb // 2, hkey(9, R.GRAD_OUT, mb, pp[i + 1]), torch.bfloat16, dev)
+                ok &= bool(torch.equal(rt.stage_buffer(R.GRAD_IN, mb).view(torch.int16), exp.view(torch.int16)))
+    flag = torch.tensor([0 if ok else 1], device=dev)
+    dist.all_reduce(flag)
+    rt.close()
+    # overlap: the same table with one traffic class skipped
+    times = {}
+    for label, skip in (("nc_only", R.SKIP_COMPUTE | R.SKIP_P2P), ("p2p_only", R.SKIP_COMPUTE | R.SKIP_NC),
+                        ("both", R.SKIP_COMPUTE)):
+        r2 = R.HostRuntime(mods, edges, B, W, nmb=4, pp_bytes=ppb, skip=skip)
+        r2.step()
+        r2.last_step_ms()
+        ts = []
+        for _ in range(steps):
+            dist.barrier()
+            r2.step()
+            ts.append(r2.last_step_ms())
+        t = torch.tensor([statistics.median(ts)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        times[label] = round(t.item(), 4)
+        r2.close()
+    tb, tp, both = times["nc_only"], times["p2p_only"], times["both"]
+    overlap = (tb + tp - both) / max(1e-9, min(tb, tp))
+    return {"topology": name, "n_gpus": world, "parity": flag.item() == 0, "rows": rt.rows,
+            "first_step_ms": round(ms_first, 3), "step_ms": times, "overlap": round(overlap, 3),
+            "how": "HostRuntime.step over the 1F1B dispatch table (event-only compute); NC = boundary exec "
+                   "fwd/bwd on the boundary stream, P2P = NCCL send/recv on the PP communicator"}
 
 
 def copy_kernel_name(args):
@@ -879,6 +1038,7 @@ def run_matrix_config(args, name, N, rank, dev, barrier, stream, pk):
     tm = traffic_model(cfg, N)
     per_gpu_step = max(f + b for f, b in zip(tm["fwd_hbm"], tm["bwd_hbm"]))
     slots = max(4, min(8, math.ceil(3 * L2_BYTES / max(per_gpu_step, 1))))
+    phase("runtime create")
     rt = hbb.BridgeRuntime(plan, sp, n_gpus=N, my_gpu=rank, rank_to_gpu=r2g, act_dtype=tdt[cfg.act],
                            grad_in_dtype=tdt[cfg.grad_in], grad_out_dtype=tdt[cfg.grad_out], mb_slots=slots)
     try:

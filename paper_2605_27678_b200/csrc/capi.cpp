@@ -536,6 +536,9 @@ int hb_exec_status(hb_exec* x, unsigned* device_error) {
     const unsigned e = x->x->device_error();
     if (device_error) *device_error = e;
     if (e == hb::dev::kErrBadId) hb::raise(hb::ErrorCode::InvalidArgument, "text token id outside [0, vocab)");
+    if (e == hb::dev::kErrOutOfTurn)
+      hb::raise(hb::ErrorCode::GroupMismatch,
+                "a peer GPU started a boundary op two or more ahead of this one: the group's op sequences diverged");
     if (e) hb::raise(hb::ErrorCode::Timeout, "cross-GPU flag wait timed out on the device");
   });
 }

@@ -525,8 +525,9 @@ uint64_t Exec::pad_unit(int mode, bool copy) const {
 
 void Exec::build_partition(const std::vector<uint64_t>& w0, const std::vector<uint64_t>& n,
                            const std::vector<char>& remote, double local_bytes, double remote_bytes, int grid,
-                           int mode, uint64_t unit, DevPartition* out) {
+                           int mode, uint64_t unit, DevPartition* out, uint64_t runit) {
   const uint64_t total = w0.empty() ? 0 : w0.back() + n.back();
+  if (runit == 0) runit = unit;
   cudaFree(out->first_seg);
   cudaFree(out->chunks);
   cudaFree(out->rchunks);
@@ -535,6 +536,7 @@ void Exec::build_partition(const std::vector<uint64_t>& w0, const std::vector<ui
   out->grid = grid;
   out->mode = mode;
   out->chunk = unit;
+  out->rchunk = runit;
   out->total_chunks = out->rtotal_chunks = 0;
   out->remote_ctas = 0;
   out->lstatic = out->rstatic = 0;
@@ -547,7 +549,8 @@ void Exec::build_partition(const std::vector<uint64_t>& w0, const std::vector<ui
       std::vector<std::pair<double, uint2>> order;
       for (size_t s = 0; s < n.size(); ++s) {
         if ((remote[s] != 0) != (q == 1)) continue;
-        const uint64_t k = (n[s] + unit - 1) / unit;
+        const uint64_t u = q ? runit : unit;
+        const uint64_t k = (n[s] + u - 1) / u;
         for (uint64_t j = 0; j < k; ++j)
           order.push_back({(j + 0.5) / static_cast<double>(k),
                            make_uint2(static_cast<unsigned>(s), static_cast<unsigned>(j))});
@@ -579,6 +582,7 @@ void Exec::build_partition(const std::vector<uint64_t>& w0, const std::vector<ui
     } else if (out->total_chunks == 0) {
       out->remote_ctas = grid;
     } else {
+      // remote_bytes: NVLink bytes; local_bytes: HBM bytes counted as a copy's (read + write) / 2
       const double tr = remote_bytes / 770e9, tl = 2.0 * local_bytes / 6.5e12;
       // HB_REMOTE_PCT overrides the remote share of the grid (tuning knob)
       static const double frac = static_cast<double>(env_u64("HB_REMOTE_PCT", 0)) / 100.0;
@@ -771,16 +775,44 @@ void Exec::prepare_bwd() {
   const int bps = cfg_.blocks_per_sm > 0 ? std::min(cfg_.blocks_per_sm, occ) : occ;
   std::vector<char> rem;
   double lb = 0, rb = 0;
+  uint64_t rtotal = 0;
   for (size_t i = 0; i < groups.size(); ++i) {
-    bool r = false;
-    for (const auto& t : bwd_local_[groups[i][0]].terms) r |= gpu_of(t.rank) != my_gpu_;
-    rem.push_back(r);
-    (r ? rb : lb) += static_cast<double>(ns[i]) * (es_in + 2 * es_out * groups[i].size());
+    int rterms = 0;
+    for (const auto& t : bwd_local_[groups[i][0]].terms) rterms += gpu_of(t.rank) != my_gpu_;
+    rem.push_back(rterms > 0);
+    // time weights: a remote group costs its NVLink ingress (each remote term
+    // once; its HBM read-modify-write runs under the link time), a local one
+    // its HBM reads + accumulator read-modify-writes
+    if (rterms) {
+      rb += static_cast<double>(ns[i]) * es_in * rterms;
+      rtotal += ns[i];
+    } else {
+      lb += 0.5 * static_cast<double>(ns[i]) * (es_in * bwd_local_[groups[i][0]].terms.size() +
+                                                 2 * es_out * groups[i].size());
+    }
   }
   bwd_groups_ = static_cast<int>(groups.size());
   int fan = 0;
   for (const auto& g : groups) fan |= g.size() > 1;
-  build_partition(w0s, ns, rem, lb, rb, grid_cap(sm_count_ * bps), mode, unit, &bwd_part_);
+  const int bgrid = grid_cap(sm_count_ * bps);
+  // Remote chunks: longer than local ones when the return is large (every
+  // stage of a chunk is in flight at once), up to half the TMA ring and while
+  // every CTA still gets >= 4 remote chunks. Measured at N=4 (one box, A/B):
+  // c3x4 bwd 239.6 -> 232.3 us with 16K-element remote chunks; c4 (9.4M
+  // remote elements per GPU) is 2-4% slower with 16K or 32K than with 8K.
+  // HB_RED_RCHUNK sets it (elements; A/B knob).
+  uint64_t runit = unit;
+  if (mode == dev::kPartDynamic) {
+    static const uint64_t env_r = env_u64("HB_RED_RCHUNK", 0);
+    const uint64_t ring_elems = dev::red_ring_elems(cfg_.grad_in_dtype);
+    if (env_r) {
+      runit = pad_to(env_r, 8);
+    } else {
+      runit = 8192;
+      while (runit * 2 <= ring_elems / 2 && rtotal / (runit * 2) >= 4 * static_cast<uint64_t>(bgrid)) runit *= 2;
+    }
+  }
+  build_partition(w0s, ns, rem, lb, rb, bgrid, mode, unit, &bwd_part_, runit);
   bwd_part_.ring = static_cast<int>(env_u64("HB_RED_RING", 1));  // A/B knob: 0 = LDG for remote chunks too
   bwd_part_.fan = fan;
   dirty_bwd_ = false;
@@ -815,7 +847,7 @@ dev::SyncArgs Exec::make_sync_args(int kind, bool push) const {
   }
   s.timeout_cycles = static_cast<uint64_t>(cfg_.timeout_s * clock_khz_ * 1e3);
   if (trace_) s.trace = trace_ + static_cast<size_t>(kind) * dev::kTraceMaxCtas * dev::kTraceWords;
-  s.pdl = shared_device_ ? 0 : 1;
+  s.pdl = cfg_.pdl && !shared_device_ ? 1 : 0;
   return s;
 }
 

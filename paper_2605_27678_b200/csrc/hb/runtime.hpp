@@ -43,6 +43,8 @@ struct ExecConfig {
   int text_embedding = 0;           // splice: TEXT holds int32 token ids, rows gathered from an embedding table
   int max_ctas = 0;                 // cap on every boundary kernel's grid (0: fill the GPU); leaves SMs to
                                     // concurrent work (PP P2P, compute) and lets several execs share one GPU
+  int pdl = 1;                      // launch with programmatic dependent launch (off: execs sharing a device,
+                                    // the host runtime whose NCCL kernels need SMs next to boundary kernels)
 };
 
 class Exec {
@@ -194,13 +196,14 @@ class Exec {
     uint2* chunks = nullptr;
     uint32_t rtotal_chunks = 0;
     uint2* rchunks = nullptr;
+    uint64_t rchunk = 0;
     int remote_ctas = 0;
     uint32_t lstatic = 0, rstatic = 0;
     int ring = 1;
     int prefetch_other = 1;
     int fan = 0;
     dev::Partition dev() const {
-      return {first_seg, per_cta, mode, total_chunks, chunk, chunks, rtotal_chunks, rchunks, remote_ctas,
+      return {first_seg, per_cta, mode, total_chunks, chunk, chunks, rtotal_chunks, rchunks, rchunk, remote_ctas,
               lstatic, rstatic, ring, prefetch_other, fan};
     }
   };
@@ -213,7 +216,7 @@ class Exec {
   // remote[s]: segment s reads (pull) or writes (push) a peer's buffer; cost_local/remote in bytes
   void build_partition(const std::vector<uint64_t>& w0, const std::vector<uint64_t>& n,
                        const std::vector<char>& remote, double local_bytes, double remote_bytes, int grid,
-                       int mode, uint64_t unit, DevPartition* out);
+                       int mode, uint64_t unit, DevPartition* out, uint64_t runit = 0);
   bool dirty_fwd_ = true, dirty_bwd_ = true;
   bool graphs_invalidated_ = false;
   bool shared_device_ = false;  // a peer exec of the group runs on this device (no PDL)

@@ -97,6 +97,9 @@ HostRuntime::HostRuntime(std::vector<grid::ModuleLayout> modules, std::vector<st
   }
   graph_ = sched::build_stage_graph(modules_, module_edges_);
   table_ = sched::generate_1f1b_dispatch(graph_, cfg_.nmb);
+  // the table the runtime executes must pass the checker
+  if (const auto bad = sched::validate_dispatch(graph_, table_.cells, cfg_.nmb); !bad.empty())
+    raise(ErrorCode::InfeasibleSchedule, "dispatch table fails validate_dispatch: " + bad.front());
   for (size_t m = 0; m < modules_.size(); ++m)
     if (modules_[m].contains(rank_)) {
       module_ = static_cast<int>(m);
@@ -142,6 +145,8 @@ HostRuntime::HostRuntime(std::vector<grid::ModuleLayout> modules, std::vector<st
     ec.mb_slots = cfg_.nmb;
     ec.max_ctas = cfg_.max_ctas;
     ec.timeout_s = cfg_.timeout_s;
+    // no early-scheduled boundary CTAs holding SMs the PP stream's NCCL kernels need
+    ec.pdl = 0;
     auto x = std::make_unique<Exec>(*plans_.back(), nullptr, world_, rank_, ident, ec);
     unsigned char h[64] = {0};
     x->ipc_handle(h);

@@ -189,7 +189,8 @@ __device__ __forceinline__ void run_shares(const S* __restrict__ segs, int nseg,
       if (c != kNoChunk && (!cur_remote || cs.ok)) {
         const uint2 t = (cur_remote ? part.rchunks : part.chunks)[c];
         const S sg = segs[t.x];
-        const uint64_t a = static_cast<uint64_t>(t.y) * part.chunk, e = a + part.chunk, n = len(sg);
+        const uint64_t cu = cur_remote ? part.rchunk : part.chunk;
+        const uint64_t a = static_cast<uint64_t>(t.y) * cu, e = a + cu, n = len(sg);
         body(sg, a, e < n ? e : n, cur_remote != 0);
         if (threadIdx.x == 0 && sync.trace) {
           ++nch;
@@ -1141,6 +1142,8 @@ static int occ_t(int threads) {
     case kFP32 * 4 + kFP32: MACRO(float, float); break;                 \
     default: break;                                                   \
   }
+
+uint64_t red_ring_elems(int in_dtype) { return kRedRingBytes / dtype_size(in_dtype); }
 
 int reduce_blocks_per_sm(int threads, int in_dtype, int out_dtype) {
   int n = 1;

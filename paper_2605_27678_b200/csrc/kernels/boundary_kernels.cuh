@@ -41,7 +41,11 @@ struct CopySeg {
   uint32_t peers;      // GPUs this run reads (pull) or writes (push) besides this one
   uint32_t pad_;
 };
-constexpr uint32_t kErrTimeout = 1, kErrBadId = 2;
+// kErrOutOfTurn: a peer's "started" count ran 2+ ops ahead of this launch's
+// epoch, which the end-of-launch contract makes impossible unless the GPUs'
+// op sequences diverged (the device analogue of simnet's out-of-turn check,
+// R:core/src/simnet.cpp:202-207).
+constexpr uint32_t kErrTimeout = 1, kErrBadId = 2, kErrOutOfTurn = 3;
 
 // dst[i] = beta*dst[i] + sum_t term_t[i], fp32 accumulation, terms summed in
 // order starting from +0.0f; term pointers live in a side array. A segment
@@ -80,6 +84,7 @@ struct Partition {
   const uint2* chunks;       // [total_chunks] (segment, chunk within segment), in hand-out order
   uint32_t rtotal_chunks;    // dynamic / TMA: chunks that read (pull) or write (push) a peer
   const uint2* rchunks;      // [rtotal_chunks]
+  uint64_t rchunk;           // dynamic: remote chunk size (copy / TMA: = chunk)
   int remote_ctas;           // CTAs that start on the remote queue
   // Static first chunks: CTA b < remote_ctas starts on remote chunk b, CTA
   // b >= remote_ctas on local chunk b - remote_ctas (no claim round trip);
@@ -166,5 +171,6 @@ int copy_blocks_per_sm(int threads);
 int tma_blocks_per_sm(uint64_t chunk);
 uint64_t tma_chunk_bytes(int kib);  // 32 (default), 16 or 8 KiB stages
 int reduce_blocks_per_sm(int threads, int in_dtype, int out_dtype);
+uint64_t red_ring_elems(int in_dtype);  // elements of the reduce kernel's remote TMA ring
 
 }  // namespace hb::dev

@@ -66,15 +66,23 @@ struct CtaSync {
   int ok;         // no timeout
 };
 
-// Bounded spin until *flag >= e; false on timeout (error word set).
+// Bounded spin until *flag >= e; false on timeout (error word set). A peer
+// may be at most one op ahead (it can finish op e only after every peer
+// started e, so it cannot start e+2 before we start e+1): a count of e+2 or
+// more is a protocol violation and is reported, not waited past.
 __device__ __forceinline__ bool spin_until(const SyncArgs& s, const uint32_t* flag, uint32_t e) {
   const long long t0 = clock64();
-  while (static_cast<int32_t>(ld_acquire_sys(flag) - e) < 0) {
+  uint32_t v;
+  while (static_cast<int32_t>((v = ld_acquire_sys(flag)) - e) < 0) {
     __nanosleep(64);
     if (static_cast<uint64_t>(clock64() - t0) > s.timeout_cycles) {
       atomicExch(s.err, kErrTimeout);
       return false;
     }
+  }
+  if (static_cast<int32_t>(v - e) > 1) {
+    atomicExch(s.err, kErrOutOfTurn);
+    return false;
   }
   return true;
 }

@@ -117,3 +117,31 @@ def test_caller_bound_buffers_across_execs(name, pad):
                 assert not bool(torch.isnan(v.float()).any()), f"rank {r} slot {slot}: row not written"
     finally:
         g.close()
+
+
+def test_out_of_turn_peer_detected():
+    """Race/protocol check (the device analogue of simnet's out-of-turn check,
+    R:core/src/simnet.cpp:202-207): a peer's "started" count two ops ahead of
+    this launch's epoch cannot happen under the end-of-launch contract, so the
+    kernel reports it (GroupMismatch) instead of reading the peer's buffers."""
+    from paper_2605_27678_b200.bridge import _CAI
+
+    cfg, g = _group("c2", 2, [0, 0])
+    try:
+        ok, _ = group_parity(cfg, LocalGroupDriver(g), steps=1)
+        assert ok and g.status() == 0
+        rt0 = g.rts[0]
+        # region base of exec 0: its first buffer sits 4 KiB after the signal pad
+        ptrs = [rt0.buffer(r, s).data_ptr() for r in range(g.plan.world) if g.rank_to_gpu[r] == 0
+                for s in range(5) if rt0.buffer_numel(r, s)]
+        words = torch.as_tensor(_CAI(min(ptrs) - 4096, 4096), device="cuda:0").view(torch.int32)
+        words[1] += 2  # forward "started" word of GPU 1 in GPU 0's pad: two ops too many
+        torch.cuda.synchronize()
+        g.forward(1)
+        g.synchronize()
+        with pytest.raises(hbb.HetBridgeError) as ei:
+            rt0.status()
+        assert ei.value.code == "GroupMismatch"
+        assert g.rts[1].status() == 0
+    finally:
+        g.close()
