@@ -238,6 +238,16 @@ int hb_exec_stats(hb_exec* x, long long* fwd_segments, long long* bwd_segments,
  * kind (0 forward, 1 backward) into out[max_ctas x 8]; *n_ctas = CTAs copied
  * (0 when tracing is off), *grid = that launch's grid. Synchronises. */
 int hb_exec_trace(hb_exec* x, int kind, unsigned long long* out, int max_ctas, int* n_ctas, int* grid);
+/* Static race and bounds check (no reference counterpart; stands in for
+ * compute-sanitizer, which this pool does not allow). Downloads every buffer
+ * set's device tables and checks that each copy run, reduce term and
+ * accumulator lies inside one planned buffer of its slot, that pull mode
+ * writes only this GPU's destinations and the gradient return only its
+ * accumulators, that no two writes of a launch overlap and no read overlaps a
+ * write, that every run touching a peer is handed out behind the peer wait,
+ * and that every chunk is handed out exactly once. *checks = items checked.
+ * Returns ValidationError (23) with the first violation in hb_last_error(). */
+int hb_exec_validate(hb_exec* x, long long* checks);
 
 /* ---- projector GEMM with a boundary epilogue (the
  *      encoder projector of tinymodel.hpp:62) ----------------------------------

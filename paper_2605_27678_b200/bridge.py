@@ -456,6 +456,14 @@ class BridgeRuntime:
         keys = ["fwd_segments", "bwd_segments", "fwd_bytes", "bwd_elems", "launches"]
         return dict(zip(keys, (x.value for x in v)))
 
+    def validate(self) -> int:
+        """Static race and bounds check of this exec's device tables
+        (hb_exec_validate); raises HetBridgeError("ValidationError") on the
+        first violation, else returns the number of items checked."""
+        n = ctypes.c_longlong()
+        check(lib().hb_exec_validate(self._h, ctypes.byref(n)))
+        return n.value
+
     def trace(self, kind: int):
         """HB_TRACE=1 diagnostics: per-CTA stamps of the last launch of `kind`
         (0 fwd, 1 bwd) as a [ctas x 8] uint64 numpy array (empty when off)."""

@@ -562,6 +562,16 @@ int hb_exec_trace(hb_exec* x, int kind, unsigned long long* out, int max_ctas, i
   });
 }
 
+int hb_exec_validate(hb_exec* x, long long* checks) {
+  return guard([&] {
+    need(x, "exec");
+    uint64_t n = 0;
+    const std::string why = x->x->validate(&n);
+    if (checks) *checks = static_cast<long long>(n);
+    if (!why.empty()) hb::raise(hb::ErrorCode::ValidationError, "device tables: " + why);
+  });
+}
+
 int hb_exec_set_text_embedding(hb_exec* x, const void* table, long long vocab) {
   return guard([&] {
     need(x, "exec");

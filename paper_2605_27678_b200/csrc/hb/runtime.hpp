@@ -106,6 +106,11 @@ class Exec {
   // (dev::kTraceWords u64 each) into out; returns CTAs copied (0: tracing off).
   int read_trace(int kind, unsigned long long* out, int max_ctas, int* grid) const;
 
+  // Static race and bounds check of every buffer set's device tables as the
+  // kernels will read them (runtime_validate.cpp): "" when clean, else the
+  // first violation; *checks = items checked.
+  std::string validate(uint64_t* checks);
+
   const index::IndexMap& map() const { return map_; }
   int local_fwd_segments() const { return static_cast<int>(fwd_local_.size()); }
   int local_bwd_segments() const { return static_cast<int>(bwd_local_.size()); }

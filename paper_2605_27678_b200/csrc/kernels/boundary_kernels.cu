@@ -980,6 +980,213 @@ __global__ void __launch_bounds__(512, 2) reduce_segments_kernel(const ReduceSeg
   });
 }
 
+// Streaming gradient return (dynamic partition, the default): one continuous
+// stage ring per CTA across chunk boundaries. Thread 0 is the producer: it
+// claims chunks (the same two queues, static first chunks and claim prefetch
+// as run_shares) and turns them into a sequence of work items, one per ring
+// slot:
+//   staged : <= kRedSub elements of a remote single-term chunk, TMA-loaded from
+//            the peer into the slot's stage (the slot's mbarrier completes on
+//            the bytes);
+//   direct : a whole local (or multi-term / unaligned) chunk, reduced straight
+//            from global memory by reduce_range (the slot's mbarrier completes
+//            on a plain arrive);
+//   end    : no more work.
+// Every thread consumes the items in order; after item k the producer refills
+// its slot with item k + S. So while the CTA reduces one item, the next S-1
+// items' loads are in flight whatever chunk they belong to: the NVLink round
+// trip is paid once per CTA, not once per chunk (the per-chunk ring of
+// RedRing drained at each chunk boundary). Item metadata is written by thread
+// 0 at least one __syncthreads before it is read (S >= 2).
+enum : uint32_t { kItStaged = 0, kItDirect = 1, kItEnd = 2 };
+struct RedItem {
+  uint32_t seg, kind;
+  uint64_t a, b;  // elements [a, b) of segment seg
+};
+struct RedProducer {  // thread 0's state (shared memory keeps it out of the consumers' registers)
+  Claimer cl;
+  unsigned long long arr;
+  uint32_t seg;
+  uint64_t pa, pmid, pb;  // staged [pa, pmid), then a direct tail [pmid, pb)
+  int more, arrived, use_first;
+  uint32_t nch, nrem;
+};
+
+template <class TIn, class TOut, bool FAN>
+__global__ void __launch_bounds__(512, 2) reduce_stream_kernel(const ReduceSeg* __restrict__ segs, int nseg,
+                                                            const void* const* __restrict__ terms, Partition part,
+                                                            float beta, SyncArgs sync) {
+  constexpr int S = red_stages<TIn>();
+  static_assert(S >= 2, "items are published one __syncthreads ahead");
+  extern __shared__ __align__(128) unsigned char red_mem[];
+  __shared__ __align__(8) uint64_t full[S];
+  __shared__ RedItem item[S];
+  __shared__ CtaSync cs;
+  __shared__ RedProducer pr;
+  griddep_wait();
+  if (blockIdx.x == 0 && threadIdx.x < 32) {
+    post_peers_warp(sync, 0);
+    __syncwarp();
+  }
+  auto arrive = [&]() {
+    if (!pr.arrived) {
+      cta_arrive_finish(sync, cs, pr.arr);
+      pr.arrived = 1;
+    }
+  };
+  // thread 0: write item k into its slot (claiming chunks as needed)
+  auto produce = [&](uint32_t k) {
+    const int st = k % S;
+    RedItem& it = item[st];
+    while (true) {
+      if (pr.pa < pr.pmid) {  // next stage of the current remote chunk
+        const ReduceSeg& sg = segs[pr.seg];
+        const TIn* tp = reinterpret_cast<const TIn*>(terms[sg.term0]);
+        const uint64_t n = min(static_cast<uint64_t>(kRedSub), pr.pmid - pr.pa);
+        it = RedItem{pr.seg, kItStaged, pr.pa, pr.pa + n};
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the slot's generic reads are done
+        mbar_expect(&full[st], static_cast<uint32_t>(n * sizeof(TIn)));
+        bulk_g2s(red_mem + st * (kRedSub * sizeof(TIn)), tp + pr.pa, static_cast<uint32_t>(n * sizeof(TIn)),
+                 &full[st]);
+        pr.pa += n;
+        return;
+      }
+      if (pr.pmid < pr.pb) {  // direct remainder of the current chunk
+        it = RedItem{pr.seg, kItDirect, pr.pmid, pr.pb};
+        pr.pmid = pr.pb;
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[st])) : "memory");
+        return;
+      }
+      if (!pr.more) {
+        it.kind = kItEnd;
+        return;
+      }
+      uint32_t c;
+      int rq;
+      if (pr.use_first) {
+        pr.use_first = 0;
+        c = pr.cl.first;
+        rq = pr.cl.q;
+      } else {
+        arrive();
+        c = pr.cl.next(part, sync, cs.e, &rq);
+        if (c == kNoChunk) {
+          pr.more = 0;
+          continue;
+        }
+      }
+      if (c == kNoChunk) continue;
+      const uint2 t = (rq ? part.rchunks : part.chunks)[c];
+      const ReduceSeg& sg = segs[t.x];
+      const uint64_t cu = rq ? part.rchunk : part.chunk;
+      const uint64_t a = static_cast<uint64_t>(t.y) * cu;
+      const uint64_t b = min(a + cu, sg.nelem);
+      if (rq) {
+        arrive();
+        if (!sync_wait_lane(sync, cs)) continue;  // timed out: claimed, not executed
+        ++pr.nrem;
+      }
+      ++pr.nch;
+      pr.seg = t.x;
+      pr.pa = pr.pmid = a;
+      pr.pb = b;
+      if (rq && sg.nterms == 1 && part.ring) {
+        uint64_t al = reinterpret_cast<uint64_t>(static_cast<const TIn*>(terms[sg.term0]) + a);
+        if constexpr (FAN) {
+          for (int d = 0; d < sg.ndst; ++d) al |= reinterpret_cast<uint64_t>(static_cast<const TOut*>(terms[sg.dst0 + d]) + a);
+        } else {
+          al |= reinterpret_cast<uint64_t>(static_cast<const TOut*>(sg.dst) + a);
+        }
+        if ((al & 15) == 0) pr.pmid = a + ((b - a) & ~uint64_t(7));
+      }
+    }
+  };
+  if (threadIdx.x == 0) {
+    trace_at(sync, kTrEntry);
+    pr.arr = cta_arrive_issue(sync);
+    pr.arrived = 0;
+    pr.nch = pr.nrem = 0;
+    for (int i = 0; i < S; ++i) mbar_init(&full[i]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    pr.cl.init(part);
+    pr.more = !pr.cl.done();
+    pr.use_first = pr.more;
+    pr.pa = pr.pmid = pr.pb = 0;
+    if (pr.more) pr.cl.issue(part, sync, pr.cl.first);  // the claim after the static chunk, in flight
+    for (uint32_t k = 0; k < static_cast<uint32_t>(S); ++k) produce(k);
+  }
+  __syncthreads();
+  for (uint32_t k = 0;; ++k) {
+    const int st = k % S;
+    const RedItem it = item[st];
+    if (it.kind == kItEnd) break;
+    const ReduceSeg sg = segs[it.seg];
+    const TIn* const* tp = reinterpret_cast<const TIn* const*>(terms + sg.term0);
+    if (it.kind == kItStaged) {
+      const TIn* T = reinterpret_cast<const TIn*>(red_mem + st * (kRedSub * sizeof(TIn)));
+      const uint32_t len = static_cast<uint32_t>(it.b - it.a);
+      if constexpr (FAN) {
+        TOut* const* dl = reinterpret_cast<TOut* const*>(const_cast<void* const*>(terms + sg.dst0));
+        mbar_wait(&full[st], (k / S) & 1u);
+        for (uint32_t j = threadIdx.x * 8; j < len; j += blockDim.x * 8) {
+          float acc[8];
+          load8_coherent(T + j, acc);
+          for (int d = 0; d < sg.ndst; ++d) {
+            TOut* p = dl[d] + it.a + j;
+            float o[8];
+            if (beta != 0.0f) {
+              load8_coherent(p, o);
+#pragma unroll
+              for (int q = 0; q < 8; ++q) o[q] = fmaf(beta, o[q], 0.0f + acc[q]);
+            } else {
+#pragma unroll
+              for (int q = 0; q < 8; ++q) o[q] = 0.0f + acc[q];
+            }
+            store8(p, o);
+          }
+        }
+      } else {
+        TOut* d = static_cast<TOut*>(sg.dst) + it.a;
+        // the first group's accumulator load goes out before the stage wait
+        const uint32_t j0 = threadIdx.x * 8;
+        float o[8];
+        if (beta != 0.0f && j0 < len) load8_coherent(d + j0, o);
+        mbar_wait(&full[st], (k / S) & 1u);
+        for (uint32_t j = j0; j < len; j += blockDim.x * 8) {
+          if (j != j0 && beta != 0.0f) load8_coherent(d + j, o);
+          float acc[8];
+          load8_coherent(T + j, acc);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) acc[q] = beta != 0.0f ? fmaf(beta, o[q], 0.0f + acc[q]) : 0.0f + acc[q];
+          store8(d + j, acc);
+        }
+      }
+    } else {
+      mbar_wait(&full[st], (k / S) & 1u);  // (a plain arrive: keeps the slot's phases in step)
+      if constexpr (FAN) {
+        TOut* const* dl = reinterpret_cast<TOut* const*>(const_cast<void* const*>(terms + sg.dst0));
+        reduce_range_fan<TIn, TOut>(dl, sg.ndst, tp, sg.nterms, it.a, it.b, beta);
+      } else {
+        reduce_range<TIn, TOut>(static_cast<TOut*>(sg.dst), tp, sg.nterms, it.a, it.b, beta);
+      }
+    }
+    __syncthreads();  // slot st fully read
+    if (threadIdx.x == 0) {
+      if (k == 0) trace_at(sync, kTrFirst);
+      produce(k + S);
+    }
+  }
+  griddep_launch_dependents();  // this CTA's work is done: the next op may take its slot
+  if (threadIdx.x == 0) {
+    arrive();
+    trace_at(sync, kTrDone);
+    launch_end_lane(sync, cs);
+    trace_at(sync, kTrExit);
+    trace_val(sync, kTrChunks, pr.nch);
+    trace_val(sync, kTrRemote, pr.nrem);
+  }
+}
+
 }  // namespace
 
 int device_sm_count() {
@@ -1075,6 +1282,28 @@ static int red_ring_smem() {
   return static_cast<int>(kRedRingBytes);
 }
 
+// HB_RED_STREAM=0 selects the per-chunk ring kernel (reduce_segments_kernel)
+// for the dynamic partition instead of the streaming one (A/B knob).
+static bool red_stream() {
+  static const bool on = [] {
+    const char* v = std::getenv("HB_RED_STREAM");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
+template <class TIn, class TOut, bool FAN>
+static int red_stream_smem() {
+  static PerDeviceOnce once;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  once(dev, [] {
+    cudaFuncSetAttribute(reduce_stream_kernel<TIn, TOut, FAN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kRedRingBytes);
+  });
+  return static_cast<int>(kRedRingBytes);
+}
+
 // HB_RED_CARVEOUT (A/B knob, percent of the unified L1/smem given to shared
 // memory for the reduce kernels; 0 = driver default). Setting it to the TMA
 // copy kernel's 100 avoids an L1/smem reconfiguration between a forward and a
@@ -1105,8 +1334,12 @@ static void launch_reduce_f(const ReduceSeg* segs, int nseg, const void* const* 
   if (part.mode == kPartInterleaved)
     launch_pdl(reduce_segments_kernel<TIn, TOut, kPartInterleaved, FAN>, grid, block, 0, st, segs, nseg, terms, part,
                beta, sync);
-  else if (part.mode == kPartDynamic)
+  else if (part.mode == kPartDynamic && red_stream())
     // the ring's shared memory only when there are remote chunks to stage
+    launch_pdl(reduce_stream_kernel<TIn, TOut, FAN>, grid, block,
+               part.ring && part.rtotal_chunks ? red_stream_smem<TIn, TOut, FAN>() : 0, st, segs, nseg, terms, part,
+               beta, sync);
+  else if (part.mode == kPartDynamic)
     launch_pdl(reduce_segments_kernel<TIn, TOut, kPartDynamic, FAN>, grid, block,
                part.ring && part.rtotal_chunks ? red_ring_smem<TIn, TOut, FAN>() : 0, st, segs, nseg, terms, part,
                beta, sync);

@@ -135,7 +135,11 @@ def test_out_of_turn_peer_detected():
         ptrs = [rt0.buffer(r, s).data_ptr() for r in range(g.plan.world) if g.rank_to_gpu[r] == 0
                 for s in range(5) if rt0.buffer_numel(r, s)]
         words = torch.as_tensor(_CAI(min(ptrs) - 4096, 4096), device="cuda:0").view(torch.int32)
-        words[1] += 2  # forward "started" word of GPU 1 in GPU 0's pad: two ops too many
+        # forward "started" word of GPU 1 in GPU 0's pad, pushed past any legal value:
+        # GPU 1's own post of the next op may land before or after GPU 0 reads the
+        # word, so +3 keeps it >= e+2 (two ops ahead) either way (+2 could read e+1,
+        # which is legal: a peer may already have started the following op)
+        words[1] += 3
         torch.cuda.synchronize()
         g.forward(1)
         g.synchronize()

@@ -43,3 +43,20 @@ def test_reference_side_binding_matches_reference():
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert " 0 mismatches" in r.stdout
+
+
+@pytest.mark.gpu
+def test_reference_side_device_bridge_matches_oracle():
+    """The same binding's DeviceBridge (hetsim::grid::BoundaryEdge -> hb_exec_* on
+    cuda:0) executed for C1, C2, C3, C3', C5, App-C and a cp
+    reduce: forward placement and the backward return equal the oracle's
+    bridge_forward / bridge_backward bit for bit (oracle/refcheck/shim/device_check.cpp)."""
+    exe = os.path.join(BIN, "shim_device_check")
+    if not os.path.exists(exe):
+        if os.path.isdir("/root/reference/proj"):
+            subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "refcheck"], check=True)
+        else:
+            pytest.skip("device check not built and /root/reference absent")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert " 0 mismatches" in r.stdout
