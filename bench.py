@@ -920,6 +920,10 @@ def hkey(*a):
 
 
 def run_host_runtime(name, rank, world, dev, steps=5):
+    """One topology through the host-owned runtime. Every rank issues the same
+    collectives whatever happens on it: a failure (a device flag-wait timeout
+    raised by step(), a construction error) is recorded and reduced at the end,
+    so a diagnostic leg can never leave its peers waiting in a barrier."""
     import torch
     import torch.distributed as dist
 
@@ -930,84 +934,118 @@ def run_host_runtime(name, rank, world, dev, steps=5):
     mods, edges, B, W, ppb = rt_topology(name)
     if max(m.rank_end() for m in mods) > world:
         return None
-    rt = R.HostRuntime(mods, edges, B, W, nmb=4, pp_bytes=ppb, skip=R.SKIP_COMPUTE)
-    ok = True
-    views = [rt.edge_runtime(k) for k in range(len(edges))]
-    # fill boundary shards (every buffer set = microbatch slot) and stage buffers
-    for k, v in enumerate(views):
+    errors = []
+
+    def attempt(what, fn, default=None):
+        try:
+            return fn()
+        except Exception as exc:  # recorded, reduced over ranks below
+            errors.append(f"{what}: {type(exc).__name__}: {exc}"[:300])
+            return default
+
+    rt = attempt("create", lambda: R.HostRuntime(mods, edges, B, W, nmb=4, pp_bytes=ppb, skip=R.SKIP_COMPUTE,
+                                                  timeout_s=5.0))
+    ok = rt is not None
+    ms_first = 0.0
+    rows = rt.rows if rt is not None else None
+    if rt is not None:
+        views = [rt.edge_runtime(k) for k in range(len(edges))]
+        # fill boundary shards (every buffer set = microbatch slot) and stage buffers
+        for k, v in enumerate(views):
+            for mb in range(rt.nmb):
+                for slot in (hbb.SLOT_SRC_ACT, hbb.SLOT_DST_GRAD):
+                    if v.buffer_numel(rank, slot) and v.rank_to_gpu[rank] == rank:
+                        try:
+                            b = v.buffer(rank, slot, mb)
+                        except hbb.HetBridgeError:
+                            b = None
+                        if b is not None:
+                            b.copy_(fill_values(b.numel(), hkey(k, slot, mb, rank), b.dtype, dev))
         for mb in range(rt.nmb):
-            for slot in (hbb.SLOT_SRC_ACT, hbb.SLOT_DST_GRAD):
-                if v.buffer_numel(rank, slot) and v.rank_to_gpu[rank] == rank:
-                    try:
-                        b = v.buffer(rank, slot, mb)
-                    except hbb.HetBridgeError:
-                        b = None
-                    if b is not None:
-                        b.copy_(fill_values(b.numel(), hkey(k, slot, mb, rank), b.dtype, dev))
-    for mb in range(rt.nmb):
-        for which in (R.ACT_OUT, R.GRAD_OUT):
-            t = rt.stage_buffer(which, mb)
-            if t is not None:
-                t.view(torch.int16).copy_(fill_values(t.numel() // 2, hkey(9, which, mb, rank), torch.bfloat16,
-                                                            dev).view(torch.int16))
+            for which in (R.ACT_OUT, R.GRAD_OUT):
+                t = rt.stage_buffer(which, mb)
+                if t is not None:
+                    t.view(torch.int16).copy_(fill_values(t.numel() // 2, hkey(9, which, mb, rank), torch.bfloat16,
+                                                                dev).view(torch.int16))
     torch.cuda.synchronize()
     dist.barrier()
-    rt.step()
-    ms_first = rt.last_step_ms()
+    if rt is not None:
+        def first():
+            rt.step()
+            return rt.last_step_ms()
+        ms_first = attempt("step", first, 0.0)
     torch.cuda.synchronize()
     dist.barrier()
-    # NC checks
-    for k, v in enumerate(views):
-        fwd_map, bwd_map = hbb.index_forward(v.plan), hbb.index_backward(v.plan, balanced=True)
-        for mb in range(rt.nmb):
-            def regen(r, slot, _k=k, _mb=mb, _v=v):
-                n = _v.buffer_numel(r, slot)
-                dt = _v.act_dtype if slot == hbb.SLOT_SRC_ACT else _v.grad_in_dtype
-                return fill_values(n, hkey(_k, slot, _mb, r), dt, dev)
-            if v.buffer_numel(rank, hbb.SLOT_DST_ACT):
-                out = v.buffer(rank, hbb.SLOT_DST_ACT, mb)
-                exp, cov = P.expected_forward(fwd_map, rank, out.numel(), regen)
-                ok &= cov == out.numel() and bool(torch.equal(out.view(torch.int16), exp.view(torch.int16)))
-            if v.buffer_numel(rank, hbb.SLOT_SRC_GRAD):
-                got = v.buffer(rank, hbb.SLOT_SRC_GRAD, mb)
-                exp = P.expected_backward(bwd_map, rank, torch.zeros_like(got), 0.0, regen)
-                ok &= bool(torch.equal(got, exp))
-    # P2P checks: neighbours in my module's PP group
-    pp = rt.group(2)
-    if rt.module >= 0 and len(pp) > 1:
-        i = pp.index(rank)
-        for mb in range(rt.nmb):
-            if i > 0:
-                exp = fill_values(ppb // 2, hkey(9, R.ACT_OUT, mb, pp[i - 1]), torch.bfloat16, dev)
-                ok &= bool(torch.equal(rt.stage_buffer(R.ACT_IN, mb).view(torch.int16), exp.view(torch.int16)))
-            if i + 1 < len(pp):
-                exp = fill_values(ppb // 2, hkey(9, R.GRAD_OUT, mb, pp[i + 1]), torch.bfloat16, dev)
-                ok &= bool(torch.equal(rt.stage_buffer(R.GRAD_IN, mb).view(torch.int16), exp.view(torch.int16)))
-    flag = torch.tensor([0 if ok else 1], device=dev)
+    if rt is not None and not errors:
+        # NC checks
+        for k, v in enumerate(views):
+            fwd_map, bwd_map = hbb.index_forward(v.plan), hbb.index_backward(v.plan, balanced=True)
+            for mb in range(rt.nmb):
+                def regen(r, slot, _k=k, _mb=mb, _v=v):
+                    n = _v.buffer_numel(r, slot)
+                    dt = _v.act_dtype if slot == hbb.SLOT_SRC_ACT else _v.grad_in_dtype
+                    return fill_values(n, hkey(_k, slot, _mb, r), dt, dev)
+                if v.buffer_numel(rank, hbb.SLOT_DST_ACT):
+                    out = v.buffer(rank, hbb.SLOT_DST_ACT, mb)
+                    exp, cov = P.expected_forward(fwd_map, rank, out.numel(), regen)
+                    ok &= cov == out.numel() and bool(torch.equal(out.view(torch.int16), exp.view(torch.int16)))
+                if v.buffer_numel(rank, hbb.SLOT_SRC_GRAD):
+                    got = v.buffer(rank, hbb.SLOT_SRC_GRAD, mb)
+                    exp = P.expected_backward(bwd_map, rank, torch.zeros_like(got), 0.0, regen)
+                    ok &= bool(torch.equal(got, exp))
+        # P2P checks: neighbours in my module's PP group
+        pp = rt.group(2)
+        if rt.module >= 0 and len(pp) > 1:
+            i = pp.index(rank)
+            for mb in range(rt.nmb):
+                if i > 0:
+                    exp = fill_values(ppb // 2, hkey(9, R.ACT_OUT, mb, pp[i - 1]), torch.bfloat16, dev)
+                    ok &= bool(torch.equal(rt.stage_buffer(R.ACT_IN, mb).view(torch.int16), exp.view(torch.int16)))
+                if i + 1 < len(pp):
+                    exp = fill_values(ppb // 2, hkey(9, R.GRAD_OUT, mb, pp[i + 1]), torch.bfloat16, dev)
+                    ok &= bool(torch.equal(rt.stage_buffer(R.GRAD_IN, mb).view(torch.int16), exp.view(torch.int16)))
+    flag = torch.tensor([0 if ok and not errors else 1], device=dev)
     dist.all_reduce(flag)
-    rt.close()
-    # overlap: the same table with one traffic class skipped
+    if rt is not None:
+        attempt("close", rt.close)
+    # overlap: the same table with one traffic class skipped (only after a clean first step on every rank)
     times = {}
-    for label, skip in (("nc_only", R.SKIP_COMPUTE | R.SKIP_P2P), ("p2p_only", R.SKIP_COMPUTE | R.SKIP_NC),
-                        ("both", R.SKIP_COMPUTE)):
-        r2 = R.HostRuntime(mods, edges, B, W, nmb=4, pp_bytes=ppb, skip=skip)
-        r2.step()
-        r2.last_step_ms()
-        ts = []
-        for _ in range(steps):
-            dist.barrier()
-            r2.step()
-            ts.append(r2.last_step_ms())
-        t = torch.tensor([statistics.median(ts)], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        times[label] = round(t.item(), 4)
-        r2.close()
-    tb, tp, both = times["nc_only"], times["p2p_only"], times["both"]
-    overlap = (tb + tp - both) / max(1e-9, min(tb, tp))
-    return {"topology": name, "n_gpus": world, "parity": flag.item() == 0, "rows": rt.rows,
-            "first_step_ms": round(ms_first, 3), "step_ms": times, "overlap": round(overlap, 3),
-            "how": "HostRuntime.step over the 1F1B dispatch table (event-only compute); NC = boundary exec "
-                   "fwd/bwd on the boundary stream, P2P = NCCL send/recv on the PP communicator"}
+    if flag.item() == 0:
+        for label, skip in (("nc_only", R.SKIP_COMPUTE | R.SKIP_P2P), ("p2p_only", R.SKIP_COMPUTE | R.SKIP_NC),
+                            ("both", R.SKIP_COMPUTE)):
+            r2 = attempt("create", lambda: R.HostRuntime(mods, edges, B, W, nmb=4, pp_bytes=ppb, skip=skip,
+                                                          timeout_s=5.0))
+            ts = []
+            if r2 is not None:
+                def one():
+                    r2.step()
+                    return r2.last_step_ms()
+                attempt("step", one)
+            for _ in range(steps):
+                dist.barrier()
+                if r2 is not None and not errors:
+                    v = attempt("step", one)
+                    if v is not None:
+                        ts.append(v)
+            t = torch.tensor([statistics.median(ts) if ts else float("nan")], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            times[label] = round(t.item(), 4)
+            if r2 is not None:
+                attempt("close", r2.close)
+    err = torch.tensor([len(errors)], device=dev)
+    dist.all_reduce(err)
+    res = {"topology": name, "n_gpus": world, "parity": flag.item() == 0 and err.item() == 0, "rows": rows,
+           "first_step_ms": round(ms_first or 0.0, 3), "step_ms": times,
+           "how": "HostRuntime.step over the 1F1B dispatch table (event-only compute); NC = boundary exec "
+                  "fwd/bwd on the boundary stream, P2P = NCCL send/recv on the PP communicator"}
+    if times and all(math.isfinite(v) for v in times.values()):
+        tb, tp, both = times["nc_only"], times["p2p_only"], times["both"]
+        res["overlap"] = round((tb + tp - both) / max(1e-9, min(tb, tp)), 3)
+    if err.item():
+        res["errors_on_ranks"] = int(err.item())
+        if errors:
+            res["error_here"] = errors[0]
+    return res
 
 
 def copy_kernel_name(args):

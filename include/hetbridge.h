@@ -312,6 +312,11 @@ int hb_dispatch_generate(const hb_stage_graph* g, int nmb, hb_cell* cells, size_
 int hb_dispatch_validate(const hb_stage_graph* g, const hb_cell* cells, size_t n, int nmb, char* report, size_t cap,
                          size_t* len, int* n_violations);
 int hb_dispatch_render(const hb_stage_graph* g, int nmb, char* buf, size_t cap, size_t* len);
+/* The NC cells of `node` in the order the host runtime issues them on its
+ * boundary stream: by row, then module edge, then forward before backward —
+ * one global order for every GPU, so each op's in-kernel rendezvous is met
+ * (no reference counterpart; the execution rule of hb_runtime_step). */
+int hb_dispatch_nc_order(const hb_stage_graph* g, int nmb, int node, hb_cell* cells, size_t cap, size_t* n);
 
 /* ---- host-owned per-module runtime (per-module rank groups,
  *      communicators and streams; §8(f) row 2: executes the graph-aware

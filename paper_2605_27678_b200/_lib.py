@@ -37,7 +37,7 @@ EXPORTS = [
     "hb_exec_forward_projected", "hb_exec_set_text_embedding",
     "hb_exec_graph_launch", "hb_exec_trace", "hb_exec_validate",
     "hb_stage_graph_create", "hb_stage_graph_destroy", "hb_stage_graph_nodes", "hb_stage_graph_edges",
-    "hb_dispatch_generate", "hb_dispatch_validate", "hb_dispatch_render",
+    "hb_dispatch_generate", "hb_dispatch_validate", "hb_dispatch_render", "hb_dispatch_nc_order",
     "hb_nccl_unique_id", "hb_runtime_config_default", "hb_runtime_create", "hb_runtime_destroy", "hb_runtime_info",
     "hb_runtime_group", "hb_runtime_edge_exec", "hb_runtime_stage_buffer", "hb_runtime_stream", "hb_runtime_step",
     "hb_runtime_last_step_ms",
@@ -155,6 +155,7 @@ def _declare(L):
         "hb_dispatch_generate": (I, [V, I, P(Cell), Sz, P(Sz), P(I)]),
         "hb_dispatch_validate": (I, [V, P(Cell), Sz, I, C, Sz, P(Sz), P(I)]),
         "hb_dispatch_render": (I, [V, I, C, Sz, P(Sz)]),
+        "hb_dispatch_nc_order": (I, [V, I, I, P(Cell), Sz, P(Sz)]),
         "hb_config_parse": (I, [C, P(V)]),
         "hb_config_destroy": (None, [V]),
         "hb_config_num_modules": (I, [V, P(I)]),

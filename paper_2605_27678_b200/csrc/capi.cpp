@@ -719,6 +719,16 @@ int hb_dispatch_validate(const hb_stage_graph* g, const hb_cell* cells, size_t n
   });
 }
 
+int hb_dispatch_nc_order(const hb_stage_graph* g, int nmb, int node, hb_cell* cells, size_t cap, size_t* n) {
+  return guard([&] {
+    need(g, "graph");
+    need(n, "n");
+    const auto v = hb::sched::nc_issue_order(g->g, hb::sched::generate_1f1b_dispatch(g->g, nmb), node);
+    *n = v.size();
+    for (size_t i = 0; cells && i < v.size() && i < cap; ++i) cells[i] = to_c(v[i]);
+  });
+}
+
 int hb_dispatch_render(const hb_stage_graph* g, int nmb, char* buf, size_t cap, size_t* len) {
   return guard([&] {
     need(g, "graph");

@@ -271,6 +271,9 @@ void HostRuntime::step(ComputeFn fn, void* user) {
         if (c->op == sched::Op::RecvFwd || c->op == sched::Op::RecvBwd)
           ck(cudaEventRecord(ev(c->op == sched::Op::RecvFwd ? 0 : 2, c->mb), sp), "record recv");
     }
+    // one global order of boundary ops across the GPUs (sched::nc_issue_order)
+    std::stable_sort(nc.begin(), nc.end(),
+                     [&](const sched::Cell* a, const sched::Cell* b) { return sched::nc_before(graph_, *a, *b); });
     for (const auto* c : nc) {
       Exec* x = execs_.at(graph_.edges[c->edge].boundary).get();
       const int64_t id = base + c->mb;

@@ -278,6 +278,22 @@ std::vector<std::string> validate_dispatch(const StageGraph& g, const std::vecto
   return v;
 }
 
+bool nc_before(const StageGraph& g, const Cell& a, const Cell& b) {
+  auto key = [&](const Cell& c) {
+    const bool bwd = c.op == Op::SendBwd || c.op == Op::RecvBwd;
+    return std::make_tuple(c.row, g.edges.at(c.edge).boundary, bwd ? 1 : 0, c.mb);
+  };
+  return key(a) < key(b);
+}
+
+std::vector<Cell> nc_issue_order(const StageGraph& g, const DispatchTable& t, int node) {
+  std::vector<Cell> v;
+  for (const auto& c : t.cells)
+    if (c.node == node && c.op != Op::Compute && c.kind == EdgeKind::NC) v.push_back(c);
+  std::stable_sort(v.begin(), v.end(), [&](const Cell& a, const Cell& b) { return nc_before(g, a, b); });
+  return v;
+}
+
 std::string render(const StageGraph& g, const DispatchTable& t) {
   const int Nn = static_cast<int>(g.nodes.size());
   std::vector<std::vector<std::string>> grid(t.rows, std::vector<std::string>(Nn));

@@ -89,6 +89,18 @@ DispatchTable generate_1f1b_dispatch(const StageGraph& g, int nmb);
 // kinds matching the graph. Returns the violations (never throws).
 std::vector<std::string> validate_dispatch(const StageGraph& g, const std::vector<Cell>& cells, int nmb);
 
+// nc_issue_order: the NC cells of `node` in the order its boundary stream
+// executes them — by row, then by module edge (the BridgePlan identity), then
+// forward before backward. A boundary op is a rendezvous of its endpoints'
+// kernels (the in-kernel "started" barrier), and both endpoints see it in the
+// same row, so with this order every GPU's boundary stream is a linear
+// extension of one global order (row, edge, direction) and every rendezvous
+// is met. The table's own within-row order is not enough: at a join the
+// source may list F2 before B1 while the destination lists B1 before F2, and
+// two serial streams waiting on each other deadlock.
+std::vector<Cell> nc_issue_order(const StageGraph& g, const DispatchTable& t, int node);
+bool nc_before(const StageGraph& g, const Cell& a, const Cell& b);
+
 // Text grid (rows = schedule calls, columns = nodes): compute "F3"/"B3",
 // communication "sf3:p2p", "rf3:NC", "sb3:NC", "rb3:p2p".
 std::string render(const StageGraph& g, const DispatchTable& t);

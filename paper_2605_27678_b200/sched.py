@@ -146,6 +146,16 @@ def validate_dispatch(graph: StageGraph, table: DispatchTable | list, nmb: int |
     return [x for x in buf.value.decode().split("\n") if x]
 
 
+def nc_issue_order(graph: StageGraph, nmb: int, node: int) -> list:
+    """The NC cells of ``node`` in the order the host runtime issues them on its
+    boundary stream (row, module edge, forward before backward)."""
+    n = ctypes.c_size_t()
+    check(lib().hb_dispatch_nc_order(graph._h, nmb, node, None, 0, ctypes.byref(n)))
+    arr = (_lib.Cell * max(1, n.value))()
+    check(lib().hb_dispatch_nc_order(graph._h, nmb, node, arr, n.value, ctypes.byref(n)))
+    return [Cell(c.row, c.node, Op(c.op), c.edge, EdgeKind(c.kind), c.mb, bool(c.bwd)) for c in arr[: n.value]]
+
+
 def render(graph: StageGraph, nmb: int) -> str:
     ln = ctypes.c_size_t()
     check(lib().hb_dispatch_render(graph._h, nmb, None, 0, ctypes.byref(ln)))

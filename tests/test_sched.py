@@ -188,3 +188,65 @@ def test_host_runtime_rejects_colocated_modules_before_nccl():
     mods2 = (_lib.Layout * 2)(_lib.Layout(b"vit", 1, 1, 1, 1, 0), _lib.Layout(b"llm", 1, 1, 1, 1, 1))
     st = L.hb_runtime_create(mods2, 2, src, dst, 1, 4, 8, 2, 0, b"\0" * 128, ctypes.byref(cfg), ctypes.byref(out))
     assert st == 19  # InfeasibleSchedule
+
+
+def _rendezvous(graph, seqs):
+    """Serial boundary streams, one per node: an NC op (module edge, direction,
+    mb) runs when it is at the head of BOTH endpoints' streams (the in-kernel
+    "started" barrier). Returns the ops left when no stream can advance."""
+    ep = {}
+    for e in graph.edges:
+        if e.kind == S.EdgeKind.NC:
+            ep[e.boundary] = (e.src, e.dst)
+
+    def key(c):
+        return (graph.edges[c.edge].boundary, c.op in (S.Op.SendBwd, S.Op.RecvBwd), c.mb)
+
+    q = {n: [key(c) for c in v] for n, v in seqs.items()}
+    moved = True
+    while moved:
+        moved = False
+        for n, v in q.items():
+            if not v:
+                continue
+            a, b = ep[v[0][0]]
+            other = b if n == a else a
+            if q[other] and q[other][0] == v[0]:
+                q[n].pop(0)
+                q[other].pop(0)
+                moved = True
+    return {n: v for n, v in q.items() if v}
+
+
+def _topologies():
+    mods, edges = S.fig4a_modules()
+    yield "fig4a", mods, edges
+    yield "join4", [ModuleLayout("E1", pp=2, rank_offset=0), ModuleLayout("E2", rank_offset=2),
+                    ModuleLayout("LLM", rank_offset=3)], [(0, 2), (1, 2)]
+    yield "c5", [ModuleLayout("vit", dp=2), ModuleLayout("llm", tp=2, pp=3, rank_offset=2)], [(0, 1)]
+    yield "three-encoders", [ModuleLayout("A", pp=3), ModuleLayout("B", pp=2, rank_offset=3),
+                             ModuleLayout("C", rank_offset=5), ModuleLayout("LLM", pp=2, rank_offset=6)], \
+        [(0, 3), (1, 3), (2, 3)]
+
+
+@pytest.mark.parametrize("nmb", [1, 2, 4, 8])
+def test_nc_issue_order_meets_every_rendezvous(nmb):
+    """The host runtime's boundary-stream order (hb_dispatch_nc_order) drains on
+    every topology: each NC op is issued by its two endpoints in the same
+    relative order (row, module edge, forward before backward)."""
+    for name, mods, edges in _topologies():
+        g = S.build_stage_graph(mods, edges)
+        seqs = {n: S.nc_issue_order(g, nmb, n) for n in range(len(g.nodes))}
+        assert all(a.row <= b.row for v in seqs.values() for a, b in zip(v, v[1:]))
+        assert _rendezvous(g, seqs) == {}, name
+
+
+def test_table_order_would_deadlock_at_a_join():
+    """Regression (round-2 N=4 hang): issuing a row's NC cells in the table's own
+    order makes E1P1 run F2 before B1 while LLMP0 runs B1 before F2 at the join."""
+    _, mods, edges = next(t for t in _topologies() if t[0] == "join4")
+    g = S.build_stage_graph(mods, edges)
+    t = S.generate_1f1b_dispatch(g, 4)
+    raw = {n: [c for c in t.cells if c.node == n and c.op != S.Op.Compute and c.kind == S.EdgeKind.NC]
+           for n in range(len(g.nodes))}
+    assert _rendezvous(g, raw) != {}
