@@ -65,6 +65,10 @@ def parse():
     ap.add_argument("--no-runtime", action="store_true",
                     help="skip the host-runtime leg (a24 + f2: 1F1B dispatch table with NC || PP P2P, N = 4, 6, 8)")
     ap.add_argument("--ref-procs", type=int, default=0, help="reference arm: worker processes (0 = auto)")
+    ap.add_argument("--diag-budget", type=float, default=420.0,
+                    help="seconds the diagnostic legs (e2e, NCCL comparison, overlap, config matrix, host runtime, "
+                         "CPU baseline) may take after the headline; past it the line is printed with what was "
+                         "measured and every rank exits")
     return ap.parse_args()
 
 
@@ -792,18 +796,80 @@ def main():
     roofline["step_tstar_ms_nominal"] = round((tstar_nominal(tm["fwd_hbm"], tm["fwd_nvl"]) +
                                                tstar_nominal(tm["bwd_hbm"], tm["bwd_nvl"])) * 1e3, 4)
 
+    # The line as it stands after the headline; every later leg fills its key.
+    # Diagnostic legs run under a deadline: if one of them stalls (a peer that
+    # never arrives, an NCCL call that never completes), the watchdog prints the
+    # line with what was measured and ends every rank, so the headline is never lost.
+    line = {
+        "metric": METRIC,
+        "value": round(value, 2), "unit": "GB/s", "n_gpus": N, "steps": K, "warmup": args.warmup,
+        "ms_per_step": round(ms_step, 5), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": cfg.act, "data": "synthetic",
+        "config": workload_config(cfg, N, slots, args.scale),
+        "value_semantics": "whole job: boundary payload bytes of all N GPUs per second (bench contract); "
+                           "per GPU = per_gpu_gbs",
+        "per_gpu_gbs": round(value / N, 2), "tokens_per_s": round(tokens_s, 1),
+        "method": {"launch": (f"one CUDA graph per cycle of {slots} steps (fwd+bwd on each buffer set in "
+                              f"turn; K % {slots} steps as one graph each)") if cycle else
+                             ("one CUDA graph (fwd+bwd) per step" if use_graph else "per-op C-ABI launches"),
+                   "ms_per_step_one_graph_per_step": ms_graph_per_step,
+                   "timing": "CUDA events on the launching stream, barrier + synchronize on both sides, "
+                             "max over ranks"},
+        "payload_bytes_per_step": {"fwd": fwd_b, "bwd": bwd_b},
+        "parity": parity,
+        "roofline": roofline, "cpu_baseline": None, "e2e": None, "gpu_launches": launches,
+        "clocks": clocks,
+        "nccl_comparison": None,
+        "overlap_with_pp_p2p": None,
+        "config_matrix": None,
+        "host_runtime": None,
+    }
+    pending = ["e2e", "nccl_comparison", "overlap_with_pp_p2p", "config_matrix", "host_runtime", "cpu_baseline"]
+    printed = threading.Lock()
+
+    def emit(extra=None):
+        if printed.acquire(blocking=False):
+            if rank == 0:
+                out = dict(line)
+                if extra:
+                    out.update(extra)
+                print(json.dumps(out), flush=True)
+            return True
+        return False
+
+    def on_deadline():
+        emit({"diagnostics_incomplete": list(pending),
+              "diagnostics_deadline_s": args.diag_budget})
+        sys.stdout.flush()
+        os._exit(0)
+
+    watchdog = threading.Timer(args.diag_budget, on_deadline)
+    watchdog.daemon = True
+    watchdog.start()
+
+    def done(key, val):
+        line[key] = val
+        if key in pending:
+            pending.remove(key)
+
     # ---- end to end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(args, cfg, rt, local, stream, N, dev, barrier, fwd_b + bwd_b, slots)
+    done("e2e", e2e)
 
     nccl = None
     if N > 1 and N == plan.world and not args.no_nccl:
-        nccl = run_nccl_comparison(args, cfg, plan, sp, rt, rank, dev, barrier, fwd_b + bwd_b, stream)
+        try:
+            nccl = run_nccl_comparison(args, cfg, plan, sp, rt, rank, dev, barrier, fwd_b + bwd_b, stream)
+        except Exception as exc:  # a diagnostic leg never voids the headline line
+            nccl = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+    done("nccl_comparison", nccl)
 
     overlap = None
     if N > 1 and cfg.dst.pp > 1 and cfg.src.rank_offset != cfg.dst.rank_offset and not args.no_overlap:
         overlap = run_pp_overlap(args, cfg, plan, rt, r2g, rank, dev, barrier, stream, slots)
+    done("overlap_with_pp_p2p", overlap)
 
     matrix = None
     names = [c for c in args.matrix.split(",") if c and c != cfg.name]
@@ -813,6 +879,7 @@ def main():
                              "fwd_ms": fk["ms"], "fwd_tstar_ms": fk["tstar_ms"], "fwd_bound": fk["bound"],
                              "bwd_ms": bk["ms"], "bwd_tstar_ms": bk["tstar_ms"], "bwd_bound": bk["bound"],
                              "overlap_with_pp_p2p": overlap, "parity": parity}}
+        line["config_matrix"] = matrix  # filled in place, config by config
         rt.close()
         rt = None
         torch.cuda.synchronize()
@@ -822,6 +889,7 @@ def main():
                 matrix[name] = run_matrix_config(args, name, N, rank, dev, barrier, stream, pk)
             except Exception as exc:  # a diagnostic leg never voids the headline line
                 matrix[name] = {"error": f"{type(exc).__name__}: {exc}"}
+    done("config_matrix", matrix)
 
     host_rt = None
     if N > 1 and host_runtime_topologies(N) and not args.no_runtime:
@@ -830,6 +898,7 @@ def main():
             rt = None
         torch.cuda.synchronize()
         host_rt = []
+        line["host_runtime"] = host_rt
         for name in host_runtime_topologies(N):
             phase(f"host runtime {name}")
             try:
@@ -838,6 +907,7 @@ def main():
                 res = {"topology": name, "error": f"{type(exc).__name__}: {exc}"}
             if res is not None:
                 host_rt.append(res)
+    done("host_runtime", host_rt)
 
     cpu = None
     if rank == 0 and not args.no_cpu:  # rank 0 at every N (host cores of the GPU box)
@@ -853,33 +923,10 @@ def main():
                                  "sample": d[3]}
         except Exception as exc:  # the oracle is a reported baseline, never the product
             cpu = {"value": None, "unit": "GB/s", "cores": 1, "kind": "port", "sample": f"unavailable: {exc}"}
+    done("cpu_baseline", cpu)
 
-    if rank == 0:
-        line = {
-            "metric": METRIC,
-            "value": round(value, 2), "unit": "GB/s", "n_gpus": N, "steps": K, "warmup": args.warmup,
-            "ms_per_step": round(ms_step, 5), "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": cfg.act, "data": "synthetic",
-            "config": workload_config(cfg, N, slots, args.scale),
-            "value_semantics": "whole job: boundary payload bytes of all N GPUs per second (bench contract); "
-                               "per GPU = per_gpu_gbs",
-            "per_gpu_gbs": round(value / N, 2), "tokens_per_s": round(tokens_s, 1),
-            "method": {"launch": (f"one CUDA graph per cycle of {slots} steps (fwd+bwd on each buffer set in "
-                                  f"turn; K % {slots} steps as one graph each)") if cycle else
-                                 ("one CUDA graph (fwd+bwd) per step" if use_graph else "per-op C-ABI launches"),
-                       "ms_per_step_one_graph_per_step": ms_graph_per_step,
-                       "timing": "CUDA events on the launching stream, barrier + synchronize on both sides, "
-                                 "max over ranks"},
-            "payload_bytes_per_step": {"fwd": fwd_b, "bwd": bwd_b},
-            "parity": parity,
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-            "clocks": clocks,
-            "nccl_comparison": nccl,
-            "overlap_with_pp_p2p": overlap,
-            "config_matrix": matrix,
-            "host_runtime": host_rt,
-        }
-        print(json.dumps(line), flush=True)
+    watchdog.cancel()
+    emit()
     if rt is not None:
         rt.close()
     if N > 1:
