@@ -62,6 +62,9 @@ def parse():
                     help="configs also measured (short) in the same run, so every N of the driver's scaling "
                          "run records the fan-in / fan-out / CP-splice / non-colocated step ('' = none)")
     ap.add_argument("--matrix-steps", type=int, default=200)
+    ap.add_argument("--paired", default="c2,c3,c4",
+                    help="configs also measured as 1F1B-paired steps (fwd of microbatch k+1 concurrent with bwd "
+                         "of microbatch k, hb_exec_graph_capture what=4) ('' = none)")
     ap.add_argument("--no-runtime", action="store_true",
                     help="skip the host-runtime leg (a24 + f2: 1F1B dispatch table with NC || PP P2P, N = 4, 6, 8)")
     ap.add_argument("--ref-procs", type=int, default=0, help="reference arm: worker processes (0 = auto)")
@@ -128,7 +131,7 @@ def traffic_model(cfg, n_gpus):
     r2g = configs.rank_to_gpu(plan.world, n_gpus)
     a, gi, go = DT_SIZE[cfg.act], DT_SIZE[cfg.grad_in], DT_SIZE[cfg.grad_out]
     z = lambda: [0] * n_gpus  # noqa: E731
-    out = {"fwd_hbm": z(), "fwd_nvl": z(), "bwd_hbm": z(), "bwd_nvl": z()}
+    out = {"fwd_hbm": z(), "fwd_nvl": z(), "bwd_hbm": z(), "bwd_nvl": z(), "fwd_nvl_out": z(), "bwd_nvl_out": z()}
 
     def account(kind, reads, esize):
         # reads: {(reader_gpu, src_rank, src_slot): [(start, end), ...]} in elements
@@ -137,6 +140,7 @@ def traffic_model(cfg, n_gpus):
             out[kind + "_hbm"][r2g[sr]] += nbytes
             if r2g[sr] != g_rd:
                 out[kind + "_nvl"][g_rd] += nbytes
+                out[kind + "_nvl_out"][r2g[sr]] += nbytes
 
     reads = {}
     for (sr, ss, so, dr, ds, do, n) in hbb.index_forward(plan, sp):
@@ -822,9 +826,11 @@ def main():
         "nccl_comparison": None,
         "overlap_with_pp_p2p": None,
         "config_matrix": None,
+        "paired_1f1b": None,
         "host_runtime": None,
     }
-    pending = ["e2e", "nccl_comparison", "overlap_with_pp_p2p", "config_matrix", "host_runtime", "cpu_baseline"]
+    pending = ["e2e", "nccl_comparison", "overlap_with_pp_p2p", "config_matrix", "paired_1f1b", "host_runtime",
+               "cpu_baseline"]
     printed = threading.Lock()
 
     def emit(extra=None):
@@ -890,6 +896,23 @@ def main():
             except Exception as exc:  # a diagnostic leg never voids the headline line
                 matrix[name] = {"error": f"{type(exc).__name__}: {exc}"}
     done("config_matrix", matrix)
+
+    paired = None
+    names_p = [c for c in args.paired.split(",") if c]
+    if names_p and args.scale == 1:
+        if rt is not None:
+            rt.close()
+            rt = None
+        torch.cuda.synchronize()
+        paired = {}
+        line["paired_1f1b"] = paired
+        for name in names_p:
+            phase(f"paired {name}")
+            try:
+                paired[name] = run_paired(args, name, N, rank, dev, barrier, stream, pk)
+            except Exception as exc:  # a diagnostic leg never voids the headline line
+                paired[name] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+    done("paired_1f1b", paired)
 
     host_rt = None
     if N > 1 and host_runtime_topologies(N) and not args.no_runtime:
@@ -990,8 +1013,13 @@ def run_host_runtime(name, rank, world, dev, steps=5):
             errors.append(f"{what}: {type(exc).__name__}: {exc}"[:300])
             return default
 
-    rt = attempt("create", lambda: R.HostRuntime(mods, edges, B, W, nmb=4, pp_bytes=ppb, skip=R.SKIP_COMPUTE,
-                                                  timeout_s=5.0))
+    # 8 microbatches (warm-up and drain, where boundary ops sit on the critical
+    # path, are a smaller share of the step); boundary kernels capped at one CTA
+    # per SM so the PP stream's NCCL kernels always find room beside them
+    nmb = int(os.environ.get("HB_RT_NMB", "8"))
+    cap = int(os.environ.get("HB_RT_CAP", str(torch.cuda.get_device_properties(dev).multi_processor_count)))
+    rt = attempt("create", lambda: R.HostRuntime(mods, edges, B, W, nmb=nmb, max_ctas=cap, pp_bytes=ppb,
+                                                  skip=R.SKIP_COMPUTE, timeout_s=5.0))
     ok = rt is not None
     ms_first = 0.0
     rows = rt.rows if rt is not None else None
@@ -1060,8 +1088,8 @@ def run_host_runtime(name, rank, world, dev, steps=5):
     if flag.item() == 0:
         for label, skip in (("nc_only", R.SKIP_COMPUTE | R.SKIP_P2P), ("p2p_only", R.SKIP_COMPUTE | R.SKIP_NC),
                             ("both", R.SKIP_COMPUTE)):
-            r2 = attempt("create", lambda: R.HostRuntime(mods, edges, B, W, nmb=4, pp_bytes=ppb, skip=skip,
-                                                          timeout_s=5.0))
+            r2 = attempt("create", lambda: R.HostRuntime(mods, edges, B, W, nmb=nmb, max_ctas=cap, pp_bytes=ppb,
+                                                          skip=skip, timeout_s=5.0))
             ts = []
             if r2 is not None:
                 def one():
@@ -1082,6 +1110,7 @@ def run_host_runtime(name, rank, world, dev, steps=5):
     err = torch.tensor([len(errors)], device=dev)
     dist.all_reduce(err)
     res = {"topology": name, "n_gpus": world, "parity": flag.item() == 0 and err.item() == 0, "rows": rows,
+           "nmb": nmb, "max_ctas": cap,
            "first_step_ms": round(ms_first or 0.0, 3), "step_ms": times,
            "how": "HostRuntime.step over the 1F1B dispatch table (event-only compute); NC = boundary exec "
                   "fwd/bwd on the boundary stream, P2P = NCCL send/recv on the PP communicator"}
@@ -1102,6 +1131,105 @@ def copy_kernel_name(args):
 def reduce_kernel_name(cfg):
     tn = {"bf16": "__nv_bfloat16", "fp16": "__half", "fp32": "float"}
     return f"reduce_segments_kernel<{tn[cfg.grad_in]},{tn[cfg.grad_out]}>"
+
+
+def paired_bound(tm, pk, N):
+    """T* of a 1F1B-paired step (forward of one microbatch concurrent with the
+    backward of the previous one): both ops' bytes share each GPU's HBM and
+    NVLink, so the bound is max over GPUs of max(HBM_fwd+HBM_bwd over the HBM
+    peak, NVLink in (and out) of both over the link peak), not the sum of the
+    two kernels' bounds."""
+    best, crit = 0.0, None
+    for g in range(N):
+        h = tm["fwd_hbm"][g] + tm["bwd_hbm"][g]
+        ni = tm["fwd_nvl"][g] + tm["bwd_nvl"][g]
+        no = tm["fwd_nvl_out"][g] + tm["bwd_nvl_out"][g]
+        t = max(h / (pk["hbm_gbs"] * 1e9), max(ni, no) / (pk["nvl_gbs"] * 1e9))
+        if t > best:
+            best, crit = t, (g, "hbm" if h / (pk["hbm_gbs"] * 1e9) >= max(ni, no) / (pk["nvl_gbs"] * 1e9)
+                             else "nvlink")
+    return best * 1e3, crit
+
+
+def run_paired(args, name, N, rank, dev, barrier, stream, pk):
+    """1F1B-paired boundary steps: a pipeline schedule call returns microbatch
+    k's gradient in the same call that receives microbatch k+1, so the runtime's
+    paired cycle graph (hb_exec_graph_capture what=4) runs the forward of buffer
+    set k concurrently with the backward of set k-1. Each step still moves one
+    full forward and one full backward; the two ops' fixed costs (launch,
+    handshake, pipeline fill, tail) overlap and HBM and NVLink work at once.
+    Both grids are capped at one CTA per SM so they are co-resident. Parity is
+    checked on the same runtime (same tables and kernels) with serial steps."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_27678_b200 import bridge as hbb
+    from paper_2605_27678_b200 import configs
+
+    cfg = configs.get(name)
+    plan = hbb.plan_bridge(cfg.edge())
+    sp = make_splice(cfg)
+    r2g = configs.rank_to_gpu(plan.world, N)
+    local = [r for r in range(plan.world) if r2g[r] == rank]
+    tdt = {"bf16": torch.bfloat16, "fp16": torch.float16, "fp32": torch.float32}
+    tm = traffic_model(cfg, N)
+    per_gpu_step = max(f + b for f, b in zip(tm["fwd_hbm"], tm["bwd_hbm"]))
+    slots = max(4, min(8, math.ceil(3 * L2_BYTES / max(per_gpu_step, 1))))
+    cap = torch.cuda.get_device_properties(dev).multi_processor_count
+    rt = hbb.BridgeRuntime(plan, sp, n_gpus=N, my_gpu=rank, rank_to_gpu=r2g, act_dtype=tdt[cfg.act],
+                           grad_in_dtype=tdt[cfg.grad_in], grad_out_dtype=tdt[cfg.grad_out], mb_slots=slots,
+                           max_ctas=cap)
+    try:
+        if N > 1:
+            rt.exchange_handles()
+        fill_inputs(rt, local, slots, dev)
+        for mb in range(3):
+            rt.forward(mb, stream)
+            rt.backward(mb, cfg.beta, stream)
+        barrier()
+
+        def timed(what, cycles):
+            rt.capture_step(0, cfg.beta, True, stream, what=what)
+            rt.replay_step(0, stream, what)
+            barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(cycles):
+                rt.replay_step(0, stream, what)
+            b.record(stream)
+            stream.synchronize()
+            t = torch.tensor([a.elapsed_time(b) / (cycles * slots)], dtype=torch.float64, device=dev)
+            if N > 1:
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            barrier()
+            return t.item()
+
+        cycles = max(4, args.matrix_steps // slots)
+        ms_paired = timed(rt.GRAPH_PAIRED, cycles)
+        ms_serial = timed(rt.GRAPH_CYCLE, cycles)  # the same capped runtime, ops one after the other
+        if rt.status():
+            raise RuntimeError("device flag wait timed out")
+        for k in range(slots):
+            rt.capture_step(k, cfg.beta, True, stream)
+        parity = check_parity(rt, cfg, plan, sp, r2g, rank, N, dev, stream, barrier,
+                              lambda k: rt.replay_step(k, stream), 0)
+        fwd_b, bwd_b = payload_bytes(cfg)
+        tp_ms, crit = paired_bound(tm, pk, N)
+        fk, bk = kernel_bound(tm, "fwd", 1.0, pk, N), kernel_bound(tm, "bwd", 1.0, pk, N)
+        return {"ms_per_step": round(ms_paired, 5),
+                "value_gbs": round((fwd_b + bwd_b) / (ms_paired * 1e-3) / 1e9, 2),
+                "tokens_per_s": round(cfg.batch * cfg.tokens / (ms_paired * 1e-3), 1),
+                "tstar_paired_ms": round(tp_ms, 4), "frac_of_tstar_paired": round(tp_ms / ms_paired, 4),
+                "critical": {"gpu": crit[0], "bound": crit[1]} if crit else None,
+                "serial_tstar_ms": round(fk["tstar_ms"] + bk["tstar_ms"], 4),
+                "serial_same_cap_ms_per_step": round(ms_serial, 5),
+                "max_ctas": cap, "buffer_sets": slots, "steps": cycles * slots, "parity": parity,
+                "how": "hb_exec_graph_capture what=4: step k = fwd(set k) || bwd(set k-1) on two streams, "
+                       "one graph per cycle of buffer sets; CUDA events, max over ranks"}
+    finally:
+        barrier()
+        rt.close()
+        torch.cuda.synchronize()
 
 
 def run_matrix_config(args, name, N, rank, dev, barrier, stream, pk):

@@ -224,8 +224,11 @@ int hb_exec_seed_forward_record(hb_exec* x, int mb); /* bridge.hpp:165 */
 int hb_exec_set_text_embedding(hb_exec* x, const void* table, long long vocab);
 /* CUDA graph of one buffer set's boundary ops; what: 0 forward, 1 forward +
  * backward(beta), 2 backward(beta), 3 forward + backward(beta) of every buffer
- * set in order (one launch replays mb_slots steps; mb_slot ignored). One graph
- * launch replays the ops; replays bypass the microbatch records. */
+ * set in order (one launch replays mb_slots steps; mb_slot ignored), 4 the
+ * 1F1B-paired cycle: step k runs the forward of set k concurrently with the
+ * backward(beta) of set k-1 (a pipeline schedule call pairs them the same way;
+ * mb_slots >= 2; size max_ctas so both grids fit on the GPU together). One
+ * graph launch replays the ops; replays bypass the microbatch records. */
 int hb_exec_graph_capture(hb_exec* x, int mb_slot, int what, float beta, void* cuda_stream);
 int hb_exec_graph_launch(hb_exec* x, int mb_slot, int what, void* cuda_stream);
 int hb_exec_status(hb_exec* x, unsigned* device_error);

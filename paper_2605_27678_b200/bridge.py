@@ -430,12 +430,13 @@ class BridgeRuntime:
     def backward(self, mb: int = 0, beta: float = 0.0, stream=None):
         check(lib().hb_exec_backward(self._h, mb, ctypes.c_float(beta), self._stream(stream)))
 
-    GRAPH_FWD, GRAPH_STEP, GRAPH_BWD, GRAPH_CYCLE = 0, 1, 2, 3
+    GRAPH_FWD, GRAPH_STEP, GRAPH_BWD, GRAPH_CYCLE, GRAPH_PAIRED = 0, 1, 2, 3, 4
 
     def capture_step(self, mb_slot: int = 0, beta: float = 1.0, with_backward: bool = True, stream=None,
                      what: int | None = None):
         """Capture one buffer set's ops into a CUDA graph (what: 0 fwd, 1 fwd+bwd, 2 bwd;
-        3 = fwd+bwd of every buffer set in order, one graph per cycle of mb_slots steps)."""
+        3 = fwd+bwd of every buffer set in order, one graph per cycle of mb_slots steps;
+        4 = the 1F1B-paired cycle: step k = fwd of set k concurrently with bwd of set k-1)."""
         what = (1 if with_backward else 0) if what is None else what
         check(lib().hb_exec_graph_capture(self._h, mb_slot, what, ctypes.c_float(beta), self._stream(stream)))
 

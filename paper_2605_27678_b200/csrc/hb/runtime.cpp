@@ -119,6 +119,12 @@ Exec::Exec(const bridge::BridgePlan& plan, const index::SpliceSpec* splice, int 
 }
 
 Exec::~Exec() {
+  if (side_) {
+    cudaStreamSynchronize(side_);
+    cudaStreamDestroy(side_);
+    cudaEventDestroy(fork_);
+    cudaEventDestroy(join_);
+  }
   DeviceGuard dg(device_);
   for (auto& kv : graphs_) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(kv.second.first));
   for (auto& t : proj_) cudaFree(t.rows_dev);
@@ -968,9 +974,11 @@ void Exec::backward(int mb, float beta, void* stream) {
 void Exec::graph_capture(int mb_slot, int what, float beta, void* stream) {
   DeviceGuard dg(device_);
   if (mb_slot < 0 || mb_slot >= cfg_.mb_slots) raise(ErrorCode::InvalidArgument, "mb slot out of range");
-  if (what < 0 || what > 3)
-    raise(ErrorCode::InvalidArgument, "graph 'what' must be 0 (fwd), 1 (fwd+bwd), 2 (bwd), 3 (a step per buffer set)");
-  if (what == 3) mb_slot = 0;  // the cycle graph is keyed on slot 0
+  if (what < 0 || what > 4)
+    raise(ErrorCode::InvalidArgument, "graph 'what' must be 0 (fwd), 1 (fwd+bwd), 2 (bwd), 3 (a step per buffer "
+                                      "set), 4 (a 1F1B-paired cycle)");
+  if (what == 4 && cfg_.mb_slots < 2) raise(ErrorCode::InvalidArgument, "a paired cycle needs mb_slots >= 2");
+  if (what >= 3) mb_slot = 0;  // cycle graphs are keyed on slot 0
   if (!stream) raise(ErrorCode::InvalidArgument, "graph capture needs a non-default stream");
   if (what != 2) prepare_fwd();
   if (what != 0) prepare_bwd();
@@ -988,6 +996,29 @@ void Exec::graph_capture(int mb_slot, int what, float beta, void* stream) {
       launch_forward(k, stream);
       launch_backward(k, beta, stream);
     }
+  } else if (what == 4) {
+    // 1F1B pairing, as a pipeline's schedule call issues it (the LLM's first
+    // stage receives mb k+1 and returns mb k's gradient in the same call):
+    // step k = forward of set k on `stream` concurrently with the backward of
+    // set k-1 on a side stream, joined before step k+1. The two ops touch
+    // disjoint buffers (SRC_ACT/DST_ACT of k, DST_GRAD/SRC_GRAD of k-1) and use
+    // separate per-kind counters and pads, so the only requirement is that
+    // both grids fit on the GPU together (the exec's max_ctas).
+    if (!side_) {
+      int least = 0, greatest = 0;
+      ck(cudaDeviceGetStreamPriorityRange(&least, &greatest), "priority range");
+      ck(cudaStreamCreateWithPriority(&side_, cudaStreamNonBlocking, greatest), "side stream");
+      ck(cudaEventCreateWithFlags(&fork_, cudaEventDisableTiming), "event");
+      ck(cudaEventCreateWithFlags(&join_, cudaEventDisableTiming), "event");
+    }
+    for (int k = 0; k < cfg_.mb_slots; ++k) {
+      ck(cudaEventRecord(fork_, st), "fork");
+      ck(cudaStreamWaitEvent(side_, fork_, 0), "fork");
+      launch_forward(k, stream);
+      launch_backward((k + cfg_.mb_slots - 1) % cfg_.mb_slots, beta, side_);
+      ck(cudaEventRecord(join_, side_), "join");
+      ck(cudaStreamWaitEvent(st, join_, 0), "join");
+    }
   } else {
     if (what != 2) launch_forward(mb_slot, stream);
     if (what != 0) launch_backward(mb_slot, beta, stream);
@@ -1003,7 +1034,7 @@ void Exec::graph_capture(int mb_slot, int what, float beta, void* stream) {
 
 void Exec::graph_launch(int mb_slot, int what, void* stream) {
   DeviceGuard dg(device_);
-  auto it = graphs_.find(std::make_pair(what == 3 ? 0 : mb_slot, what));
+  auto it = graphs_.find(std::make_pair(what >= 3 ? 0 : mb_slot, what));
   if (it == graphs_.end())
     raise(ErrorCode::InvalidArgument,
           graphs_invalidated_ ? "graph invalidated by bind / open_peers / set_text_embedding: recapture it"

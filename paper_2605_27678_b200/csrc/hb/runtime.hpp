@@ -22,6 +22,8 @@
 #include <string>
 #include <vector>
 
+#include <cuda_runtime.h>
+
 #include "hb/bridge.hpp"
 #include "hb/index_map.hpp"
 #include "kernels/boundary_kernels.cuh"
@@ -98,7 +100,9 @@ class Exec {
   // CUDA-graph capture of one buffer set's forward (+ backward with `beta`):
   // the step is replayed with one graph launch (no per-kernel host overhead).
   // Replays bypass the microbatch records (a replay is a complete fwd+bwd).
-  // what: 0 forward only, 1 forward + backward, 2 backward only.
+  // what: 0 forward only, 1 forward + backward, 2 backward only, 3 forward +
+  // backward of every buffer set in turn, 4 the 1F1B-paired cycle (step k =
+  // forward of set k concurrently with the backward of set k-1).
   void graph_capture(int mb_slot, int what, float beta, void* stream);
   void graph_launch(int mb_slot, int what, void* stream);
   uint32_t device_error() const;  // synchronises
@@ -236,6 +240,8 @@ class Exec {
   int launches_ = 0;
   std::set<int> fwd_done_;
   std::map<std::pair<int, int>, std::pair<void*, int>> graphs_;  // (slot, what) -> (cudaGraphExec_t, kernels)
+  cudaStream_t side_ = nullptr;  // the 1F1B-paired graph's backward stream (what = 4)
+  cudaEvent_t fork_ = nullptr, join_ = nullptr;
   void launch_forward(int mb_slot, void* stream);
   void launch_backward(int mb_slot, float beta, void* stream);
 };

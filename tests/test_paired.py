@@ -1,0 +1,100 @@
+"""1F1B-paired cycle graph (hb_exec_graph_capture what=4): step k runs the
+forward of buffer set k concurrently with the backward of set k-1. The two ops
+touch disjoint buffers, so one paired cycle must leave every buffer bit for bit
+as the same ops run one after the other: fwd(0), bwd(S-1), fwd(1), bwd(0), ...
+Checked at one GPU and on a 2-GPU exec group (virtual GPUs sharing cuda:0 when
+the box has one GPU; both grids capped so all four kernels are co-resident)."""
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from parity_core import make_splice  # noqa: E402
+
+from paper_2605_27678_b200 import bridge as hbb  # noqa: E402
+from paper_2605_27678_b200 import configs  # noqa: E402
+
+DT = {"bf16": torch.bfloat16, "fp16": torch.float16, "fp32": torch.float32}
+SLOTS = (hbb.SLOT_SRC_ACT, hbb.SLOT_DST_ACT, hbb.SLOT_DST_GRAD, hbb.SLOT_SRC_GRAD, hbb.SLOT_TEXT)
+
+
+def _bufs(rts, plan, r2g, S):
+    out = {}
+    for r in range(plan.world):
+        rt = rts[r2g[r]]
+        for slot in SLOTS:
+            if rt.buffer_numel(r, slot) == 0:
+                continue
+            for k in range(S):
+                b = rt.buffer(r, slot, k)
+                if b is not None:
+                    out[(r, slot, k)] = b
+    return out
+
+
+def _run(name, n, devices, cap):
+    cfg = configs.get(name, scale=64)
+    plan = hbb.plan_bridge(cfg.edge())
+    S = 3
+    kw = dict(act_dtype=DT[cfg.act], grad_in_dtype=DT[cfg.grad_in], grad_out_dtype=torch.float32, mb_slots=S,
+              max_ctas=cap, timeout_s=20.0)
+    if n == 1:
+        rts = [hbb.BridgeRuntime(plan, make_splice(cfg), **kw)]
+        r2g = [0] * plan.world
+        streams = [torch.cuda.Stream()]
+        group = None
+    else:
+        group = hbb.LocalGroup(plan, make_splice(cfg), devices=devices, **kw)
+        rts, r2g, streams = group.rts, group.rank_to_gpu, group.streams
+    try:
+        bufs = _bufs(rts, plan, r2g, S)
+        gen = torch.Generator(device="cpu").manual_seed(7)
+        for key, b in sorted(bufs.items()):
+            if key[1] == hbb.SLOT_TEXT and b.dtype == torch.int32:
+                continue
+            b.copy_(torch.randn(b.numel(), generator=gen).to(b.dtype))
+        torch.cuda.synchronize()
+        init = {k: b.clone() for k, b in bufs.items()}
+
+        # serial reference on the same buffers: fwd(k), bwd(k-1) in cycle order (graphs, one op each)
+        for rt, st in zip(rts, streams):
+            for k in range(S):
+                rt.capture_step(k, 1.0, stream=st, what=rt.GRAPH_FWD)
+                rt.capture_step(k, 1.0, stream=st, what=rt.GRAPH_BWD)
+        for k in range(S):
+            for rt, st in zip(rts, streams):
+                rt.replay_step(k, st, rt.GRAPH_FWD)
+            for rt, st in zip(rts, streams):
+                rt.replay_step((k + S - 1) % S, st, rt.GRAPH_BWD)
+        torch.cuda.synchronize()
+        serial = {k: b.clone() for k, b in bufs.items()}
+
+        for k, b in bufs.items():
+            b.copy_(init[k])
+        torch.cuda.synchronize()
+        for rt, st in zip(rts, streams):
+            rt.capture_step(0, 1.0, stream=st, what=rt.GRAPH_PAIRED)
+        for rt, st in zip(rts, streams):
+            rt.replay_step(0, st, rt.GRAPH_PAIRED)
+        torch.cuda.synchronize()
+        for rt in rts:
+            assert rt.status() == 0
+        for k, b in bufs.items():
+            assert torch.equal(b.view(torch.uint8), serial[k].view(torch.uint8)), f"buffer {k} differs"
+    finally:
+        if group is not None:
+            group.close()
+        else:
+            rts[0].close()
+
+
+@pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5"])
+def test_paired_cycle_equals_serial_one_gpu(name):
+    _run(name, 1, [0], 148)
+
+
+@pytest.mark.parametrize("name", ["c2", "c4"])
+def test_paired_cycle_equals_serial_group(name):
+    n = 2
+    devs = list(range(n)) if torch.cuda.device_count() >= n else [0] * n
+    _run(name, n, devs, 48)
