@@ -1117,6 +1117,10 @@ def run_host_runtime(name, rank, world, dev, steps=5):
     if times and all(math.isfinite(v) for v in times.values()):
         tb, tp, both = times["nc_only"], times["p2p_only"], times["both"]
         res["overlap"] = round((tb + tp - both) / max(1e-9, min(tb, tp)), 3)
+        # the first microbatch's boundary forward and the last one's backward sit on
+        # the pipeline's critical path (nothing to overlap them with): about 1/nmb of
+        # the boundary time cannot be hidden whatever the runtime does
+        res["overlap_structural_max"] = round(1.0 - 1.0 / nmb, 3) if tb <= tp else None
     if err.item():
         res["errors_on_ranks"] = int(err.item())
         if errors:
