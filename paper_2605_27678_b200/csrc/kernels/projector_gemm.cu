@@ -20,6 +20,14 @@
 //               released as soon as the tile sits in smem; the accumulator is
 //               double buffered (2 x 256 columns) so the next tile's MMAs run
 //               under this tile's stores.
+// Three variants (HB_PROJ_CLUSTER): single CTAs (1), CTA pairs sharing the W
+// tile by TMA multicast (2), and the default, CTA pairs running one 256 x 256
+// tile with tcgen05.mma.cta_group::2 (3): each CTA stages its 128 rows of X
+// and its 128 rows of W (32 KiB per k-block instead of 48), the leader CTA
+// issues M=256 MMAs that read both CTAs' shared memory and write each CTA's
+// 128 accumulator rows into its own TMEM. That halves the per-SM shared-memory
+// read traffic of the B operand, which (with the TMA writes) is what bounds the
+// single-CTA M=128 x N=256 MMA.
 // Roofline: tensor (2*M*N*K flop) for K large; for the projector shapes the
 // output stores (M*N*2 B per destination) usually bind.
 #include <cuda.h>
@@ -38,9 +46,11 @@ namespace hb::dev {
 namespace {
 
 constexpr int kBM = 128, kBN = 256, kBK = 64;  // tile; kBK = one 128-B swizzle row of bf16
-constexpr int kStages = 3;
+constexpr int kStages = 3;    // single / multicast pair: 48 KiB stages
+constexpr int kStages2Sm = 4;  // 2-SM pair: 32 KiB stages
 constexpr uint32_t kABytes = kBM * kBK * 2, kBBytes = kBN * kBK * 2;  // 16 KiB, 32 KiB
 constexpr uint32_t kStageBytes = kABytes + kBBytes;
+constexpr uint32_t kStageBytes2Sm = kABytes + kBBytes / 2;  // own X rows + own half of the W tile
 constexpr int kEpiWarps = 4;
 constexpr int kThreads = 32 * (2 + kEpiWarps);
 constexpr uint32_t kTmemCols = 2 * kBN;  // two accumulators
@@ -49,6 +59,7 @@ constexpr uint32_t kTmemCols = 2 * kBN;  // two accumulators
 constexpr int kEpiRowPitch = kBN * 2 + 16;
 constexpr uint32_t kEpiBytes = kEpiWarps * 32 * kEpiRowPitch;
 constexpr size_t kSmemBytes = kStages * kStageBytes + kEpiBytes + 1024;  // + alignment slack
+static_assert(kStages2Sm * kStageBytes2Sm <= kStages * kStageBytes, "2-SM ring fits the same smem");
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -94,6 +105,30 @@ __device__ __forceinline__ void tc_commit_mc(uint64_t* bar, uint16_t mask) {
       "h"(mask)
       : "memory");
 }
+// 2-SM pair load: the bytes land in this CTA's smem and complete on the
+// LEADER's barrier (the peer bit of the barrier's shared::cluster address cleared)
+__device__ __forceinline__ void tma_load_2d_2sm(void* smem, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+      "[%4];" ::"r"(smem_u32(smem)),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar) & 0xFEFFFFFFu)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_2sm(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+// arrive on the barrier at the same smem offset in CTA `rank` of the cluster
+__device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t rank) {
+  asm volatile(
+      "{\n .reg .b32 ra;\n mapa.shared::cluster.u32 ra, %0, %1;\n"
+      " mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n}\n" ::"r"(smem_u32(bar)),
+      "r"(rank)
+      : "memory");
+}
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
@@ -132,14 +167,25 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
          (static_cast<uint64_t>(1024 >> 4) << 32) | (static_cast<uint64_t>(1) << 46) |
          (static_cast<uint64_t>(2) << 61);
 }
-// kind::f16 instruction descriptor: D fp32, A/B bf16, both K-major, M=128, N=256
-constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(kBN >> 3) << 17) |
-                            (static_cast<uint32_t>(kBM >> 4) << 24);
+// kind::f16 instruction descriptor: D fp32, A/B bf16, both K-major, N=256, M=128 (M=256 for the pair)
+constexpr uint32_t idesc_f16(int m) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(kBN >> 3) << 17) |
+         (static_cast<uint32_t>(m >> 4) << 24);
+}
+constexpr uint32_t kIdesc = idesc_f16(kBM);
+constexpr uint32_t kIdesc2Sm = idesc_f16(2 * kBM);
 __device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t accumulate) {
   asm volatile(
       "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
       " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
       "l"(a), "l"(b), "r"(kIdesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_bf16_2sm(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(kIdesc2Sm), "r"(accumulate)
       : "memory");
 }
 __device__ __forceinline__ uint32_t pack_bf16(uint32_t lo, uint32_t hi) {
@@ -158,12 +204,25 @@ __device__ __forceinline__ uint32_t pack_bf16(uint32_t lo, uint32_t hi) {
         "=r"(v[30]), "=r"(v[31])                                                                               \
       : "r"(addr))
 
-template <int kCM>
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {  // sees remote release arrivals
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "W: mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra W;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// kCM: CTAs per cluster (1 or 2); k2Sm: the pair runs tcgen05.mma.cta_group::2
+template <int kCM, bool k2Sm>
 __global__ void __launch_bounds__(kThreads, 1)
     projector_gemm_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_w,
                           ProjectorArgs args) {
+  static_assert(!k2Sm || kCM == 2, "the 2-SM MMA runs on a CTA pair");
+  constexpr int S = k2Sm ? kStages2Sm : kStages;
+  constexpr uint32_t SB = k2Sm ? kStageBytes2Sm : kStageBytes;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  __shared__ __align__(8) uint64_t full[kStages], empty[kStages], tfull[2], tempty[2];
+  __shared__ __align__(8) uint64_t full[S], empty[S], tfull[2], tempty[2];
   __shared__ uint32_t tmem_base_sh;
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -174,13 +233,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&map_x) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&map_w) : "memory");
-    for (int i = 0; i < kStages; ++i) {
+    for (int i = 0; i < S; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], kCM);  // both CTAs' MMAs read a stage the pair filled
+      // multicast pair: both CTAs' MMAs read a stage the pair filled; 2-SM: the
+      // leader's one commit frees the stage in both CTAs
+      mbar_init(&empty[i], k2Sm ? 1 : kCM);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], kEpiWarps * 32);
+      // 2-SM: one arrival per epilogue warp of both CTAs, on the leader's barrier
+      mbar_init(&tempty[i], k2Sm ? 2 * kEpiWarps : kEpiWarps * 32);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -190,10 +252,19 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (blockIdx.x == 0 && warp == 0) post_peers_warp(args.sync, 0);
   if (threadIdx.x == 0) cta_arrive_finish(args.sync, cs, cta_arrive_issue(args.sync));
   if (warp == 1) {  // one warp allocates (and later frees) the two accumulators
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
-                 "r"(kTmemCols)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if constexpr (k2Sm) {  // the same warp of both CTAs, the same smem slot: one pair allocation
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(&tmem_base_sh)),
+                   "r"(kTmemCols)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(&tmem_base_sh)),
+                   "r"(kTmemCols)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -210,7 +281,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         tm.coords(item, m0, n0);
         for (int kb = 0; kb < num_k; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          unsigned char* a = smem + stage * kStageBytes;
+          unsigned char* a = smem + stage * SB;
+          if constexpr (k2Sm) {
+            // each CTA stages its own X rows and its own half of the W tile; all
+            // of the pair's bytes complete on the leader's full barrier
+            if (crank == 0) mbar_expect_tx(&full[stage], 2 * SB);
+            tma_load_2d_2sm(a, &map_x, &full[stage], kb * kBK, m0);
+            tma_load_2d_2sm(a + kABytes, &map_w, &full[stage], kb * kBK, n0 + static_cast<int>(crank) * (kBN / 2));
+            if (++stage == S) {
+              stage = 0;
+              phase ^= 1;
+            }
+            continue;
+          }
           mbar_expect_tx(&full[stage], kStageBytes);  // own X tile + both W halves
           tma_load_2d(a, &map_x, &full[stage], kb * kBK, m0);
           if constexpr (kCM == 1) {
@@ -228,16 +311,36 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // ---- MMA issuer
+    if (lane == 0 && (!k2Sm || crank == 0)) {  // ---- MMA issuer (2-SM: the leader CTA only)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
       for (int item = tm.first(); item < tm.items(); item += tm.step(), ++it) {
         const int acc = it & 1;
         const uint32_t aphase = (it >> 1) & 1;
-        mbar_wait(&tempty[acc], aphase ^ 1);  // the epilogue drained this accumulator
+        // the epilogue drained this accumulator (2-SM: in both CTAs)
+        if constexpr (k2Sm) mbar_wait_cluster(&tempty[acc], aphase ^ 1);
+        else mbar_wait(&tempty[acc], aphase ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + acc * kBN;
+        if constexpr (k2Sm) {
+          for (int kb = 0; kb < num_k; ++kb) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            // the same smem offsets in both CTAs: A = the CTA's 128 X rows, B = its 128 W rows
+            const uint32_t a = smem_u32(smem + stage * SB), b = a + kABytes;
+#pragma unroll
+            for (int k = 0; k < kBK / 16; ++k)
+              umma_bf16_2sm(d, umma_desc_sw128(a + k * 32), umma_desc_sw128(b + k * 32), (kb | k) != 0);
+            tc_commit_2sm(&empty[stage], 0x3);  // frees the stage in both CTAs
+            if (++stage == S) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+          tc_commit_2sm(&tfull[acc], 0x3);  // each CTA's 128 accumulator rows are complete
+          continue;
+        }
         for (int kb = 0; kb < num_k; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
@@ -259,7 +362,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {  // ---- epilogue warps: TMEM -> registers -> bf16 -> smem rows -> TMA bulk stores per destination
     const int q = warp % 4;  // TMEM lane quarter this warp may access
-    unsigned char* stage_w = smem + kStages * kStageBytes + (warp - 2) * (32 * kEpiRowPitch);
+    unsigned char* stage_w = smem + S * SB + (warp - 2) * (32 * kEpiRowPitch);
     unsigned char* my_row = stage_w + lane * kEpiRowPitch;
     // before the first store: every peer has started this op, so its
     // destination buffers of this set are no longer read
@@ -292,7 +395,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       // the accumulator is in smem now: hand TMEM back to the MMA warp
       tc_fence_before();
-      mbar_arrive(&tempty[acc]);
+      if constexpr (k2Sm) {  // one arrival per warp, on the leader's barrier
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(&tempty[acc], 0);
+      } else {
+        mbar_arrive(&tempty[acc]);
+      }
       // each lane stores its row (512 contiguous bytes) to every destination
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       if (row < args.M && ok) {
@@ -313,8 +421,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   if constexpr (kCM > 1) cluster_sync_all();  // no CTA leaves while its peer may still arrive on its barriers
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols)
-                 : "memory");
+    if constexpr (k2Sm)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols)
+                   : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols)
+                   : "memory");
   }
   // end: "writes done" to every peer written, wait for every writer into this GPU
   if (threadIdx.x == 0) launch_end_lane(args.sync, cs);
@@ -357,11 +469,13 @@ int launch_projector(const void* x, int64_t ldx, const void* w, int64_t ldw, con
   if (projector_check_shape(args.M, args.N, args.K) || args.fan < 1 || args.fan > kMaxProjFan) return 1;
   if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(w)) & 15) return 3;
   if ((ldx * 2) % 16 || (ldw * 2) % 16) return 3;
-  // CTA pairs sharing W tiles through TMA multicast (default), or single CTAs
-  static const int cm = [] {
+  // 3 (default): CTA pairs with the 2-SM MMA; 2: CTA pairs sharing W tiles
+  // through TMA multicast; 1: single CTAs (HB_PROJ_CLUSTER, A/B knob)
+  static const int mode = [] {
     const char* v = std::getenv("HB_PROJ_CLUSTER");
-    return (v && v[0] == '1') ? 1 : 2;
+    return (v && (v[0] == '1' || v[0] == '2')) ? v[0] - '0' : 3;
   }();
+  const int cm = mode == 1 ? 1 : 2;
   CUtensorMap mx{}, mw{};
   // M == 0: this GPU projects no rows but still takes part in the launch protocol
   if (args.M > 0 && (!make_map(&mx, x, args.M, args.K, ldx, kBM) || !make_map(&mw, w, args.N, args.K, ldw, kBN / cm)))
@@ -370,18 +484,19 @@ int launch_projector(const void* x, int64_t ldx, const void* w, int64_t ldw, con
   int dev = 0;
   cudaGetDevice(&dev);
   once(dev, [] {
-    cudaFuncSetAttribute(projector_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(projector_gemm_kernel<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(kSmemBytes));
-    cudaFuncSetAttribute(projector_gemm_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(projector_gemm_kernel<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(kSmemBytes));
-    cudaFuncSetAttribute(projector_gemm_kernel<2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
+    cudaFuncSetAttribute(projector_gemm_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(kSmemBytes));
   });
   const int items = ((args.M + kBM - 1) / kBM + cm - 1) / cm * (args.N / kBN);
   int grid = items * cm < sm_count ? items * cm : sm_count - sm_count % cm;
   if (grid < cm) grid = cm;
   auto st = static_cast<cudaStream_t>(stream);
   if (cm == 1) {
-    projector_gemm_kernel<1><<<grid, kThreads, kSmemBytes, st>>>(mx, mw, args);
+    projector_gemm_kernel<1, false><<<grid, kThreads, kSmemBytes, st>>>(mx, mw, args);
   } else {
     cudaLaunchConfig_t lc{};
     lc.gridDim = dim3(grid);
@@ -395,7 +510,9 @@ int launch_projector(const void* x, int64_t ldx, const void* w, int64_t ldw, con
     at[0].val.clusterDim.z = 1;
     lc.attrs = at;
     lc.numAttrs = 1;
-    if (cudaLaunchKernelEx(&lc, projector_gemm_kernel<2>, mx, mw, args) != cudaSuccess) return 5;
+    const cudaError_t e = mode == 3 ? cudaLaunchKernelEx(&lc, projector_gemm_kernel<2, true>, mx, mw, args)
+                                    : cudaLaunchKernelEx(&lc, projector_gemm_kernel<2, false>, mx, mw, args);
+    if (e != cudaSuccess) return 5;
   }
   return cudaGetLastError() == cudaSuccess ? 0 : 5;
 }
