@@ -86,8 +86,8 @@ class Exec {
   // X . W^T for every local source rank (X: their token rows stacked in
   // ascending rank order, [rows x K]; W: [d_h x K]) on the tensor cores and
   // stores each output row straight into every destination row the plan maps
-  // it to; the source shards are never materialised. One GPU (all destinations
-  // resident) for now.
+  // it to, local or on a peer GPU (push over NVSwitch); the source shards are
+  // never materialised. Any GPU count, non-splice edges.
   // x_rows: rows of x (must equal the local source ranks' token rows).
   void forward_projected(int mb, const void* x, int64_t ldx, const void* w, int64_t ldw, int d_h, int K,
                          int64_t x_rows, void* stream);
