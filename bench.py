@@ -774,19 +774,21 @@ def main():
     fk, bk = kernel_bound(tm, "fwd", iso_fwd_ms, pk, N), kernel_bound(tm, "bwd", iso_bwd_ms, pk, N)
     dom_is_fwd = iso_fwd_ms >= iso_bwd_ms
     dom = fk if dom_is_fwd else bk
-    traffic = None
+    traffic, traffic_src = None, None
     prof = os.path.join(ROOT, "profiles", f"traffic_{cfg.name}_n{N}.json")
     if os.path.exists(prof):
         try:
             with open(prof) as f:
-                traffic = json.load(f).get("fwd" if dom_is_fwd else "bwd")
+                tj = json.load(f)
+            traffic = tj.get("fwd" if dom_is_fwd else "bwd")
+            traffic_src = tj.get("source", f"profiles/traffic_{cfg.name}_n{N}.json (ncu --set full, per launch)")
         except Exception:
             traffic = None
     tstar_step = fk["tstar_ms"] + bk["tstar_ms"]
     roofline = {
-        "bound": dom["bound"], "kernel": copy_kernel_name(args) if dom_is_fwd else reduce_kernel_name(cfg),
+        "bound": dom["bound"], "kernel": copy_kernel_name(args) if dom_is_fwd else reduce_kernel_name(cfg, tm),
         "achieved": dom["achieved_gbs"], "peak": dom["peak_gbs"], "unit": "GB/s", "frac": dom["frac"],
-        "traffic": traffic,
+        "traffic": traffic, "traffic_source": traffic_src,
         "peak_source": pk["src"] if dom["bound"] == "hbm" else "measured peer copy 770 GB/s (B200_PROFILING.md)",
         "per_kernel": {"fwd": fk, "bwd": bk,
                        "timing": "each op alone replayed back to back as a CUDA graph (steady state incl. "
@@ -1132,9 +1134,13 @@ def copy_kernel_name(args):
     return "copy_segments_tma_kernel" if args.partition in (0, 4) else "copy_segments_kernel"
 
 
-def reduce_kernel_name(cfg):
+def reduce_kernel_name(cfg, tm=None):
+    """The gradient-return kernel that runs: the streaming variant when the launch
+    has remote chunks (some GPU pulls terms over NVLink), else the per-chunk one."""
     tn = {"bf16": "__nv_bfloat16", "fp16": "__half", "fp32": "float"}
-    return f"reduce_segments_kernel<{tn[cfg.grad_in]},{tn[cfg.grad_out]}>"
+    remote = tm is not None and any(tm["bwd_nvl"]) and os.environ.get("HB_RED_STREAM", "1") != "0"
+    k = "reduce_segments_stream_kernel" if remote else "reduce_segments_kernel"
+    return f"{k}<{tn[cfg.grad_in]},{tn[cfg.grad_out]}>"
 
 
 def paired_bound(tm, pk, N):

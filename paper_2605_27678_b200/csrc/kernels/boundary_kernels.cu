@@ -1013,7 +1013,7 @@ struct RedProducer {  // thread 0's state (shared memory keeps it out of the con
 };
 
 template <class TIn, class TOut, bool FAN>
-__global__ void __launch_bounds__(512, 2) reduce_stream_kernel(const ReduceSeg* __restrict__ segs, int nseg,
+__global__ void __launch_bounds__(512, 2) reduce_segments_stream_kernel(const ReduceSeg* __restrict__ segs, int nseg,
                                                             const void* const* __restrict__ terms, Partition part,
                                                             float beta, SyncArgs sync) {
   constexpr int S = red_stages<TIn>();
@@ -1298,7 +1298,7 @@ static int red_stream_smem() {
   int dev = 0;
   cudaGetDevice(&dev);
   once(dev, [] {
-    cudaFuncSetAttribute(reduce_stream_kernel<TIn, TOut, FAN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(reduce_segments_stream_kernel<TIn, TOut, FAN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          kRedRingBytes);
   });
   return static_cast<int>(kRedRingBytes);
@@ -1338,7 +1338,7 @@ static void launch_reduce_f(const ReduceSeg* segs, int nseg, const void* const* 
     // remote chunks to stage: the streaming ring (a launch with local chunks only
     // measured 3-7% faster in the per-chunk kernel at N=1, which skips the
     // per-item slot bookkeeping)
-    launch_pdl(reduce_stream_kernel<TIn, TOut, FAN>, grid, block, red_stream_smem<TIn, TOut, FAN>(), st, segs, nseg,
+    launch_pdl(reduce_segments_stream_kernel<TIn, TOut, FAN>, grid, block, red_stream_smem<TIn, TOut, FAN>(), st, segs, nseg,
                terms, part, beta, sync);
   else if (part.mode == kPartDynamic)
     launch_pdl(reduce_segments_kernel<TIn, TOut, kPartDynamic, FAN>, grid, block,
