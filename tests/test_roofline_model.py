@@ -94,3 +94,41 @@ def test_reference_arm_line_contract():
     assert line["e2e"] == {"value": line["value"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
     cb = line["cpu_baseline"]
     assert cb["kind"] == "port" and cb["cores"] >= 1 and cb["value"] == line["value"] and cb["sample"]
+
+
+def test_nvlink_egress_balances_ingress():
+    """Every byte one GPU pulls over NVLink is served by another: total egress
+    equals total ingress, per direction, for every config at 2, 4 and 8 GPUs."""
+    for name in ("c2", "c3", "c4", "c5"):
+        for n in (2, 4, 8):
+            t = bench.traffic_model(configs.get(name), n)
+            for kind in ("fwd", "bwd"):
+                assert sum(t[kind + "_nvl"]) == sum(t[kind + "_nvl_out"])
+
+
+def test_paired_bound_is_the_shared_resource_bound():
+    """A 1F1B-paired step shares each GPU's HBM and links between the two ops:
+    its bound is max over GPUs of max(HBM sum, NVLink sum), never more than the
+    serial sum of the two kernels' bounds and never less than either of them."""
+    for name in ("c2", "c3", "c4"):
+        for n in (1, 4, 8):
+            t = bench.traffic_model(configs.get(name), n)
+            paired, crit = bench.paired_bound(t, PK, n)
+            f = bench.kernel_bound(t, "fwd", 1.0, PK, n)["tstar_ms"]
+            b = bench.kernel_bound(t, "bwd", 1.0, PK, n)["tstar_ms"]
+            assert max(f, b) * (1 - 1e-3) <= paired <= (f + b) * (1 + 1e-3)  # (kernel_bound rounds to 0.1 us)
+            assert crit is not None and crit[1] in ("hbm", "nvlink")
+    # one GPU: everything is HBM, so pairing cannot beat the serial sum
+    t = bench.traffic_model(configs.get("c2"), 1)
+    paired, _ = bench.paired_bound(t, PK, 1)
+    f = bench.kernel_bound(t, "fwd", 1.0, PK, 1)["tstar_ms"]
+    b = bench.kernel_bound(t, "bwd", 1.0, PK, 1)["tstar_ms"]
+    assert paired == pytest.approx(f + b, rel=1e-3)
+
+
+def test_reduce_kernel_label_follows_the_kernel_that_runs(monkeypatch):
+    cfg = configs.get("c4")
+    assert bench.reduce_kernel_name(cfg, bench.traffic_model(cfg, 1)).startswith("reduce_segments_kernel<")
+    assert bench.reduce_kernel_name(cfg, bench.traffic_model(cfg, 4)).startswith("reduce_segments_stream_kernel<")
+    monkeypatch.setenv("HB_RED_STREAM", "0")
+    assert bench.reduce_kernel_name(cfg, bench.traffic_model(cfg, 4)).startswith("reduce_segments_kernel<")
