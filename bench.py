@@ -58,11 +58,11 @@ def parse():
     ap.add_argument("--graph-per-step", action="store_true",
                     help="timed loop: one graph launch per step instead of one per cycle of buffer sets")
     ap.add_argument("--no-overlap", action="store_true", help="skip the boundary || PP-P2P overlap leg (C5)")
-    ap.add_argument("--matrix", default="c2,c3,c4,c5",
+    ap.add_argument("--matrix", default="c2,c3,c4,c4ip,c5",
                     help="configs also measured (short) in the same run, so every N of the driver's scaling "
                          "run records the fan-in / fan-out / CP-splice / non-colocated step ('' = none)")
     ap.add_argument("--matrix-steps", type=int, default=200)
-    ap.add_argument("--paired", default="c2,c3,c4",
+    ap.add_argument("--paired", default="c2,c3,c4,c4ip",
                     help="configs also measured as 1F1B-paired steps (fwd of microbatch k+1 concurrent with bwd "
                          "of microbatch k, hb_exec_graph_capture what=4) ('' = none)")
     ap.add_argument("--no-runtime", action="store_true",
@@ -79,16 +79,18 @@ def parse():
 
 
 def payload_bytes(cfg):
-    """Algorithmic boundary payload per step: destination shards materialised
-    (fwd, act dtype) + gradients returned to source owners (bwd, grad_in dtype),
-    summed over all logical ranks. Identical for every implementation."""
+    """Algorithmic boundary payload per step: destination elements the boundary
+    writes (fwd, act dtype; every element of the destination shards, or only the
+    vision rows of an in-place splice) + gradients returned to source owners
+    (bwd, grad_in dtype), summed over all logical ranks. Identical for every
+    implementation."""
     from paper_2605_27678_b200 import bridge as hbb
 
     plan = hbb.plan_bridge(cfg.edge())
     sp = make_splice(cfg)
-    fwd = bwd = 0
+    fwd = sum(seg[6] for seg in hbb.index_forward(plan, sp)) * DT_SIZE[cfg.act]
+    bwd = 0
     for r in range(plan.world):
-        fwd += hbb.buffer_elems(plan, r, hbb.SLOT_DST_ACT, sp) * DT_SIZE[cfg.act]
         bwd += hbb.buffer_elems(plan, r, hbb.SLOT_SRC_GRAD, sp) * DT_SIZE[cfg.grad_in]
     return fwd, bwd
 
@@ -320,6 +322,15 @@ def check_parity(rt, cfg, plan, sp, r2g, rank, N, dev, stream, barrier, run_step
         b = rt.buffer(r, hbb.SLOT_SRC_GRAD, buffer_set)
         if b is not None:
             prev[r] = b.float().clone()
+    # an in-place splice writes only the vision rows: the rest of each slice
+    # (the caller's text rows) must come out of the step unchanged
+    in_place = sp is not None and sp.text_mode == hbb.TEXT_INPLACE
+    prev_dst = {}
+    if in_place:
+        for r in local:
+            b = rt.buffer(r, hbb.SLOT_DST_ACT, buffer_set)
+            if b is not None:
+                prev_dst[r] = b.clone()
     barrier()
     run_step(buffer_set)
     stream.synchronize()
@@ -339,8 +350,8 @@ def check_parity(rt, cfg, plan, sp, r2g, rank, N, dev, stream, barrier, run_step
     for r in local:
         out = rt.buffer(r, hbb.SLOT_DST_ACT, buffer_set)
         if out is not None:
-            exp, cov = P.expected_forward(fwd_map, r, out.numel(), regen)
-            covered_ok &= cov == out.numel()
+            exp, cov = P.expected_forward(fwd_map, r, out.numel(), regen, base=prev_dst.get(r))
+            covered_ok &= in_place or cov == out.numel()
             ib = torch.int16 if out.element_size() == 2 else torch.int32
             fwd_ok &= exp is not None and bool(torch.equal(out.view(ib), exp.to(out.dtype).view(ib)))
             checked_fwd.append(r)
@@ -363,7 +374,7 @@ def check_parity(rt, cfg, plan, sp, r2g, rank, N, dev, stream, barrier, run_step
     f = flags.tolist()
     res = {"pass": f[0] == 0 and f[1] == 0 and f[3] <= 1e-6, "fwd_bitexact": f[0] == 0,
            "fwd_fully_covered": f[1] == 0, "bwd_bitexact": f[2] == 0, "bwd_max_rel": f[3], "bwd_tolerance": 1e-6,
-           "beta": cfg.beta, "buffer_set": buffer_set,
+           "beta": cfg.beta, "buffer_set": buffer_set, "in_place_splice": in_place,
            "checked_ranks": {"fwd": sorted(x for g in gathered for x in g[0]),
                              "bwd": sorted(x for g in gathered for x in g[1])},
            "ranks_checked_on": "each GPU checks its resident ranks; flags max-reduced over all GPUs",

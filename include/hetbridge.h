@@ -51,6 +51,9 @@ extern "C" {
 /* splice text numbering */
 #define HB_TEXT_FULL 0  /* text buffer row = global text index (-1-code)    */
 #define HB_TEXT_SLICE 1 /* text buffer row = k-th text position of the slice */
+#define HB_TEXT_INPLACE 2 /* no text buffer: the caller wrote the text rows into the
+                           * destination slice; only vision rows are written (the
+                           * masked scatter of VLM input embeddings)            */
 
 typedef struct hb_plan hb_plan;
 typedef struct hb_splice hb_splice;

@@ -22,7 +22,7 @@ from ._lib import HetBridgeError, check, lib
 from .grid import BatchInterval, BoundaryEdge, ModuleLayout, Placement, partition_batch
 
 SLOT_SRC_ACT, SLOT_DST_ACT, SLOT_DST_GRAD, SLOT_SRC_GRAD, SLOT_TEXT = range(5)
-TEXT_FULL, TEXT_SLICE = 0, 1
+TEXT_FULL, TEXT_SLICE, TEXT_INPLACE = 0, 1, 2
 HB_BF16, HB_FP16, HB_FP32, HB_FP64 = range(4)
 
 

@@ -79,6 +79,13 @@ def get(name: str, scale: int = 1) -> BoundaryConfig:
                               ModuleLayout("vit", dp=8), ModuleLayout("llm", tp=2, cp=4), 16, tokens, h(4096),
                               splice={"Q": 1, "S": S, "codes": codes, "text_mode": 1},
                               extra={"perm": perm.tolist()})
+    if name == "c4ip":  # C4 with the in-place splice: the LLM's embedding layer wrote the text rows
+        base = get("c4", scale)
+        base.name = "c4ip"
+        base.description = ("CP splice in place vit{dp8} -> llm{tp2,cp4}, S=32768, 16 img x 576 scattered into "
+                            "the LLM's input embeddings at placeholders")
+        base.splice = dict(base.splice, text_mode=2)
+        return base
     if name == "c5":
         return BoundaryConfig("c5", "non-colocated vit{dp2}@0-1 -> llm{tp2,pp3}@2-7, bf16 h4096, 16 img x 576",
                               ModuleLayout("vit", dp=2), ModuleLayout("llm", tp=2, pp=3, rank_offset=2), 16,

@@ -302,7 +302,7 @@ int hb_splice_create(int Q, int S, int d_h, int S_v, int text_mode, const int* c
     need(out, "out");
     need(codes, "codes");
     if (Q < 1 || S < 1) hb::raise(hb::ErrorCode::InvalidArgument, "Q and S must be >= 1");
-    if (text_mode != HB_TEXT_FULL && text_mode != HB_TEXT_SLICE)
+    if (text_mode != HB_TEXT_FULL && text_mode != HB_TEXT_SLICE && text_mode != HB_TEXT_INPLACE)
       hb::raise(hb::ErrorCode::InvalidArgument, "unknown text mode");
     auto s = std::make_unique<hb_splice>();
     s->spec.Q = Q;

@@ -240,7 +240,7 @@ IndexMap build_index_map(const BridgePlan& p, const SpliceSpec* sp, bool balance
           const int jl = code / sp->S_v, t = code % sp->S_v;
           const RowRef o = forward_origin(p, r, p.dest_intervals[d].start + jl);
           push_copy(m.fwd, {{o.rank, kSrcAct, o.row * W + t * dh}, dst, dh});
-        } else {
+        } else if (sp->text_mode != TextMode::InPlace) {
           const int64_t row = sp->text_mode == TextMode::Slice ? text_k++ : (-1 - int64_t{code});
           text_max = std::max(text_max, row);
           push_copy(m.fwd, {{r, kText, row * dh}, dst, dh});

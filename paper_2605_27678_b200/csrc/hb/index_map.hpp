@@ -53,7 +53,14 @@ struct ReduceSeg {
   std::vector<Ref> terms;  // each covers n contiguous elements from term.off; summed in order
 };
 
-enum class TextMode { Full = 0, Slice = 1 };
+// Text rows of a CP slice: Full / Slice — the boundary copies them from the
+// TEXT buffer (indexed by global text row / by position within the slice);
+// InPlace — the caller's embedding layer already wrote them into the
+// destination slice (DST_ACT bound to the LLM's input-embedding tensor), and
+// the boundary writes only the vision rows at the placeholder positions (the
+// masked scatter `inputs_embeds[image_mask] = image_features` of VLM
+// implementations): no TEXT buffer, no text bytes through the boundary.
+enum class TextMode { Full = 0, Slice = 1, InPlace = 2 };
 
 struct SpliceSpec {
   int Q = 0;        // sequences per destination shard

@@ -52,6 +52,8 @@ Exec::Exec(const bridge::BridgePlan& plan, const index::SpliceSpec* splice, int 
   splice_d_h_ = splice ? splice->d_h : 0;
   if (cfg.text_embedding && !splice)
     raise(ErrorCode::InvalidArgument, "text_embedding needs a splice edge (text rows to gather)");
+  if (cfg.text_embedding && splice->text_mode == index::TextMode::InPlace)
+    raise(ErrorCode::InvalidArgument, "text_embedding gathers text rows; an in-place splice has none to gather");
   if (static_cast<int>(rank_to_gpu_.size()) < map_.world)
     raise(ErrorCode::InvalidArgument, "rank_to_gpu must cover every logical rank of the edge");
   for (int r = 0; r < map_.world; ++r)

@@ -97,14 +97,17 @@ def parity_compare(distributed: dict, reference: dict, distributed_loss: float =
 # ---------------------------------------------------------------------------- restatement
 
 
-def expected_forward(fwd_map, rank: int, numel: int, src_of):
+def expected_forward(fwd_map, rank: int, numel: int, src_of, base=None):
     """Destination buffer of ``rank`` the forward must produce.
 
     fwd_map: ``bridge.index_forward`` tuples; src_of(rank, slot) -> 1-D tensor of
-    that source buffer (any device). Returns (expected, covered elements)."""
+    that source buffer (any device). base: the buffer before the op, for maps
+    that write only part of it (an in-place splice leaves the text rows the
+    caller wrote); elements outside the map must keep it. Returns (expected,
+    covered elements)."""
     import torch
 
-    out = None
+    out = None if base is None else base.clone()
     covered = 0
     for (sr, ss, so, dr, ds, do, n) in fwd_map:
         if dr != rank:

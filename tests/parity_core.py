@@ -68,6 +68,19 @@ def group_parity(cfg, drv, steps: int = 3, strict: bool = False):
             sl = codes.reshape(-1, sp["S"])[:, c * L:(c + 1) * L].reshape(-1)
             b.copy_(torch.from_numpy(text[[-1 - int(x) for x in sl if x < 0]]).to(b.device).to(b.dtype).reshape(b.shape))
     ref, _, _ = O.bridge_forward(src, dst, B, W, shards)
+    if sp and sp.get("text_mode") == hbb.TEXT_INPLACE:
+        # the caller's embedding layer already wrote the text rows into the
+        # slice; vision positions hold garbage (NaN) the boundary must replace
+        for r in drv.local:
+            if r not in ref:
+                continue
+            c = dst.coord(r)[1]
+            full = O.splice_forward(sp["codes"], sp["Q"], sp["S"], cfg.hidden, c * L, L,
+                                    np.zeros_like(ref[r]).reshape(-1, cfg.hidden), text)
+            sl = np.asarray(sp["codes"]).reshape(-1, sp["S"])[:, c * L:(c + 1) * L].reshape(-1)
+            full[sl >= 0] = np.nan
+            b = drv.buf(r, hbb.SLOT_DST_ACT)
+            b.copy_(torch.from_numpy(full.reshape(-1)).to(b.device).to(b.dtype).reshape(b.shape))
     ok = True
     worst = 0.0
     acc = {}

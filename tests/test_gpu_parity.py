@@ -81,6 +81,18 @@ def run_case(cfg, seed=0, beta=0.0, perturb=True, partition=0):
                 rows = T[: buf.numel() // cfg.hidden]
             buf.copy_(torch.from_numpy(rows.reshape(-1)).to(DEV).to(buf.dtype))
             text_np[r] = torch.from_numpy(T).to(buf.dtype).double().numpy()
+        if cfg.splice["text_mode"] == hbb.TEXT_INPLACE:
+            # in place: the LLM's embedding layer wrote the text rows into the slice;
+            # the vision positions hold NaN until the boundary scatters into them
+            for r in dst.stage_ranks(0):
+                t, c, p, d = dst.coord(r)
+                out = rt.buffer(r, hbb.SLOT_DST_ACT)
+                text_np[r] = torch.from_numpy(T).to(out.dtype).double().numpy()
+                full = O.splice_forward(codes, cfg.splice["Q"], cfg.splice["S"], cfg.hidden, c * L, L,
+                                        np.zeros((DI[d][1] * cfg.tokens, cfg.hidden)), text_np[r])
+                sl = codes.reshape(-1, cfg.splice["S"])[:, c * L:(c + 1) * L].reshape(-1)
+                full[sl >= 0] = np.nan
+                out.copy_(torch.from_numpy(full.reshape(-1)).to(DEV).to(out.dtype))
     rt.forward(0)
     torch.cuda.synchronize()
     ref, _, _ = O.bridge_forward(src, dst, B, W, shards)
@@ -142,7 +154,7 @@ def run_case(cfg, seed=0, beta=0.0, perturb=True, partition=0):
     rt.close()
 
 
-@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c4ip", "c5"])
 @pytest.mark.parametrize("beta", [0.0, 1.0])
 def test_configs_scaled_vs_oracle(name, beta):
     run_case(configs.get(name, scale=64), seed=sum(map(ord, name)), beta=beta)

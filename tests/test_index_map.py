@@ -252,3 +252,37 @@ def test_random_placeholder_tables(seed, text_mode):
     n_vis = (B // d.dp) * S_v
     codes = random_codes(rng, n_vis, Q, S)
     splice_case(s, d, B, S_v, d_h, Q, S, codes, text_mode, seed=seed)
+
+
+@pytest.mark.parametrize("name", ["c4", "c4w4"])
+def test_in_place_splice_writes_only_vision_rows(name):
+    """HB_TEXT_INPLACE: the forward map is the copy splice's map without its text
+    runs (the caller's embedding layer wrote those rows), the TEXT buffer is
+    gone, and the backward map is unchanged."""
+    base = configs.get(name, scale=64)
+    ip = configs.get(name, scale=64)
+    ip.splice = dict(ip.splice, text_mode=hbb.TEXT_INPLACE)
+    plan = hbb.plan_bridge(base.edge())
+
+    def spec(cfg):
+        s = cfg.splice
+        return hbb.SpliceSpec(s["Q"], s["S"], cfg.hidden, cfg.tokens, s["codes"], s["text_mode"])
+
+    f_copy, f_ip = hbb.index_forward(plan, spec(base)), hbb.index_forward(plan, spec(ip))
+    assert all(s[1] != hbb.SLOT_TEXT for s in f_ip)
+    # same vision placements (runs may coalesce differently once text runs are gone)
+    def cover(fm):
+        out = set()
+        for (sr, ss, so, dr, ds, do, n) in fm:
+            if ss == hbb.SLOT_TEXT:
+                continue
+            for k in range(0, n, base.hidden):
+                out.add((sr, ss, so + k, dr, ds, do + k))
+        return out
+    assert cover(f_ip) == cover(f_copy)
+    assert any(s[1] == hbb.SLOT_TEXT for s in f_copy)
+    for r in range(plan.world):
+        assert hbb.buffer_elems(plan, r, hbb.SLOT_TEXT, spec(ip)) == 0
+        assert hbb.buffer_elems(plan, r, hbb.SLOT_DST_ACT, spec(ip)) == hbb.buffer_elems(plan, r, hbb.SLOT_DST_ACT,
+                                                                                         spec(base))
+    assert hbb.index_backward(plan, spec(ip)) == hbb.index_backward(plan, spec(base))

@@ -21,7 +21,7 @@ from paper_2605_27678_b200 import configs  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 
-CONFIGS = ["c1", "c2", "c3", "c4", "c5", "c3p", "appc", "c2x4", "c3x4", "c4w4"]
+CONFIGS = ["c1", "c2", "c3", "c4", "c4ip", "c5", "c3p", "appc", "c2x4", "c3x4", "c4w4"]
 
 
 def _group(name, n, devices, **kw):

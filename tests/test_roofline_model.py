@@ -132,3 +132,24 @@ def test_reduce_kernel_label_follows_the_kernel_that_runs(monkeypatch):
     assert bench.reduce_kernel_name(cfg, bench.traffic_model(cfg, 4)).startswith("reduce_segments_stream_kernel<")
     monkeypatch.setenv("HB_RED_STREAM", "0")
     assert bench.reduce_kernel_name(cfg, bench.traffic_model(cfg, 4)).startswith("reduce_segments_kernel<")
+
+
+def test_payload_counts_what_the_boundary_writes():
+    """The forward payload is the destination elements the boundary writes: the
+    whole destination shards for copy splices (= DST_ACT sizes), only the vision
+    rows for the in-place splice (the LLM's embedding layer wrote the text)."""
+    from paper_2605_27678_b200 import bridge as hbb
+
+    for name in ("c1", "c2", "c3", "c4", "c5"):
+        cfg = configs.get(name)
+        plan = hbb.plan_bridge(cfg.edge())
+        sp = bench.make_splice(cfg)
+        dst = sum(hbb.buffer_elems(plan, r, hbb.SLOT_DST_ACT, sp) for r in range(plan.world))
+        assert bench.payload_bytes(cfg)[0] == dst * bench.DT_SIZE[cfg.act]
+    c4, ip = configs.get("c4"), configs.get("c4ip")
+    vision = 16 * 576 * 4096 * 2 * 2  # 16 images x 576 tokens x d_h, bf16, written into both tp replicas
+    assert bench.payload_bytes(ip)[0] == vision
+    assert bench.payload_bytes(ip)[1] == bench.payload_bytes(c4)[1]
+    t, ti = bench.traffic_model(c4, 8), bench.traffic_model(ip, 8)
+    assert all(a < b for a, b in zip(ti["fwd_hbm"], t["fwd_hbm"]))
+    assert ti["fwd_nvl"] == t["fwd_nvl"]

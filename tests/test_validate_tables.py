@@ -21,7 +21,7 @@ from parity_core import make_splice  # noqa: E402
 from paper_2605_27678_b200 import bridge as hbb  # noqa: E402
 from paper_2605_27678_b200 import configs  # noqa: E402
 
-ALL = ["c1", "c2", "c3", "c4", "c5", "c3p", "appc", "c2x4", "c3x4", "c4w4", "c5w4"]
+ALL = ["c1", "c2", "c3", "c4", "c4ip", "c5", "c3p", "appc", "c2x4", "c3x4", "c4w4", "c5w4"]
 DT = {"bf16": torch.bfloat16, "fp16": torch.float16, "fp32": torch.float32}
 
 
