@@ -62,9 +62,10 @@ def parse():
                     help="configs also measured (short) in the same run, so every N of the driver's scaling "
                          "run records the fan-in / fan-out / CP-splice / non-colocated step ('' = none)")
     ap.add_argument("--matrix-steps", type=int, default=200)
-    ap.add_argument("--paired", default="c2,c3,c4,c4ip",
+    ap.add_argument("--paired", default="c2,c4,c4ip",
                     help="configs also measured as 1F1B-paired steps (fwd of microbatch k+1 concurrent with bwd "
-                         "of microbatch k, hb_exec_graph_capture what=4) ('' = none)")
+                         "of microbatch k, hb_exec_graph_capture what=4) at N > 1 ('' = none). C3 is left out by "
+                         "default: its fan-out gradient return needs more than the one CTA per SM pairing leaves it")
     ap.add_argument("--no-runtime", action="store_true",
                     help="skip the host-runtime leg (a24 + f2: 1F1B dispatch table with NC || PP P2P, N = 4, 6, 8)")
     ap.add_argument("--ref-procs", type=int, default=0, help="reference arm: worker processes (0 = auto)")
@@ -911,7 +912,8 @@ def main():
     done("config_matrix", matrix)
 
     paired = None
-    names_p = [c for c in args.paired.split(",") if c]
+    # at N=1 everything is HBM: pairing has nothing to overlap (measured slower, profiles/r02/bench_n1_paired.json)
+    names_p = [c for c in args.paired.split(",") if c] if N > 1 else []
     if names_p and args.scale == 1:
         if rt is not None:
             rt.close()
