@@ -823,6 +823,9 @@ void Exec::prepare_bwd() {
   build_partition(w0s, ns, rem, lb, rb, bgrid, mode, unit, &bwd_part_, runit);
   bwd_part_.ring = static_cast<int>(env_u64("HB_RED_RING", 1));  // A/B knob: 0 = LDG for remote chunks too
   bwd_part_.fan = fan;
+  // HB_RED_STAGE_LOCAL=1: the streaming kernel stages local single-term chunks
+  // through its TMA ring as well (A/B knob; off: local chunks are reduced by LDG)
+  bwd_part_.stage_local = static_cast<int>(env_u64("HB_RED_STAGE_LOCAL", 0));
   dirty_bwd_ = false;
 }
 

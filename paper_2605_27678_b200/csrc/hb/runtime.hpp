@@ -211,9 +211,10 @@ class Exec {
     int ring = 1;
     int prefetch_other = 1;
     int fan = 0;
+    int stage_local = 0;
     dev::Partition dev() const {
       return {first_seg, per_cta, mode, total_chunks, chunk, chunks, rtotal_chunks, rchunks, rchunk, remote_ctas,
-              lstatic, rstatic, ring, prefetch_other, fan};
+              lstatic, rstatic, ring, prefetch_other, fan, stage_local};
     }
   };
   DevPartition fwd_part_, bwd_part_;

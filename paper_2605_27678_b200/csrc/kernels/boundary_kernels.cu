@@ -1090,7 +1090,7 @@ __global__ void __launch_bounds__(512, 2) reduce_segments_stream_kernel(const Re
       pr.seg = t.x;
       pr.pa = pr.pmid = a;
       pr.pb = b;
-      if (rq && sg.nterms == 1 && part.ring) {
+      if ((rq || part.stage_local) && sg.nterms == 1 && part.ring) {
         uint64_t al = reinterpret_cast<uint64_t>(static_cast<const TIn*>(terms[sg.term0]) + a);
         if constexpr (FAN) {
           for (int d = 0; d < sg.ndst; ++d) al |= reinterpret_cast<uint64_t>(static_cast<const TOut*>(terms[sg.dst0 + d]) + a);
@@ -1334,7 +1334,7 @@ static void launch_reduce_f(const ReduceSeg* segs, int nseg, const void* const* 
   if (part.mode == kPartInterleaved)
     launch_pdl(reduce_segments_kernel<TIn, TOut, kPartInterleaved, FAN>, grid, block, 0, st, segs, nseg, terms, part,
                beta, sync);
-  else if (part.mode == kPartDynamic && red_stream() && part.ring && part.rtotal_chunks)
+  else if (part.mode == kPartDynamic && red_stream() && part.ring && (part.rtotal_chunks || part.stage_local))
     // remote chunks to stage: the streaming ring (a launch with local chunks only
     // measured 3-7% faster in the per-chunk kernel at N=1, which skips the
     // per-item slot bookkeeping)

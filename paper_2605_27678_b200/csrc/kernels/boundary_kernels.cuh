@@ -94,6 +94,7 @@ struct Partition {
   int ring;                  // reduce: stage remote single-term chunks through the TMA ring
   int prefetch_other;        // start the other queue's first claim near the current queue's end
   int fan;                   // reduce: some segment has ndst > 1 (fan-out kernel variant)
+  int stage_local;           // reduce (streaming kernel): stage local single-term chunks through the ring too
 };
 
 // Cross-GPU epoch barrier over peer-mapped flag words. Every GPU of an exec
