@@ -1028,10 +1028,10 @@ def run_host_runtime(name, rank, world, dev, steps=5):
             errors.append(f"{what}: {type(exc).__name__}: {exc}"[:300])
             return default
 
-    # 8 microbatches (warm-up and drain, where boundary ops sit on the critical
+    # 16 microbatches (warm-up and drain, where boundary ops sit on the critical
     # path, are a smaller share of the step); boundary kernels capped at one CTA
     # per SM so the PP stream's NCCL kernels always find room beside them
-    nmb = int(os.environ.get("HB_RT_NMB", "8"))
+    nmb = int(os.environ.get("HB_RT_NMB", "16"))
     cap = int(os.environ.get("HB_RT_CAP", str(torch.cuda.get_device_properties(dev).multi_processor_count)))
     rt = attempt("create", lambda: R.HostRuntime(mods, edges, B, W, nmb=nmb, max_ctas=cap, pp_bytes=ppb,
                                                   skip=R.SKIP_COMPUTE, timeout_s=5.0))
