@@ -225,6 +225,16 @@ int hb_exec_backward(hb_exec* x, int mb, float beta, void* cuda_stream);
 int hb_exec_seed_forward_record(hb_exec* x, int mb); /* bridge.hpp:165 */
 /* Embedding table [vocab x d_h] (activation dtype, device memory of this GPU). */
 int hb_exec_set_text_embedding(hb_exec* x, const void* table, long long vocab);
+/* Vocab-parallel table (Megatron's VocabParallelEmbedding, the LLM side of
+ * tinymodel.hpp:97-101): resident logical rank `rank` holds rows
+ * [vocab_begin, vocab_begin + rows) of the [vocab x d_h] table at `shard`
+ * (activation dtype, this GPU). The shards of a destination TP group are
+ * equal-sized and ordered by tp index (vocab_begin = tp_idx * rows). The splice
+ * then gathers each text row from the rank owning its id, on this GPU or a
+ * peer's over NVSwitch, instead of a masked lookup and a TP all-reduce. Peers'
+ * shards arrive with hb_exec_export_bindings / hb_exec_import_bindings. */
+int hb_exec_set_text_embedding_shard(hb_exec* x, int rank, const void* shard, long long vocab_begin, long long rows,
+                                     long long vocab);
 /* CUDA graph of one buffer set's boundary ops; what: 0 forward, 1 forward +
  * backward(beta), 2 backward(beta), 3 forward + backward(beta) of every buffer
  * set in order (one launch replays mb_slots steps; mb_slot ignored), 4 the

@@ -34,7 +34,7 @@ EXPORTS = [
     "hb_exec_open_peers", "hb_exec_open_peers_local", "hb_exec_buffer", "hb_exec_bind", "hb_exec_bind_strided",
     "hb_exec_export_bindings", "hb_exec_import_bindings", "hb_exec_forward", "hb_exec_backward",
     "hb_exec_seed_forward_record", "hb_exec_status", "hb_exec_stats", "hb_exec_graph_capture", "hb_projector_gemm",
-    "hb_exec_forward_projected", "hb_exec_set_text_embedding",
+    "hb_exec_forward_projected", "hb_exec_set_text_embedding", "hb_exec_set_text_embedding_shard",
     "hb_exec_graph_launch", "hb_exec_trace", "hb_exec_validate",
     "hb_stage_graph_create", "hb_stage_graph_destroy", "hb_stage_graph_nodes", "hb_stage_graph_edges",
     "hb_dispatch_generate", "hb_dispatch_validate", "hb_dispatch_render", "hb_dispatch_nc_order",
@@ -146,6 +146,7 @@ def _declare(L):
         "hb_projector_gemm": (I, [V, LL, V, LL, V, I, I, I, I, V]),
         "hb_exec_forward_projected": (I, [V, I, V, LL, LL, V, LL, I, I, V]),
         "hb_exec_set_text_embedding": (I, [V, V, LL]),
+        "hb_exec_set_text_embedding_shard": (I, [V, I, V, LL, LL, LL]),
         "hb_exec_trace": (I, [V, I, V, I, P(I), P(I)]),
         "hb_exec_validate": (I, [V, P(LL)]),
         "hb_stage_graph_create": (I, [P(Layout), I, P(I), P(I), I, P(V)]),

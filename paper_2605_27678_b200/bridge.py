@@ -303,6 +303,20 @@ class BridgeRuntime:
         check(lib().hb_exec_set_text_embedding(self._h, ctypes.c_void_p(table.data_ptr()), table.shape[0]))
         self._keep["embedding"] = table
 
+    def set_text_embedding_shard(self, rank: int, shard, vocab_begin: int, vocab: int):
+        """Vocab-parallel table: resident ``rank`` holds rows [vocab_begin,
+        vocab_begin + shard.shape[0]) of the [vocab, d_h] embedding table
+        (Megatron's VocabParallelEmbedding; shards of a TP group equal-sized, in
+        tp order). The splice gathers each text row from the rank owning its id,
+        locally or from a peer GPU. In a multi-process group call
+        :meth:`exchange_bindings` on every process afterwards (collective)."""
+        if not shard.is_cuda or not shard.is_contiguous() or shard.dtype != self.act_dtype or shard.dim() != 2:
+            raise HetBridgeError(24, "embedding shard must be a contiguous 2-D CUDA tensor of the activation dtype")
+        check(lib().hb_exec_set_text_embedding_shard(self._h, rank, ctypes.c_void_p(shard.data_ptr()), vocab_begin,
+                                                     shard.shape[0], vocab))
+        self._keep[("embedding_shard", rank)] = shard
+        self._bind_dirty = True
+
     def buffer(self, rank: int, slot: int, mb_slot: int = 0):
         """Device tensor view (1-D, element dtype of the slot) of a resident rank's buffer."""
         import torch
@@ -538,6 +552,9 @@ class LocalGroup:
         self.runtime_of(rank).bind(rank, slot, tensor, mb_slot, row_stride)
         for rt in self.rts:
             rt.open_peers_local(self.rts)
+
+    def set_text_embedding_shard(self, rank: int, shard, vocab_begin: int, vocab: int):
+        self.runtime_of(rank).set_text_embedding_shard(rank, shard, vocab_begin, vocab)
 
     def forward(self, mb: int = 0):
         for rt, st in zip(self.rts, self.streams):

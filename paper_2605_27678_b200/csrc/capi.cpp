@@ -572,6 +572,14 @@ int hb_exec_validate(hb_exec* x, long long* checks) {
   });
 }
 
+int hb_exec_set_text_embedding_shard(hb_exec* x, int rank, const void* shard, long long vocab_begin, long long rows,
+                                     long long vocab) {
+  return guard([&] {
+    need(x, "exec");
+    x->x->set_text_embedding_shard(rank, shard, vocab_begin, rows, vocab);
+  });
+}
+
 int hb_exec_set_text_embedding(hb_exec* x, const void* table, long long vocab) {
   return guard([&] {
     need(x, "exec");

@@ -81,6 +81,7 @@ Exec::Exec(const bridge::BridgePlan& plan, const index::SpliceSpec* splice, int 
     region_bytes_ = std::max(region_bytes_, kPadBytes + off * cfg.mb_slots);
   }
   bound_.assign(map_.world * index::kNumSlots, std::vector<Binding>(cfg.mb_slots));
+  shard_.assign(map_.world, EmbedShard{});
   peer_bound_.assign(map_.world * index::kNumSlots, std::vector<Binding>(cfg.mb_slots));
   peer_exec_.assign(n_gpus_, nullptr);
 
@@ -147,6 +148,7 @@ Exec::~Exec() {
   cudaFree(local_base_);
   cudaFree(ctr_);
   cudaFree(trace_);
+  cudaFree(shard_dev_);
 }
 
 // Elements per row of a slot's buffer: a sample (W) for activations and
@@ -233,6 +235,11 @@ void Exec::build_work() {
       f.src = first.src;
       f.n = first.n;
       f.remote = !fwd_push_ && gpu_of(first.src.rank) != my_gpu_;
+      // a vocab-parallel gather reads the shards of the destination's TP group:
+      // behind the peer wait when any of them sits on another GPU
+      if (first.src.slot == index::kText && cfg_.text_embedding && sharded())
+        for (int m : grid::module_group(plan_.edge.dest, first.src.rank, grid::GroupKind::TP))
+          if (gpu_of(m) != my_gpu_) f.remote = true;
       for (size_t j = k; j < std::min(idx.size(), k + dev::kMaxFan); ++j) {
         const auto& d = fwd[idx[j]].dst;
         f.dsts.push_back(d);
@@ -422,6 +429,9 @@ struct BindRecord {  // one exported binding (fixed 96-byte record)
   unsigned char handle[64];
 };
 static_assert(sizeof(BindRecord) == 96, "record layout");
+// a vocab-parallel embedding shard travels as a record with this slot:
+// mb_slot = 0, pad = first vocab row, stride = rows
+constexpr int32_t kShardSlot = 1000;
 }  // namespace
 
 size_t Exec::export_bindings(void* out, size_t cap) const {
@@ -447,6 +457,22 @@ size_t Exec::export_bindings(void* out, size_t cap) const {
         recs.push_back(rec);
       }
   }
+  for (int r = 0; r < map_.world; ++r) {
+    if (gpu_of(r) != my_gpu_ || !shard_[r].ptr) continue;
+    if (shard_[r].begin > 0x7fffffffll) raise(ErrorCode::InvalidArgument, "vocab-parallel shard begins beyond 2^31");
+    BindRecord rec{};
+    rec.rank = r;
+    rec.slot = kShardSlot;
+    rec.pad = static_cast<int32_t>(shard_[r].begin);
+    size_t sz = 0;
+    void* base = allocation_base(const_cast<unsigned char*>(shard_[r].ptr), &sz);
+    rec.offset = shard_[r].ptr - static_cast<unsigned char*>(base);
+    rec.stride = shard_[r].rows;
+    cudaIpcMemHandle_t h;
+    ck(cudaIpcGetMemHandle(&h, base), "cudaIpcGetMemHandle(embedding shard)");
+    std::memcpy(rec.handle, &h, 64);
+    recs.push_back(rec);
+  }
   const size_t need = 8 + recs.size() * sizeof(BindRecord);
   if (out && cap >= need) {
     const uint64_t n = recs.size();
@@ -466,12 +492,29 @@ void Exec::import_bindings(int gpu, const void* blob, size_t len) {
   if (len < 8 + n * sizeof(BindRecord)) raise(ErrorCode::InvalidArgument, "binding blob truncated");
   // bindings of `gpu`'s ranks not in the blob revert to the peer region
   for (int r = 0; r < map_.world; ++r)
-    if (gpu_of(r) == gpu)
+    if (gpu_of(r) == gpu) {
       for (int s = 0; s < index::kNumSlots; ++s)
         for (auto& b : peer_bound_[r * index::kNumSlots + s]) b = {};
+      shard_[r] = {};
+    }
   for (uint64_t i = 0; i < n; ++i) {
     BindRecord rec;
     std::memcpy(&rec, static_cast<const unsigned char*>(blob) + 8 + i * sizeof(BindRecord), sizeof(rec));
+    if (rec.slot == kShardSlot) {  // a peer rank's vocab-parallel embedding shard
+      if (rec.rank < 0 || rec.rank >= map_.world || gpu_of(rec.rank) != gpu || rec.stride < 1)
+        raise(ErrorCode::InvalidArgument, "embedding shard record does not match this group's layout");
+      const std::string key(reinterpret_cast<const char*>(rec.handle), 64);
+      auto it = ipc_open_.find(key);
+      if (it == ipc_open_.end()) {
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, rec.handle, 64);
+        void* p = nullptr;
+        ck(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle(embedding shard)");
+        it = ipc_open_.emplace(key, static_cast<unsigned char*>(p)).first;
+      }
+      shard_[rec.rank] = {it->second + rec.offset, rec.pad, rec.stride};
+      continue;
+    }
     if (rec.rank < 0 || rec.rank >= map_.world || gpu_of(rec.rank) != gpu || rec.slot < 0 ||
         rec.slot >= index::kNumSlots || rec.mb_slot < 0 || rec.mb_slot >= cfg_.mb_slots)
       raise(ErrorCode::InvalidArgument, "binding record does not match this group's layout");
@@ -622,12 +665,42 @@ void Exec::upload_copies(int mb, uint64_t unit, std::vector<uint64_t>* w0s, std:
   uint64_t w = 0;
   w0s->clear();
   ns->clear();
+  // vocab-parallel gathers: each destination rank's TP-group shard bases, [world x tp]
+  const size_t tp_ = static_cast<size_t>(plan_.edge.dest.tp);
+  std::vector<const unsigned char*> shard_host;
+  if (cfg_.text_embedding && sharded()) {
+    shard_host.assign(static_cast<size_t>(map_.world) * tp_, nullptr);
+    if (!shard_dev_)
+      ck(cudaMalloc(reinterpret_cast<void**>(&shard_dev_), shard_host.size() * sizeof(void*)), "cudaMalloc(shards)");
+  }
   for (const auto& f : fwd_local_) {
     const bool gather = f.src.slot == index::kText && cfg_.text_embedding;
     const int es = dev::dtype_size(gather ? cfg_.act_dtype : slot_dtype(f.src.slot));
     const uint64_t nbytes = static_cast<uint64_t>(f.n) * es;
     dev::CopySeg c{};
-    if (gather) {  // rows table[ids[k]] for the run's text rows k
+    if (gather && sharded()) {  // rows of the destination's TP-group shards
+      const int r = f.src.rank;  // the TEXT ids belong to the destination rank
+      const auto grp = grid::module_group(plan_.edge.dest, r, grid::GroupKind::TP);
+      const int64_t rows = shard_of(grp[0]).rows;
+      for (size_t i = 0; i < grp.size(); ++i) {
+        const EmbedShard e = shard_of(grp[i]);
+        if (!e.ptr) raise(ErrorCode::InvalidArgument, "vocab-parallel embedding: no shard set for rank " +
+                                                          std::to_string(grp[i]) + " (peers: exchange bindings)");
+        if (e.rows != rows || e.begin != static_cast<int64_t>(i) * rows)
+          raise(ErrorCode::ShapeMismatch, "vocab-parallel embedding: shards of a TP group must be equal-sized and "
+                                          "ordered by tp index (begin = tp_idx * rows)");
+        shard_host[static_cast<size_t>(r) * tp_ + i] = e.ptr;
+        if (gpu_of(grp[i]) != my_gpu_) c.peers |= 1u << gpu_of(grp[i]);
+      }
+      if (rows * static_cast<int64_t>(grp.size()) < embed_vocab_)
+        raise(ErrorCode::ShapeMismatch, "vocab-parallel embedding: the TP group's shards do not cover the vocabulary");
+      c.src = shard_of(grp[0]).ptr;
+      c.shards = shard_dev_ + static_cast<size_t>(r) * tp_;
+      c.shard_rows = static_cast<uint32_t>(rows);
+      c.ids = reinterpret_cast<const int32_t*>(addr(f.src.rank, f.src.slot, mb, f.src.off / splice_d_h_, 4));
+      c.row_bytes = static_cast<uint32_t>(splice_d_h_ * es);
+      c.vocab = embed_vocab_;
+    } else if (gather) {  // rows table[ids[k]] for the run's text rows k
       if (!embed_table_) raise(ErrorCode::InvalidArgument, "text_embedding: call set_text_embedding first");
       c.src = embed_table_;
       c.ids = reinterpret_cast<const int32_t*>(addr(f.src.rank, f.src.slot, mb, f.src.off / splice_d_h_, 4));
@@ -651,6 +724,9 @@ void Exec::upload_copies(int mb, uint64_t unit, std::vector<uint64_t>* w0s, std:
     ns->push_back(nbytes);
     w = pad_to(w + nbytes, unit);
   }
+  if (!shard_host.empty())
+    ck(cudaMemcpy(shard_dev_, shard_host.data(), shard_host.size() * sizeof(void*), cudaMemcpyHostToDevice),
+       "upload(shards)");
   dev::CopySeg*& out = tables_[mb].copy;
   cudaFree(out);
   out = nullptr;
@@ -1060,6 +1136,36 @@ void Exec::set_text_embedding(const void* table, int64_t vocab) {
   embed_table_ = static_cast<const unsigned char*>(table);
   embed_vocab_ = vocab;
   mark_dirty();
+}
+
+void Exec::set_text_embedding_shard(int rank, const void* shard, int64_t begin, int64_t rows, int64_t vocab) {
+  if (!cfg_.text_embedding) raise(ErrorCode::InvalidArgument, "exec was created without text_embedding");
+  if (rank < 0 || rank >= map_.world || gpu_of(rank) != my_gpu_)
+    raise(ErrorCode::InvalidArgument, "a vocab-parallel shard belongs to a rank resident on this GPU");
+  if (!shard || rows < 1 || begin < 0 || vocab < 1 || rows > 0xffffffffll)
+    raise(ErrorCode::InvalidArgument, "vocab-parallel shard: non-null, 1 <= rows < 2^32, begin >= 0, vocab >= 1");
+  shard_[rank] = {static_cast<const unsigned char*>(shard), begin, rows};
+  embed_vocab_ = vocab;
+  work_dirty_ = true;  // gather runs may turn remote
+  mark_dirty();
+  for (Exec* p : peer_exec_)  // single-process groups read this shard directly
+    if (p && p != this) {
+      p->embed_vocab_ = vocab;
+      p->work_dirty_ = true;
+      p->mark_dirty();
+    }
+}
+
+Exec::EmbedShard Exec::shard_of(int rank) const {
+  const int g = gpu_of(rank);
+  if (g != my_gpu_ && peer_exec_[g]) return peer_exec_[g]->shard_[rank];
+  return shard_[rank];
+}
+
+bool Exec::sharded() const {
+  for (int r = 0; r < map_.world; ++r)
+    if (shard_of(r).ptr) return true;
+  return false;
 }
 
 int Exec::read_trace(int kind, unsigned long long* out, int max_ctas, int* grid) const {

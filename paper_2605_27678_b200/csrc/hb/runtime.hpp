@@ -96,6 +96,12 @@ class Exec {
   // Embedding table [vocab x d_h] (act dtype, on this GPU) the splice gathers
   // text rows from when cfg.text_embedding.
   void set_text_embedding(const void* table, int64_t vocab);
+  // Vocab-parallel table (Megatron's VocabParallelEmbedding): resident rank
+  // `rank` holds rows [begin, begin + rows) of the [vocab x d_h] table at
+  // `shard`. Shards of one TP group are equal-sized and ordered by tp index
+  // (begin = tp_idx * rows); the splice gathers each text row from the shard
+  // that owns its id, on this GPU or a peer's (exported with the bindings).
+  void set_text_embedding_shard(int rank, const void* shard, int64_t begin, int64_t rows, int64_t vocab);
 
   // CUDA-graph capture of one buffer set's forward (+ backward with `beta`):
   // the step is replayed with one graph launch (no per-kernel host overhead).
@@ -131,6 +137,14 @@ class Exec {
   int64_t splice_d_h_ = 0;
   const unsigned char* embed_table_ = nullptr;
   int64_t embed_vocab_ = 0;
+  struct EmbedShard {
+    const unsigned char* ptr = nullptr;
+    int64_t begin = 0, rows = 0;
+  };
+  std::vector<EmbedShard> shard_;        // [rank]: vocab-parallel shards (resident: set; peers: imported)
+  EmbedShard shard_of(int rank) const;   // a peer exec's own entry in single-process groups
+  bool sharded() const;                  // some rank has a shard: gathers use the TP group's shards
+  const unsigned char** shard_dev_ = nullptr;  // [world * tp]: each dest rank's TP-group shard bases
   uint64_t offset_of(int gpu, int rank, int slot, int mb_slot) const;
   void prepare_fwd();  // resolve pointers, upload descriptors (after bind/open)
   void prepare_bwd();

@@ -177,10 +177,26 @@ std::string Exec::validate(uint64_t* checks) {
         const uint64_t rows = c.row_bytes ? c.nbytes / c.row_bytes : 0;
         const uintptr_t i0 = reinterpret_cast<uintptr_t>(c.ids);
         const Extent* e = find(i0, i0 + rows * 4, {index::kText});
-        if (!e || c.row_bytes == 0 || rows * c.row_bytes != c.nbytes || s0 != reinterpret_cast<uintptr_t>(embed_table_))
+        if (!e || c.row_bytes == 0 || rows * c.row_bytes != c.nbytes ||
+            (c.shards ? c.shard_rows == 0 : s0 != reinterpret_cast<uintptr_t>(embed_table_)))
           fail("copy segment " + std::to_string(i) + ": gather ids/table out of bounds" + at);
         else if (gpu_of(e->rank) != my_gpu_) touches_peer = true;
         reads.push_back({i0, i0 + rows * 4, "gather ids", i});
+        if (c.shards) {  // vocab-parallel: every shard base is a known rank's shard; peers' behind the wait
+          const auto sp = download(c.shards, static_cast<size_t>(plan_.edge.dest.tp));
+          for (const unsigned char* p : sp) {
+            int owner = -1;
+            for (int r = 0; r < map_.world && owner < 0; ++r)
+              if (shard_of(r).ptr == p) owner = r;
+            if (owner < 0) {
+              fail("copy segment " + std::to_string(i) + ": gather shard base is no rank's embedding shard");
+            } else if (gpu_of(owner) != my_gpu_) {
+              touches_peer = true;
+              if (!((c.peers >> gpu_of(owner)) & 1u))
+                fail("copy segment " + std::to_string(i) + ": peers mask misses shard GPU " + std::to_string(gpu_of(owner)));
+            }
+          }
+        }
       } else {
         const Extent* e = find(s0, s0 + c.nbytes, {index::kSrcAct, index::kText});
         if (!e) {

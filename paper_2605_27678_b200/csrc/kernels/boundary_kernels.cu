@@ -271,6 +271,10 @@ __device__ __forceinline__ const unsigned char* gather_src(const CopySeg& sg, ui
     atomicExch(err, kErrBadId);
     return nullptr;
   }
+  if (sg.shards) {  // vocab-parallel: the owner shard of the TP group (local or a peer's)
+    const uint64_t s = static_cast<uint64_t>(id) / sg.shard_rows;
+    return sg.shards[s] + (static_cast<uint64_t>(id) - s * sg.shard_rows) * sg.row_bytes + off % sg.row_bytes;
+  }
   return sg.src + static_cast<uint64_t>(id) * sg.row_bytes + off % sg.row_bytes;
 }
 

@@ -29,6 +29,10 @@ constexpr int kMaxFan = 8;
 // the run is nbytes/row_bytes rows and row i comes from src + ids[i]*row_bytes
 // (src = the embedding table, `vocab` rows); an id outside [0, vocab) sets the
 // error word to kErrBadId and that row of the destination is left unwritten.
+// Vocab-parallel tables (`shards` set): the table is split over the
+// destination rank's TP group in `shard_rows`-row pieces, piece s at shards[s]
+// (this GPU's or a peer's memory): row id comes from
+// shards[id / shard_rows] + (id % shard_rows) * row_bytes.
 struct CopySeg {
   const unsigned char* src;
   unsigned char* dst[kMaxFan];
@@ -39,7 +43,8 @@ struct CopySeg {
   const int32_t* ids;  // nullptr: contiguous run
   int64_t vocab;
   uint32_t peers;      // GPUs this run reads (pull) or writes (push) besides this one
-  uint32_t pad_;
+  uint32_t shard_rows;                   // vocab-parallel gather: rows per shard
+  const unsigned char* const* shards;    // vocab-parallel gather: shard bases (nullptr: one table at src)
 };
 // kErrOutOfTurn: a peer's "started" count ran 2+ ops ahead of this launch's
 // epoch, which the end-of-launch contract makes impossible unless the GPUs'

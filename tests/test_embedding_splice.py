@@ -109,3 +109,108 @@ def test_embedding_bad_row_left_unwritten(partition):
             assert int(sentinel.sum()) == 0, f"rank {r}"
     assert untouched == 1
     rt.close()
+
+
+def _vp_case(n_gpus, rank_to_gpu=None, partition=0, vocab=998):
+    """Vocab-parallel table (each TP rank of a destination cell holds vocab/tp
+    rows, separate allocations, tp order) against splicing pre-embedded rows
+    table[ids] with a plain runtime: bit-identical destination slices."""
+    cfg = configs.get("c4", scale=64)  # llm{tp2, cp4}: TP groups {0,1}, {2,3}, ...
+    plan = hbb.plan_bridge(cfg.edge())
+    sp = _spec(cfg)
+    tp = cfg.dst.tp
+    table = torch.randn(vocab, cfg.hidden, device="cuda").to(torch.bfloat16)
+    rows = (vocab + tp - 1) // tp
+    if n_gpus == 1:
+        grp = None
+        rts = [hbb.BridgeRuntime(plan, sp, text_embedding=True, partition=partition)]
+        r2g = [0] * plan.world
+        devs = [torch.device("cuda", 0)]
+    else:
+        devs_i = list(range(n_gpus)) if torch.cuda.device_count() >= n_gpus else [0] * n_gpus
+        grp = hbb.LocalGroup(plan, sp, devices=devs_i, rank_to_gpu=rank_to_gpu, text_embedding=True,
+                             partition=partition, timeout_s=20.0)
+        rts, r2g = grp.rts, grp.rank_to_gpu
+        devs = [torch.device("cuda", d) for d in devs_i]
+    rt_p = hbb.BridgeRuntime(plan, sp, partition=partition)
+    shards = {}
+    try:
+        for r in range(plan.world):
+            rt = rts[r2g[r]]
+            if rt.buffer_numel(r, hbb.SLOT_DST_ACT) == 0:
+                continue
+            t = configs_tp_index(cfg, r)
+            piece = torch.zeros(rows, cfg.hidden, dtype=torch.bfloat16, device=devs[r2g[r]])
+            lo, hi = t * rows, min(vocab, (t + 1) * rows)
+            piece[: hi - lo].copy_(table[lo:hi])
+            shards[r] = piece
+            rt.set_text_embedding_shard(r, piece, t * rows, vocab)
+        g = torch.Generator(device="cpu").manual_seed(5)
+        for r in range(plan.world):
+            rt = rts[r2g[r]]
+            if rt.buffer_numel(r, hbb.SLOT_SRC_ACT):
+                x = torch.randn(rt.buffer_numel(r, hbb.SLOT_SRC_ACT), generator=g).to(torch.bfloat16)
+                rt.buffer(r, hbb.SLOT_SRC_ACT).copy_(x)
+                rt_p.buffer(r, hbb.SLOT_SRC_ACT).copy_(x)
+            if rt.buffer_numel(r, hbb.SLOT_TEXT):
+                ids_buf = rt.buffer(r, hbb.SLOT_TEXT)
+                ids = torch.randint(0, vocab, (ids_buf.numel(),), generator=g, dtype=torch.int32)
+                ids_buf.copy_(ids)
+                rt_p.buffer(r, hbb.SLOT_TEXT).copy_(table[ids.long().cuda()].reshape(-1))
+        for rt in rts:
+            assert rt.validate() > 0
+        if grp is not None:
+            grp.forward(0)
+            grp.synchronize()
+        else:
+            rts[0].forward(0)
+        rt_p.forward(0)
+        torch.cuda.synchronize()
+        for rt in rts:
+            assert rt.status() == 0
+        for r in range(plan.world):
+            rt = rts[r2g[r]]
+            if rt.buffer_numel(r, hbb.SLOT_DST_ACT):
+                got = rt.buffer(r, hbb.SLOT_DST_ACT).cpu()
+                assert torch.equal(got, rt_p.buffer(r, hbb.SLOT_DST_ACT).cpu()), f"rank {r}"
+    finally:
+        if grp is not None:
+            grp.close()
+        else:
+            rts[0].close()
+        rt_p.close()
+
+
+def configs_tp_index(cfg, r):
+    from paper_2605_27678_b200 import grid as hbg
+
+    return hbg.coord_of_rank(cfg.dst, r).tp_idx
+
+
+@pytest.mark.parametrize("partition", [0, 1, 3])
+def test_vocab_parallel_gather_one_gpu(partition):
+    _vp_case(1, partition=partition)
+
+
+@pytest.mark.parametrize("partition", [0, 3])
+def test_vocab_parallel_gather_across_gpus(partition):
+    """TP pairs split over two GPUs (rank r on GPU r % 2): half of every text
+    row's owners sit on the peer, so the gathers cross the peer wait."""
+    _vp_case(2, rank_to_gpu=[r % 2 for r in range(8)], partition=partition)
+
+
+def test_vocab_parallel_shards_must_tile_the_vocab():
+    cfg = configs.get("c4", scale=64)
+    plan = hbb.plan_bridge(cfg.edge())
+    rt = hbb.BridgeRuntime(plan, _spec(cfg), text_embedding=True)
+    try:
+        a = torch.zeros(10, cfg.hidden, device="cuda", dtype=torch.bfloat16)
+        b = torch.zeros(12, cfg.hidden, device="cuda", dtype=torch.bfloat16)
+        for r in rt.local_ranks(hbb.SLOT_DST_ACT):
+            t = configs_tp_index(cfg, r)
+            rt.set_text_embedding_shard(r, a if t == 0 else b, 10 * t, 22)
+        with pytest.raises(hbb.HetBridgeError) as ei:
+            rt.forward(0)
+        assert ei.value.code == "ShapeMismatch"
+    finally:
+        rt.close()
