@@ -162,6 +162,67 @@ def run_autograd(name, rank, N, dev):
     return flag.item() == 0, 0.0, r2g
 
 
+def run_vocab_parallel(name, rank, N, dev):
+    """Vocab-parallel text embedding across processes: logical rank r on GPU
+    r % N, so the TP pairs of the CP splice straddle GPUs; every rank's table
+    shard is exported with the bindings (CUDA IPC) and the splice gathers each
+    text row from its owner's shard. Checked against splicing table[ids] on a
+    one-GPU runtime of this process (all ranks resident)."""
+    from paper_2605_27678_b200 import grid as hbg
+
+    cfg = configs.get(name, scale=64)
+    plan = hbb.plan_bridge(cfg.edge())
+    sp = make_splice(cfg)
+    r2g = [r % N for r in range(plan.world)]
+    vocab, tp = 998, cfg.dst.tp
+    rows = (vocab + tp - 1) // tp
+    g = torch.Generator(device="cpu").manual_seed(11)
+    table = torch.randn(vocab, cfg.hidden, generator=g).to(torch.bfloat16)
+    rt = hbb.BridgeRuntime(plan, sp, n_gpus=N, my_gpu=rank, rank_to_gpu=r2g, text_embedding=True, timeout_s=30.0)
+    rt.exchange_handles()
+    ref = hbb.BridgeRuntime(plan, sp)  # every rank resident here, text pre-embedded
+    keep = []
+    for r in range(plan.world):
+        if rt.buffer_numel(r, hbb.SLOT_DST_ACT) and r2g[r] == rank:
+            t = hbg.coord_of_rank(cfg.dst, r).tp_idx
+            piece = torch.zeros(rows, cfg.hidden, dtype=torch.bfloat16)
+            lo, hi = t * rows, min(vocab, (t + 1) * rows)
+            piece[: hi - lo] = table[lo:hi]
+            piece = piece.to(dev)
+            keep.append(piece)
+            rt.set_text_embedding_shard(r, piece, t * rows, vocab)
+    rt.exchange_bindings()
+    for r in range(plan.world):
+        n = rt.buffer_numel(r, hbb.SLOT_SRC_ACT)
+        if n:
+            x = torch.randn(n, generator=g).to(torch.bfloat16)
+            ref.buffer(r, hbb.SLOT_SRC_ACT).copy_(x)
+            if r2g[r] == rank:
+                rt.buffer(r, hbb.SLOT_SRC_ACT).copy_(x)
+        n = rt.buffer_numel(r, hbb.SLOT_TEXT) // cfg.hidden  # text rows = token ids
+        if n:
+            ids = torch.randint(0, vocab, (n,), generator=g, dtype=torch.int32)
+            ref.buffer(r, hbb.SLOT_TEXT).copy_(table[ids.long()].reshape(-1))
+            if r2g[r] == rank:
+                rt.buffer(r, hbb.SLOT_TEXT).copy_(ids)
+    torch.cuda.synchronize()
+    dist.barrier()
+    rt.validate()
+    rt.forward(0)
+    ref.forward(0)
+    torch.cuda.synchronize()
+    ok = rt.status() == 0
+    for r in range(plan.world):
+        if r2g[r] == rank and rt.buffer_numel(r, hbb.SLOT_DST_ACT):
+            ok &= bool(torch.equal(rt.buffer(r, hbb.SLOT_DST_ACT), ref.buffer(r, hbb.SLOT_DST_ACT)))
+    dist.barrier()
+    flag = torch.tensor([0 if ok else 1], device=dev)
+    dist.all_reduce(flag)
+    rt.close()
+    ref.close()
+    return flag.item() == 0, 0.0, r2g
+
+
 def main():
     rank = int(os.environ["RANK"])
     N = int(os.environ["WORLD_SIZE"])
@@ -173,8 +234,10 @@ def main():
     all_ok = True
     proj = os.environ.get("HB_PROJ", "0") == "1"
     ag = os.environ.get("HB_AUTOGRAD", "0") == "1"
+    vp = os.environ.get("HB_VOCAB_PAR", "0") == "1"
     for name in names:
-        ok, worst, r2g = (run_projected if proj else run_autograd if ag else run)(name, rank, N, dev)
+        fn = run_projected if proj else run_autograd if ag else run_vocab_parallel if vp else run
+        ok, worst, r2g = fn(name, rank, N, dev)
         all_ok &= ok
         if rank == 0:
             print(json.dumps({"config": name, "n_gpus": N, "parity": ok, "bwd_max_rel": worst,

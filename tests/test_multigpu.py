@@ -47,6 +47,20 @@ def test_multigpu_caller_buffers(n, mode):
     assert r.returncode == 0
 
 
+@pytest.mark.parametrize("n", [2, 4])
+def test_multigpu_vocab_parallel_embedding(n):
+    """Vocab-parallel text embedding with the TP pairs split over processes:
+    peers' shards mapped through the binding exchange (CUDA IPC)."""
+    if torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    env = dict(os.environ, HB_VOCAB_PAR="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29750 + n), os.path.join(HERE, "mgpu_worker.py"), "c4"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
+    print(r.stdout[-4000:], r.stderr[-4000:])
+    assert r.returncode == 0
+
+
 @pytest.mark.parametrize("n,topologies", [(4, ["c5w4", "join4"]), (6, ["fig4a"]), (8, ["fig4a", "c5"])])
 def test_host_runtime_dispatch(n, topologies):
     """a24 + f2: the host-owned runtime (NCCL world + PP communicators split per
