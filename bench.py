@@ -283,6 +283,20 @@ def fill_values(n: int, key: int, dtype, device):
     return v if dtype == torch.bfloat16 else v.to(dtype)
 
 
+def key_rank(plan, slot, rank):
+    """Whose values a buffer holds: the destination gradients of the tp replicas
+    of one cell are identical (the contract of R:core/include/hetsim/bridge.hpp:
+    33-36, and what a TP all-reduce leaves in training), so they are keyed by
+    the cell's tp=0 rank; every other buffer by its own rank."""
+    from paper_2605_27678_b200 import bridge as hbb
+    from paper_2605_27678_b200 import grid as hbg
+
+    d = plan.edge.dest
+    if slot != hbb.SLOT_DST_GRAD or not d.rank_begin() <= rank < d.rank_end():
+        return rank
+    return min(hbg.module_group(d, rank, "tp"))
+
+
 def fill_inputs(rt, local, slots, dev):
     """Inputs of every buffer set: hashed activations, gradients and text rows;
     source-gradient accumulators start at zero."""
@@ -297,7 +311,7 @@ def fill_inputs(rt, local, slots, dev):
                 if slot == hbb.SLOT_SRC_GRAD:
                     b.zero_()
                 else:
-                    b.copy_(fill_values(b.numel(), input_key(s, slot, r), b.dtype, dev))
+                    b.copy_(fill_values(b.numel(), input_key(s, slot, key_rank(rt.plan, slot, r)), b.dtype, dev))
 
 
 def check_parity(rt, cfg, plan, sp, r2g, rank, N, dev, stream, barrier, run_step, buffer_set):
@@ -341,7 +355,7 @@ def check_parity(rt, cfg, plan, sp, r2g, rank, N, dev, stream, barrier, run_step
     def regen(r, slot):
         if (r, slot) not in cache:
             n = hbb.buffer_elems(plan, r, slot, sp)
-            cache[(r, slot)] = fill_values(n, input_key(buffer_set, slot, r), dt_of[slot], dev)
+            cache[(r, slot)] = fill_values(n, input_key(buffer_set, slot, key_rank(plan, slot, r)), dt_of[slot], dev)
         return cache[(r, slot)]
 
     fwd_map = hbb.index_forward(plan, sp)
