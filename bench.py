@@ -69,6 +69,9 @@ def parse():
     ap.add_argument("--no-runtime", action="store_true",
                     help="skip the host-runtime leg (a24 + f2: 1F1B dispatch table with NC || PP P2P, N = 4, 6, 8)")
     ap.add_argument("--ref-procs", type=int, default=0, help="reference arm: worker processes (0 = auto)")
+    ap.add_argument("--ref-budget", type=float, default=240.0,
+                    help="reference arm: seconds the timed full-workload steps may take (fewer steps are timed "
+                         "when --steps would exceed it; the line reports steps timed and steps_requested)")
     ap.add_argument("--diag-budget", type=float, default=420.0,
                     help="seconds the diagnostic legs (e2e, NCCL comparison, overlap, config matrix, host runtime, "
                          "CPU baseline) may take after the headline; past it the line is printed with what was "
@@ -582,8 +585,13 @@ def run_reference(args):
         procs = args.ref_procs
     ctx = mp.get_context("fork")
     t_init = time.time()
+    K_req = K
     with ctx.Pool(procs, initializer=_ref_worker_init, initargs=(cfg.name,)) as pool:
-        pool.map(_ref_step, range(max(Wm, procs)), chunksize=1)  # warm-up (every worker has its inputs)
+        warm = pool.map(_ref_step, range(max(Wm, procs)), chunksize=1)  # warm-up (every worker has its inputs)
+        # a full-workload step takes seconds on one core: keep the timed run within
+        # --ref-budget seconds (the line then reports the steps actually timed)
+        fit = max(procs, int(args.ref_budget * procs / max(1e-3, statistics.median(warm))))
+        K = min(K, fit)
         t0 = time.time()
         step_s = pool.map(_ref_step, range(K), chunksize=1)
         wall = time.time() - t0
@@ -609,6 +617,7 @@ def run_reference(args):
                     "bytes_per_step": payload, "f64_bytes_moved_per_step": f64,
                     "gbs_at_f64_bytes": round(f64 * K / wall / 1e9, 4)},
         "setup_s": round(t0 - t_init, 1),
+        "steps_requested": K_req,
         "note": "reference bridge body is a stub (bridge.cpp); the oracle restatement runs over the reference's own "
                 "simnet/grid compiled from /root/reference sources (oracle/_ref)",
     }
