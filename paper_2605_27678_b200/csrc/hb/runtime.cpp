@@ -670,8 +670,11 @@ void Exec::upload_copies(int mb, uint64_t unit, std::vector<uint64_t>* w0s, std:
   std::vector<const unsigned char*> shard_host;
   if (cfg_.text_embedding && sharded()) {
     shard_host.assign(static_cast<size_t>(map_.world) * tp_, nullptr);
-    if (!shard_dev_)
+    if (mb == 0) {  // a fresh array per table rebuild (cudaFree waits for launches still reading the old one)
+      cudaFree(shard_dev_);
+      shard_dev_ = nullptr;
       ck(cudaMalloc(reinterpret_cast<void**>(&shard_dev_), shard_host.size() * sizeof(void*)), "cudaMalloc(shards)");
+    }
   }
   for (const auto& f : fwd_local_) {
     const bool gather = f.src.slot == index::kText && cfg_.text_embedding;
