@@ -4,8 +4,10 @@
 #include "kernels/projector_gemm.cuh"
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -13,6 +15,16 @@
 #include <tuple>
 
 namespace hb::rt {
+
+// NVTX range for the scope (header-only NVTX3: free unless a tool such as
+// ncu --nvtx or nsys is attached): every boundary op shows up by name and
+// microbatch on the profiler's timeline.
+NvtxRange::NvtxRange(const char* what, int mb) {
+  char b[64];
+  std::snprintf(b, sizeof b, "hetbridge %s mb %d", what, mb);
+  nvtxRangePushA(b);
+}
+NvtxRange::~NvtxRange() { nvtxRangePop(); }
 
 namespace {
 void ck(cudaError_t e, const char* what) {
@@ -973,6 +985,7 @@ void Exec::check_forward_mb(int mb) const {
 }
 
 void Exec::forward(int mb, void* stream) {
+  NvtxRange nv("forward", mb);
   DeviceGuard dg(device_);
   check_forward_mb(mb);
   prepare_fwd();
@@ -982,6 +995,7 @@ void Exec::forward(int mb, void* stream) {
 
 void Exec::forward_projected(int mb, const void* x, int64_t ldx, const void* w, int64_t ldw, int d_h, int K,
                              int64_t x_rows, void* stream) {
+  NvtxRange nv("forward_projected", mb);
   DeviceGuard dg(device_);
   check_forward_mb(mb);
   if (cfg_.act_dtype != dev::kBF16) raise(ErrorCode::InvalidArgument, "the fused projector writes bf16 activations");
@@ -1047,6 +1061,7 @@ void Exec::forward_projected(int mb, const void* x, int64_t ldx, const void* w, 
 }
 
 void Exec::backward(int mb, float beta, void* stream) {
+  NvtxRange nv("backward", mb);
   DeviceGuard dg(device_);
   if (!fwd_done_.count(mb))
     raise(ErrorCode::UnknownMicrobatch, "no forward record for microbatch " + std::to_string(mb));
@@ -1117,6 +1132,8 @@ void Exec::graph_capture(int mb_slot, int what, float beta, void* stream) {
 }
 
 void Exec::graph_launch(int mb_slot, int what, void* stream) {
+  NvtxRange nv(what == 0 ? "graph fwd" : what == 1 ? "graph step" : what == 2 ? "graph bwd"
+               : what == 3 ? "graph cycle" : "graph paired cycle", mb_slot);
   DeviceGuard dg(device_);
   auto it = graphs_.find(std::make_pair(what >= 3 ? 0 : mb_slot, what));
   if (it == graphs_.end())

@@ -30,6 +30,13 @@
 
 namespace hb::rt {
 
+struct NvtxRange {  // profiler range for a host call (runtime.cpp)
+  NvtxRange(const char* what, int mb);
+  ~NvtxRange();
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 struct ExecConfig {
   int act_dtype = dev::kBF16;       // source / destination activations (copy width)
   int grad_in_dtype = dev::kBF16;   // destination gradients

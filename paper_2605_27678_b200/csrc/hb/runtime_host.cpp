@@ -214,6 +214,7 @@ cudaStream_t HostRuntime::stream(int which) const {
 }
 
 void HostRuntime::step(ComputeFn fn, void* user) {
+  NvtxRange nv("runtime step", static_cast<int>(steps_));
   int prev = -1;
   cudaGetDevice(&prev);
   if (prev != device_) cudaSetDevice(device_);
