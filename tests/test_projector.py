@@ -12,7 +12,10 @@ def _ref(x, w):
     return (x.float() @ w.float().t()).to(torch.bfloat16)
 
 
-@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (300, 512, 128), (576, 4096, 1024), (4608, 4096, 1280)])
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (300, 512, 128), (576, 4096, 1024), (4608, 4096, 1280),
+                                   # long K (the deep 2-SM ring, half-row epilogue) and more m-tile groups
+                                   # than one rasterisation group, with a ragged last group and last pair
+                                   (4480, 1024, 4096), (2400, 768, 2048)])
 def test_projector_gemm_vs_torch(M, N, K):
     from paper_2605_27678_b200.projector import projector_gemm
 
