@@ -1008,7 +1008,8 @@ void Exec::forward_projected(int mb, const void* x, int64_t ldx, const void* w, 
     raise(ErrorCode::ShapeMismatch, "projector GEMM needs d_h % 256 == 0 and K % 64 == 0");
   const int slot = mb % cfg_.mb_slots;
   ProjTable& P = proj_[slot];
-  if (P.d_h != d_h || !P.rows_dev || dirty_fwd_) {
+  const bool staged = proj_staged();
+  if (P.d_h != d_h || !P.rows_dev || dirty_fwd_ || P.staged != static_cast<int>(staged)) {
     prepare_fwd();
     // token row -> destination rows, from the forward map (every destination,
     // in map order); rows are numbered over the local source ranks ascending
@@ -1021,7 +1022,13 @@ void Exec::forward_projected(int mb, const void* x, int64_t ldx, const void* w, 
       }
     std::vector<std::vector<unsigned char*>> dst(rows);
     const int es = dev::dtype_size(cfg_.act_dtype);
+    if (staged) {  // every row to its own source shard; the pulled forward does the rest
+      for (const auto& [r, base] : row_base)
+        for (int64_t i = 0; i < map_.elems[r][index::kSrcAct] / d_h; ++i)
+          dst[base + i].push_back(addr(r, index::kSrcAct, slot, i * d_h, es));
+    }
     for (const auto& sg : map_.fwd) {
+      if (staged) break;
       // rows this GPU projects: its own source ranks' (pushed to local and peer destinations)
       if (sg.src.slot != index::kSrcAct || gpu_of(sg.src.rank) != my_gpu_) continue;
       if (sg.src.off % d_h || sg.dst.off % d_h || sg.n % d_h)
@@ -1042,6 +1049,7 @@ void Exec::forward_projected(int mb, const void* x, int64_t ldx, const void* w, 
     P.d_h = d_h;
     P.fan = fan;
     P.rows = static_cast<int>(rows);
+    P.staged = staged;
   }
   if (P.rows > 0 && !x) raise(ErrorCode::InvalidArgument, "null projector input for the local source rows");
   // the TMA map spans P.rows x K of x: a shorter or narrower operand would be read out of bounds
@@ -1050,14 +1058,34 @@ void Exec::forward_projected(int mb, const void* x, int64_t ldx, const void* w, 
                                         std::to_string(P.rows));
   if (P.rows > 0 && ldx < K) raise(ErrorCode::ShapeMismatch, "projector input leading dimension < K");
   if (ldw < K) raise(ErrorCode::ShapeMismatch, "projector weight leading dimension < K");
-  const dev::ProjectorArgs a{P.rows, d_h, K, P.rows_dev, P.fan, sync_proj_};
+  dev::SyncArgs ps = sync_proj_;
+  if (staged) ps.wait_mask = ps.post_mask = 0, ps.end_sync = 0;  // local stores only: no cross-GPU protocol
+  const dev::ProjectorArgs a{P.rows, d_h, K, P.rows_dev, P.fan, ps};
   // persistent GEMM: one CTA per SM in CTA pairs, so the cap is rounded down to even
   const int proj_ctas = cfg_.max_ctas > 0 ? std::max(2, std::min(sm_count_, cfg_.max_ctas) & ~1) : sm_count_;
   const int st = dev::launch_projector(x, ldx, w, ldw, a, proj_ctas, stream);
   if (st) raise(st == 3 ? ErrorCode::InvalidArgument : ErrorCode::CudaError,
                 "projector GEMM launch failed (" + std::to_string(st) + ")");
   ++launches_;
+  if (staged) launch_forward(slot, stream);  // the pulled reshard of the freshly projected shards
   fwd_done_.insert(mb);
+}
+
+bool Exec::proj_staged() const {
+  static const int env = [] {  // HB_PROJ_FUSE: 1 always push, 0 always stage, unset/other: auto
+    const char* v = std::getenv("HB_PROJ_FUSE");
+    return v && (v[0] == '0' || v[0] == '1') ? v[0] - '0' : -1;
+  }();
+  if (env >= 0) return env == 0;
+  // auto: stage when some row would reach one GPU more than once over NVLink
+  std::map<std::tuple<int, int64_t, int>, int> arrivals;  // (source rank, element, destination GPU)
+  for (const auto& sg : map_.fwd) {
+    if (sg.src.slot != index::kSrcAct) continue;
+    const int gs = gpu_of(sg.src.rank), gd = gpu_of(sg.dst.rank);
+    if (gs == gd) continue;
+    if (++arrivals[{sg.src.rank, sg.src.off, gd}] > 1) return true;
+  }
+  return false;
 }
 
 void Exec::backward(int mb, float beta, void* stream) {

@@ -212,8 +212,15 @@ class Exec {
     int d_h = 0;
     int fan = 0;
     int rows = 0;
+    int staged = -1;                     // the table is for the staged path (rows -> own source shard)
     unsigned char** rows_dev = nullptr;  // [rows * fan]
   };
+  // The fused projector pushes each row to every destination, so a GPU hosting
+  // several consumers of a row receives it once per consumer over NVLink. When
+  // that happens anywhere in the group (decided from the plan: every GPU takes
+  // the same path), forward_projected stages instead: the projector writes the
+  // source shards and the pulled forward fans each row out on its GPU.
+  bool proj_staged() const;
   std::vector<ProjTable> proj_;  // per mb slot
   // Static contiguous partition of each direction's work space over the grid.
   struct DevPartition {

@@ -47,6 +47,26 @@ def test_multigpu_caller_buffers(n, mode):
     assert r.returncode == 0
 
 
+@pytest.mark.parametrize("fuse", ["auto", "0", "1"])
+@pytest.mark.parametrize("n", [2, 4])
+def test_multigpu_fused_projector(n, fuse):
+    """hb_exec_forward_projected across processes == our GEMM into the source
+    shards + the pulled reshard, bit for bit: pushed from the projector's
+    epilogue (HB_PROJ_FUSE=1), staged through the source shards (0), or chosen
+    from the plan (auto: staged when a GPU would receive a row more than once)."""
+    if torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    env = dict(os.environ, HB_PROJ="1")
+    if fuse != "auto":
+        env["HB_PROJ_FUSE"] = fuse
+    names = ["c2", "c3", "c5"] + (["c2x4", "c3x4"] if n == 4 else [])
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29760 + n), os.path.join(HERE, "mgpu_worker.py")] + names
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
+    print(r.stdout[-4000:], r.stderr[-4000:])
+    assert r.returncode == 0
+
+
 @pytest.mark.parametrize("n", [2, 4])
 def test_multigpu_vocab_parallel_embedding(n):
     """Vocab-parallel text embedding with the TP pairs split over processes:
