@@ -7,6 +7,7 @@
 #include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -588,9 +589,15 @@ uint64_t Exec::pad_unit(int mode, bool copy) const {
 
 void Exec::build_partition(const std::vector<uint64_t>& w0, const std::vector<uint64_t>& n,
                            const std::vector<char>& remote, double local_bytes, double remote_bytes, int grid,
-                           int mode, uint64_t unit, DevPartition* out, uint64_t runit) {
+                           int mode, uint64_t unit, DevPartition* out, uint64_t runit, bool taper) {
   const uint64_t total = w0.empty() ? 0 : w0.back() + n.back();
   if (runit == 0) runit = unit;
+  // Tapered hand-out (the gradient return): chunks are described in quarter
+  // units; the tail of every segment (the last ~2 grids' worth of work of the
+  // queue, at most half of it) goes out in single quarter units, so the
+  // launch's last claims are short and the CTAs finish together. A table
+  // entry is (segment, start | (units - 1) << 24), in units of the quarter.
+  const uint64_t div = taper ? 4 : 1;
   cudaFree(out->first_seg);
   cudaFree(out->chunks);
   cudaFree(out->rchunks);
@@ -598,8 +605,8 @@ void Exec::build_partition(const std::vector<uint64_t>& w0, const std::vector<ui
   out->chunks = out->rchunks = nullptr;
   out->grid = grid;
   out->mode = mode;
-  out->chunk = unit;
-  out->rchunk = runit;
+  out->chunk = unit / div;
+  out->rchunk = runit / div;
   out->total_chunks = out->rtotal_chunks = 0;
   out->remote_ctas = 0;
   out->lstatic = out->rstatic = 0;
@@ -610,13 +617,22 @@ void Exec::build_partition(const std::vector<uint64_t>& w0, const std::vector<ui
     // the same fractional pace; ties keep segment order.
     for (int q = 0; q < 2; ++q) {
       std::vector<std::pair<double, uint2>> order;
+      const uint64_t u = q ? runit : unit, su = u / div;
+      uint64_t qtotal = 0;
+      for (size_t s = 0; s < n.size(); ++s)
+        if ((remote[s] != 0) == (q == 1)) qtotal += n[s];
+      const double tail = taper && qtotal ? std::min(0.5, 2.0 * grid * static_cast<double>(u) / qtotal) : 0.0;
       for (size_t s = 0; s < n.size(); ++s) {
         if ((remote[s] != 0) != (q == 1)) continue;
-        const uint64_t u = q ? runit : unit;
-        const uint64_t k = (n[s] + u - 1) / u;
-        for (uint64_t j = 0; j < k; ++j)
-          order.push_back({(j + 0.5) / static_cast<double>(k),
-                           make_uint2(static_cast<unsigned>(s), static_cast<unsigned>(j))});
+        const uint64_t k = (n[s] + su - 1) / su;  // quarter units of this segment
+        if (k >= (1u << 24)) raise(ErrorCode::InvalidArgument, "segment too long for the chunk table");
+        const uint64_t small = taper ? std::min<uint64_t>(k, static_cast<uint64_t>(std::ceil(tail * k))) : 0;
+        for (uint64_t j = 0; j < k;) {
+          const uint64_t len = j < k - small ? std::min<uint64_t>(div, k - small - j) : 1;
+          order.push_back({(j + 0.5 * len) / static_cast<double>(k),
+                           make_uint2(static_cast<unsigned>(s), static_cast<unsigned>(j | (len - 1) << 24))});
+          j += len;
+        }
       }
       std::stable_sort(order.begin(), order.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
       std::vector<uint2> table(order.size());
@@ -911,7 +927,8 @@ void Exec::prepare_bwd() {
       while (runit * 2 <= ring_elems / 2 && rtotal / (runit * 2) >= 4 * static_cast<uint64_t>(bgrid)) runit *= 2;
     }
   }
-  build_partition(w0s, ns, rem, lb, rb, bgrid, mode, unit, &bwd_part_, runit);
+  static const bool taper = env_u64("HB_RED_TAPER", 0) != 0;  // A/B knob (off: measured slower)
+  build_partition(w0s, ns, rem, lb, rb, bgrid, mode, unit, &bwd_part_, runit, taper && mode == dev::kPartDynamic);
   bwd_part_.ring = static_cast<int>(env_u64("HB_RED_RING", 1));  // A/B knob: 0 = LDG for remote chunks too
   bwd_part_.fan = fan;
   // HB_RED_STAGE_LOCAL=1: the streaming kernel stages local single-term chunks

@@ -254,7 +254,7 @@ class Exec {
   // remote[s]: segment s reads (pull) or writes (push) a peer's buffer; cost_local/remote in bytes
   void build_partition(const std::vector<uint64_t>& w0, const std::vector<uint64_t>& n,
                        const std::vector<char>& remote, double local_bytes, double remote_bytes, int grid,
-                       int mode, uint64_t unit, DevPartition* out, uint64_t runit = 0);
+                       int mode, uint64_t unit, DevPartition* out, uint64_t runit = 0, bool taper = false);
   bool dirty_fwd_ = true, dirty_bwd_ = true;
   bool graphs_invalidated_ = false;
   bool shared_device_ = false;  // a peer exec of the group runs on this device (no PDL)

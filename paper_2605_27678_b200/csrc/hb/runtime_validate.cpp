@@ -292,7 +292,7 @@ std::string Exec::validate(uint64_t* checks) {
             if (remote_of(c.x) && q == 0)
               fail(std::string(dir) + " segment " + std::to_string(c.x) + " touches a peer but is handed out "
                    "before the peer wait (local queue)");
-            seen[c.x].push_back(c.y);
+            for (uint32_t u = 0; u <= (c.y >> 24); ++u) seen[c.x].push_back((c.y & 0xffffffu) + u);
           }
         for (size_t s = 0; s < nseg; ++s) {
           const uint64_t u = remote_of(s) ? P.rchunk : P.chunk;

@@ -190,7 +190,7 @@ __device__ __forceinline__ void run_shares(const S* __restrict__ segs, int nseg,
         const uint2 t = (cur_remote ? part.rchunks : part.chunks)[c];
         const S sg = segs[t.x];
         const uint64_t cu = cur_remote ? part.rchunk : part.chunk;
-        const uint64_t a = static_cast<uint64_t>(t.y) * cu, e = a + cu, n = len(sg);
+        const uint64_t a = static_cast<uint64_t>(t.y & 0xffffffu) * cu, e = a + ((t.y >> 24) + 1) * cu, n = len(sg);
         body(sg, a, e < n ? e : n, cur_remote != 0);
         if (threadIdx.x == 0 && sync.trace) {
           ++nch;
@@ -449,7 +449,7 @@ __global__ void __launch_bounds__(32) copy_segments_tma_kernel(const CopySeg* __
         arrive();
         if (!sync_wait_peers(sync, cs, sg.peers)) continue;  // timed out: claimed, not executed
       }
-      const uint64_t a = static_cast<uint64_t>(t.y) * part.chunk;
+      const uint64_t a = static_cast<uint64_t>(t.y & 0xffffffu) * part.chunk;  // (copy chunks are one unit)
       const uint64_t e = a + part.chunk < sg.nbytes ? a + part.chunk : sg.nbytes;
       const uint32_t bytes = static_cast<uint32_t>(e - a);
       const int nd = sg.ndst;
@@ -1083,8 +1083,8 @@ __global__ void __launch_bounds__(512, 2) reduce_segments_stream_kernel(const Re
       const uint2 t = (rq ? part.rchunks : part.chunks)[c];
       const ReduceSeg& sg = segs[t.x];
       const uint64_t cu = rq ? part.rchunk : part.chunk;
-      const uint64_t a = static_cast<uint64_t>(t.y) * cu;
-      const uint64_t b = min(a + cu, sg.nelem);
+      const uint64_t a = static_cast<uint64_t>(t.y & 0xffffffu) * cu;
+      const uint64_t b = min(a + ((t.y >> 24) + 1) * cu, sg.nelem);
       if (rq) {
         arrive();
         if (!sync_wait_lane(sync, cs)) continue;  // timed out: claimed, not executed

@@ -86,7 +86,7 @@ struct Partition {
   int mode;
   uint32_t total_chunks;     // dynamic / TMA: chunks with no peer dependency
   uint64_t chunk;            // dynamic / TMA chunk size
-  const uint2* chunks;       // [total_chunks] (segment, chunk within segment), in hand-out order
+  const uint2* chunks;       // [total_chunks] (segment, first unit | (units - 1) << 24), in hand-out order
   uint32_t rtotal_chunks;    // dynamic / TMA: chunks that read (pull) or write (push) a peer
   const uint2* rchunks;      // [rtotal_chunks]
   uint64_t rchunk;           // dynamic: remote chunk size (copy / TMA: = chunk)
