@@ -245,6 +245,12 @@ int hb_exec_set_text_embedding_shard(hb_exec* x, int rank, const void* shard, lo
 int hb_exec_graph_capture(hb_exec* x, int mb_slot, int what, float beta, void* cuda_stream);
 int hb_exec_graph_launch(hb_exec* x, int mb_slot, int what, void* cuda_stream);
 int hb_exec_status(hb_exec* x, unsigned* device_error);
+/* Recovery after a Timeout (26) or GroupMismatch (12): zeroes the exec's launch
+ * counters, claim queues, error word and signal pad and drops its microbatch
+ * records; tables and captured graphs stay valid. Collective: every exec of
+ * the group calls it with its device idle, between two group-wide barriers
+ * (no reference counterpart; simnet aborts the whole fabric instead). */
+int hb_exec_reset_protocol(hb_exec* x);
 int hb_exec_stats(hb_exec* x, long long* fwd_segments, long long* bwd_segments,
                   long long* fwd_bytes, long long* bwd_elems, long long* launches);
 /* Diagnostics (no reference counterpart): with HB_TRACE=1 in the environment

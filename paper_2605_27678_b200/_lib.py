@@ -33,7 +33,7 @@ EXPORTS = [
     "hb_exec_config_default", "hb_exec_create", "hb_exec_destroy", "hb_exec_ipc_handle",
     "hb_exec_open_peers", "hb_exec_open_peers_local", "hb_exec_buffer", "hb_exec_bind", "hb_exec_bind_strided",
     "hb_exec_export_bindings", "hb_exec_import_bindings", "hb_exec_forward", "hb_exec_backward",
-    "hb_exec_seed_forward_record", "hb_exec_status", "hb_exec_stats", "hb_exec_graph_capture", "hb_projector_gemm",
+    "hb_exec_seed_forward_record", "hb_exec_status", "hb_exec_reset_protocol", "hb_exec_stats", "hb_exec_graph_capture", "hb_projector_gemm",
     "hb_exec_forward_projected", "hb_exec_set_text_embedding", "hb_exec_set_text_embedding_shard",
     "hb_exec_graph_launch", "hb_exec_trace", "hb_exec_validate",
     "hb_stage_graph_create", "hb_stage_graph_destroy", "hb_stage_graph_nodes", "hb_stage_graph_edges",
@@ -142,6 +142,7 @@ def _declare(L):
         "hb_exec_graph_capture": (I, [V, I, I, ctypes.c_float, V]),
         "hb_exec_graph_launch": (I, [V, I, I, V]),
         "hb_exec_status": (I, [V, P(U)]),
+        "hb_exec_reset_protocol": (I, [V]),
         "hb_exec_stats": (I, [V, P(LL), P(LL), P(LL), P(LL), P(LL)]),
         "hb_projector_gemm": (I, [V, LL, V, LL, V, I, I, I, I, V]),
         "hb_exec_forward_projected": (I, [V, I, V, LL, LL, V, LL, I, I, V]),

@@ -465,6 +465,21 @@ class BridgeRuntime:
         check(lib().hb_exec_status(self._h, ctypes.byref(e)))
         return e.value
 
+    def reset_protocol(self, group=None):
+        """Recover the exec group after a Timeout / GroupMismatch (collective:
+        every process calls it; barriers on both sides of the reset)."""
+        import torch
+
+        torch.cuda.synchronize(self.device)
+        multi = self.n_gpus > 1 and self._local_group is None
+        if multi:
+            import torch.distributed as dist
+
+            dist.barrier(group)
+        check(lib().hb_exec_reset_protocol(self._h))
+        if multi:
+            dist.barrier(group)
+
     def stats(self) -> dict:
         v = [ctypes.c_longlong() for _ in range(5)]
         check(lib().hb_exec_stats(self._h, *(ctypes.byref(x) for x in v)))
@@ -555,6 +570,12 @@ class LocalGroup:
 
     def set_text_embedding_shard(self, rank: int, shard, vocab_begin: int, vocab: int):
         self.runtime_of(rank).set_text_embedding_shard(rank, shard, vocab_begin, vocab)
+
+    def reset_protocol(self):
+        """Recover every exec of the group after a Timeout / GroupMismatch."""
+        self.synchronize()
+        for rt in self.rts:
+            rt.reset_protocol()
 
     def forward(self, mb: int = 0):
         for rt, st in zip(self.rts, self.streams):

@@ -530,6 +530,13 @@ int hb_exec_seed_forward_record(hb_exec* x, int mb) {
   });
 }
 
+int hb_exec_reset_protocol(hb_exec* x) {
+  return guard([&] {
+    need(x, "exec");
+    x->x->reset_protocol();
+  });
+}
+
 int hb_exec_status(hb_exec* x, unsigned* device_error) {
   return guard([&] {
     need(x, "exec");

@@ -1245,6 +1245,15 @@ int Exec::read_trace(int kind, unsigned long long* out, int max_ctas, int* grid)
   return n;
 }
 
+void Exec::reset_protocol() {
+  DeviceGuard dg(device_);
+  ck(cudaDeviceSynchronize(), "reset: synchronize");
+  ck(cudaMemset(ctr_, 0, kNumKinds * dev::kCtrBytes), "reset: counters");
+  if (local_base_) ck(cudaMemset(local_base_, 0, kPadBytes), "reset: signal pad");
+  ck(cudaDeviceSynchronize(), "reset: synchronize");
+  fwd_done_.clear();
+}
+
 uint32_t Exec::device_error() const {
   DeviceGuard dg(device_);
   uint32_t v = 0;

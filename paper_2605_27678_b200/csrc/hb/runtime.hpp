@@ -119,6 +119,12 @@ class Exec {
   void graph_capture(int mb_slot, int what, float beta, void* stream);
   void graph_launch(int mb_slot, int what, void* stream);
   uint32_t device_error() const;  // synchronises
+  // Recovery after a timeout or GroupMismatch: zero this exec's launch
+  // counters, claim queues, error word and signal pad, and drop the
+  // microbatch records. Collective: every exec of the group calls it with its
+  // device idle, between two group-wide barriers; the group then starts again
+  // from epoch 0 with its tables and captured graphs intact.
+  void reset_protocol();
   // HB_TRACE=1 diagnostics: copies the last launch of `kind`'s per-CTA stamps
   // (dev::kTraceWords u64 each) into out; returns CTAs copied (0: tracing off).
   int read_trace(int kind, unsigned long long* out, int max_ctas, int* grid) const;

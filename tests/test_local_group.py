@@ -147,5 +147,11 @@ def test_out_of_turn_peer_detected():
             rt0.status()
         assert ei.value.code == "GroupMismatch"
         assert g.rts[1].status() == 0
+        # recovery: every exec of the group resets its protocol state, then the
+        # same execs (tables, peers) run correct steps again
+        g.reset_protocol()
+        assert all(rt.status() == 0 for rt in g.rts)
+        ok, _ = group_parity(cfg, LocalGroupDriver(g), steps=2)
+        assert ok and all(rt.status() == 0 for rt in g.rts)
     finally:
         g.close()
