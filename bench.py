@@ -1224,7 +1224,7 @@ def run_paired(args, name, N, rank, dev, barrier, stream, pk):
     cap = torch.cuda.get_device_properties(dev).multi_processor_count
     rt = hbb.BridgeRuntime(plan, sp, n_gpus=N, my_gpu=rank, rank_to_gpu=r2g, act_dtype=tdt[cfg.act],
                            grad_in_dtype=tdt[cfg.grad_in], grad_out_dtype=tdt[cfg.grad_out], mb_slots=slots,
-                           max_ctas=cap)
+                           max_ctas=cap, timeout_s=5.0)  # (a failed co-residency would time out fast)
     try:
         if N > 1:
             rt.exchange_handles()
