@@ -1221,10 +1221,19 @@ def run_paired(args, name, N, rank, dev, barrier, stream, pk):
     tm = traffic_model(cfg, N)
     per_gpu_step = max(f + b for f, b in zip(tm["fwd_hbm"], tm["bwd_hbm"]))
     slots = max(4, min(8, math.ceil(3 * L2_BYTES / max(per_gpu_step, 1))))
-    cap = torch.cuda.get_device_properties(dev).multi_processor_count
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    # one CTA of each kind per SM (32 KiB TMA stages). HB_PAIRED_CAPS=2 sizes the
+    # kinds apart: two forward CTAs with 8 x 8 KiB stages beside one gradient-return
+    # CTA per SM; measured slower at N=4 (C2 0.205 vs 0.175 ms, C4 0.123 vs 0.086 ms:
+    # 8 KiB stages cost the copy more than the second CTA gains)
+    if os.environ.get("HB_PAIRED_CAPS") == "2":
+        caps = dict(max_ctas=2 * sms, max_ctas_bwd=sms, tma_chunk_kib=8)
+    else:
+        caps = dict(max_ctas=sms)
+    cap = caps["max_ctas"]
     rt = hbb.BridgeRuntime(plan, sp, n_gpus=N, my_gpu=rank, rank_to_gpu=r2g, act_dtype=tdt[cfg.act],
                            grad_in_dtype=tdt[cfg.grad_in], grad_out_dtype=tdt[cfg.grad_out], mb_slots=slots,
-                           max_ctas=cap, timeout_s=5.0)  # (a failed co-residency would time out fast)
+                           timeout_s=5.0, **caps)  # (a failed co-residency would time out fast)
     try:
         if N > 1:
             rt.exchange_handles()
@@ -1269,7 +1278,7 @@ def run_paired(args, name, N, rank, dev, barrier, stream, pk):
                 "critical": {"gpu": crit[0], "bound": crit[1]} if crit else None,
                 "serial_tstar_ms": round(fk["tstar_ms"] + bk["tstar_ms"], 4),
                 "serial_same_cap_ms_per_step": round(ms_serial, 5),
-                "max_ctas": cap, "buffer_sets": slots, "steps": cycles * slots, "parity": parity,
+                "grid_caps": caps, "buffer_sets": slots, "steps": cycles * slots, "parity": parity,
                 "how": "hb_exec_graph_capture what=4: step k = fwd(set k) || bwd(set k-1) on two streams, "
                        "one graph per cycle of buffer sets; CUDA events, max over ranks"}
     finally:

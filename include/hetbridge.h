@@ -181,6 +181,13 @@ typedef struct {
    * concurrent work such as pipeline P2P, and lets several execs of one group
    * share a device (hb_exec_open_peers_local). */
   int max_ctas;
+  /* cap on the backward (gradient-return) grid alone; 0 = max_ctas. With a
+   * forward and a backward in flight at once (the 1F1B-paired graph) the two
+   * kinds can be sized separately so both grids fit on the GPU. */
+  int max_ctas_bwd;
+  /* TMA copy stage size in KiB (8, 16 or 32; 0 = HB_TMA_CHUNK_KB or 32): smaller
+   * stages leave shared memory for a concurrent gradient-return grid. */
+  int tma_chunk_kib;
 } hb_exec_config;
 void hb_exec_config_default(hb_exec_config* c);
 

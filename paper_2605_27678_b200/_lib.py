@@ -91,7 +91,8 @@ class ExecConfig(ctypes.Structure):
                 ("internal_alloc", ctypes.c_int), ("blocks_per_sm", ctypes.c_int),
                 ("threads", ctypes.c_int), ("timeout_s", ctypes.c_double), ("fwd_mode", ctypes.c_int),
                 ("partition", ctypes.c_int), ("strict_provenance", ctypes.c_int),
-                ("text_embedding", ctypes.c_int), ("max_ctas", ctypes.c_int)]
+                ("text_embedding", ctypes.c_int), ("max_ctas", ctypes.c_int), ("max_ctas_bwd", ctypes.c_int),
+                ("tma_chunk_kib", ctypes.c_int)]
 
 
 _lib = None

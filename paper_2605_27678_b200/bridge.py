@@ -210,7 +210,8 @@ class BridgeRuntime:
                  grad_out_dtype=None, mb_slots: int = 1, internal_alloc: bool = True,
                  blocks_per_sm: int = 0, threads: int = 0, timeout_s: float = 0.0,
                  fwd_mode: int = 0, partition: int = 0, strict_provenance: bool = False,
-                 text_embedding: bool = False, max_ctas: int = 0):
+                 text_embedding: bool = False, max_ctas: int = 0, max_ctas_bwd: int = 0,
+                 tma_chunk_kib: int = 0):
         import torch
 
         self.plan, self.splice = plan, splice
@@ -235,6 +236,8 @@ class BridgeRuntime:
         cfg.strict_provenance = 1 if strict_provenance else 0
         cfg.text_embedding = 1 if text_embedding else 0
         cfg.max_ctas = max_ctas
+        cfg.max_ctas_bwd = max_ctas_bwd
+        cfg.tma_chunk_kib = tma_chunk_kib
         self.text_embedding = bool(text_embedding)
         if not torch.cuda.is_available():
             raise HetBridgeError(25, "BridgeRuntime needs a CUDA device (no CPU fallback)")

@@ -390,6 +390,8 @@ void hb_exec_config_default(hb_exec_config* c) {
   c->strict_provenance = d.strict_provenance;
   c->text_embedding = d.text_embedding;
   c->max_ctas = d.max_ctas;
+  c->max_ctas_bwd = d.max_ctas_bwd;
+  c->tma_chunk_kib = d.tma_chunk_kib;
 }
 
 int hb_exec_create(const hb_plan* p, const hb_splice* s, int n_gpus, int my_gpu, const int* rank_to_gpu,
@@ -413,6 +415,10 @@ int hb_exec_create(const hb_plan* p, const hb_splice* s, int n_gpus, int my_gpu,
       c.strict_provenance = cfg->strict_provenance;
       c.text_embedding = cfg->text_embedding;
       c.max_ctas = cfg->max_ctas > 0 ? cfg->max_ctas : 0;
+      c.max_ctas_bwd = cfg->max_ctas_bwd > 0 ? cfg->max_ctas_bwd : 0;
+      c.tma_chunk_kib = cfg->tma_chunk_kib;
+      if (c.tma_chunk_kib && c.tma_chunk_kib != 8 && c.tma_chunk_kib != 16 && c.tma_chunk_kib != 32)
+        hb::raise(hb::ErrorCode::InvalidArgument, "tma_chunk_kib must be 0, 8, 16 or 32");
     }
     std::vector<int> map;
     if (rank_to_gpu) map.assign(rank_to_gpu, rank_to_gpu + n_ranks);

@@ -582,7 +582,7 @@ int Exec::reduce_mode() const {
 }
 
 uint64_t Exec::pad_unit(int mode, bool copy) const {
-  if (mode == dev::kPartTma) return dev::tma_chunk_bytes(kTmaChunkKiB);
+  if (mode == dev::kPartTma) return dev::tma_chunk_bytes(tma_kib());
   if (mode == dev::kPartDynamic) return copy ? kDynCopyChunk : kDynReduceChunk;
   return dev::kQuantum;
 }
@@ -767,9 +767,11 @@ void Exec::upload_copies(int mb, uint64_t unit, std::vector<uint64_t>* w0s, std:
   }
 }
 
+int Exec::tma_kib() const { return cfg_.tma_chunk_kib > 0 ? cfg_.tma_chunk_kib : kTmaChunkKiB; }
+
 int Exec::copy_grid() const {
   if (copy_mode() == dev::kPartTma) {
-    const int occ = dev::tma_blocks_per_sm(dev::tma_chunk_bytes(kTmaChunkKiB));
+    const int occ = dev::tma_blocks_per_sm(dev::tma_chunk_bytes(tma_kib()));
     return grid_cap(sm_count_ * (cfg_.blocks_per_sm > 0 ? std::min(cfg_.blocks_per_sm, occ) : occ));
   }
   const int occ = dev::copy_blocks_per_sm(cfg_.threads);
@@ -811,7 +813,7 @@ void Exec::prepare_bwd() {
     uint64_t total = 0;
     for (const auto& s : bwd_local_) total += static_cast<uint64_t>(s.n);
     const uint64_t grid = static_cast<uint64_t>(
-        grid_cap(sm_count_ * dev::reduce_blocks_per_sm(cfg_.threads, cfg_.grad_in_dtype, cfg_.grad_out_dtype)));
+        grid_cap_bwd(sm_count_ * dev::reduce_blocks_per_sm(cfg_.threads, cfg_.grad_in_dtype, cfg_.grad_out_dtype)));
     unit = 8192;
     while (unit < 32768 && total / (2 * unit) >= 2 * grid) unit *= 2;
   }
@@ -909,7 +911,7 @@ void Exec::prepare_bwd() {
   bwd_groups_ = static_cast<int>(groups.size());
   int fan = 0;
   for (const auto& g : groups) fan |= g.size() > 1;
-  const int bgrid = grid_cap(sm_count_ * bps);
+  const int bgrid = grid_cap_bwd(sm_count_ * bps);
   // Remote chunks: longer than local ones when the return is large (every
   // stage of a chunk is in flight at once), up to half the TMA ring and while
   // every CTA still gets >= 4 remote chunks. Measured at N=4 (one box, A/B):

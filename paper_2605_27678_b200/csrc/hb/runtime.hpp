@@ -52,6 +52,8 @@ struct ExecConfig {
   int text_embedding = 0;           // splice: TEXT holds int32 token ids, rows gathered from an embedding table
   int max_ctas = 0;                 // cap on every boundary kernel's grid (0: fill the GPU); leaves SMs to
                                     // concurrent work (PP P2P, compute) and lets several execs share one GPU
+  int max_ctas_bwd = 0;             // cap on the backward grid alone (0: max_ctas)
+  int tma_chunk_kib = 0;            // TMA copy stage KiB (0: HB_TMA_CHUNK_KB or 32)
   int pdl = 1;                      // launch with programmatic dependent launch (off: execs sharing a device,
                                     // the host runtime whose NCCL kernels need SMs next to boundary kernels)
 };
@@ -180,6 +182,11 @@ class Exec {
   std::vector<unsigned char*> peer_base_;
   std::vector<char> peer_ipc_;  // peer_base_[g] was opened with cudaIpcOpenMemHandle (closed at exit)
   int grid_cap(int grid) const { return cfg_.max_ctas > 0 && cfg_.max_ctas < grid ? cfg_.max_ctas : grid; }
+  int grid_cap_bwd(int grid) const {
+    const int c = cfg_.max_ctas_bwd > 0 ? cfg_.max_ctas_bwd : cfg_.max_ctas;
+    return c > 0 && c < grid ? c : grid;
+  }
+  int tma_kib() const;
   struct Binding {
     void* ptr = nullptr;
     int64_t stride = 0;  // elements between rows (0: packed)
