@@ -1197,6 +1197,51 @@ def paired_bound(tm, pk, N):
     return best * 1e3, crit
 
 
+def fused_paired_ms(rt_kw, rank, N, local, slots, dev, stream, barrier, cfg, cycles):
+    """The same paired cycle through the fused step kernel (graph what=5): one
+    launch per step, a TMA forward lane and a 15-warp gradient return in every
+    CTA, grid uncapped (two CTAs per SM; the kinds cannot starve each other).
+    Its results are checked bit for bit against the serial cycle in
+    tests/test_paired.py. Returns ms per step (max over ranks), or None when
+    HB_BENCH_FUSED=0."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_27678_b200 import bridge as hbb
+
+    if os.environ.get("HB_BENCH_FUSED", "1") == "0":
+        return None
+    barrier()
+    rt = hbb.BridgeRuntime(**rt_kw)
+    try:
+        if N > 1:
+            rt.exchange_handles()
+        fill_inputs(rt, local, slots, dev)
+        what = rt.GRAPH_PAIRED_FUSED
+        rt.capture_step(0, cfg.beta, True, stream, what=what)
+        rt.replay_step(0, stream, what)
+        barrier()
+        n0 = rt.stats()["launches"]
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(cycles):
+            rt.replay_step(0, stream, what)
+        b.record(stream)
+        stream.synchronize()
+        if rt.stats()["launches"] - n0 != cycles * slots:  # a fallback to two kernels per step
+            raise RuntimeError("fused paired kernel not used")
+        t = torch.tensor([a.elapsed_time(b) / (cycles * slots)], dtype=torch.float64, device=dev)
+        if N > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        if rt.status():
+            raise RuntimeError("device flag wait timed out (fused paired)")
+        return t.item()
+    finally:
+        barrier()
+        rt.close()
+        torch.cuda.synchronize()
+
+
 def run_paired(args, name, N, rank, dev, barrier, stream, pk):
     """1F1B-paired boundary steps: a pipeline schedule call returns microbatch
     k's gradient in the same call that receives microbatch k+1, so the runtime's
@@ -1231,9 +1276,9 @@ def run_paired(args, name, N, rank, dev, barrier, stream, pk):
     else:
         caps = dict(max_ctas=sms)
     cap = caps["max_ctas"]
-    rt = hbb.BridgeRuntime(plan, sp, n_gpus=N, my_gpu=rank, rank_to_gpu=r2g, act_dtype=tdt[cfg.act],
-                           grad_in_dtype=tdt[cfg.grad_in], grad_out_dtype=tdt[cfg.grad_out], mb_slots=slots,
-                           timeout_s=5.0, **caps)  # (a failed co-residency would time out fast)
+    rt_kw = dict(plan=plan, splice=sp, n_gpus=N, my_gpu=rank, rank_to_gpu=r2g, act_dtype=tdt[cfg.act],
+                 grad_in_dtype=tdt[cfg.grad_in], grad_out_dtype=tdt[cfg.grad_out], mb_slots=slots, timeout_s=5.0)
+    rt = hbb.BridgeRuntime(**rt_kw, **caps)  # (a failed co-residency would time out fast)
     try:
         if N > 1:
             rt.exchange_handles()
@@ -1268,6 +1313,7 @@ def run_paired(args, name, N, rank, dev, barrier, stream, pk):
             rt.capture_step(k, cfg.beta, True, stream)
         parity = check_parity(rt, cfg, plan, sp, r2g, rank, N, dev, stream, barrier,
                               lambda k: rt.replay_step(k, stream), 0)
+        ms_fused = fused_paired_ms(rt_kw, rank, N, local, slots, dev, stream, barrier, cfg, cycles)
         fwd_b, bwd_b = payload_bytes(cfg)
         tp_ms, crit = paired_bound(tm, pk, N)
         fk, bk = kernel_bound(tm, "fwd", 1.0, pk, N), kernel_bound(tm, "bwd", 1.0, pk, N)
@@ -1278,6 +1324,8 @@ def run_paired(args, name, N, rank, dev, barrier, stream, pk):
                 "critical": {"gpu": crit[0], "bound": crit[1]} if crit else None,
                 "serial_tstar_ms": round(fk["tstar_ms"] + bk["tstar_ms"], 4),
                 "serial_same_cap_ms_per_step": round(ms_serial, 5),
+                "fused_ms_per_step": round(ms_fused, 5) if ms_fused else None,
+                "frac_of_tstar_paired_fused": round(tp_ms / ms_fused, 4) if ms_fused else None,
                 "grid_caps": caps, "buffer_sets": slots, "steps": cycles * slots, "parity": parity,
                 "how": "hb_exec_graph_capture what=4: step k = fwd(set k) || bwd(set k-1) on two streams, "
                        "one graph per cycle of buffer sets; CUDA events, max over ranks"}

@@ -247,7 +247,9 @@ int hb_exec_set_text_embedding_shard(hb_exec* x, int rank, const void* shard, lo
  * set in order (one launch replays mb_slots steps; mb_slot ignored), 4 the
  * 1F1B-paired cycle: step k runs the forward of set k concurrently with the
  * backward(beta) of set k-1 (a pipeline schedule call pairs them the same way;
- * mb_slots >= 2; size max_ctas so both grids fit on the GPU together). One
+ * mb_slots >= 2; size max_ctas so both grids fit on the GPU together), 5 the
+ * same cycle with each pair in ONE warp-specialised launch (a TMA lane for the
+ * forward, 15 warps for the gradient return; no co-residency condition). One
  * graph launch replays the ops; replays bypass the microbatch records. */
 int hb_exec_graph_capture(hb_exec* x, int mb_slot, int what, float beta, void* cuda_stream);
 int hb_exec_graph_launch(hb_exec* x, int mb_slot, int what, void* cuda_stream);

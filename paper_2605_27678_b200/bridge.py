@@ -447,7 +447,7 @@ class BridgeRuntime:
     def backward(self, mb: int = 0, beta: float = 0.0, stream=None):
         check(lib().hb_exec_backward(self._h, mb, ctypes.c_float(beta), self._stream(stream)))
 
-    GRAPH_FWD, GRAPH_STEP, GRAPH_BWD, GRAPH_CYCLE, GRAPH_PAIRED = 0, 1, 2, 3, 4
+    GRAPH_FWD, GRAPH_STEP, GRAPH_BWD, GRAPH_CYCLE, GRAPH_PAIRED, GRAPH_PAIRED_FUSED = 0, 1, 2, 3, 4, 5
 
     def capture_step(self, mb_slot: int = 0, beta: float = 1.0, with_backward: bool = True, stream=None,
                      what: int | None = None):

@@ -988,6 +988,23 @@ void Exec::launch_backward(int mb_slot, float beta, void* stream) {
   ++launches_;
 }
 
+// The forward of set f and the gradient return of set b in one warp-specialised
+// launch (dev::launch_paired); two launches when the partitions do not allow it.
+void Exec::launch_paired(int fslot, int bslot, float beta, void* stream) {
+  const DevTables& F = tables_[fslot];
+  const DevTables& R = tables_[bslot];
+  const int grid = std::max(fwd_part_.grid, bwd_part_.grid);
+  const int rc = dev::launch_paired(F.copy, fwd_part_.dev(), sync_fwd_, R.reduce, R.terms, bwd_part_.dev(),
+                                    cfg_.grad_in_dtype, cfg_.grad_out_dtype, beta, sync_bwd_, grid, stream);
+  if (rc == 5) ck(cudaGetLastError(), "paired_step launch");
+  if (rc == 0) {
+    ++launches_;
+    return;
+  }
+  launch_forward(fslot, stream);
+  launch_backward(bslot, beta, stream);
+}
+
 // A forward writes buffer set mb % mb_slots; a microbatch still awaiting its
 // backward on the same set would have its activations (and, later, its
 // gradients) overwritten, so in-flight microbatches must map to distinct sets
@@ -1120,10 +1137,10 @@ void Exec::backward(int mb, float beta, void* stream) {
 void Exec::graph_capture(int mb_slot, int what, float beta, void* stream) {
   DeviceGuard dg(device_);
   if (mb_slot < 0 || mb_slot >= cfg_.mb_slots) raise(ErrorCode::InvalidArgument, "mb slot out of range");
-  if (what < 0 || what > 4)
+  if (what < 0 || what > 5)
     raise(ErrorCode::InvalidArgument, "graph 'what' must be 0 (fwd), 1 (fwd+bwd), 2 (bwd), 3 (a step per buffer "
-                                      "set), 4 (a 1F1B-paired cycle)");
-  if (what == 4 && cfg_.mb_slots < 2) raise(ErrorCode::InvalidArgument, "a paired cycle needs mb_slots >= 2");
+                                      "set), 4 (a 1F1B-paired cycle), 5 (the same cycle with fused paired steps)");
+  if (what >= 4 && cfg_.mb_slots < 2) raise(ErrorCode::InvalidArgument, "a paired cycle needs mb_slots >= 2");
   if (what >= 3) mb_slot = 0;  // cycle graphs are keyed on slot 0
   if (!stream) raise(ErrorCode::InvalidArgument, "graph capture needs a non-default stream");
   if (what != 2) prepare_fwd();
@@ -1142,6 +1159,8 @@ void Exec::graph_capture(int mb_slot, int what, float beta, void* stream) {
       launch_forward(k, stream);
       launch_backward(k, beta, stream);
     }
+  } else if (what == 5) {  // 1F1B pairing, each pair in one fused launch
+    for (int k = 0; k < cfg_.mb_slots; ++k) launch_paired(k, (k + cfg_.mb_slots - 1) % cfg_.mb_slots, beta, stream);
   } else if (what == 4) {
     // 1F1B pairing, as a pipeline's schedule call issues it (the LLM's first
     // stage receives mb k+1 and returns mb k's gradient in the same call):

@@ -117,7 +117,8 @@ class Exec {
   // Replays bypass the microbatch records (a replay is a complete fwd+bwd).
   // what: 0 forward only, 1 forward + backward, 2 backward only, 3 forward +
   // backward of every buffer set in turn, 4 the 1F1B-paired cycle (step k =
-  // forward of set k concurrently with the backward of set k-1).
+  // forward of set k concurrently with the backward of set k-1), 5 the same
+  // cycle with each pair in one warp-specialised launch.
   void graph_capture(int mb_slot, int what, float beta, void* stream);
   void graph_launch(int mb_slot, int what, void* stream);
   uint32_t device_error() const;  // synchronises
@@ -255,7 +256,7 @@ class Exec {
     int stage_local = 0;
     dev::Partition dev() const {
       return {first_seg, per_cta, mode, total_chunks, chunk, chunks, rtotal_chunks, rchunks, rchunk, remote_ctas,
-              lstatic, rstatic, ring, prefetch_other, fan, stage_local};
+              lstatic, rstatic, ring, prefetch_other, fan, stage_local, static_cast<uint32_t>(grid)};
     }
   };
   DevPartition fwd_part_, bwd_part_;
@@ -285,6 +286,7 @@ class Exec {
   cudaStream_t side_ = nullptr;  // the 1F1B-paired graph's backward stream (what = 4)
   cudaEvent_t fork_ = nullptr, join_ = nullptr;
   void launch_forward(int mb_slot, void* stream);
+  void launch_paired(int fslot, int bslot, float beta, void* stream);
   void launch_backward(int mb_slot, float beta, void* stream);
 };
 

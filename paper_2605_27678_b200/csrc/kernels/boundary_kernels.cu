@@ -76,6 +76,11 @@ struct Claimer {
     q = b < p.remote_ctas ? 1 : 0;
     passes = 0;
     has[0] = has[1] = false;
+    if (blockIdx.x >= p.claimers) {  // outside this kind's partition (fused launch with a larger grid)
+      passes = 2;
+      first = kNoChunk;
+      return;
+    }
     const uint32_t idx = q ? static_cast<uint32_t>(b) : static_cast<uint32_t>(b - p.remote_ctas);
     first = idx < (q ? p.rstatic : p.lstatic) ? idx : kNoChunk;
     if (total_of(p, q) == 0) advance_queue(p);
@@ -97,13 +102,13 @@ struct Claimer {
     claim(s, q);
     const int o = q ^ 1;
     if (p.prefetch_other && passes == 0 && !has[o] && total_of(p, o) != 0 &&
-        (c == kNoChunk || static_cast<unsigned long long>(c) + gridDim.x >= total_of(p, q)))
+        (c == kNoChunk || static_cast<unsigned long long>(c) + p.claimers >= total_of(p, q)))
       claim(s, o);
   }
   __device__ uint32_t resolve(const Partition& p, uint32_t e, unsigned long long raw, int qq) const {
     const uint32_t total = total_of(p, qq);
     const uint32_t stat = qq ? p.rstatic : p.lstatic;
-    const unsigned long long adv = static_cast<unsigned long long>(total - stat) + gridDim.x;
+    const unsigned long long adv = static_cast<unsigned long long>(total - stat) + p.claimers;
     const unsigned long long idx = raw - static_cast<unsigned long long>(e - 1) * adv + stat;
     return idx < total ? static_cast<uint32_t>(idx) : kNoChunk;
   }
@@ -393,18 +398,13 @@ __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wa
 // shared-memory stages: loads for the next stages are in flight while the
 // current stage is stored (once per destination of the run). Chunks (= one
 // stage) come from the work queues; unaligned runs are copied by lane 0.
+// The issuing lane of a TMA copy: arrival, the stage ring over the claimed
+// chunks, and the end-of-launch protocol (called by exactly one thread of the
+// CTA; `full` and `cs` are that CTA's shared memory).
 template <int kTmaStages, uint32_t kTmaStageBytes>
-__global__ void __launch_bounds__(32) copy_segments_tma_kernel(const CopySeg* __restrict__ segs, int nseg,
-                                                               Partition part, SyncArgs sync) {
-  extern __shared__ __align__(128) unsigned char stage_mem[];
-  __shared__ __align__(8) uint64_t full[kTmaStages];
-  __shared__ CtaSync cs;
-  griddep_wait();
-  if (blockIdx.x == 0) {
-    post_peers_warp(sync, 0);
-    __syncwarp();
-  }
-  if (threadIdx.x != 0) return;  // one issuing lane; the rest of the warp has nothing to do
+__device__ __forceinline__ void tma_copy_lane(const CopySeg* __restrict__ segs, const Partition& part,
+                                              const SyncArgs& sync, unsigned char* stage_mem, uint64_t* full,
+                                              CtaSync& cs) {
   trace_at(sync, kTrEntry);
   const unsigned long long arr = cta_arrive_issue(sync);
   for (int i = 0; i < kTmaStages; ++i) mbar_init(&full[i]);
@@ -528,6 +528,21 @@ __global__ void __launch_bounds__(32) copy_segments_tma_kernel(const CopySeg* __
   trace_at(sync, kTrExit);
   trace_val(sync, kTrChunks, issued);
   trace_val(sync, kTrRemote, nremote);
+}
+
+template <int kTmaStages, uint32_t kTmaStageBytes>
+__global__ void __launch_bounds__(32) copy_segments_tma_kernel(const CopySeg* __restrict__ segs, int nseg,
+                                                               Partition part, SyncArgs sync) {
+  extern __shared__ __align__(128) unsigned char stage_mem[];
+  __shared__ __align__(8) uint64_t full[kTmaStages];
+  __shared__ CtaSync cs;
+  griddep_wait();
+  if (blockIdx.x == 0) {
+    post_peers_warp(sync, 0);
+    __syncwarp();
+  }
+  if (threadIdx.x != 0) return;  // one issuing lane; the rest of the warp has nothing to do
+  tma_copy_lane<kTmaStages, kTmaStageBytes>(segs, part, sync, stage_mem, full, cs);
 }
 
 // ---- reduction ---------------------------------------------------------------
@@ -718,14 +733,14 @@ __device__ __forceinline__ void finish8(TOut* __restrict__ dst, uint64_t i, floa
 // thread per iteration (their loads are issued together).
 template <class TIn, class TOut>
 __device__ __forceinline__ void reduce_range(TOut* __restrict__ dst, const TIn* const* __restrict__ tp, int nterms,
-                                             uint64_t a, uint64_t b, float beta) {
+                                             uint64_t a, uint64_t b, float beta, uint32_t tid, uint32_t nthr) {
   uint64_t align = reinterpret_cast<uint64_t>(dst + a);
   for (int t = 0; t < nterms; ++t) align |= reinterpret_cast<uint64_t>(tp[t] + a);
   uint64_t i = a;
   if ((align & 15) == 0 && nterms > 0) {
     const uint64_t vend = a + ((b - a) & ~uint64_t(7));
-    const uint64_t step = static_cast<uint64_t>(blockDim.x) * 8;
-    for (i = a + threadIdx.x * 8; i + step < vend; i += 2 * step) {
+    const uint64_t step = static_cast<uint64_t>(nthr) * 8;
+    for (i = a + tid * 8; i + step < vend; i += 2 * step) {
       float acc0[8], acc1[8];
       sum_terms8x2(tp, nterms, i, step, acc0, acc1);
       if (beta != 0.0f) {  // both accumulator loads in flight before either store
@@ -748,27 +763,33 @@ __device__ __forceinline__ void reduce_range(TOut* __restrict__ dst, const TIn* 
     }
     i = vend;
   }
-  for (uint64_t e = i + threadIdx.x; e < b; e += blockDim.x) {  // tail / unaligned
+  for (uint64_t e = i + tid; e < b; e += nthr) {  // tail / unaligned
     float acc = 0.0f;
     for (int t = 0; t < nterms; ++t) acc += Cvt<TIn>::to(tp[t][e]);
     if (beta != 0.0f) acc = fmaf(beta, Cvt<TOut>::to(dst[e]), acc);
     dst[e] = Cvt<TOut>::from(acc);
   }
 }
+template <class TIn, class TOut>
+__device__ __forceinline__ void reduce_range(TOut* __restrict__ dst, const TIn* const* __restrict__ tp, int nterms,
+                                             uint64_t a, uint64_t b, float beta) {
+  reduce_range<TIn, TOut>(dst, tp, nterms, a, b, beta, threadIdx.x, blockDim.x);
+}
 
 // reduce_range for a fan-out segment: the terms' sum is formed once per
 // 8-element group and read-modify-written into each of the nd accumulators.
 template <class TIn, class TOut>
 __device__ __forceinline__ void reduce_range_fan(TOut* const* __restrict__ dl, int nd, const TIn* const* __restrict__ tp,
-                                              int nterms, uint64_t a, uint64_t b, float beta) {
+                                              int nterms, uint64_t a, uint64_t b, float beta, uint32_t tid,
+                                              uint32_t nthr) {
   uint64_t align = 0;
   for (int d = 0; d < nd; ++d) align |= reinterpret_cast<uint64_t>(dl[d] + a);
   for (int t = 0; t < nterms; ++t) align |= reinterpret_cast<uint64_t>(tp[t] + a);
   uint64_t i = a;
   if ((align & 15) == 0 && nterms > 0) {
     const uint64_t vend = a + ((b - a) & ~uint64_t(7));
-    const uint64_t step = static_cast<uint64_t>(blockDim.x) * 8;
-    for (i = a + threadIdx.x * 8; i + step < vend; i += 2 * step) {
+    const uint64_t step = static_cast<uint64_t>(nthr) * 8;
+    for (i = a + tid * 8; i + step < vend; i += 2 * step) {
       float acc0[8], acc1[8];
       sum_terms8x2(tp, nterms, i, step, acc0, acc1);
       for (int d = 0; d < nd; ++d) {
@@ -805,7 +826,7 @@ __device__ __forceinline__ void reduce_range_fan(TOut* const* __restrict__ dl, i
     }
     i = vend;
   }
-  for (uint64_t e = i + threadIdx.x; e < b; e += blockDim.x) {  // tail / unaligned
+  for (uint64_t e = i + tid; e < b; e += nthr) {  // tail / unaligned
     float acc = 0.0f;
     for (int t = 0; t < nterms; ++t) acc += Cvt<TIn>::to(tp[t][e]);
     for (int d = 0; d < nd; ++d) {
@@ -813,6 +834,11 @@ __device__ __forceinline__ void reduce_range_fan(TOut* const* __restrict__ dl, i
       dl[d][e] = Cvt<TOut>::from(v);
     }
   }
+}
+template <class TIn, class TOut>
+__device__ __forceinline__ void reduce_range_fan(TOut* const* __restrict__ dl, int nd, const TIn* const* __restrict__ tp,
+                                              int nterms, uint64_t a, uint64_t b, float beta) {
+  reduce_range_fan<TIn, TOut>(dl, nd, tp, nterms, a, b, beta, threadIdx.x, blockDim.x);
 }
 
 struct ReduceLen {
@@ -1191,7 +1217,134 @@ __global__ void __launch_bounds__(512, 2) reduce_segments_stream_kernel(const Re
   }
 }
 
+// ---- fused 1F1B-paired step ----------------------------------------------------
+// One launch runs a forward and a gradient return at once (the pair a pipeline
+// schedule call issues: microbatch k+1's activations in, microbatch k's
+// gradient back), warp-specialised inside each CTA: lane 0 of warp 0 drives the
+// TMA copy ring of the forward (tma_copy_lane), warps 1-15 run the gradient
+// return with LDG.128 loads (remote terms too), synchronised among themselves
+// by a named barrier. Each side keeps its own claim queues, arrival counter,
+// pads and end-of-launch protocol (op kinds 0 and 1), so the pair is exactly
+// one forward op and one backward op for the peers. Unlike two concurrent
+// kernels, nothing depends on both grids being co-resident: both halves of
+// every CTA are resident together by construction.
+constexpr uint32_t kPairedThreads = 512, kPairedRedThreads = kPairedThreads - 32;
+
+__device__ __forceinline__ void group_sync(uint32_t nthr) {
+  asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
+}
+
+template <class TIn, class TOut, bool FAN>
+__device__ __forceinline__ void reduce_group_loop(const ReduceSeg* __restrict__ segs, const void* const* __restrict__ terms,
+                                                  const Partition& part, float beta, const SyncArgs& sync, CtaSync& cs,
+                                                  uint32_t tid, uint32_t nthr) {
+  __shared__ Claimer cl;
+  __shared__ uint32_t cur;
+  __shared__ int cur_remote;
+  unsigned long long arr = 0;
+  if (tid == 0) {
+    arr = cta_arrive_issue(sync);
+    cl.init(part);
+    cur = cl.done() ? kNoChunk : cl.first;
+    cur_remote = cl.q;
+    if (!cl.done()) cl.issue(part, sync, cl.first);
+    if (cur != kNoChunk && cl.q == 1) {
+      cta_arrive_finish(sync, cs, arr);
+      arr = ~0ull;
+      sync_wait_lane(sync, cs);
+    }
+  }
+  group_sync(nthr);
+  bool first = true;
+  while (true) {
+    const uint32_t c = cur;
+    if (c != kNoChunk && (!cur_remote || cs.ok)) {
+      const uint2 t = (cur_remote ? part.rchunks : part.chunks)[c];
+      const ReduceSeg sg = segs[t.x];
+      const uint64_t cu = cur_remote ? part.rchunk : part.chunk;
+      const uint64_t a = static_cast<uint64_t>(t.y & 0xffffffu) * cu, e = a + ((t.y >> 24) + 1) * cu;
+      const uint64_t b = e < sg.nelem ? e : sg.nelem;
+      const TIn* const* tp = reinterpret_cast<const TIn* const*>(terms + sg.term0);
+      if constexpr (FAN) {
+        TOut* const* dl = reinterpret_cast<TOut* const*>(const_cast<void* const*>(terms + sg.dst0));
+        reduce_range_fan<TIn, TOut>(dl, sg.ndst, tp, sg.nterms, a, b, beta, tid, nthr);
+      } else {
+        reduce_range<TIn, TOut>(static_cast<TOut*>(sg.dst), tp, sg.nterms, a, b, beta, tid, nthr);
+      }
+    }
+    group_sync(nthr);
+    if (tid == 0) {
+      if (first && arr != ~0ull) cta_arrive_finish(sync, cs, arr);
+      first = false;
+      int rq = 0;
+      cur = cl.next(part, sync, cs.e, &rq);
+      cur_remote = rq;
+      if (cur != kNoChunk && rq) sync_wait_lane(sync, cs);
+    }
+    group_sync(nthr);
+    if (cur == kNoChunk) break;
+  }
+  if (tid == 0) launch_end_lane(sync, cs);
+}
+
+template <class TIn, class TOut, bool FAN>
+__global__ void __launch_bounds__(kPairedThreads, 2)
+    paired_step_kernel(const CopySeg* __restrict__ csegs, Partition cpart, SyncArgs csync,
+                       const ReduceSeg* __restrict__ rsegs, const void* const* __restrict__ terms, Partition rpart,
+                       float beta, SyncArgs rsync) {
+  extern __shared__ __align__(128) unsigned char stage_mem[];
+  __shared__ __align__(8) uint64_t full[3];
+  __shared__ CtaSync ccs, rcs;
+  griddep_wait();
+  if (blockIdx.x == 0 && threadIdx.x < 32) {  // "started" of both ops to every peer
+    post_peers_warp(csync, 0);
+    post_peers_warp(rsync, 0);
+    __syncwarp();
+  }
+  if (threadIdx.x < 32) {
+    if (threadIdx.x == 0) tma_copy_lane<3, 32 * 1024>(csegs, cpart, csync, stage_mem, full, ccs);
+  } else {
+    reduce_group_loop<TIn, TOut, FAN>(rsegs, terms, rpart, beta, rsync, rcs, threadIdx.x - 32, kPairedRedThreads);
+  }
+}
+
 }  // namespace
+
+template <class TIn, class TOut, bool FAN>
+static int launch_paired_t(const CopySeg* csegs, const Partition& cpart, const SyncArgs& csync,
+                           const ReduceSeg* rsegs, const void* const* terms, const Partition& rpart, float beta,
+                           const SyncArgs& rsync, int grid, cudaStream_t st) {
+  static PerDeviceOnce once;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  once(dev, [] {
+    cudaFuncSetAttribute(paired_step_kernel<TIn, TOut, FAN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         3 * 32 * 1024);
+    cudaFuncSetAttribute(paired_step_kernel<TIn, TOut, FAN>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  });
+  paired_step_kernel<TIn, TOut, FAN><<<grid, kPairedThreads, 3 * 32 * 1024, st>>>(csegs, cpart, csync, rsegs, terms,
+                                                                                 rpart, beta, rsync);
+  return cudaGetLastError() == cudaSuccess ? 0 : 5;
+}
+
+int launch_paired(const CopySeg* csegs, Partition cpart, const SyncArgs& csync, const ReduceSeg* rsegs,
+                  const void* const* terms, Partition rpart, int in_dtype, int out_dtype, float beta,
+                  const SyncArgs& rsync, int grid, void* stream) {
+  if (cpart.mode != kPartTma || cpart.chunk != 32 * 1024 || rpart.mode != kPartDynamic) return 1;
+  auto st = static_cast<cudaStream_t>(stream);
+  int rc = 2;
+#define HB_PAIRED(TI, TO)                                                                                        \
+  rc = rpart.fan ? launch_paired_t<TI, TO, true>(csegs, cpart, csync, rsegs, terms, rpart, beta, rsync, grid, st) \
+                 : launch_paired_t<TI, TO, false>(csegs, cpart, csync, rsegs, terms, rpart, beta, rsync, grid, st)
+  switch (in_dtype * 4 + out_dtype) {
+    case kBF16 * 4 + kFP32: HB_PAIRED(__nv_bfloat16, float); break;
+    case kBF16 * 4 + kBF16: HB_PAIRED(__nv_bfloat16, __nv_bfloat16); break;
+    case kFP32 * 4 + kFP32: HB_PAIRED(float, float); break;
+    default: break;
+  }
+#undef HB_PAIRED
+  return rc;
+}
 
 int device_sm_count() {
   int dev = 0, n = 0;

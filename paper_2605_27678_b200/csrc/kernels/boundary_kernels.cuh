@@ -100,6 +100,9 @@ struct Partition {
   int prefetch_other;        // start the other queue's first claim near the current queue's end
   int fan;                   // reduce: some segment has ndst > 1 (fan-out kernel variant)
   int stage_local;           // reduce (streaming kernel): stage local single-term chunks through the ring too
+  uint32_t claimers;         // dynamic / TMA: CTAs that take part in the queues (the partition's grid). A
+                             // launch with a larger grid (the fused paired kernel) leaves the extra CTAs out,
+                             // so the queue counters advance by the same amount in every launch of the kind.
 };
 
 // Cross-GPU epoch barrier over peer-mapped flag words. Every GPU of an exec
@@ -113,8 +116,8 @@ struct Partition {
 //            at start and learns e = epoch + 1; the last to arrive advances the
 //            epoch and zeroes the arrivals (no CTA of this launch reads it after).
 //   queue[2]: monotone 64-bit claim counters of the local / remote work queue.
-//            Every CTA claims until one claim fails in each non-empty queue, so a
-//            launch advances queue q by exactly (total_q - static_q) + grid and
+//            Every claiming CTA claims until one claim fails in each non-empty queue, so
+//            a launch advances queue q by exactly (total_q - static_q) + claimers and
 //            launch e's chunk index is raw - (e-1)*advance + static_q: no reset,
 //            no end-of-launch counter, no fence.
 //   fin    : push mode only — CTAs done writing (last CTA posts "writes done").
@@ -172,6 +175,13 @@ void launch_copy(const CopySeg* segs, int nseg, Partition part, const SyncArgs& 
 void launch_reduce(const ReduceSeg* segs, int nseg, const void* const* terms, Partition part,
                    int in_dtype, int out_dtype, float beta, const SyncArgs& sync, LaunchCfg cfg,
                    void* stream);
+// Fused 1F1B-paired step (one forward + one gradient return in one launch,
+// warp-specialised). Needs the TMA copy partition with 32 KiB stages and the
+// dynamic reduce partition; 0 on launch, 1 unsupported partition, 2 unsupported
+// dtype pair (bf16->fp32, bf16->bf16, fp32->fp32), 5 launch error.
+int launch_paired(const CopySeg* csegs, Partition cpart, const SyncArgs& csync, const ReduceSeg* rsegs,
+                  const void* const* terms, Partition rpart, int in_dtype, int out_dtype, float beta,
+                  const SyncArgs& rsync, int grid, void* stream);
 int device_sm_count();
 int copy_blocks_per_sm(int threads);
 int tma_blocks_per_sm(uint64_t chunk);

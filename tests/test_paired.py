@@ -32,7 +32,7 @@ def _bufs(rts, plan, r2g, S):
     return out
 
 
-def _run(name, n, devices, cap):
+def _run(name, n, devices, cap, what=None):
     cfg = configs.get(name, scale=64)
     plan = hbb.plan_bridge(cfg.edge())
     S = 3
@@ -72,10 +72,14 @@ def _run(name, n, devices, cap):
         for k, b in bufs.items():
             b.copy_(init[k])
         torch.cuda.synchronize()
+        w = rts[0].GRAPH_PAIRED if what is None else what
         for rt, st in zip(rts, streams):
-            rt.capture_step(0, 1.0, stream=st, what=rt.GRAPH_PAIRED)
+            rt.capture_step(0, 1.0, stream=st, what=w)
+        before = [rt.stats()["launches"] for rt in rts]
         for rt, st in zip(rts, streams):
-            rt.replay_step(0, st, rt.GRAPH_PAIRED)
+            rt.replay_step(0, st, w)
+        if w == rts[0].GRAPH_PAIRED_FUSED:  # one launch per pair: the fused kernel ran
+            assert [rt.stats()["launches"] - b for rt, b in zip(rts, before)] == [S] * len(rts)
         torch.cuda.synchronize()
         for rt in rts:
             assert rt.status() == 0
@@ -98,3 +102,17 @@ def test_paired_cycle_equals_serial_group(name):
     n = 2
     devs = list(range(n)) if torch.cuda.device_count() >= n else [0] * n
     _run(name, n, devs, 48)
+
+
+@pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5"])
+def test_fused_paired_cycle_equals_serial_one_gpu(name):
+    """what=5: each pair in one warp-specialised launch (TMA lane for the forward,
+    15 warps for the gradient return)."""
+    _run(name, 1, [0], 0, what=hbb.BridgeRuntime.GRAPH_PAIRED_FUSED)
+
+
+@pytest.mark.parametrize("name", ["c2", "c4"])
+def test_fused_paired_cycle_equals_serial_group(name):
+    n = 2
+    devs = list(range(n)) if torch.cuda.device_count() >= n else [0] * n
+    _run(name, n, devs, 48, what=hbb.BridgeRuntime.GRAPH_PAIRED_FUSED)
