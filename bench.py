@@ -62,10 +62,10 @@ def parse():
                     help="configs also measured (short) in the same run, so every N of the driver's scaling "
                          "run records the fan-in / fan-out / CP-splice / non-colocated step ('' = none)")
     ap.add_argument("--matrix-steps", type=int, default=200)
-    ap.add_argument("--paired", default="c2,c4,c4ip",
+    ap.add_argument("--paired", default="c2,c3,c4,c4ip,c5",
                     help="configs also measured as 1F1B-paired steps (fwd of microbatch k+1 concurrent with bwd "
-                         "of microbatch k, hb_exec_graph_capture what=4) at N > 1 ('' = none). C3 is left out by "
-                         "default: its fan-out gradient return needs more than the one CTA per SM pairing leaves it")
+                         "of microbatch k: two capped streams, hb_exec_graph_capture what=4, and the fused step "
+                         "kernel, what=5) at N > 1 ('' = none)")
     ap.add_argument("--no-runtime", action="store_true",
                     help="skip the host-runtime leg (a24 + f2: 1F1B dispatch table with NC || PP P2P, N = 4, 6, 8)")
     ap.add_argument("--ref-procs", type=int, default=0, help="reference arm: worker processes (0 = auto)")
@@ -1197,20 +1197,21 @@ def paired_bound(tm, pk, N):
     return best * 1e3, crit
 
 
-def fused_paired_ms(rt_kw, rank, N, local, slots, dev, stream, barrier, cfg, cycles):
+def fused_paired_ms(rt_kw, rank, N, local, slots, dev, stream, barrier, cfg, cycles):  # -> (ms, parity)
     """The same paired cycle through the fused step kernel (graph what=5): one
     launch per step, a TMA forward lane and a 15-warp gradient return in every
     CTA, grid uncapped (two CTAs per SM; the kinds cannot starve each other).
-    Its results are checked bit for bit against the serial cycle in
-    tests/test_paired.py. Returns ms per step (max over ranks), or None when
-    HB_BENCH_FUSED=0."""
+    Parity: one more cycle after the timed ones runs the forward and the
+    backward of every buffer set once, so buffer set 0 is checked like a step
+    (check_parity with the cycle as the step). Returns (ms per step, max over
+    ranks, parity block), or (None, None) when HB_BENCH_FUSED=0."""
     import torch
     import torch.distributed as dist
 
     from paper_2605_27678_b200 import bridge as hbb
 
     if os.environ.get("HB_BENCH_FUSED", "1") == "0":
-        return None
+        return None, None
     barrier()
     rt = hbb.BridgeRuntime(**rt_kw)
     try:
@@ -1235,7 +1236,9 @@ def fused_paired_ms(rt_kw, rank, N, local, slots, dev, stream, barrier, cfg, cyc
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         if rt.status():
             raise RuntimeError("device flag wait timed out (fused paired)")
-        return t.item()
+        parity = check_parity(rt, cfg, rt_kw["plan"], rt_kw["splice"], rt_kw["rank_to_gpu"], rank, N, dev, stream,
+                              barrier, lambda k: rt.replay_step(0, stream, what), 0)
+        return t.item(), parity
     finally:
         barrier()
         rt.close()
@@ -1313,7 +1316,7 @@ def run_paired(args, name, N, rank, dev, barrier, stream, pk):
             rt.capture_step(k, cfg.beta, True, stream)
         parity = check_parity(rt, cfg, plan, sp, r2g, rank, N, dev, stream, barrier,
                               lambda k: rt.replay_step(k, stream), 0)
-        ms_fused = fused_paired_ms(rt_kw, rank, N, local, slots, dev, stream, barrier, cfg, cycles)
+        ms_fused, parity_fused = fused_paired_ms(rt_kw, rank, N, local, slots, dev, stream, barrier, cfg, cycles)
         fwd_b, bwd_b = payload_bytes(cfg)
         tp_ms, crit = paired_bound(tm, pk, N)
         fk, bk = kernel_bound(tm, "fwd", 1.0, pk, N), kernel_bound(tm, "bwd", 1.0, pk, N)
@@ -1326,9 +1329,11 @@ def run_paired(args, name, N, rank, dev, barrier, stream, pk):
                 "serial_same_cap_ms_per_step": round(ms_serial, 5),
                 "fused_ms_per_step": round(ms_fused, 5) if ms_fused else None,
                 "frac_of_tstar_paired_fused": round(tp_ms / ms_fused, 4) if ms_fused else None,
+                "parity_fused": parity_fused,
                 "grid_caps": caps, "buffer_sets": slots, "steps": cycles * slots, "parity": parity,
                 "how": "hb_exec_graph_capture what=4: step k = fwd(set k) || bwd(set k-1) on two streams, "
-                       "one graph per cycle of buffer sets; CUDA events, max over ranks"}
+                       "one graph per cycle of buffer sets; fused: what=5, one paired_step_kernel launch per step "
+                       "on an uncapped runtime; CUDA events, max over ranks"}
     finally:
         barrier()
         rt.close()
