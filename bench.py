@@ -1027,7 +1027,7 @@ def hkey(*a):
     return k * 7919
 
 
-def run_host_runtime(name, rank, world, dev, steps=5):
+def run_host_runtime(name, rank, world, dev, steps=None):
     """One topology through the host-owned runtime. Every rank issues the same
     collectives whatever happens on it: a failure (a device flag-wait timeout
     raised by step(), a construction error) is recorded and reduced at the end,
@@ -1039,6 +1039,7 @@ def run_host_runtime(name, rank, world, dev, steps=5):
     from paper_2605_27678_b200 import parity as P
     from paper_2605_27678_b200 import runtime as R
 
+    steps = steps or int(os.environ.get("HB_RT_STEPS", "5"))
     mods, edges, B, W, ppb = rt_topology(name)
     if max(m.rank_end() for m in mods) > world:
         return None
@@ -1060,6 +1061,7 @@ def run_host_runtime(name, rank, world, dev, steps=5):
                                                   skip=R.SKIP_COMPUTE, timeout_s=5.0))
     ok = rt is not None
     ms_first = 0.0
+    paired_ops = 0
     rows = rt.rows if rt is not None else None
     if rt is not None:
         views = [rt.edge_runtime(k) for k in range(len(edges))]
@@ -1124,8 +1126,13 @@ def run_host_runtime(name, rank, world, dev, steps=5):
     # overlap: the same table with one traffic class skipped (only after a clean first step on every rank)
     times = {}
     if flag.item() == 0:
+        # (the *_paired runs issue a call's fwd + bwd of one edge as one fused launch, HB_RT_PAIRED=1)
         for label, skip in (("nc_only", R.SKIP_COMPUTE | R.SKIP_P2P), ("p2p_only", R.SKIP_COMPUTE | R.SKIP_NC),
-                            ("both", R.SKIP_COMPUTE)):
+                            ("both", R.SKIP_COMPUTE), ("nc_only_paired", R.SKIP_COMPUTE | R.SKIP_P2P),
+                            ("both_paired", R.SKIP_COMPUTE)):
+            prev_env = os.environ.get("HB_RT_PAIRED")
+            if label.endswith("_paired"):
+                os.environ["HB_RT_PAIRED"] = "1"
             r2 = attempt("create", lambda: R.HostRuntime(mods, edges, B, W, nmb=nmb, max_ctas=cap, pp_bytes=ppb,
                                                           skip=skip, timeout_s=5.0))
             ts = []
@@ -1144,14 +1151,24 @@ def run_host_runtime(name, rank, world, dev, steps=5):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             times[label] = round(t.item(), 4)
             if r2 is not None:
+                if label == "both_paired":
+                    paired_ops = attempt("paired_ops", r2.paired_ops, 0) or 0
                 attempt("close", r2.close)
+            if prev_env is None:
+                os.environ.pop("HB_RT_PAIRED", None)
+            else:
+                os.environ["HB_RT_PAIRED"] = prev_env
     err = torch.tensor([len(errors)], device=dev)
     dist.all_reduce(err)
+    po = torch.tensor([paired_ops], device=dev)
+    dist.all_reduce(po)  # pairs issued by all ranks over the both_paired run
+    paired_ops = int(po.item())
     res = {"topology": name, "n_gpus": world, "parity": flag.item() == 0 and err.item() == 0, "rows": rows,
-           "nmb": nmb, "max_ctas": cap,
+           "nmb": nmb, "max_ctas": cap, "paired_ops_all_ranks": paired_ops,
            "first_step_ms": round(ms_first or 0.0, 3), "step_ms": times,
            "how": "HostRuntime.step over the 1F1B dispatch table (event-only compute); NC = boundary exec "
-                  "fwd/bwd on the boundary stream, P2P = NCCL send/recv on the PP communicator"}
+                  "fwd/bwd on the boundary stream (*_paired: a call's fwd + bwd of one edge as one fused "
+                  "paired launch, HB_RT_PAIRED=1), P2P = NCCL send/recv on the PP communicator"}
     if times and all(math.isfinite(v) for v in times.values()):
         tb, tp, both = times["nc_only"], times["p2p_only"], times["both"]
         res["overlap"] = round((tb + tp - both) / max(1e-9, min(tb, tp)), 3)

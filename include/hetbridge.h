@@ -230,6 +230,12 @@ int hb_exec_forward(hb_exec* x, int mb, void* cuda_stream);
 /* backward: BridgeRuntime::backward_* ; src_grad = beta*src_grad + returned gradient */
 int hb_exec_backward(hb_exec* x, int mb, float beta, void* cuda_stream);
 int hb_exec_seed_forward_record(hb_exec* x, int mb); /* bridge.hpp:165 */
+/* 1F1B pair (no reference counterpart: the reference issues the two calls
+ * one after the other): forward of fwd_mb and backward of bwd_mb in one launch
+ * of the fused paired step kernel, as hb_exec_forward(fwd_mb) followed by
+ * hb_exec_backward(bwd_mb, beta) would leave every buffer. Peers may issue the
+ * same two ops as separate calls. *fused (may be NULL) = 1 if one launch ran. */
+int hb_exec_paired(hb_exec* x, int fwd_mb, int bwd_mb, float beta, void* cuda_stream, int* fused);
 /* Embedding table [vocab x d_h] (activation dtype, device memory of this GPU). */
 int hb_exec_set_text_embedding(hb_exec* x, const void* table, long long vocab);
 /* Vocab-parallel table (Megatron's VocabParallelEmbedding, the LLM side of
@@ -389,6 +395,9 @@ int hb_runtime_stage_buffer(hb_runtime* r, int which, int mb, void** ptr, size_t
 int hb_runtime_stream(hb_runtime* r, int which, void** stream); /* 0 boundary, 1 PP, 2 compute */
 int hb_runtime_step(hb_runtime* r, hb_compute_fn fn, void* user);
 int hb_runtime_last_step_ms(hb_runtime* r, float* ms); /* synchronises; Timeout if a flag wait expired */
+/* Boundary forward/backward pairs that shared one call of this rank's column
+ * and went out as one hb_exec_paired launch (only with HB_RT_PAIRED=1), all steps. */
+int hb_runtime_paired_ops(const hb_runtime* r, long long* n);
 
 #ifdef __cplusplus
 }

@@ -32,7 +32,7 @@ EXPORTS = [
     "hb_index_forward", "hb_index_backward", "hb_index_backward_balanced", "hb_index_buffer_elems",
     "hb_exec_config_default", "hb_exec_create", "hb_exec_destroy", "hb_exec_ipc_handle",
     "hb_exec_open_peers", "hb_exec_open_peers_local", "hb_exec_buffer", "hb_exec_bind", "hb_exec_bind_strided",
-    "hb_exec_export_bindings", "hb_exec_import_bindings", "hb_exec_forward", "hb_exec_backward",
+    "hb_exec_export_bindings", "hb_exec_import_bindings", "hb_exec_forward", "hb_exec_backward", "hb_exec_paired",
     "hb_exec_seed_forward_record", "hb_exec_status", "hb_exec_reset_protocol", "hb_exec_stats", "hb_exec_graph_capture", "hb_projector_gemm",
     "hb_exec_forward_projected", "hb_exec_set_text_embedding", "hb_exec_set_text_embedding_shard",
     "hb_exec_graph_launch", "hb_exec_trace", "hb_exec_validate",
@@ -40,7 +40,7 @@ EXPORTS = [
     "hb_dispatch_generate", "hb_dispatch_validate", "hb_dispatch_render", "hb_dispatch_nc_order",
     "hb_nccl_unique_id", "hb_runtime_config_default", "hb_runtime_create", "hb_runtime_destroy", "hb_runtime_info",
     "hb_runtime_group", "hb_runtime_edge_exec", "hb_runtime_stage_buffer", "hb_runtime_stream", "hb_runtime_step",
-    "hb_runtime_last_step_ms",
+    "hb_runtime_last_step_ms", "hb_runtime_paired_ops",
     "hb_config_parse", "hb_config_destroy", "hb_config_num_modules", "hb_config_module", "hb_config_run",
     "hb_config_edge", "hb_config_render",
 ]
@@ -139,6 +139,7 @@ def _declare(L):
         "hb_exec_import_bindings": (I, [V, I, V, Sz]),
         "hb_exec_forward": (I, [V, I, V]),
         "hb_exec_backward": (I, [V, I, ctypes.c_float, V]),
+        "hb_exec_paired": (I, [V, I, I, ctypes.c_float, V, ctypes.POINTER(ctypes.c_int)]),
         "hb_exec_seed_forward_record": (I, [V, I]),
         "hb_exec_graph_capture": (I, [V, I, I, ctypes.c_float, V]),
         "hb_exec_graph_launch": (I, [V, I, I, V]),

@@ -447,6 +447,15 @@ class BridgeRuntime:
     def backward(self, mb: int = 0, beta: float = 0.0, stream=None):
         check(lib().hb_exec_backward(self._h, mb, ctypes.c_float(beta), self._stream(stream)))
 
+    def paired(self, fwd_mb: int, bwd_mb: int, beta: float = 0.0, stream=None) -> bool:
+        """forward(fwd_mb) and backward(bwd_mb, beta) in one fused launch (a
+        1F1B schedule call). Peers may issue the two ops separately. Returns
+        True if the fused kernel ran (False: two launches)."""
+        fused = ctypes.c_int(0)
+        check(lib().hb_exec_paired(self._h, fwd_mb, bwd_mb, ctypes.c_float(beta), self._stream(stream),
+                                   ctypes.byref(fused)))
+        return bool(fused.value)
+
     GRAPH_FWD, GRAPH_STEP, GRAPH_BWD, GRAPH_CYCLE, GRAPH_PAIRED, GRAPH_PAIRED_FUSED = 0, 1, 2, 3, 4, 5
 
     def capture_step(self, mb_slot: int = 0, beta: float = 1.0, with_backward: bool = True, stream=None,
@@ -587,6 +596,13 @@ class LocalGroup:
     def backward(self, mb: int = 0, beta: float = 0.0):
         for rt, st in zip(self.rts, self.streams):
             rt.backward(mb, beta, st)
+
+    def paired(self, fwd_mb: int, bwd_mb: int, beta: float = 0.0, fuse=None):
+        """fuse[g] False: GPU g issues the two ops as separate launches (the
+        peers' fused launches must interoperate with it)."""
+        return [rt.paired(fwd_mb, bwd_mb, beta, st) if fuse is None or fuse[g] else
+                (rt.forward(fwd_mb, st), rt.backward(bwd_mb, beta, st))[0]
+                for g, (rt, st) in enumerate(zip(self.rts, self.streams))]
 
     def synchronize(self):
         for st in self.streams:

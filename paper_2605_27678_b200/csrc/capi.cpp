@@ -515,6 +515,14 @@ int hb_exec_backward(hb_exec* x, int mb, float beta, void* stream) {
   });
 }
 
+int hb_exec_paired(hb_exec* x, int fwd_mb, int bwd_mb, float beta, void* stream, int* fused) {
+  return guard([&] {
+    need(x, "exec");
+    const bool f = x->x->paired(fwd_mb, bwd_mb, beta, stream);
+    if (fused) *fused = f ? 1 : 0;
+  });
+}
+
 int hb_exec_graph_capture(hb_exec* x, int mb_slot, int what, float beta, void* stream) {
   return guard([&] {
     need(x, "exec");
@@ -870,6 +878,14 @@ int hb_runtime_last_step_ms(hb_runtime* r, float* ms) {
     need(r, "runtime");
     need(ms, "ms");
     *ms = r->r->last_step_ms();
+  });
+}
+
+int hb_runtime_paired_ops(const hb_runtime* r, long long* n) {
+  return guard([&] {
+    need(r, "runtime");
+    need(n, "n");
+    *n = r->r->paired_ops();
   });
 }
 

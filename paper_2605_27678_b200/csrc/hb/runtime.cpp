@@ -990,7 +990,7 @@ void Exec::launch_backward(int mb_slot, float beta, void* stream) {
 
 // The forward of set f and the gradient return of set b in one warp-specialised
 // launch (dev::launch_paired); two launches when the partitions do not allow it.
-void Exec::launch_paired(int fslot, int bslot, float beta, void* stream) {
+bool Exec::launch_paired(int fslot, int bslot, float beta, void* stream) {
   const DevTables& F = tables_[fslot];
   const DevTables& R = tables_[bslot];
   const int grid = std::max(fwd_part_.grid, bwd_part_.grid);
@@ -999,10 +999,32 @@ void Exec::launch_paired(int fslot, int bslot, float beta, void* stream) {
   if (rc == 5) ck(cudaGetLastError(), "paired_step launch");
   if (rc == 0) {
     ++launches_;
-    return;
+    return true;
   }
   launch_forward(fslot, stream);
   launch_backward(bslot, beta, stream);
+  return false;
+}
+
+bool Exec::paired(int fwd_mb, int bwd_mb, float beta, void* stream) {
+  NvtxRange nv("paired", fwd_mb);
+  DeviceGuard dg(device_);
+  if (!fwd_done_.count(bwd_mb))
+    raise(ErrorCode::UnknownMicrobatch, "no forward record for microbatch " + std::to_string(bwd_mb));
+  // bwd_mb's set is released by this call: its backward reads only the
+  // gradient slots, the forward writes only the activation slots
+  fwd_done_.erase(bwd_mb);
+  try {
+    check_forward_mb(fwd_mb);
+  } catch (...) {
+    fwd_done_.insert(bwd_mb);
+    throw;
+  }
+  prepare_fwd();
+  prepare_bwd();
+  const bool fused = launch_paired(fwd_mb % cfg_.mb_slots, bwd_mb % cfg_.mb_slots, beta, stream);
+  fwd_done_.insert(fwd_mb);
+  return fused;
 }
 
 // A forward writes buffer set mb % mb_slots; a microbatch still awaiting its

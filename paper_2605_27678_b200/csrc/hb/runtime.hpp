@@ -101,6 +101,11 @@ class Exec {
   void forward_projected(int mb, const void* x, int64_t ldx, const void* w, int64_t ldw, int d_h, int K,
                          int64_t x_rows, void* stream);
   void backward(int mb, float beta, void* stream);
+  // 1F1B pair in one launch: forward of fwd_mb and backward of bwd_mb (its
+  // forward recorded), both ops of every peer's epoch sequence, run together by
+  // the fused paired step kernel (two launches when the partitions cannot fuse).
+  // Returns true if the fused kernel ran.
+  bool paired(int fwd_mb, int bwd_mb, float beta, void* stream);
   void seed_forward_record(int mb);
   // Embedding table [vocab x d_h] (act dtype, on this GPU) the splice gathers
   // text rows from when cfg.text_embedding.
@@ -286,7 +291,7 @@ class Exec {
   cudaStream_t side_ = nullptr;  // the 1F1B-paired graph's backward stream (what = 4)
   cudaEvent_t fork_ = nullptr, join_ = nullptr;
   void launch_forward(int mb_slot, void* stream);
-  void launch_paired(int fslot, int bslot, float beta, void* stream);
+  bool launch_paired(int fslot, int bslot, float beta, void* stream);
   void launch_backward(int mb_slot, float beta, void* stream);
 };
 

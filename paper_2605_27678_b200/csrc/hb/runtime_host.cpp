@@ -275,9 +275,40 @@ void HostRuntime::step(ComputeFn fn, void* user) {
     // one global order of boundary ops across the GPUs (sched::nc_issue_order)
     std::stable_sort(nc.begin(), nc.end(),
                      [&](const sched::Cell* a, const sched::Cell* b) { return sched::nc_before(graph_, *a, *b); });
-    for (const auto* c : nc) {
+    // A call that hands one microbatch's gradient back and takes the next
+    // microbatch's activation (Megatron's send_backward_recv_forward /
+    // send_forward_recv_backward) issues both boundary ops of the same edge
+    // as one fused paired launch (HB_RT_PAIRED=1, read per step; default off):
+    // the two ops overlap on every SM. Peers that issue the ops separately
+    // interoperate (each op is still one op of its kind's epoch sequence).
+    // Measured at N=4 with event-only compute (profiles/r02/host_runtime_paired_n4.json):
+    // boundary-only steps 24-32% shorter, but a paired Recv also waits for its
+    // partner Send's compute event, so on a P2P-bound table (c5w4) the
+    // forward can no longer run ahead and the full step is 9% longer; on join4
+    // it is 16% shorter. Pairing only Send->Recv (where the Recv was queued
+    // behind that wait anyway) measured no gain either way.
+    const char* pe = std::getenv("HB_RT_PAIRED");
+    const bool pair_ops = pe && pe[0] == '1';
+    auto is_fwd = [](sched::Op o) { return o == sched::Op::SendFwd || o == sched::Op::RecvFwd; };
+    for (size_t j = 0; j < nc.size(); ++j) {
+      const auto* c = nc[j];
       Exec* x = execs_.at(graph_.edges[c->edge].boundary).get();
       const int64_t id = base + c->mb;
+      if (pair_ops && !(cfg_.skip & 1) && j + 1 < nc.size() &&
+          graph_.edges[nc[j + 1]->edge].boundary == graph_.edges[c->edge].boundary &&
+          is_fwd(c->op) != is_fwd(nc[j + 1]->op) &&
+          c->mb != nc[j + 1]->mb) {
+        const auto* f = is_fwd(c->op) ? c : nc[j + 1];
+        const auto* b = is_fwd(c->op) ? nc[j + 1] : c;
+        if (f->op == sched::Op::SendFwd) ck(cudaStreamWaitEvent(sb, ev(1, f->mb), 0), "wait");
+        if (b->op == sched::Op::SendBwd) ck(cudaStreamWaitEvent(sb, ev(3, b->mb), 0), "wait");
+        x->paired(static_cast<int>(base + f->mb), static_cast<int>(base + b->mb), 0.0f, sb);
+        ++paired_ops_;
+        if (f->op == sched::Op::RecvFwd) ck(cudaEventRecord(ev(0, f->mb), sb), "record");
+        if (b->op == sched::Op::RecvBwd) ck(cudaEventRecord(ev(2, b->mb), sb), "record");
+        ++j;
+        continue;
+      }
       switch (c->op) {
         case sched::Op::SendFwd:  // encoder last stage: its activation is ready
           ck(cudaStreamWaitEvent(sb, ev(1, c->mb), 0), "wait");

@@ -71,6 +71,8 @@ class HostRuntime {
   // it, joined with the other streams); synchronises.
   float last_step_ms();
   int64_t steps() const { return steps_; }
+  // forward/backward boundary-op pairs issued as one paired call (all steps)
+  int64_t paired_ops() const { return paired_ops_; }
 
  private:
   struct Nccl;
@@ -90,6 +92,7 @@ class HostRuntime {
   std::vector<cudaEvent_t> ev_;        // per microbatch: fwd in, fwd done, bwd in, bwd done
   cudaEvent_t t0_ = nullptr, t1_ = nullptr;
   int64_t steps_ = 0;
+  int64_t paired_ops_ = 0;
   cudaEvent_t& ev(int kind, int mb) { return ev_[kind * cfg_.nmb + mb]; }
 };
 

@@ -50,6 +50,7 @@ def _declare():
         "hb_runtime_stream": (I, [V, I, P(V)]),
         "hb_runtime_step": (I, [V, COMPUTE_FN, V]),
         "hb_runtime_last_step_ms": (I, [V, P(ctypes.c_float)]),
+        "hb_runtime_paired_ops": (I, [V, P(ctypes.c_longlong)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -164,6 +165,12 @@ class HostRuntime:
         ms = ctypes.c_float()
         check(_declare().hb_runtime_last_step_ms(self._h, ctypes.byref(ms)))
         return ms.value
+
+    def paired_ops(self) -> int:
+        """Boundary forward/backward pairs issued as one fused call so far."""
+        n = ctypes.c_longlong()
+        check(_declare().hb_runtime_paired_ops(self._h, ctypes.byref(n)))
+        return n.value
 
     def close(self):
         h = getattr(self, "_h", None)

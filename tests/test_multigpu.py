@@ -93,3 +93,19 @@ def test_host_runtime_dispatch(n, topologies):
     r = subprocess.run(cmd + topologies, capture_output=True, text=True, timeout=900)
     print(r.stdout[-4000:], r.stderr[-4000:])
     assert r.returncode == 0
+
+
+def test_host_runtime_dispatch_paired():
+    """The same tables with HB_RT_PAIRED=1: a call's forward and backward of
+    one edge go out as one fused paired launch; every NC shard and P2P stage
+    buffer must still match."""
+    n = 4
+    if torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", "29814", os.path.join(HERE, "runtime_worker.py")]
+    env = dict(os.environ, HB_RT_PAIRED="1")
+    r = subprocess.run(cmd + ["c5w4", "join4"], capture_output=True, text=True, timeout=900, env=env)
+    print(r.stdout[-4000:], r.stderr[-4000:])
+    assert r.returncode == 0
+    assert '"paired_ops_all_ranks": 0' not in r.stdout

@@ -116,3 +116,73 @@ def test_fused_paired_cycle_equals_serial_group(name):
     n = 2
     devs = list(range(n)) if torch.cuda.device_count() >= n else [0] * n
     _run(name, n, devs, 48, what=hbb.BridgeRuntime.GRAPH_PAIRED_FUSED)
+
+
+def _schedule(name, n, fuse):
+    """Exec.paired in a 1F1B order (F0 F1 [F2|B0] [F3|B1] B2 B3, beta=1) against
+    the same ops issued one by one; `fuse[g]` False makes GPU g issue its pairs
+    as two launches while its peers fuse."""
+    cfg = configs.get(name, scale=64)
+    plan = hbb.plan_bridge(cfg.edge())
+    S = 3
+    devs = list(range(n)) if torch.cuda.device_count() >= n else [0] * n
+    kw = dict(act_dtype=DT[cfg.act], grad_in_dtype=DT[cfg.grad_in], grad_out_dtype=torch.float32, mb_slots=S,
+              max_ctas=48, timeout_s=20.0)
+    group = hbb.LocalGroup(plan, make_splice(cfg), devices=devs, **kw)
+    try:
+        bufs = _bufs(group.rts, plan, group.rank_to_gpu, S)
+        gen = torch.Generator(device="cpu").manual_seed(11)
+        for key, b in sorted(bufs.items()):
+            if key[1] == hbb.SLOT_TEXT and b.dtype == torch.int32:
+                continue
+            b.copy_(torch.randn(b.numel(), generator=gen).to(b.dtype))
+        torch.cuda.synchronize()
+        init = {k: b.clone() for k, b in bufs.items()}
+        for op, mb in (("f", 0), ("f", 1), ("b", 0), ("f", 2), ("b", 1), ("f", 3), ("b", 2), ("b", 3)):
+            group.forward(mb) if op == "f" else group.backward(mb, 1.0)
+        group.synchronize()
+        serial = {k: b.clone() for k, b in bufs.items()}
+        for k, b in bufs.items():
+            b.copy_(init[k])
+        torch.cuda.synchronize()
+        group.forward(0)
+        group.forward(1)
+        fused = group.paired(2, 0, 1.0, fuse) + group.paired(3, 1, 1.0, fuse)
+        group.backward(2, 1.0)
+        group.backward(3, 1.0)
+        group.synchronize()
+        assert all(rt.status() == 0 for rt in group.rts)
+        for k, b in bufs.items():
+            assert torch.equal(b.view(torch.uint8), serial[k].view(torch.uint8)), f"buffer {k} differs"
+        return fused
+    finally:
+        group.close()
+
+
+@pytest.mark.parametrize("name", ["c2", "c4", "c5"])
+def test_exec_paired_schedule(name):
+    fused = _schedule(name, 2, None)
+    assert all(fused), "the fused kernel should serve these partitions"
+
+
+def test_exec_paired_mixed_with_separate_launches():
+    """GPU 1 issues its pairs as two launches while GPU 0 fuses: each op is
+    still one op of every peer's epoch sequence."""
+    _schedule("c2", 2, [True, False])
+
+
+def test_exec_paired_rejects_unknown_backward():
+    cfg = configs.get("c2", scale=64)
+    rt = hbb.BridgeRuntime(hbb.plan_bridge(cfg.edge()), make_splice(cfg), mb_slots=2, act_dtype=torch.bfloat16,
+                           grad_in_dtype=torch.bfloat16, grad_out_dtype=torch.float32)
+    try:
+        with pytest.raises(hbb.HetBridgeError) as ei:
+            rt.paired(1, 0)
+        assert ei.value.code == "UnknownMicrobatch"
+        rt.forward(0)
+        rt.forward(1)
+        with pytest.raises(hbb.HetBridgeError):  # 3 % 2 == 1: set 1 still holds microbatch 1
+            rt.paired(3, 0)
+        assert rt.paired(2, 0) in (True, False)
+    finally:
+        rt.close()
