@@ -1044,12 +1044,13 @@ def run_host_runtime(name, rank, world, dev, steps=None):
     if max(m.rank_end() for m in mods) > world:
         return None
     errors = []
+    perrs = []  # the HB_RT_PAIRED=1 variant's own (an option, not the parity of the leg)
 
-    def attempt(what, fn, default=None):
+    def attempt(what, fn, default=None, into=None):
         try:
             return fn()
         except Exception as exc:  # recorded, reduced over ranks below
-            errors.append(f"{what}: {type(exc).__name__}: {exc}"[:300])
+            (errors if into is None else into).append(f"{what}: {type(exc).__name__}: {exc}"[:300])
             return default
 
     # 16 microbatches (warm-up and drain, where boundary ops sit on the critical
@@ -1131,45 +1132,51 @@ def run_host_runtime(name, rank, world, dev, steps=None):
                             ("both", R.SKIP_COMPUTE), ("nc_only_paired", R.SKIP_COMPUTE | R.SKIP_P2P),
                             ("both_paired", R.SKIP_COMPUTE)):
             prev_env = os.environ.get("HB_RT_PAIRED")
+            errs = errors
             if label.endswith("_paired"):
                 os.environ["HB_RT_PAIRED"] = "1"
+                errs = perrs
             r2 = attempt("create", lambda: R.HostRuntime(mods, edges, B, W, nmb=nmb, max_ctas=cap, pp_bytes=ppb,
-                                                          skip=skip, timeout_s=5.0))
+                                                          skip=skip, timeout_s=5.0), into=errs)
             ts = []
             if r2 is not None:
                 def one():
                     r2.step()
                     return r2.last_step_ms()
-                attempt("step", one)
+                attempt("step", one, into=errs)
             for _ in range(steps):
                 dist.barrier()
-                if r2 is not None and not errors:
-                    v = attempt("step", one)
+                if r2 is not None and not errs:
+                    v = attempt("step", one, into=errs)
                     if v is not None:
                         ts.append(v)
             t = torch.tensor([statistics.median(ts) if ts else float("nan")], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            times[label] = round(t.item(), 4)
+            times[label] = round(t.item(), 4) if math.isfinite(t.item()) else None  # (None: no clean step)
             if r2 is not None:
                 if label == "both_paired":
-                    paired_ops = attempt("paired_ops", r2.paired_ops, 0) or 0
-                attempt("close", r2.close)
+                    paired_ops = attempt("paired_ops", r2.paired_ops, 0, into=errs) or 0
+                attempt("close", r2.close, into=errs)
             if prev_env is None:
                 os.environ.pop("HB_RT_PAIRED", None)
             else:
                 os.environ["HB_RT_PAIRED"] = prev_env
     err = torch.tensor([len(errors)], device=dev)
     dist.all_reduce(err)
-    po = torch.tensor([paired_ops], device=dev)
-    dist.all_reduce(po)  # pairs issued by all ranks over the both_paired run
-    paired_ops = int(po.item())
+    po = torch.tensor([paired_ops, len(perrs)], device=dev)
+    dist.all_reduce(po)  # pairs issued by all ranks over the both_paired run, paired-variant errors
+    paired_ops, paired_errs = int(po[0].item()), int(po[1].item())
     res = {"topology": name, "n_gpus": world, "parity": flag.item() == 0 and err.item() == 0, "rows": rows,
            "nmb": nmb, "max_ctas": cap, "paired_ops_all_ranks": paired_ops,
            "first_step_ms": round(ms_first or 0.0, 3), "step_ms": times,
            "how": "HostRuntime.step over the 1F1B dispatch table (event-only compute); NC = boundary exec "
                   "fwd/bwd on the boundary stream (*_paired: a call's fwd + bwd of one edge as one fused "
                   "paired launch, HB_RT_PAIRED=1), P2P = NCCL send/recv on the PP communicator"}
-    if times and all(math.isfinite(v) for v in times.values()):
+    if paired_errs:
+        res["paired_variant_errors_on_ranks"] = paired_errs
+        if perrs:
+            res["paired_variant_error_here"] = perrs[0]
+    if times and all(times.get(k) is not None for k in ("nc_only", "p2p_only", "both")):
         tb, tp, both = times["nc_only"], times["p2p_only"], times["both"]
         res["overlap"] = round((tb + tp - both) / max(1e-9, min(tb, tp)), 3)
         # the first microbatch's boundary forward and the last one's backward sit on
