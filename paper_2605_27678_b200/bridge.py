@@ -599,10 +599,17 @@ class LocalGroup:
 
     def paired(self, fwd_mb: int, bwd_mb: int, beta: float = 0.0, fuse=None):
         """fuse[g] False: GPU g issues the two ops as separate launches (the
-        peers' fused launches must interoperate with it)."""
-        return [rt.paired(fwd_mb, bwd_mb, beta, st) if fuse is None or fuse[g] else
-                (rt.forward(fwd_mb, st), rt.backward(bwd_mb, beta, st))[0]
-                for g, (rt, st) in enumerate(zip(self.rts, self.streams))]
+        peers' fused launches must interoperate with it). Returns, per GPU,
+        whether one fused launch ran."""
+        out = []
+        for g, (rt, st) in enumerate(zip(self.rts, self.streams)):
+            if fuse is None or fuse[g]:
+                out.append(rt.paired(fwd_mb, bwd_mb, beta, st))
+            else:
+                rt.forward(fwd_mb, st)
+                rt.backward(bwd_mb, beta, st)
+                out.append(False)
+        return out
 
     def synchronize(self):
         for st in self.streams:

@@ -169,7 +169,7 @@ def test_exec_paired_schedule(name):
 def test_exec_paired_mixed_with_separate_launches():
     """GPU 1 issues its pairs as two launches while GPU 0 fuses: each op is
     still one op of every peer's epoch sequence."""
-    _schedule("c2", 2, [True, False])
+    assert _schedule("c2", 2, [True, False]) == [True, False, True, False]
 
 
 def test_exec_paired_rejects_unknown_backward():
