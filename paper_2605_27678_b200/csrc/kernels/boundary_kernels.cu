@@ -1310,43 +1310,6 @@ __global__ void __launch_bounds__(kPairedThreads, 2)
 
 }  // namespace
 
-template <class TIn, class TOut, bool FAN>
-static int launch_paired_t(const CopySeg* csegs, const Partition& cpart, const SyncArgs& csync,
-                           const ReduceSeg* rsegs, const void* const* terms, const Partition& rpart, float beta,
-                           const SyncArgs& rsync, int grid, cudaStream_t st) {
-  static PerDeviceOnce once;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  once(dev, [] {
-    cudaFuncSetAttribute(paired_step_kernel<TIn, TOut, FAN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         3 * 32 * 1024);
-    cudaFuncSetAttribute(paired_step_kernel<TIn, TOut, FAN>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-  });
-  paired_step_kernel<TIn, TOut, FAN><<<grid, kPairedThreads, 3 * 32 * 1024, st>>>(csegs, cpart, csync, rsegs, terms,
-                                                                                 rpart, beta, rsync);
-  return cudaGetLastError() == cudaSuccess ? 0 : 5;
-}
-
-int launch_paired(const CopySeg* csegs, Partition cpart, const SyncArgs& csync, const ReduceSeg* rsegs,
-                  const void* const* terms, Partition rpart, int in_dtype, int out_dtype, float beta,
-                  const SyncArgs& rsync, int grid, void* stream) {
-  // A fan-out gradient return (some run writes several TP replicas) needs the
-  // full 1024 threads per SM of its own launch: fused it measured 10% slower
-  // than forward-then-backward at N=1 and 8% at N=4 (C3), so it is not fused.
-  if (cpart.mode != kPartTma || cpart.chunk != 32 * 1024 || rpart.mode != kPartDynamic || rpart.fan) return 1;
-  auto st = static_cast<cudaStream_t>(stream);
-  int rc = 2;
-#define HB_PAIRED(TI, TO) rc = launch_paired_t<TI, TO, false>(csegs, cpart, csync, rsegs, terms, rpart, beta, rsync, grid, st)
-  switch (in_dtype * 4 + out_dtype) {
-    case kBF16 * 4 + kFP32: HB_PAIRED(__nv_bfloat16, float); break;
-    case kBF16 * 4 + kBF16: HB_PAIRED(__nv_bfloat16, __nv_bfloat16); break;
-    case kFP32 * 4 + kFP32: HB_PAIRED(float, float); break;
-    default: break;
-  }
-#undef HB_PAIRED
-  return rc;
-}
-
 int device_sm_count() {
   int dev = 0, n = 0;
   cudaGetDevice(&dev);
@@ -1406,6 +1369,44 @@ static void launch_pdl(void (*k)(KArgs...), int grid, int block, size_t smem, cu
   lc.attrs = at;
   lc.numAttrs = pdl ? 1 : 0;
   cudaLaunchKernelEx(&lc, k, args...);
+}
+
+template <class TIn, class TOut, bool FAN>
+static int launch_paired_t(const CopySeg* csegs, const Partition& cpart, const SyncArgs& csync,
+                           const ReduceSeg* rsegs, const void* const* terms, const Partition& rpart, float beta,
+                           const SyncArgs& rsync, int grid, cudaStream_t st) {
+  static PerDeviceOnce once;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  once(dev, [] {
+    cudaFuncSetAttribute(paired_step_kernel<TIn, TOut, FAN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         3 * 32 * 1024);
+    cudaFuncSetAttribute(paired_step_kernel<TIn, TOut, FAN>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  });
+  // (PDL: the next step's CTAs may be scheduled once every CTA's copy lane is done)
+  launch_pdl(paired_step_kernel<TIn, TOut, FAN>, grid, static_cast<int>(kPairedThreads), 3 * 32 * 1024, st, csegs,
+             cpart, csync, rsegs, terms, rpart, beta, rsync);
+  return cudaGetLastError() == cudaSuccess ? 0 : 5;
+}
+
+int launch_paired(const CopySeg* csegs, Partition cpart, const SyncArgs& csync, const ReduceSeg* rsegs,
+                  const void* const* terms, Partition rpart, int in_dtype, int out_dtype, float beta,
+                  const SyncArgs& rsync, int grid, void* stream) {
+  // A fan-out gradient return (some run writes several TP replicas) needs the
+  // full 1024 threads per SM of its own launch: fused it measured 10% slower
+  // than forward-then-backward at N=1 and 8% at N=4 (C3), so it is not fused.
+  if (cpart.mode != kPartTma || cpart.chunk != 32 * 1024 || rpart.mode != kPartDynamic || rpart.fan) return 1;
+  auto st = static_cast<cudaStream_t>(stream);
+  int rc = 2;
+#define HB_PAIRED(TI, TO) rc = launch_paired_t<TI, TO, false>(csegs, cpart, csync, rsegs, terms, rpart, beta, rsync, grid, st)
+  switch (in_dtype * 4 + out_dtype) {
+    case kBF16 * 4 + kFP32: HB_PAIRED(__nv_bfloat16, float); break;
+    case kBF16 * 4 + kBF16: HB_PAIRED(__nv_bfloat16, __nv_bfloat16); break;
+    case kFP32 * 4 + kFP32: HB_PAIRED(float, float); break;
+    default: break;
+  }
+#undef HB_PAIRED
+  return rc;
 }
 
 void launch_copy(const CopySeg* segs, int nseg, Partition part, const SyncArgs& sync, LaunchCfg cfg,
