@@ -1221,6 +1221,18 @@ def paired_bound(tm, pk, N):
     return best * 1e3, crit
 
 
+def status_any(rt, N, dev):
+    """A device flag-wait timeout on any rank (collective: every rank of a
+    diagnostic leg raises together, so none is left waiting in a barrier)."""
+    import torch
+    import torch.distributed as dist
+
+    f = torch.tensor([1 if rt.status() else 0], device=dev)
+    if N > 1:
+        dist.all_reduce(f, op=dist.ReduceOp.MAX)
+    return bool(f.item())
+
+
 def fused_paired_ms(rt_kw, rank, N, local, slots, dev, stream, barrier, cfg, cycles):  # -> (ms, parity, fused)
     """The same paired cycle through the fused step kernel (graph what=5): one
     launch per step, a TMA forward lane and a 15-warp gradient return in every
@@ -1258,7 +1270,7 @@ def fused_paired_ms(rt_kw, rank, N, local, slots, dev, stream, barrier, cfg, cyc
         t = torch.tensor([a.elapsed_time(b) / (cycles * slots)], dtype=torch.float64, device=dev)
         if N > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        if rt.status():
+        if status_any(rt, N, dev):
             raise RuntimeError("device flag wait timed out (fused paired)")
         parity = check_parity(rt, cfg, rt_kw["plan"], rt_kw["splice"], rt_kw["rank_to_gpu"], rank, N, dev, stream,
                               barrier, lambda k: rt.replay_step(0, stream, what), 0)
@@ -1334,7 +1346,7 @@ def run_paired(args, name, N, rank, dev, barrier, stream, pk):
         cycles = max(4, args.matrix_steps // slots)
         ms_paired = timed(rt.GRAPH_PAIRED, cycles)
         ms_serial = timed(rt.GRAPH_CYCLE, cycles)  # the same capped runtime, ops one after the other
-        if rt.status():
+        if status_any(rt, N, dev):
             raise RuntimeError("device flag wait timed out")
         for k in range(slots):
             rt.capture_step(k, cfg.beta, True, stream)
@@ -1434,7 +1446,7 @@ def run_matrix_config(args, name, N, rank, dev, barrier, stream, pk):
         parity = check_parity(rt, cfg, plan, sp, r2g, rank, N, dev, stream, barrier,
                               lambda k: rt.replay_step(k, stream), 0)
         f_ms, b_ms = timed(0, K), timed(2, K)
-        if rt.status():
+        if status_any(rt, N, dev):
             raise RuntimeError("device flag wait timed out")
         fk, bk = kernel_bound(tm, "fwd", f_ms, pk, N), kernel_bound(tm, "bwd", b_ms, pk, N)
         fwd_b, bwd_b = payload_bytes(cfg)
