@@ -1241,9 +1241,12 @@ __device__ __forceinline__ void reduce_group_loop(const ReduceSeg* __restrict__ 
   __shared__ Claimer cl;
   __shared__ uint32_t cur;
   __shared__ int cur_remote;
+  __shared__ uint32_t nch, nrem;  // trace counters (HB_TRACE)
   unsigned long long arr = 0;
   if (tid == 0) {
+    trace_at(sync, kTrEntry);
     arr = cta_arrive_issue(sync);
+    nch = nrem = 0;
     cl.init(part);
     cur = cl.done() ? kNoChunk : cl.first;
     cur_remote = cl.q;
@@ -1271,9 +1274,14 @@ __device__ __forceinline__ void reduce_group_loop(const ReduceSeg* __restrict__ 
       } else {
         reduce_range<TIn, TOut>(static_cast<TOut*>(sg.dst), tp, sg.nterms, a, b, beta, tid, nthr);
       }
+      if (tid == 0 && sync.trace) {
+        ++nch;
+        nrem += cur_remote != 0;
+      }
     }
     group_sync(nthr);
     if (tid == 0) {
+      if (first) trace_at(sync, kTrFirst);
       if (first && arr != ~0ull) cta_arrive_finish(sync, cs, arr);
       first = false;
       int rq = 0;
@@ -1284,7 +1292,13 @@ __device__ __forceinline__ void reduce_group_loop(const ReduceSeg* __restrict__ 
     group_sync(nthr);
     if (cur == kNoChunk) break;
   }
-  if (tid == 0) launch_end_lane(sync, cs);
+  if (tid == 0) {
+    trace_at(sync, kTrDone);
+    launch_end_lane(sync, cs);
+    trace_at(sync, kTrExit);
+    trace_val(sync, kTrChunks, nch);
+    trace_val(sync, kTrRemote, nrem);
+  }
 }
 
 template <class TIn, class TOut, bool FAN>
